@@ -1,0 +1,147 @@
+/*
+ * upscale_b200.h -- C ABI of the B200-native UPSCALE export/inference hot path.
+ *
+ * The reference (`reslice` 0.1.0, /root/reference/pkg) has no FFI: its boundary is
+ * the Python API.  Each entry point below replaces the weight math or the op
+ * semantics of one reference function; the citation names the function whose
+ * behaviour the call reproduces (file:line in /root/reference/pkg/src/reslice).
+ *
+ * Conventions:
+ *   - callers own every buffer; all pointers are DEVICE pointers unless stated;
+ *   - every call takes a cudaStream_t and is stream-ordered (no implicit sync);
+ *   - return 0 (UB_OK) or a negative status; ub_last_error() returns the
+ *     message of the last failing call on the calling thread;
+ *   - activations are NHWC bf16 with a per-tensor channel stride ("cstride",
+ *     a multiple of 8 elements) and a channel offset ("coff") so that a
+ *     reference SLICE node (planner.py:774-777) is a zero-copy view.
+ */
+#ifndef UPSCALE_B200_H
+#define UPSCALE_B200_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UB_OK 0
+#define UB_EINVAL (-1)       /* invalid argument */
+#define UB_EUNSUPPORTED (-2) /* shape/layout this build does not support */
+#define UB_ECUDA (-3)        /* CUDA runtime / driver error */
+
+/* element types */
+#define UB_F32 0
+#define UB_F64 1
+#define UB_BF16 2
+
+/* weight layouts produced by ub_permute_weights */
+#define UB_LAYOUT_OIHW 0 /* [n_rows][n_cols][kh][kw]: the plain 4-D result of apply_plan */
+#define UB_LAYOUT_GEMM 1 /* [n_rows][kh*kw][cpad]: K-major B operand of ub_conv_fwd,
+                            column c of tap t at (lead + c); zeros elsewhere */
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* ub_last_error(void);
+
+/* ABI version (bumped on any signature change). */
+int ub_abi_version(void);
+
+/* Number of kernel launches issued by this library on the calling thread since
+ * the last reset (used by bench.py's gpu_launches claim). */
+long long ub_launch_count(void);
+void ub_reset_launch_count(void);
+
+/*
+ * Weight half of apply_plan, fused over both sides of one layer.
+ * Replaces: planner.py:661-673 (producer rows W[rows,:] and zero_rows),
+ *           planner.py:755-767 (consumer columns W[:,perm] and zero_columns).
+ * out[r][c][t] = W[rows[r]][cols[c]][t] * (row_scale ? row_scale[r] : 1)
+ * rows[r] == -1 or cols[c] == -1 yields 0 (zero_rows / zero_columns).
+ * W is [O][I][kh][kw] in dtype_in (UB_F32 or UB_F64).
+ * layout UB_LAYOUT_OIHW ignores lead/cpad; UB_LAYOUT_GEMM writes [n_rows][kh*kw][cpad]
+ * with column c at lead + c (requires lead + n_cols <= cpad).
+ * dtype_out: UB_F32, UB_F64 (bit-exact copies when row_scale is NULL) or UB_BF16.
+ */
+int ub_permute_weights(const void* W, int dtype_in, int O, int I, int kh, int kw,
+                       const int32_t* rows, int n_rows, const int32_t* cols, int n_cols,
+                       const float* row_scale, int layout, int lead, int cpad,
+                       void* out, int dtype_out, cudaStream_t stream);
+
+/*
+ * Per-channel vector permutation.  Replaces planner.py:731-733
+ * (new_weights[u] = new_weights[u][perm]).  out[i] = v[idx[i]] (idx[i] == -1 -> 0).
+ */
+int ub_permute_vector(const void* v, int dtype, const int32_t* idx, int n, void* out,
+                      cudaStream_t stream);
+
+/*
+ * Standalone channel gather (the baseline export's copy, i.e. a reference GATHER
+ * node executed as index_select).  Replaces interp.py:75-77 over NHWC tensors:
+ * y[p][y_coff + i] = idx[i] >= 0 ? x[p][x_coff + idx[i]] : 0, for p < npix.
+ */
+int ub_channel_gather(const void* x, int x_cstride, int x_coff, const int32_t* idx, int n,
+                      long long npix, void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
+/* K-chunk and padded per-tap K of the GEMM weight layout ub_conv_fwd expects for a
+ * read of `cin` channels starting at channel offset `coff` (TMA needs 16-byte
+ * aligned bases, so a misaligned SLICE start is rounded down and the first
+ * `lead` weight columns are zero).  gather != 0: fused-gather read (lead 0). */
+int ub_conv_weight_layout(int cin, int coff, int gather, int* lead, int* cpad);
+
+/* One convolution (CHANNEL_MIX over a spatial tensor; interp.py:57-63) with its
+ * read node and epilogue fused:
+ *   read:      SLICE  -> x + x_coff view (interp.py:72-74), or
+ *              GATHER -> gather_idx fused into the A-operand staging (interp.py:75-77);
+ *   epilogue:  + bias (folded PER_CHANNEL, interp.py:70-71), + residual (ADD,
+ *              interp.py:64-65), ReLU (PASS_THROUGH, interp.py:68-69), store at a
+ *              channel offset (CONCAT without a copy, interp.py:66-67).
+ * Implicit GEMM on tcgen05 tensor cores: M = N*Ho*Wo, N = cout, K = kh*kw*cpad. */
+typedef struct {
+  int N, H, W;                 /* input geometry */
+  int cin;                     /* channels read (slice length or gather count) */
+  int cout;                    /* output channels */
+  int kh, kw, stride, pad;     /* square stride/pad */
+  int Ho, Wo;                  /* output spatial size */
+  const void* x;               /* bf16 NHWC input */
+  int x_cstride, x_coff;       /* channel stride / SLICE start */
+  const int32_t* gather_idx;   /* fused GATHER indices (1x1 stride-1 only) or NULL */
+  const void* w;               /* bf16 UB_LAYOUT_GEMM weights, [cout][kh*kw][cpad] */
+  int w_lead, w_cpad;          /* from ub_conv_weight_layout */
+  const float* bias;           /* [cout] fp32 or NULL */
+  const void* residual;        /* bf16 NHWC [N*Ho*Wo][res_cstride] or NULL */
+  int res_cstride, res_coff;
+  int relu;                    /* apply max(0, .) after bias + residual */
+  void* y;                     /* output, NHWC [N*Ho*Wo][y_cstride] */
+  int y_cstride, y_coff;
+  int y_dtype;                 /* UB_BF16 or UB_F32 */
+} ub_conv_desc;
+
+int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream);
+
+/* Model-input staging: NCHW fp32 -> NHWC bf16 [N*H*W][y_cstride], channels
+ * idx[0..n) (a GATHER on the INPUT node, fused; idx == NULL: identity over C). */
+int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n,
+                   void* y, int y_cstride, cudaStream_t stream);
+
+/* Max pool (PASS_THROUGH lowering of nn.MaxPool2d), NHWC bf16, -inf padding. */
+int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff,
+                 int k, int stride, int pad, int Ho, int Wo,
+                 void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
+/* Global average pool (nn.AdaptiveAvgPool2d(1)), NHWC bf16 -> [N][y_cstride] bf16. */
+int ub_avgpool_global(const void* x, int N, int HW, int C, int x_cstride, int x_coff,
+                      void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
+/* Generic elementwise node for graphs the conv epilogue cannot absorb:
+ * y = relu?( a*scale + shift + b ) per channel over NHWC bf16 (scale/shift/b optional).
+ * Covers standalone PER_CHANNEL (interp.py:70-71), ADD (64-65), PASS_THROUGH ReLU (68-69). */
+int ub_affine_add_relu(const void* a, int a_cstride, int a_coff,
+                       const float* scale, const float* shift,
+                       const void* b, int b_cstride, int b_coff, int relu,
+                       long long npix, int C, void* y, int y_cstride, int y_coff,
+                       cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UPSCALE_B200_H */

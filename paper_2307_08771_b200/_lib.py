@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in include/upscale_b200.h.
+
+The product path has no fallback: if `libupscale_b200.so` is missing or fails
+to load, every GPU entry point raises `ExtensionMissingError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libupscale_b200.so"
+
+UB_OK = 0
+UB_EINVAL = -1
+UB_EUNSUPPORTED = -2
+UB_ECUDA = -3
+
+UB_F32, UB_F64, UB_BF16 = 0, 1, 2
+UB_LAYOUT_OIHW, UB_LAYOUT_GEMM = 0, 1
+
+c_int, c_ll, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p
+
+
+class ExtensionMissingError(RuntimeError):
+    """The sm_100a library is not built / not loadable (no CPU fallback exists)."""
+
+
+class UBError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[ub status {code}] {msg}")
+        self.code = code
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [
+        ("N", c_int), ("H", c_int), ("W", c_int),
+        ("cin", c_int), ("cout", c_int),
+        ("kh", c_int), ("kw", c_int), ("stride", c_int), ("pad", c_int),
+        ("Ho", c_int), ("Wo", c_int),
+        ("x", c_vp), ("x_cstride", c_int), ("x_coff", c_int),
+        ("gather_idx", c_vp),
+        ("w", c_vp), ("w_lead", c_int), ("w_cpad", c_int),
+        ("bias", c_vp),
+        ("residual", c_vp), ("res_cstride", c_int), ("res_coff", c_int),
+        ("relu", c_int),
+        ("y", c_vp), ("y_cstride", c_int), ("y_coff", c_int),
+        ("y_dtype", c_int),
+    ]
+
+
+# name -> (restype, argtypes); must match include/upscale_b200.h exactly.
+SIGNATURES = {
+    "ub_last_error": (ctypes.c_char_p, []),
+    "ub_abi_version": (c_int, []),
+    "ub_launch_count": (c_ll, []),
+    "ub_reset_launch_count": (None, []),
+    "ub_permute_weights": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int,
+                                   c_vp, c_int, c_int, c_int, c_vp, c_int, c_vp]),
+    "ub_permute_vector": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp]),
+    "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
+    "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "ub_conv_fwd": (c_int, [ctypes.POINTER(ConvDesc), c_vp]),
+    "ub_stage_input": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp]),
+    "ub_maxpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                             c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_avgpool_global": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_affine_add_relu": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_ll,
+                                   c_int, c_vp, c_int, c_int, c_vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ExtensionMissingError(
+                f"{LIB_PATH} not built; run `python -m paper_2307_08771_b200.build` "
+                "(or __graft_entry__.build()). There is no CPU fallback.")
+        try:
+            lib = ctypes.CDLL(str(LIB_PATH))
+        except OSError as exc:
+            raise ExtensionMissingError(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != UB_OK:
+        msg = load().ub_last_error().decode(errors="replace")
+        raise UBError(rc, msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(load().ub_launch_count())
+
+
+def reset_launch_count() -> None:
+    load().ub_reset_launch_count()
+
+
+def conv_weight_layout(cin: int, coff: int, gather: bool) -> tuple[int, int]:
+    lead, cpad = c_int(), c_int()
+    check(load().ub_conv_weight_layout(cin, coff, int(gather), ctypes.byref(lead), ctypes.byref(cpad)))
+    return lead.value, cpad.value

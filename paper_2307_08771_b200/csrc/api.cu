@@ -1,0 +1,64 @@
+// C-ABI plumbing: error reporting, launch counter, driver entry points.
+#include <mutex>
+#include <string>
+
+#include "ub_host.h"
+
+namespace {
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+std::once_flag g_once;
+PFN_cuTensorMapEncodeTiled_v12000 g_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_im2col = nullptr;
+
+void resolve() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
+}
+}  // namespace
+
+namespace ub {
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return UB_OK;
+  return fail(UB_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void count_launch() { ++g_launches; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn() {
+  std::call_once(g_once, resolve);
+  return g_tiled;
+}
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
+  std::call_once(g_once, resolve);
+  return g_im2col;
+}
+
+}  // namespace ub
+
+extern "C" {
+
+const char* ub_last_error(void) { return g_err.c_str(); }
+int ub_abi_version(void) { return 1; }
+long long ub_launch_count(void) { return g_launches; }
+void ub_reset_launch_count(void) { g_launches = 0; }
+
+}  // extern "C"

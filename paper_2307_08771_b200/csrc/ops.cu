@@ -1,0 +1,343 @@
+// Memory-bound kernels of the hot path: the export-time permute (apply_plan's
+// weight math), the baseline export's channel gather, input staging and pools.
+// All are HBM-bound: coalesced on the side that is contiguous, vectorised where
+// the layout allows, grids sized in multiples of the SM count.
+#include <cuda_bf16.h>
+
+#include "ub_common.cuh"
+#include "ub_host.h"
+
+namespace ub {
+namespace {
+
+constexpr int kSMs = 148;
+
+inline int grid_for(long long work, int block, int per_thread = 1) {
+  long long g = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
+  const long long cap = (long long)kSMs * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v) { return static_cast<float>(v); }
+
+// ------------------------------------------------------------- permute weights
+// planner.py:661-673 (rows) + 755-767 (columns), both sides of a layer fused.
+// Iterates over OUTPUT elements so the writes are coalesced; reads gather.
+template <typename TI, typename TO, int LAYOUT>
+__global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps, const int32_t* __restrict__ rows,
+                                       int n_rows, const int32_t* __restrict__ cols, int n_cols,
+                                       const float* __restrict__ scale, int lead, int cpad, TO* __restrict__ out,
+                                       long long total) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r, c, t;
+    bool inside = true;
+    if (LAYOUT == UB_LAYOUT_OIHW) {  // [r][c][t]
+      t = static_cast<int>(e % taps);
+      long long rc = e / taps;
+      c = static_cast<int>(rc % n_cols);
+      r = static_cast<int>(rc / n_cols);
+    } else {  // [r][t][k], column c at k = lead + c
+      const int k = static_cast<int>(e % cpad);
+      long long rt = e / cpad;
+      t = static_cast<int>(rt % taps);
+      r = static_cast<int>(rt / taps);
+      c = k - lead;
+      inside = c >= 0 && c < n_cols;
+    }
+    TO v = TO(0);
+    if (inside) {
+      const int src_r = rows[r];
+      const int src_c = cols[c];
+      if (src_r >= 0 && src_c >= 0) {
+        const TI w = W[((long long)src_r * I + src_c) * taps + t];
+        if (scale) {
+          v = static_cast<TO>(static_cast<float>(w) * scale[r]);
+        } else {
+          v = static_cast<TO>(w);
+        }
+      }
+    }
+    out[e] = v;
+  }
+}
+
+template <typename TI, typename TO>
+int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows, int n_rows, const int32_t* cols,
+                            int n_cols, const float* scale, int layout, int lead, int cpad, void* out,
+                            cudaStream_t s) {
+  const long long total = layout == UB_LAYOUT_OIHW ? (long long)n_rows * n_cols * taps
+                                                   : (long long)n_rows * taps * cpad;
+  const int block = 256;
+  const int grid = grid_for(total, block, 4);
+  if (layout == UB_LAYOUT_OIHW)
+    permute_weights_kernel<TI, TO, UB_LAYOUT_OIHW><<<grid, block, 0, s>>>(
+        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+  else
+    permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM><<<grid, block, 0, s>>>(
+        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "permute_weights_kernel");
+}
+
+// ------------------------------------------------------------- permute vector
+template <typename T>
+__global__ void permute_vector_kernel(const T* __restrict__ v, const int32_t* __restrict__ idx, int n,
+                                      T* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = idx[i];
+    out[i] = j >= 0 ? v[j] : T(0);
+  }
+}
+
+// ------------------------------------------------------------- channel gather
+// One warp per pixel row; lanes stride over the gathered channels so the reads
+// of a warp fall inside the source row (the covering window) and the writes
+// are contiguous.
+__global__ void channel_gather_kernel(const uint16_t* __restrict__ x, int x_cstride, int x_coff,
+                                      const int32_t* __restrict__ idx, int n, long long npix, uint16_t* __restrict__ y,
+                                      int y_cstride, int y_coff) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long p = (long long)blockIdx.x * warps + (threadIdx.x >> 5); p < npix; p += (long long)gridDim.x * warps) {
+    const uint16_t* xr = x + p * x_cstride + x_coff;
+    uint16_t* yr = y + p * y_cstride + y_coff;
+    for (int i = lane * 2; i < n; i += 64) {
+      const int j0 = __ldg(idx + i);
+      const uint16_t a = j0 >= 0 ? __ldg(xr + j0) : uint16_t(0);
+      if (i + 1 < n) {
+        const int j1 = __ldg(idx + i + 1);
+        const uint16_t b = j1 >= 0 ? __ldg(xr + j1) : uint16_t(0);
+        if (((y_coff + i) & 1) == 0) {
+          *reinterpret_cast<uint32_t*>(yr + i) = uint32_t(a) | (uint32_t(b) << 16);
+        } else {
+          yr[i] = a;
+          yr[i + 1] = b;
+        }
+      } else {
+        yr[i] = a;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- input staging
+// NCHW fp32 -> NHWC bf16 (channel-gathered), zero-filling the padded channels.
+__global__ void stage_input_kernel(const float* __restrict__ x, int N, int C, int HW, const int32_t* __restrict__ idx,
+                                   int n, __nv_bfloat16* __restrict__ y, int y_cstride) {
+  const long long total = (long long)N * HW;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long img = p / HW;
+    const long long hw = p - img * HW;
+    const float* xp = x + img * C * HW + hw;
+    __nv_bfloat16* yp = y + p * y_cstride;
+    for (int c = 0; c < y_cstride; ++c) {
+      float v = 0.f;
+      if (c < n) {
+        const int src = idx ? idx[c] : c;
+        if (src >= 0) v = __ldg(xp + (long long)src * HW);
+      }
+      yp[c] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// ------------------------------------------------------------- max pool
+// Thread = (output pixel, 8-channel group); 16-byte vectors when aligned.
+__global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_cstride,
+                               int x_coff, int k, int stride, int pad, int Ho, int Wo, __nv_bfloat16* __restrict__ y,
+                               int y_cstride, int y_coff, bool vec) {
+  const int groups = (C + 7) / 8;
+  const long long total = (long long)N * Ho * Wo * groups;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int g = static_cast<int>(e % groups);
+    long long pix = e / groups;
+    const int wo = static_cast<int>(pix % Wo);
+    const long long t = pix / Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const long long img = t / Ho;
+    const int c0 = g * 8;
+    const int nc = min(8, C - c0);
+    float m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = -INFINITY;
+    for (int r = 0; r < k; ++r) {
+      const int hi = ho * stride - pad + r;
+      if (hi < 0 || hi >= H) continue;
+      for (int s = 0; s < k; ++s) {
+        const int wi = wo * stride - pad + s;
+        if (wi < 0 || wi >= W) continue;
+        const __nv_bfloat16* xp = x + ((img * H + hi) * W + wi) * x_cstride + x_coff + c0;
+        if (vec && nc == 8) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(xp));
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = unpack_bf16x2(w4[i]);
+            m[2 * i] = fmaxf(m[2 * i], f.x);
+            m[2 * i + 1] = fmaxf(m[2 * i + 1], f.y);
+          }
+        } else {
+          for (int i = 0; i < nc; ++i) m[i] = fmaxf(m[i], __bfloat162float(xp[i]));
+        }
+      }
+    }
+    __nv_bfloat16* yp = y + pix * y_cstride + y_coff + c0;
+    if (vec && nc == 8) {
+      uint4 o;
+      o.x = pack_bf16x2(m[0], m[1]);
+      o.y = pack_bf16x2(m[2], m[3]);
+      o.z = pack_bf16x2(m[4], m[5]);
+      o.w = pack_bf16x2(m[6], m[7]);
+      *reinterpret_cast<uint4*>(yp) = o;
+    } else {
+      for (int i = 0; i < nc; ++i) yp[i] = __float2bfloat16_rn(m[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------- global avg pool
+// Block = one image x 256 channels; threads stride the HW positions per channel.
+__global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C, int x_cstride, int x_coff,
+                               __nv_bfloat16* __restrict__ y, int y_cstride, int y_coff) {
+  const int img = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const __nv_bfloat16* xp = x + (long long)img * HW * x_cstride + x_coff + c;
+  float s = 0.f;
+  for (int p = 0; p < HW; ++p) s += __bfloat162float(xp[(long long)p * x_cstride]);
+  y[(long long)img * y_cstride + y_coff + c] = __float2bfloat16_rn(s / HW);
+}
+
+// ------------------------------------------------------------- affine / add / relu
+__global__ void affine_add_relu_kernel(const __nv_bfloat16* __restrict__ a, int a_cstride, int a_coff,
+                                       const float* __restrict__ scale, const float* __restrict__ shift,
+                                       const __nv_bfloat16* __restrict__ b, int b_cstride, int b_coff, int relu,
+                                       long long npix, int C, __nv_bfloat16* __restrict__ y, int y_cstride,
+                                       int y_coff) {
+  const long long total = npix * C;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(e % C);
+    const long long p = e / C;
+    float v = __bfloat162float(a[p * a_cstride + a_coff + c]);
+    if (scale) v *= scale[c];
+    if (shift) v += shift[c];
+    if (b) v += __bfloat162float(b[p * b_cstride + b_coff + c]);
+    if (relu) v = fmaxf(v, 0.f);
+    y[p * y_cstride + y_coff + c] = __float2bfloat16_rn(v);
+  }
+}
+
+}  // namespace
+}  // namespace ub
+
+using namespace ub;
+
+extern "C" int ub_permute_weights(const void* W, int dtype_in, int O, int I, int kh, int kw, const int32_t* rows,
+                                  int n_rows, const int32_t* cols, int n_cols, const float* row_scale, int layout,
+                                  int lead, int cpad, void* out, int dtype_out, cudaStream_t stream) {
+  if (!W || !rows || !cols || !out) return fail(UB_EINVAL, "ub_permute_weights: null pointer");
+  if (O < 1 || I < 1 || kh < 1 || kw < 1 || n_rows < 1 || n_cols < 1)
+    return fail(UB_EINVAL, "ub_permute_weights: bad sizes");
+  if (layout != UB_LAYOUT_OIHW && layout != UB_LAYOUT_GEMM) return fail(UB_EINVAL, "ub_permute_weights: layout");
+  if (layout == UB_LAYOUT_GEMM && (lead < 0 || lead + n_cols > cpad))
+    return fail(UB_EINVAL, "ub_permute_weights: lead + n_cols > cpad");
+  const int taps = kh * kw;
+  if (dtype_in == UB_F32) {
+    if (dtype_out == UB_F32)
+      return permute_dispatch_layout<float, float>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+                                                   cpad, out, stream);
+    if (dtype_out == UB_BF16)
+      return permute_dispatch_layout<float, __nv_bfloat16>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout,
+                                                           lead, cpad, out, stream);
+  } else if (dtype_in == UB_F64) {
+    if (dtype_out == UB_F64)
+      return permute_dispatch_layout<double, double>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+                                                     cpad, out, stream);
+    if (dtype_out == UB_F32)
+      return permute_dispatch_layout<double, float>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+                                                    cpad, out, stream);
+  }
+  return fail(UB_EUNSUPPORTED, "ub_permute_weights: dtype pair (%d -> %d)", dtype_in, dtype_out);
+}
+
+extern "C" int ub_permute_vector(const void* v, int dtype, const int32_t* idx, int n, void* out,
+                                 cudaStream_t stream) {
+  if (!v || !idx || !out || n < 1) return fail(UB_EINVAL, "ub_permute_vector: bad arguments");
+  const int grid = grid_for(n, 256);
+  if (dtype == UB_F32)
+    permute_vector_kernel<float><<<grid, 256, 0, stream>>>(static_cast<const float*>(v), idx, n,
+                                                           static_cast<float*>(out));
+  else if (dtype == UB_F64)
+    permute_vector_kernel<double><<<grid, 256, 0, stream>>>(static_cast<const double*>(v), idx, n,
+                                                            static_cast<double*>(out));
+  else
+    return fail(UB_EUNSUPPORTED, "ub_permute_vector: dtype %d", dtype);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "permute_vector_kernel");
+}
+
+extern "C" int ub_channel_gather(const void* x, int x_cstride, int x_coff, const int32_t* idx, int n, long long npix,
+                                 void* y, int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!x || !idx || !y || n < 1 || npix < 1) return fail(UB_EINVAL, "ub_channel_gather: bad arguments");
+  if (y_coff + n > y_cstride) return fail(UB_EINVAL, "ub_channel_gather: output exceeds y_cstride");
+  const int block = 256;
+  const int grid = grid_for(npix, block / 32);
+  channel_gather_kernel<<<grid, block, 0, stream>>>(static_cast<const uint16_t*>(x), x_cstride, x_coff, idx, n, npix,
+                                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "channel_gather_kernel");
+}
+
+extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n, void* y,
+                              int y_cstride, cudaStream_t stream) {
+  if (!x || !y || N < 1 || C < 1 || H < 1 || W < 1) return fail(UB_EINVAL, "ub_stage_input: bad arguments");
+  if (!idx) n = C;
+  if (n > y_cstride) return fail(UB_EINVAL, "ub_stage_input: n > y_cstride");
+  const long long total = (long long)N * H * W;
+  stage_input_kernel<<<grid_for(total, 256), 256, 0, stream>>>(x, N, C, H * W, idx, n,
+                                                               static_cast<__nv_bfloat16*>(y), y_cstride);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "stage_input_kernel");
+}
+
+extern "C" int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int stride,
+                            int pad, int Ho, int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!x || !y || N < 1 || C < 1 || k < 1 || stride < 1) return fail(UB_EINVAL, "ub_maxpool2d: bad arguments");
+  const bool vec = aligned16(x) && aligned16(y) && (x_cstride % 8 == 0) && (x_coff % 8 == 0) &&
+                   (y_cstride % 8 == 0) && (y_coff % 8 == 0);
+  const long long total = (long long)N * Ho * Wo * ((C + 7) / 8);
+  maxpool_kernel<<<grid_for(total, 256), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(x), N, H, W, C, x_cstride, x_coff, k, stride, pad, Ho, Wo,
+      static_cast<__nv_bfloat16*>(y), y_cstride, y_coff, vec);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "maxpool_kernel");
+}
+
+extern "C" int ub_avgpool_global(const void* x, int N, int HW, int C, int x_cstride, int x_coff, void* y,
+                                 int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!x || !y || N < 1 || HW < 1 || C < 1) return fail(UB_EINVAL, "ub_avgpool_global: bad arguments");
+  if (N > 65535) return fail(UB_EUNSUPPORTED, "ub_avgpool_global: N too large");
+  dim3 grid((C + 127) / 128, N);
+  avgpool_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(x), HW, C, x_cstride, x_coff,
+                                           static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "avgpool_kernel");
+}
+
+extern "C" int ub_affine_add_relu(const void* a, int a_cstride, int a_coff, const float* scale, const float* shift,
+                                  const void* b, int b_cstride, int b_coff, int relu, long long npix, int C, void* y,
+                                  int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!a || !y || npix < 1 || C < 1) return fail(UB_EINVAL, "ub_affine_add_relu: bad arguments");
+  affine_add_relu_kernel<<<grid_for(npix * C, 256, 4), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(a), a_cstride, a_coff, scale, shift, static_cast<const __nv_bfloat16*>(b),
+      b_cstride, b_coff, relu, npix, C, static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(cudaGetLastError(), "affine_add_relu_kernel");
+}

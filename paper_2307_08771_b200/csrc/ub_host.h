@@ -1,0 +1,35 @@
+// Host-side plumbing shared by the C-ABI translation units: thread-local error
+// state, launch counting, and TMA descriptor encoding through the driver entry
+// points (resolved at run time, so the .so does not link libcuda directly).
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "upscale_b200.h"
+
+namespace ub {
+
+int fail(int code, const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);  // UB_OK or UB_ECUDA with message
+void count_launch();
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn();
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn();
+
+// Swizzle span in bytes -> CUtensorMapSwizzle.
+inline CUtensorMapSwizzle swizzle_of(int bytes) {
+  switch (bytes) {
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    default: return CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace ub

@@ -1,0 +1,157 @@
+"""Torch-tensor wrappers over the C ABI (device memory + current stream).
+
+PyTorch is plumbing here: tensors provide device allocations and the CUDA
+stream; all arithmetic happens in libupscale_b200.so.  Every wrapper raises
+if the library is missing -- there is no eager fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.UB_F32, torch.float64: _lib.UB_F64, torch.bfloat16: _lib.UB_BF16}
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev_i32(seq, device) -> torch.Tensor:
+    return torch.as_tensor(list(seq), dtype=torch.int32).to(device)
+
+
+@dataclass
+class Act:
+    """An NHWC bf16 activation view: `buf` is [N*H*W, cstride]; the logical
+    tensor is channels [coff, coff + C) (a SLICE view needs no copy)."""
+
+    buf: torch.Tensor
+    N: int
+    H: int
+    W: int
+    C: int
+    coff: int = 0
+
+    @property
+    def cstride(self) -> int:
+        return self.buf.shape[-1]
+
+    @property
+    def npix(self) -> int:
+        return self.N * self.H * self.W
+
+    def view(self, start: int, length: int) -> "Act":
+        return Act(self.buf, self.N, self.H, self.W, length, self.coff + start)
+
+    def to_nchw(self, dtype=torch.float32) -> torch.Tensor:
+        t = self.buf[:, self.coff:self.coff + self.C].reshape(self.N, self.H, self.W, self.C)
+        return t.permute(0, 3, 1, 2).to(dtype)
+
+
+def pad8(c: int) -> int:
+    return (c + 7) // 8 * 8
+
+
+def empty_act(N, H, W, C, device, cstride=None) -> Act:
+    cs = cstride or pad8(C)
+    return Act(torch.empty((N * H * W, cs), dtype=torch.bfloat16, device=device), N, H, W, C, 0)
+
+
+def act_from_nchw(x: torch.Tensor, cstride=None) -> Act:
+    N, C, H, W = x.shape
+    a = empty_act(N, H, W, C, x.device, cstride)
+    a.buf.zero_()
+    a.buf[:, :C] = x.permute(0, 2, 3, 1).reshape(N * H * W, C).to(torch.bfloat16)
+    return a
+
+
+# --------------------------------------------------------------------------- export
+def permute_weights(W: torch.Tensor, rows, cols, row_scale: torch.Tensor | None = None,
+                    layout: str = "oihw", lead: int = 0, cpad: int = 0,
+                    out_dtype=torch.float32, rows_dev=None, cols_dev=None) -> torch.Tensor:
+    """apply_plan weight math (planner.py:661-673, 755-767) on a 4-D tensor."""
+    assert W.is_cuda and W.dim() == 4 and W.is_contiguous()
+    O, I, kh, kw = W.shape
+    r = rows_dev if rows_dev is not None else _dev_i32(rows, W.device)
+    c = cols_dev if cols_dev is not None else _dev_i32(cols, W.device)
+    nr, nc = r.numel(), c.numel()
+    if layout == "oihw":
+        out = torch.empty((nr, nc, kh, kw), dtype=out_dtype, device=W.device)
+        lay = _lib.UB_LAYOUT_OIHW
+    else:
+        out = torch.empty((nr, kh * kw, cpad), dtype=out_dtype, device=W.device)
+        lay = _lib.UB_LAYOUT_GEMM
+    if row_scale is not None:
+        row_scale = row_scale.to(device=W.device, dtype=torch.float32).contiguous()
+    _lib.call("ub_permute_weights", _p(W), _DT[W.dtype], O, I, kh, kw, _p(r), nr, _p(c), nc,
+              _p(row_scale), lay, lead, cpad, _p(out), _DT[out_dtype], _stream())
+    return out
+
+
+def permute_vector(v: torch.Tensor, idx) -> torch.Tensor:
+    """planner.py:731-733: v[perm] for per-channel vectors."""
+    i = _dev_i32(idx, v.device)
+    out = torch.empty(i.numel(), dtype=v.dtype, device=v.device)
+    _lib.call("ub_permute_vector", _p(v), _DT[v.dtype], _p(i), i.numel(), _p(out), _stream())
+    return out
+
+
+# --------------------------------------------------------------------------- inference
+def channel_gather(x: Act, idx_dev: torch.Tensor, y: Act) -> None:
+    """Baseline-export copy: a reference GATHER node (interp.py:75-77) as index_select."""
+    _lib.call("ub_channel_gather", _p(x.buf), x.cstride, x.coff, _p(idx_dev), idx_dev.numel(),
+              x.npix, _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: int, stride: int, pad: int,
+         y: Act, gather_idx: torch.Tensor | None = None, bias: torch.Tensor | None = None,
+         residual: Act | None = None, relu: bool = False, y_fp32: bool = False) -> None:
+    Ho = (x.H + 2 * pad - kh) // stride + 1
+    Wo = (x.W + 2 * pad - kw) // stride + 1
+    assert y.N == x.N and y.H == Ho and y.W == Wo, "output geometry mismatch"
+    d = _lib.ConvDesc()
+    d.N, d.H, d.W = x.N, x.H, x.W
+    d.cin = gather_idx.numel() if gather_idx is not None else x.C
+    d.cout = cout
+    d.kh, d.kw, d.stride, d.pad, d.Ho, d.Wo = kh, kw, stride, pad, Ho, Wo
+    d.x, d.x_cstride, d.x_coff = x.buf.data_ptr(), x.cstride, x.coff
+    d.gather_idx = gather_idx.data_ptr() if gather_idx is not None else None
+    d.w, d.w_lead, d.w_cpad = w.data_ptr(), lead, cpad
+    d.bias = bias.data_ptr() if bias is not None else None
+    if residual is not None:
+        d.residual, d.res_cstride, d.res_coff = residual.buf.data_ptr(), residual.cstride, residual.coff
+    d.relu = int(relu)
+    d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
+    d.y_dtype = _lib.UB_F32 if y_fp32 else _lib.UB_BF16
+    _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
+
+
+def stage_input(x: torch.Tensor, y: Act, idx_dev: torch.Tensor | None = None) -> None:
+    N, C, H, W = x.shape
+    n = idx_dev.numel() if idx_dev is not None else C
+    _lib.call("ub_stage_input", _p(x), N, C, H, W, _p(idx_dev), n, _p(y.buf), y.cstride, _stream())
+
+
+def maxpool(x: Act, k: int, stride: int, pad: int, y: Act) -> None:
+    _lib.call("ub_maxpool2d", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, k, stride, pad,
+              y.H, y.W, _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def avgpool_global(x: Act, y: Act) -> None:
+    _lib.call("ub_avgpool_global", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff,
+              _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def affine_add_relu(a: Act, y: Act, scale=None, shift=None, b: Act | None = None, relu=False) -> None:
+    _lib.call("ub_affine_add_relu", _p(a.buf), a.cstride, a.coff, _p(scale), _p(shift),
+              _p(b.buf) if b is not None else None, b.cstride if b else 0, b.coff if b else 0,
+              int(relu), a.npix, a.C, _p(y.buf), y.cstride, y.coff, _stream())

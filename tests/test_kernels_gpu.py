@@ -1,0 +1,149 @@
+"""Numerics of the sm_100a kernels against plain PyTorch fp32 references.
+
+The conv kernel computes in bf16 x bf16 -> fp32 on tcgen05; the reference is
+torch fp32 (TF32 off) on the SAME bf16-rounded inputs and weights, so the only
+differences are accumulation order and the final bf16 rounding of the output.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2307_08771_b200 import _lib, kernels as K  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _no_tf32():
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+
+def _bf(t):
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+def _rel(a, b):
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-6))
+
+
+CASES = [
+    # name, N, H, W, cstride, coff, cin, cout, k, stride, pad, gather, bias, res, relu, y_fp32
+    ("1x1_aligned", 2, 14, 14, 64, 0, 64, 64, 1, 1, 0, 0, False, False, False, False),
+    ("1x1_misaligned_slice", 2, 7, 9, 128, 13, 100, 31, 1, 1, 0, 0, True, False, True, False),
+    ("1x1_bk16", 2, 10, 10, 16, 0, 12, 48, 1, 1, 0, 0, True, False, False, False),
+    ("3x3_s1", 2, 56, 56, 64, 0, 64, 64, 3, 1, 1, 0, True, False, True, False),
+    ("3x3_s2_ntail", 2, 28, 28, 128, 0, 128, 130, 3, 2, 1, 0, False, False, False, False),
+    ("1x1_s2_two_ntiles", 2, 28, 28, 256, 0, 256, 512, 1, 2, 0, 0, True, False, False, False),
+    ("7x7_s2_stem", 1, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, True, False, True, False),
+    ("gather_res_relu", 2, 14, 14, 256, 0, 256, 64, 1, 1, 0, 100, True, True, True, False),
+    ("fc_gather_fp32", 4, 1, 1, 2048, 0, 2048, 1000, 1, 1, 0, 1024, True, False, False, True),
+    ("3x3_slice_offset", 3, 14, 14, 96, 40, 48, 72, 3, 1, 1, 0, True, True, True, False),
+    ("1x1_large_m", 8, 56, 56, 256, 0, 256, 64, 1, 1, 0, 0, False, False, False, False),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_conv_matches_torch(case):
+    name, N, H, W, cs, coff, cin, cout, k, st, pad, ng, use_b, use_r, relu, yf = case
+    dev = "cuda"
+    g = torch.Generator(device="cpu").manual_seed(sum(map(ord, name)))
+    xfull = torch.randn(N, cs, H, W, generator=g)
+    x = K.act_from_nchw(xfull.to(dev))
+    x.C = cs
+    Wt = torch.randn(cout, cin if not ng else ng, k, k, generator=g) / (cin * k * k) ** 0.5
+    if ng:
+        idx = torch.randperm(cin, generator=g)[:ng].to(torch.int32)
+        xin = xfull[:, idx.long()]
+        xa = x
+        idx_dev = idx.to(dev)
+        lead, cpad = _lib.conv_weight_layout(ng, 0, True)
+    else:
+        xa = x.view(coff, cin)
+        xin = xfull[:, coff:coff + cin]
+        idx_dev = None
+        lead, cpad = _lib.conv_weight_layout(cin, coff, False)
+    nin = Wt.shape[1]
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(nin)),
+                           layout="gemm", lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
+    Ho = (H + 2 * pad - k) // st + 1
+    Wo = (W + 2 * pad - k) // st + 1
+    bias = torch.randn(cout, generator=g).to(dev) if use_b else None
+    res = None
+    ref = torch.nn.functional.conv2d(_bf(xin).to(dev), _bf(Wt).to(dev), stride=st, padding=pad)
+    if use_b:
+        ref = ref + bias.view(1, -1, 1, 1)
+    if use_r:
+        rfull = torch.randn(N, cout + 8, Ho, Wo, generator=g)
+        res = K.act_from_nchw(rfull.to(dev)).view(8, cout)
+        ref = ref + _bf(rfull[:, 8:8 + cout]).to(dev)
+    if relu:
+        ref = ref.clamp_min(0)
+    if yf:
+        y = K.Act(torch.full((N * Ho * Wo, K.pad8(cout)), float("nan"), device=dev), N, Ho, Wo, cout)
+    else:
+        y = K.empty_act(N, Ho, Wo, cout + 16, dev)
+        y.buf.fill_(float("nan"))
+        y = y.view(16, cout)
+    K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx_dev, bias=bias, residual=res,
+           relu=relu, y_fp32=yf)
+    torch.cuda.synchronize()
+    out = y.buf[:, y.coff:y.coff + cout].float().reshape(N, Ho, Wo, cout).permute(0, 3, 1, 2)
+    assert torch.isfinite(out).all(), f"{name}: non-finite output"
+    err = _rel(out, ref)
+    assert err < 1e-2, f"{name}: rel err {err}"
+    if not yf:  # channels outside the write window stay untouched
+        assert torch.isnan(y.buf[:, :16].float()).all()
+
+
+def test_permute_weights_bit_exact():
+    dev = "cuda"
+    g = torch.Generator().manual_seed(0)
+    W = torch.randn(40, 24, 3, 3, generator=g, dtype=torch.float64)
+    rows = [3, 1, 0, 39, 7, -1, 12]
+    cols = [5, 2, 23, -1, 0]
+    out = K.permute_weights(W.to(dev), rows, cols, out_dtype=torch.float64)
+    ref = torch.zeros(len(rows), len(cols), 3, 3, dtype=torch.float64)
+    for i, r in enumerate(rows):
+        for j, c in enumerate(cols):
+            if r >= 0 and c >= 0:
+                ref[i, j] = W[r, c]
+    assert torch.equal(out.cpu(), ref)
+
+
+def test_channel_gather_and_pools():
+    dev = "cuda"
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 40, 9, 9, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    idx = torch.tensor([5, 3, -1, 39, 0, 17, 18], dtype=torch.int32)
+    y = K.empty_act(2, 9, 9, len(idx), dev)
+    K.channel_gather(xa, idx.to(dev), y)
+    ref = torch.zeros(2, len(idx), 9, 9)
+    for i, j in enumerate(idx.tolist()):
+        if j >= 0:
+            ref[:, i] = _bf(x[:, j])
+    torch.cuda.synchronize()
+    assert torch.equal(y.to_nchw().cpu(), ref)
+
+    yp = K.empty_act(2, 5, 5, 40, dev)
+    K.maxpool(xa, 3, 2, 1, yp)
+    refp = torch.nn.functional.max_pool2d(_bf(x), 3, 2, 1)
+    assert torch.equal(yp.to_nchw().cpu(), refp)
+
+    ya = K.empty_act(2, 1, 1, 40, dev)
+    K.avgpool_global(xa, ya)
+    refa = _bf(x).mean(dim=(2, 3))
+    assert _rel(ya.to_nchw().cpu().reshape(2, 40), refa) < 1e-2
+
+
+def test_stage_input_gathers_channels():
+    dev = "cuda"
+    x = torch.randn(2, 3, 8, 8)
+    y = K.empty_act(2, 8, 8, 2, dev, cstride=8)
+    K.stage_input(x.to(dev), y, torch.tensor([2, 0], dtype=torch.int32, device=dev))
+    torch.cuda.synchronize()
+    got = y.buf.float().cpu().reshape(2, 8, 8, 8)
+    assert torch.equal(got[..., 0], _bf(x[:, 2]))
+    assert torch.equal(got[..., 1], _bf(x[:, 0]))
+    assert (got[..., 2:] == 0).all()
