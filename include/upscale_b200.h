@@ -104,7 +104,7 @@ typedef struct {
   int Ho, Wo;                  /* output spatial size */
   const void* x;               /* bf16 NHWC input */
   int x_cstride, x_coff;       /* channel stride / SLICE start */
-  const int32_t* gather_idx;   /* fused GATHER indices (1x1 stride-1 only) or NULL */
+  const int32_t* gather_idx;   /* fused GATHER indices (any kernel/stride) or NULL */
   const void* w;               /* bf16 UB_LAYOUT_GEMM weights, [cout][kh*kw][cpad] */
   int w_lead, w_cpad;          /* from ub_conv_weight_layout */
   const float* bias;           /* [cout] fp32 or NULL */

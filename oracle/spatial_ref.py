@@ -1,0 +1,108 @@
+"""Oracle: interp.run's op dispatch (interp.py:52-83) over real spatial tensors.
+
+Same topological schedule and per-kind semantics as the reference
+interpreter; the channel-collapsed ops are replaced by their spatial
+originals from the lowering sidecar (CHANNEL_MIX -> conv2d / linear,
+PER_CHANNEL -> BatchNorm or bias, PASS_THROUGH -> relu / max pool / global
+average pool / flatten).  Activations are [N, C, H, W] torch CPU tensors in
+float64 (parity anchor) or float32 (the timed CPU reference path).  A graph
+without specs (e.g. the reference's random DAG fixtures) runs with the
+reference's 1x1 semantics (PASS_THROUGH = ReLU, PER_CHANNEL = + vector).
+"""
+
+from __future__ import annotations
+
+from typing import Mapping
+
+import torch
+import torch.nn.functional as F
+
+
+def _kind(lay) -> str:
+    return lay.kind.value if hasattr(lay.kind, "value") else str(lay.kind)
+
+
+def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
+                vectors: Mapping[str, Mapping[str, torch.Tensor]], x: torch.Tensor,
+                masks: Mapping[str, tuple] | None = None, dtype=torch.float64) -> torch.Tensor:
+    """Returns the OUTPUT node's value ([N, C] if spatially collapsed)."""
+    masks = masks or {}
+    vals: dict[str, torch.Tensor] = {}
+    out_id = None
+    for lid in graph.topological_order():
+        lay = graph.layer(lid)
+        k = _kind(lay)
+        spec = specs.get(lid)
+        op = spec.op if spec is not None else None
+        ins = [vals[p] for p in graph.predecessors(lid)]
+        if k == "input":
+            out = x.to(dtype)
+        elif k == "channel_mix":
+            v = ins[0]
+            if lid in masks:  # interp.py:59-60
+                m = torch.zeros(v.shape[1], dtype=dtype)
+                m[list(masks[lid])] = 1.0
+                v = v * m.view(1, -1, 1, 1)
+            w = weights[lid].to(dtype)
+            if op == "conv":
+                out = F.conv2d(v, w, stride=spec.stride, padding=spec.pad)
+            else:  # linear / 1x1 channel mix over a collapsed tensor
+                out = F.conv2d(v, w)
+        elif k == "add":
+            out = ins[0]
+            for t in ins[1:]:
+                out = out + t
+        elif k == "concat":
+            out = torch.cat(ins, dim=1)
+        elif k == "pass_through":
+            v = ins[0]
+            if op == "maxpool":
+                out = F.max_pool2d(v, spec.kernel, spec.stride, spec.pad)
+            elif op == "avgpool":
+                out = v.mean(dim=(2, 3), keepdim=True)
+            elif op in ("flatten", "identity"):
+                out = v
+            else:  # relu, and the reference's PASS_THROUGH semantics
+                out = torch.clamp_min(v, 0.0)
+        elif k == "per_channel":
+            vec = vectors[lid]
+            if op == "bn":
+                scale = vec["weight"].to(dtype) / torch.sqrt(vec["var"].to(dtype) + spec.eps)
+                out = (ins[0] - vec["mean"].to(dtype).view(1, -1, 1, 1)) * scale.view(1, -1, 1, 1) \
+                    + vec["bias"].to(dtype).view(1, -1, 1, 1)
+            else:  # bias / the reference's "+ vector"
+                out = ins[0] + vec["bias"].to(dtype).view(1, -1, 1, 1)
+        elif k == "slice":
+            s, n = lay.params
+            out = ins[0][:, s:s + n]
+        elif k == "gather":
+            v = ins[0]
+            idx = torch.tensor([max(i, 0) for i in lay.params], dtype=torch.long)
+            out = v.index_select(1, idx)
+            neg = [j for j, i in enumerate(lay.params) if i < 0]
+            if neg:
+                out[:, neg] = 0.0
+        elif k == "output":
+            out = ins[0]
+            out_id = lid
+        else:
+            raise ValueError(f"{lid}: unknown kind {k}")
+        if out.shape[1] != lay.out_channels:
+            raise ValueError(f"{lid}: produced {out.shape[1]} channels, expected {lay.out_channels}")
+        vals[lid] = out
+    res = vals[out_id]
+    if res.dim() == 4 and res.shape[2] == 1 and res.shape[3] == 1:
+        res = res[:, :, 0, 0]
+    return res
+
+
+def deviation(a: torch.Tensor, b: torch.Tensor) -> float:
+    """interp.py:119-120 over all elements."""
+    a = a.double()
+    b = b.double()
+    scale = torch.clamp_min(torch.maximum(a.abs(), b.abs()), 1.0)
+    return float(((a - b).abs() / scale).max())
+
+
+def top1_agreement(a: torch.Tensor, b: torch.Tensor) -> float:
+    return float((a.argmax(dim=1) == b.argmax(dim=1)).double().mean())

@@ -36,7 +36,7 @@ struct ConvKParams {
   int cchunks;  // channel chunks per tap
   int kw;       // filter width
   int cpad;     // per-tap weight K
-  int Ho, Wo, stride, pad;
+  int H, W, Ho, Wo, stride, pad;
   int stages;
   uint32_t tmem_cols;
   // fused gather source
@@ -155,12 +155,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     if constexpr (AMODE == A_GATHER) {
-      // ---------------- fused GATHER: A[row][j] = x[m0+row][x_coff + gidx[j]]
+      // ---------------- fused GATHER (implicit im2col over gathered channels):
+      // A[row][j] of tap (r, s) = x[pixel(row) + (r, s)][x_coff + gidx[cc*64 + j]], 0 outside.
+      // Lane l owns the geometry of row q*32+l; rows are broadcast with shuffles.
+      const int hw = p.Ho * p.Wo;
+      int g_img = 0, g_hb = -(1 << 28), g_wb = 0;
+      {
+        const int m = m0 + q * 32 + lane;
+        if (m < p.M) {
+          g_img = m / hw;
+          const int rem = m - g_img * hw;
+          const int ho = rem / p.Wo;
+          g_hb = ho * p.stride - p.pad;
+          g_wb = (rem - ho * p.Wo) * p.stride - p.pad;
+        }
+      }
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % stages;
         const uint32_t ph = (kb / stages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
-        const int j = kb * 64 + lane * 2;
+        const int tap = kb / p.cchunks;
+        const int cc = kb - tap * p.cchunks;
+        const int fr = tap / p.kw;
+        const int fs = tap - fr * p.kw;
+        const int j = cc * 64 + lane * 2;
         const int i0 = j < p.n_gather ? __ldg(p.gidx + j) : -1;
         const int i1 = (j + 1) < p.n_gather ? __ldg(p.gidx + j + 1) : -1;
         uint8_t* tile = sA + s * A_BYTES;
@@ -169,10 +187,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           uint32_t vals[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int m = m0 + q * 32 + rb + u;
+            const int img = __shfl_sync(0xffffffffu, g_img, rb + u);
+            const int hi = __shfl_sync(0xffffffffu, g_hb, rb + u) + fr;
+            const int wi = __shfl_sync(0xffffffffu, g_wb, rb + u) + fs;
             uint32_t a = 0, b = 0;
-            if (m < p.M) {
-              const uint16_t* xr = p.x + static_cast<size_t>(m) * p.x_cstride + p.x_coff;
+            if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.W) {
+              const size_t pix = (static_cast<size_t>(img) * p.H + hi) * p.W + wi;
+              const uint16_t* xr = p.x + pix * p.x_cstride + p.x_coff;
               if (i0 >= 0) a = __ldg(xr + i0);
               if (i1 >= 0) b = __ldg(xr + i1);
             }
@@ -341,7 +362,6 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
 
   const bool gather = d->gather_idx != nullptr;
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
-  if (gather && !pointwise) return fail(UB_EUNSUPPORTED, "ub_conv_fwd: fused gather needs a 1x1 stride-1 conv");
   if (gather && d->x_coff % 8) return fail(UB_EINVAL, "ub_conv_fwd: gather base must be 8-aligned");
 
   int lead = 0, cpad = 0;
@@ -363,6 +383,8 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   p.num_kb = taps * p.cchunks;
   p.kw = d->kw;
   p.cpad = cpad;
+  p.H = d->H;
+  p.W = d->W;
   p.Ho = d->Ho;
   p.Wo = d->Wo;
   p.stride = d->stride;

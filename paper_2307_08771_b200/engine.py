@@ -1,0 +1,462 @@
+"""Inference engine: executes an exported IR graph on B200 with fused kernels.
+
+This is the spatial, batched twin of the reference interpreter `run`
+(interp.py:36-84).  The graph is compiled once into a launch schedule:
+
+  * CHANNEL_MIX + its `<c>.read` node + its epilogue chain
+      (PER_CHANNEL bias/BN -> ADD -> ReLU, each single-consumer) -> ONE
+      `ub_conv_fwd` launch.  SLICE reads are channel-offset views (zero copy);
+      GATHER reads are fused into the A-operand staging (gather_mode="fused")
+      or materialised by `ub_channel_gather` first (gather_mode="copy", the
+      baseline export's copy-then-conv behaviour).
+  * BN scale is folded into the weight rows at compile time (one permute
+    kernel pass per layer writes the bf16 K-major GEMM operand).
+  * INPUT (+ a GATHER reading it) -> `ub_stage_input`; max/avg pools and any
+    node the conv epilogue cannot absorb -> standalone kernels.
+  * The op list is topologically scheduled (residual producers first), every
+    value gets its own NHWC buffer, and the whole forward can be captured in a
+    CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Callable, Mapping, Sequence
+
+import torch
+
+from . import _lib
+from . import kernels as K
+from .ir import LayerKind, ModelGraph
+
+
+@dataclass
+class _Op:
+    kind: str                     # conv | stage | gather | maxpool | avgpool | eltwise
+    anchor: str                   # node id giving the topological position
+    inputs: list[str]             # value ids read
+    output: str                   # value id written
+    launch: Callable[[], None] | None = None
+    info: dict = field(default_factory=dict)
+
+
+@dataclass
+class ConvStats:
+    """Algorithmic work of one conv launch (SURVEY.md 8d formulas)."""
+
+    name: str
+    flops: float
+    bytes: float
+    gather_bytes: float
+
+
+class Engine:
+    """Compiled forward pass of one exported graph at a fixed batch size.
+
+    weight_source(lid) -> (W [O,I,kh,kw] fp32 device tensor, rows, cols)
+    vector_source(uid) -> (named vectors dict on CPU/device, perm or None)
+    `rows`/`cols`/`perm` are the composed plan index maps (None = identity).
+    """
+
+    def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
+                 input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused"):
+        assert gather_mode in ("fused", "copy")
+        self.graph = graph
+        self.specs = specs
+        self.batch = batch
+        self.device = torch.device(device)
+        self.gather_mode = gather_mode
+        self.input_chw = tuple(input_chw)
+        self.values: dict[str, K.Act] = {}
+        self.ops: list[_Op] = []
+        self.conv_stats: list[ConvStats] = []
+        self._keep: list[torch.Tensor] = []  # device tensors referenced by launches
+        self._graph_exec = None
+        self._shapes = self._infer_shapes()
+        self._compile(weight_source, vector_source)
+
+    # ------------------------------------------------------------------ shapes
+    def _infer_shapes(self) -> dict[str, tuple[int, int, int]]:
+        g, sp = self.graph, self.specs
+        shp: dict[str, tuple[int, int, int]] = {}
+        for lid in g.topological_order():
+            lay = g.layer(lid)
+            preds = g.predecessors(lid)
+            spec = sp.get(lid)
+            if lay.kind is LayerKind.INPUT:
+                c, h, w = self.input_chw
+                shp[lid] = (lay.out_channels, h, w)
+                continue
+            _, h, w = shp[preds[0]]
+            if lay.kind is LayerKind.CHANNEL_MIX and spec is not None and spec.op == "conv":
+                h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
+                w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
+            elif lay.kind is LayerKind.CHANNEL_MIX:
+                assert (h, w) == (1, 1), f"{lid}: linear layer on a spatial tensor"
+            elif lay.kind is LayerKind.PASS_THROUGH and spec is not None:
+                if spec.op == "maxpool":
+                    h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
+                    w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
+                elif spec.op == "avgpool":
+                    h, w = 1, 1
+            shp[lid] = (lay.out_channels, h, w)
+        return shp
+
+    # ------------------------------------------------------------------ helpers
+    def _single_succ(self, lid: str) -> str | None:
+        s = self.graph.successors(lid)
+        return s[0] if len(s) == 1 else None
+
+    def _alloc(self, vid: str, C: int, fp32: bool = False) -> K.Act:
+        _, h, w = self._shapes[vid]
+        cs = K.pad8(C) if not fp32 else (C + 3) // 4 * 4
+        buf = torch.zeros((self.batch * h * w, cs), dtype=torch.float32 if fp32 else torch.bfloat16,
+                          device=self.device)
+        a = K.Act(buf, self.batch, h, w, C, 0)
+        self.values[vid] = a
+        return a
+
+    def _i32(self, seq) -> torch.Tensor:
+        t = torch.as_tensor(list(seq), dtype=torch.int32, device=self.device)
+        self._keep.append(t)
+        return t
+
+    # ------------------------------------------------------------------ compile
+    def _compile(self, weight_source, vector_source):
+        g = self.graph
+        kinds = {lay.id: lay.kind for lay in g.layers}
+        absorbed: set[str] = set()   # nodes executed inside another op
+        alias: dict[str, tuple[str, int, int]] = {}  # value -> (base value, start, length) views
+        ops: list[_Op] = []
+        topo = g.topological_order()
+        pos = {lid: i for i, lid in enumerate(topo)}
+        output_feed = {g.predecessors(lid)[0] for lid in topo if kinds[lid] is LayerKind.OUTPUT}
+
+        # --- conv groups -------------------------------------------------------
+        for lid in topo:
+            if kinds[lid] is not LayerKind.CHANNEL_MIX:
+                continue
+            spec = self.specs[lid]
+            read = g.predecessors(lid)[0]
+            info = {"conv": lid, "read": None, "bn": None, "add": None, "relu": None}
+            src = read
+            if kinds[read] in (LayerKind.SLICE, LayerKind.GATHER) and read.endswith(".read") \
+                    and len(g.successors(read)) == 1:
+                info["read"] = read
+                src = g.predecessors(read)[0]
+                absorbed.add(read)
+            cur = lid
+            nxt = self._single_succ(cur)
+            if nxt is not None and kinds[nxt] is LayerKind.PER_CHANNEL and cur not in output_feed:
+                info["bn"] = nxt
+                absorbed.add(nxt)
+                cur = nxt
+                nxt = self._single_succ(cur)
+            if nxt is not None and kinds[nxt] is LayerKind.ADD and len(g.predecessors(nxt)) == 2 \
+                    and nxt not in absorbed and cur not in output_feed:
+                others = [p for p in g.predecessors(nxt) if p != cur]
+                if len(others) == 1:
+                    info["add"] = nxt
+                    info["residual"] = others[0]
+                    absorbed.add(nxt)
+                    cur = nxt
+                    nxt = self._single_succ(cur)
+            if nxt is not None and kinds[nxt] is LayerKind.PASS_THROUGH and self.specs[nxt].op == "relu" \
+                    and cur not in output_feed:
+                info["relu"] = nxt
+                absorbed.add(nxt)
+                cur = nxt
+            info["src"] = src
+            info["out"] = cur
+            inputs = [src] + ([info["residual"]] if info.get("residual") else [])
+            ops.append(_Op("conv", lid, inputs, cur, info=info))
+            del spec
+
+        # --- remaining nodes ---------------------------------------------------
+        for lid in topo:
+            k = kinds[lid]
+            if lid in absorbed or k is LayerKind.CHANNEL_MIX:
+                continue
+            spec = self.specs.get(lid)
+            preds = g.predecessors(lid)
+            if k is LayerKind.INPUT:
+                succ = g.successors(lid)
+                idx = None
+                out = lid
+                if len(succ) == 1 and kinds[succ[0]] is LayerKind.GATHER:
+                    idx = g.layer(succ[0]).params
+                    out = succ[0]
+                    absorbed.add(succ[0])
+                    # the conv that read this gather now reads the staged tensor
+                    for op in ops:
+                        if op.info.get("read") == succ[0]:
+                            op.info["read"] = None
+                            op.info["src"] = out
+                            op.inputs[0] = out
+                ops.append(_Op("stage", lid, [], out, info={"idx": idx}))
+            elif k is LayerKind.OUTPUT:
+                alias[lid] = (preds[0], 0, -1)
+            elif k is LayerKind.PASS_THROUGH and spec is not None and spec.op in ("flatten", "identity"):
+                alias[lid] = (preds[0], 0, -1)
+            elif k is LayerKind.SLICE:
+                s, n = g.layer(lid).params
+                alias[lid] = (preds[0], s, n)
+            elif k is LayerKind.PASS_THROUGH and spec is not None and spec.op == "maxpool":
+                ops.append(_Op("maxpool", lid, [preds[0]], lid, info={"spec": spec}))
+            elif k is LayerKind.PASS_THROUGH and spec is not None and spec.op == "avgpool":
+                ops.append(_Op("avgpool", lid, [preds[0]], lid))
+            elif k is LayerKind.GATHER:
+                ops.append(_Op("gather", lid, [preds[0]], lid, info={"idx": g.layer(lid).params}))
+            elif k in (LayerKind.PASS_THROUGH, LayerKind.PER_CHANNEL, LayerKind.ADD):
+                ops.append(_Op("eltwise", lid, list(preds), lid, info={"kind": k}))
+            else:
+                raise NotImplementedError(f"{lid}: {k.value} has no B200 kernel in this build")
+
+        # copy-mode gathers: materialise the read before the conv
+        if self.gather_mode == "copy":
+            extra = []
+            for op in ops:
+                r = op.info.get("read") if op.kind == "conv" else None
+                if r and kinds[r] is LayerKind.GATHER:
+                    extra.append(_Op("gather", r, [op.info["src"]], r, info={"idx": g.layer(r).params}))
+                    op.info["read"] = None
+                    op.info["src"] = r
+                    op.inputs[0] = r
+            ops.extend(extra)
+
+        # --- schedule: Kahn over value dependencies, ties by topological position
+        produced = {op.output: op for op in ops}
+
+        def base(v):
+            while v in alias:
+                v = alias[v][0]
+            return v
+
+        deps = {id(op): {id(produced[base(i)]) for i in op.inputs if base(i) in produced} for op in ops}
+        done: set[int] = set()
+        sched: list[_Op] = []
+        remaining = sorted(ops, key=lambda o: pos[o.anchor])
+        while remaining:
+            for i, op in enumerate(remaining):
+                if deps[id(op)] <= done:
+                    sched.append(op)
+                    done.add(id(op))
+                    remaining.pop(i)
+                    break
+            else:
+                raise RuntimeError("engine schedule has a cycle")
+        self._alias = alias
+        self.ops = sched
+
+        # --- allocate + bind launches -------------------------------------------
+        self.input_buf = torch.zeros((self.batch, *self.input_chw), dtype=torch.float32, device=self.device)
+        for op in self.ops:
+            getattr(self, f"_bind_{op.kind}")(op, weight_source, vector_source, output_feed)
+        out_id = next(lid for lid in topo if kinds[lid] is LayerKind.OUTPUT)
+        self.output_value = self._value(out_id)
+
+    def _value(self, vid: str) -> K.Act:
+        if vid in self.values:
+            return self.values[vid]
+        if vid in self._alias:
+            b, s, n = self._alias[vid]
+            a = self._value(b)
+            if n < 0:
+                return a
+            return a.view(s, n)
+        raise KeyError(f"value {vid} not computed")
+
+    # ------------------------------------------------------------------ binders
+    def _bind_stage(self, op, ws, vs, output_feed):
+        idx = op.info["idx"]
+        C = len(idx) if idx is not None else self.input_chw[0]
+        y = self._alloc(op.output, C)
+        idx_dev = self._i32(idx) if idx is not None else None
+        x = self.input_buf
+        op.launch = lambda: K.stage_input(x, y, idx_dev)
+
+    def _bind_maxpool(self, op, ws, vs, output_feed):
+        sp = op.info["spec"]
+        x = self._value(op.inputs[0])
+        y = self._alloc(op.output, x.C)
+        op.launch = lambda: K.maxpool(x, sp.kernel, sp.stride, sp.pad, y)
+
+    def _bind_avgpool(self, op, ws, vs, output_feed):
+        x = self._value(op.inputs[0])
+        y = self._alloc(op.output, x.C)
+        op.launch = lambda: K.avgpool_global(x, y)
+
+    def _bind_gather(self, op, ws, vs, output_feed):
+        x = self._value(op.inputs[0])
+        idx = op.info["idx"]
+        y = self._alloc(op.output, len(idx))
+        idx_dev = self._i32(idx)
+        op.launch = lambda: K.channel_gather(x, idx_dev, y)
+        n_img_pix = x.H * x.W
+        self.conv_stats.append(ConvStats(f"{op.output}(copy)", 0.0, 0.0, 2 * 2 * len(idx) * n_img_pix))
+
+    def _bind_eltwise(self, op, ws, vs, output_feed):
+        kind = op.info["kind"]
+        lid = op.anchor
+        a = self._value(op.inputs[0])
+        y = self._alloc(op.output, a.C)
+        scale = shift = None
+        b = None
+        relu = False
+        if kind is LayerKind.PER_CHANNEL:
+            vec, perm = vs(lid)
+            scale, shift = self._affine(lid, vec, perm)
+        elif kind is LayerKind.ADD:
+            assert len(op.inputs) == 2, "ADD with > 2 operands"
+            b = self._value(op.inputs[1])
+        else:
+            relu = True
+        op.launch = lambda: K.affine_add_relu(a, y, scale, shift, b, relu)
+
+    def _affine(self, uid, vec, perm):
+        spec = self.specs[uid]
+
+        def p(v):
+            v = v.detach().float().cpu()
+            return v[list(perm)] if perm is not None else v
+
+        if spec.op == "bn":
+            scale = p(vec["weight"]) / torch.sqrt(p(vec["var"]) + spec.eps)
+            shift = p(vec["bias"]) - p(vec["mean"]) * scale
+        else:
+            scale = torch.ones_like(p(vec["bias"]))
+            shift = p(vec["bias"])
+        s, t = scale.to(self.device), shift.to(self.device)
+        self._keep += [s, t]
+        return s, t
+
+    def _bind_conv(self, op, ws, vs, output_feed):
+        info = op.info
+        lid = info["conv"]
+        spec = self.specs[lid]
+        lay = self.graph.layer(lid)
+        x = self._value(info["src"])
+        read = info["read"]
+        gather_idx = None
+        if read is not None:
+            rl = self.graph.layer(read)
+            if rl.kind is LayerKind.SLICE:
+                s, n = rl.params
+                x = x.view(s, n)
+            else:
+                gather_idx = self._i32(rl.params)
+        cin = gather_idx.numel() if gather_idx is not None else x.C
+        assert cin == lay.in_channels, f"{lid}: reads {cin} channels, layer has {lay.in_channels}"
+        cout = lay.out_channels
+        kk = spec.kernel if spec.op == "conv" else 1
+        st = spec.stride if spec.op == "conv" else 1
+        pd = spec.pad if spec.op == "conv" else 0
+        lead, cpad = _lib.conv_weight_layout(cin, x.coff, gather_idx is not None)
+        W, rows, cols = ws(lid)
+        scale = bias = None
+        if info["bn"] is not None:
+            vec, perm = vs(info["bn"])
+            scale, bias = self._affine(info["bn"], vec, perm)
+            if self.specs[info["bn"]].op != "bn":
+                scale = None
+        O, I = W.shape[0], W.shape[1]
+        rows = rows if rows is not None else range(O)
+        cols = cols if cols is not None else range(I)
+        wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="gemm", lead=lead, cpad=cpad,
+                               out_dtype=torch.bfloat16)
+        self._keep.append(wg)
+        residual = self._value(info["residual"]) if info.get("residual") else None
+        fp32_out = info["out"] in output_feed
+        y = self._alloc(info["out"], cout, fp32=fp32_out)
+        relu = info["relu"] is not None
+        op.launch = lambda: K.conv(x, wg, lead, cpad, cout, kk, kk, st, pd, y, gather_idx=gather_idx, bias=bias,
+                                   residual=residual, relu=relu, y_fp32=fp32_out)
+        # roofline bookkeeping (per image)
+        _, hi, wi = self._shapes[info["src"]] if info["src"] in self._shapes else (0, x.H, x.W)
+        ho, wo = y.H, y.W
+        flops = 2.0 * cout * cin * kk * kk * ho * wo
+        byts = 2.0 * (cin * x.H * x.W + cout * ho * wo) + (2.0 * cout * cin * kk * kk) / self.batch
+        if residual is not None:
+            byts += 2.0 * cout * ho * wo
+        self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
+
+    # ------------------------------------------------------------------ execution
+    def launch_all(self) -> None:
+        for op in self.ops:
+            op.launch()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x: [N, C, H, W] fp32 (device or host).  Returns logits (device)."""
+        self.input_buf.copy_(x, non_blocking=True)
+        if self._graph_exec is not None:
+            self._graph_exec.replay()
+        else:
+            self.launch_all()
+        return self.output_tensor()
+
+    def output_tensor(self) -> torch.Tensor:
+        o = self.output_value
+        t = o.buf[:, o.coff:o.coff + o.C]
+        if o.H * o.W != 1:
+            t = t.reshape(o.N, o.H, o.W, o.C).permute(0, 3, 1, 2)
+        return t.float()
+
+    def capture(self) -> None:
+        """Capture the launch sequence in a CUDA graph (static buffers)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.launch_all()  # warm-up (first-launch attribute setup)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_all()
+        self._graph_exec = g
+
+    @property
+    def n_launches(self) -> int:
+        return len(self.ops)
+
+    def per_image_work(self) -> tuple[float, float]:
+        f = sum(c.flops for c in self.conv_stats)
+        b = sum(c.bytes + c.gather_bytes for c in self.conv_stats)
+        return f, b
+
+
+# ---------------------------------------------------------------------- builders
+def from_plans(sm, exported_graph: ModelGraph, maps, batch: int, device="cuda", gather_mode="fused",
+               masks: Mapping[str, Sequence[int]] | None = None) -> Engine:
+    """One-pass export: original sidecar weights + composed plan maps -> GEMM operands.
+    With `masks` and an identity export this runs the mask-simulated original
+    (interp.py:59-60: masked input channels == zero weight columns)."""
+    dev = torch.device(device)
+    cache: dict[str, torch.Tensor] = {}
+
+    def ws(lid):
+        if lid not in cache:
+            cache[lid] = sm.weights[lid].to(dev).contiguous()
+        cols = maps.cols.get(lid) if maps is not None else None
+        if masks is not None and lid in masks:
+            keep = set(masks[lid])
+            base = cols if cols is not None else range(sm.weights[lid].shape[1])
+            cols = tuple(c if c in keep else -1 for c in base)
+        return cache[lid], (maps.rows.get(lid) if maps is not None else None), cols
+
+    def vs(uid):
+        return sm.vectors[uid], (maps.vec.get(uid) if maps is not None else None)
+
+    return Engine(exported_graph, sm.specs, ws, vs, batch, sm.input_chw, device, gather_mode)
+
+
+def from_export(sm, result, batch: int, device="cuda", gather_mode="fused") -> Engine:
+    """Engine over an ExportResult (weights already permuted on device)."""
+
+    def ws(lid):
+        return result.weights.mix[lid].float().contiguous(), None, None
+
+    def vs(uid):
+        return result.weights.vec[uid], None
+
+    return Engine(result.graph, sm.specs, ws, vs, batch, sm.input_chw, device, gather_mode)

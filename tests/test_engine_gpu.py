@@ -1,0 +1,75 @@
+"""End-to-end parity of the B200 engine against the CPU oracle.
+
+The GPU path (bf16 activations/weights, fp32 accumulation) runs the exported
+graph; the oracle (oracle/spatial_ref.py, fp32) runs the SAME exported graph
+with weights permuted by the numpy restatement of apply_plan.  Gate (SURVEY.md
+8d): the reference's relative metric (interp.py:119-120) <= 2e-2 and top-1
+agreement.  BN statistics are randomised so a mis-permuted vector is caught.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle.apply_plan_ref import apply_plans_spatial  # noqa: E402
+from oracle.spatial_ref import deviation, run_spatial, top1_agreement  # noqa: E402
+from paper_2307_08771_b200 import engine as EN, export as E, ir, plans as P  # noqa: E402
+from paper_2307_08771_b200.configs import CONFIGS, build_spatial_model  # noqa: E402
+
+TOL = 2e-2
+
+
+def _setup(cfg_name, strategy, randomize_bn=True):
+    cfg = CONFIGS[cfg_name]
+    sm = build_spatial_model(cfg, randomize_bn=randomize_bn)
+    plans = P.load_plans(cfg.asset_dir / f"plans_{strategy}.json")
+    eg = E.export_graph(sm.graph, plans)
+    maps = E.compose_maps(sm.graph, plans)
+    return sm, plans, eg, maps
+
+
+@pytest.mark.parametrize("strategy", ["reorder", "baseline"])
+@pytest.mark.parametrize("gather_mode", ["fused", "copy"])
+def test_resnet18_logits_match_oracle(strategy, gather_mode):
+    sm, plans, eg, maps = _setup("resnet18_s50", strategy)
+    N = 4
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(0))
+    eng = EN.from_plans(sm, eg, maps, batch=N, gather_mode=gather_mode)
+    got = eng.forward(x.cuda()).cpu()
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
+    dev = deviation(got, ref)
+    assert dev <= TOL, f"deviation {dev}"
+    assert top1_agreement(got, ref) == 1.0
+
+
+def test_resnet50_reorder_logits_match_oracle_graph_replay():
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    N = 2
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(1))
+    eng = EN.from_plans(sm, eg, maps, batch=N)
+    eng.capture()
+    got = eng.forward(x.cuda()).cpu()
+    got2 = eng.forward(x.cuda()).cpu()
+    assert torch.equal(got, got2), "CUDA-graph replay is not deterministic"
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
+    assert deviation(got, ref) <= TOL
+    assert top1_agreement(got, ref) == 1.0
+
+
+def test_export_model_weights_bit_exact_vs_oracle():
+    """GPU permute (fp64, no BN fold) == numpy apply_plan restatement, bit for bit."""
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    w64 = {k: t.double() for k, t in sm.weights.items()}
+    vec64 = {k: {n: t.double() for n, t in vv.items()} for k, vv in sm.vectors.items()}
+    res = E.export_model(sm.graph, w64, vec64, ir.load_masks(CONFIGS["resnet50_s50"].asset_dir / "masks.json"),
+                         plans=plans, out_dtype=torch.float64)
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    for lid, t in w.items():
+        assert torch.equal(res.weights.mix[lid].cpu(), t), lid
+    for uid, named in v.items():
+        for n, t in named.items():
+            assert torch.equal(res.weights.vec[uid][n].cpu(), t), (uid, n)
+    assert ir.graph_to_dict(res.graph) == ir.graph_to_dict(eg)

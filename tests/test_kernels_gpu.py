@@ -40,6 +40,11 @@ CASES = [
     ("fc_gather_fp32", 4, 1, 1, 2048, 0, 2048, 1000, 1, 1, 0, 1024, True, False, False, True),
     ("3x3_slice_offset", 3, 14, 14, 96, 40, 48, 72, 3, 1, 1, 0, True, True, True, False),
     ("1x1_large_m", 8, 56, 56, 256, 0, 256, 64, 1, 1, 0, 0, False, False, False, False),
+    ("gather_s2_downsample", 2, 28, 28, 240, 0, 237, 128, 1, 2, 0, 128, True, False, False, False),
+    ("3x3_s1_misaligned_7x7", 4, 7, 7, 1824, 530, 1024, 40, 3, 1, 1, 0, True, False, True, False),
+    ("gather_3x3_s2", 2, 28, 28, 200, 0, 200, 96, 3, 2, 1, 70, True, True, True, False),
+    ("gather_3x3_s1", 3, 14, 14, 64, 0, 64, 64, 3, 1, 1, 40, False, False, True, False),
+    ("1x1_s2_misaligned", 2, 56, 56, 56, 17, 32, 256, 1, 2, 0, 0, True, False, False, False),
 ]
 
 
