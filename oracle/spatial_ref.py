@@ -24,8 +24,10 @@ def _kind(lay) -> str:
 
 def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
                 vectors: Mapping[str, Mapping[str, torch.Tensor]], x: torch.Tensor,
-                masks: Mapping[str, tuple] | None = None, dtype=torch.float64) -> torch.Tensor:
-    """Returns the OUTPUT node's value ([N, C] if spatially collapsed)."""
+                masks: Mapping[str, tuple] | None = None, dtype=torch.float64, values: dict | None = None
+                ) -> torch.Tensor:
+    """Returns the OUTPUT node's value ([N, C] if spatially collapsed).  If
+    `values` is a dict it receives every node's output (debugging aid)."""
     masks = masks or {}
     vals: dict[str, torch.Tensor] = {}
     out_id = None
@@ -90,6 +92,8 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
         if out.shape[1] != lay.out_channels:
             raise ValueError(f"{lid}: produced {out.shape[1]} channels, expected {lay.out_channels}")
         vals[lid] = out
+    if values is not None:
+        values.update(vals)
     res = vals[out_id]
     if res.dim() == 4 and res.shape[2] == 1 and res.shape[3] == 1:
         res = res[:, :, 0, 0]

@@ -44,6 +44,8 @@ CASES = [
     ("3x3_s1_misaligned_7x7", 4, 7, 7, 1824, 530, 1024, 40, 3, 1, 1, 0, True, False, True, False),
     ("gather_3x3_s2", 2, 28, 28, 200, 0, 200, 96, 3, 2, 1, 70, True, True, True, False),
     ("gather_3x3_s1", 3, 14, 14, 64, 0, 64, 64, 3, 1, 1, 40, False, False, True, False),
+    ("two_ntiles_unaligned_390", 4, 14, 14, 232, 66, 128, 390, 1, 2, 0, 0, True, True, True, False),
+    ("three_ntiles_700_gather", 2, 7, 7, 512, 0, 512, 700, 1, 1, 0, 300, True, False, False, False),
     ("1x1_s2_misaligned", 2, 56, 56, 56, 17, 32, 256, 1, 2, 0, 0, True, False, False, False),
 ]
 

@@ -1,0 +1,96 @@
+"""Conv kernel microbenchmark + correctness at production sizes (dev tool).
+
+python tools/bench_conv.py [case ...]   -- cases are ResNet-50 layer shapes at batch 256
+Each case: checks ub_conv_fwd against torch (bf16-rounded inputs, fp32 math) on
+the full output, then times it with CUDA events and prints algorithmic GB/s.
+"""
+
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2307_08771_b200 import _lib, kernels as K  # noqa: E402
+
+# name: (N, H, W, cstride, coff, cin, cout, k, stride, pad, n_gather, res, relu)
+CASES = {
+    "l1_conv3": (256, 56, 56, 32, 0, 32, 256, 1, 1, 0, 0, True, True),
+    "l1_conv1_gather": (256, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, False, True),
+    "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv2_3x3": (256, 56, 56, 64, 0, 32, 64, 3, 1, 1, 0, False, True),
+    "l2_down_gather_s2": (256, 56, 56, 240, 0, 237, 512, 1, 2, 0, 128, False, False),
+    "l3_conv2_3x3s2": (256, 28, 28, 128, 0, 128, 256, 3, 2, 1, 0, False, True),
+    "stem_7x7": (256, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),
+    "l4_conv3": (256, 7, 7, 256, 0, 256, 2048, 1, 1, 0, 0, True, True),
+    "l4_down_r18": (4, 14, 14, 232, 66, 128, 390, 1, 2, 0, 0, False, False),
+    "l4_down_r18_aligned": (4, 14, 14, 232, 64, 128, 390, 1, 2, 0, 0, False, False),
+    "l4_down_r18_c256": (4, 14, 14, 232, 66, 128, 256, 1, 2, 0, 0, False, False),
+    "l4_1x1s1_c390": (4, 7, 7, 232, 64, 128, 390, 1, 1, 0, 0, False, False),
+    "l4_1x1s1_c416": (4, 7, 7, 232, 64, 128, 416, 1, 1, 0, 0, False, False),
+    "l4_1x1s1_c390_big": (64, 7, 7, 232, 64, 128, 390, 1, 1, 0, 0, False, False),
+    "small_gather_multi": (8, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, True, True),
+    "small_3x3_res_multi": (8, 56, 56, 64, 0, 64, 64, 3, 1, 1, 0, True, True),
+    "small_stem_multi": (4, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),
+}
+
+
+def run(name, check=True, iters=20):
+    N, H, W, cs, coff, cin, cout, k, st, pad, ng, use_r, relu = CASES[name]
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(0)
+    xbuf = torch.randn(N * H * W, cs, device=dev, generator=g).to(torch.bfloat16)
+    x = K.Act(xbuf, N, H, W, cs)
+    nin = ng if ng else cin
+    Wt = (torch.randn(cout, nin, k, k, device=dev, generator=g) / (nin * k * k) ** 0.5).contiguous()
+    if ng:
+        idx = torch.randperm(cin, device=dev, generator=g)[:ng].to(torch.int32)
+        xa, lead, cpad = x, *_lib.conv_weight_layout(ng, 0, True)
+    else:
+        idx = None
+        xa = x.view(coff, cin)
+        lead, cpad = _lib.conv_weight_layout(cin, coff, False)
+    wg = K.permute_weights(Wt, list(range(cout)), list(range(nin)), layout="gemm", lead=lead, cpad=cpad,
+                           out_dtype=torch.bfloat16)
+    Ho = (H + 2 * pad - k) // st + 1
+    Wo = (W + 2 * pad - k) // st + 1
+    bias = torch.randn(cout, device=dev, generator=g)
+    res = K.empty_act(N, Ho, Wo, cout, dev) if use_r else None
+    if res is not None:
+        res.buf.normal_(generator=g)
+    y = K.empty_act(N, Ho, Wo, cout, dev)
+    K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+    torch.cuda.synchronize()
+    err = None
+    if check:
+        xin = x.to_nchw()
+        xin = xin[:, idx.long()] if idx is not None else xin[:, coff:coff + cin]
+        ref = torch.nn.functional.conv2d(xin, Wt.to(torch.bfloat16).float(), stride=st, padding=pad)
+        ref = ref + bias.view(1, -1, 1, 1)
+        if res is not None:
+            ref = ref + res.to_nchw()
+        if relu:
+            ref = ref.clamp_min(0)
+        out = y.to_nchw()
+        err = float((out - ref).abs().max() / ref.abs().max())
+        del ref, xin
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+    a.record()
+    for _ in range(iters):
+        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+    b.record()
+    torch.cuda.synchronize()
+    us = a.elapsed_time(b) / iters * 1e3
+    byts = 2 * (nin * H * W + cout * Ho * Wo * (2 if use_r else 1)) * N + wg.numel() * 2
+    flops = 2 * cout * nin * k * k * Ho * Wo * N
+    roof = max(byts / 6554.6e9, flops / 1398.9e12) * 1e6
+    print(f"{name:22s} err {err if err is None else f'{err:.2e}'}  {us:9.1f} us  {byts/us/1e3:7.1f} GB/s  "
+          f"{flops/us/1e6:7.1f} TF/s  roof {roof:7.1f} us  frac {roof/us:.2f}", flush=True)
+
+
+if __name__ == "__main__":
+    torch.backends.cudnn.allow_tf32 = False
+    for n in sys.argv[1:] or list(CASES):
+        run(n)
