@@ -39,12 +39,14 @@ extern "C" {
 #define UB_LAYOUT_OIHW 0 /* [n_rows][n_cols][kh][kw]: the plain 4-D result of apply_plan */
 #define UB_LAYOUT_GEMM 1 /* [n_rows][kh*kw][cpad]: K-major B operand of ub_conv_fwd,
                             column c of tap t at (lead + c); zeros elsewhere */
+#define UB_LAYOUT_GEMM_DENSE 2 /* [n_rows][cpad]: dense-K operand of the fused stem,
+                                  column c of tap t at t*n_cols + c; zeros beyond */
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* ub_last_error(void);
 
 /* ABI version (bumped on any signature change). */
-int ub_abi_version(void);
+int ub_abi_version(void); /* 2 */
 
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (used by bench.py's gpu_launches claim). */
@@ -114,7 +116,14 @@ typedef struct {
   void* y;                     /* output, NHWC [N*Ho*Wo][y_cstride] */
   int y_cstride, y_coff;
   int y_dtype;                 /* UB_BF16 or UB_F32 */
+  int x_nchw_f32;              /* 1: fused stem -- x is the fp32 NCHW model input
+                                  [N][x_channels][H][W]; gather_idx selects the cin planes
+                                  (the INPUT node's GATHER), weights UB_LAYOUT_GEMM_DENSE */
+  int x_channels;
 } ub_conv_desc;
+
+/* Dense-K padding (multiple of 64) of the fused-stem weight operand. */
+int ub_conv_stem_kpad(int cin, int kh, int kw);
 
 int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream);
 

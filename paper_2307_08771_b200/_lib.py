@@ -18,7 +18,7 @@ UB_EUNSUPPORTED = -2
 UB_ECUDA = -3
 
 UB_F32, UB_F64, UB_BF16 = 0, 1, 2
-UB_LAYOUT_OIHW, UB_LAYOUT_GEMM = 0, 1
+UB_LAYOUT_OIHW, UB_LAYOUT_GEMM, UB_LAYOUT_GEMM_DENSE = 0, 1, 2
 
 c_int, c_ll, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p
 
@@ -47,6 +47,7 @@ class ConvDesc(ctypes.Structure):
         ("relu", c_int),
         ("y", c_vp), ("y_cstride", c_int), ("y_coff", c_int),
         ("y_dtype", c_int),
+        ("x_nchw_f32", c_int), ("x_channels", c_int),
     ]
 
 
@@ -62,6 +63,7 @@ SIGNATURES = {
     "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_fwd": (c_int, [ctypes.POINTER(ConvDesc), c_vp]),
+    "ub_conv_stem_kpad": (c_int, [c_int, c_int, c_int]),
     "ub_stage_input": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp]),
     "ub_maxpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                              c_int, c_int, c_vp, c_int, c_int, c_vp]),
@@ -111,6 +113,10 @@ def launch_count() -> int:
 
 def reset_launch_count() -> None:
     load().ub_reset_launch_count()
+
+
+def conv_stem_kpad(cin: int, kh: int, kw: int) -> int:
+    return int(load().ub_conv_stem_kpad(cin, kh, kw))
 
 
 def conv_weight_layout(cin: int, coff: int, gather: bool) -> tuple[int, int]:

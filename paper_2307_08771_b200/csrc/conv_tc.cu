@@ -1,30 +1,35 @@
-// Implicit-GEMM convolution on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+// Implicit-GEMM convolution on sm_100a tensor cores (tcgen05 + TMEM + TMA store).
 //
 // One reference CHANNEL_MIX node (interp.py:57-63, `W @ x`) executed over real
 // NHWC activations, with the node that reads its input and the nodes that
 // consume its output fused in:
-//   * SLICE read  (interp.py:72-74): the A operand's TMA descriptor starts at the
-//     slice's channel offset -- no copy (UPSCALE's contiguous read);
-//   * GATHER read (interp.py:75-77): dedicated gather warps build the A tile
-//     (implicit im2col over the gathered channels) straight from the producer's
-//     tensor into swizzled shared memory -- the copy the baseline export
-//     materialises never touches HBM;
+//   * SLICE read  (interp.py:72-74): the A operand is addressed at the slice's
+//     channel offset -- no copy (UPSCALE's contiguous read);
+//   * GATHER read (interp.py:75-77): the producer warps gather the channels
+//     (implicit im2col over the gathered set) straight from the producer
+//     layer's tensor into swizzled shared memory -- the copy the baseline
+//     export materialises never touches HBM;
 //   * PER_CHANNEL bias (BN shift; the scale is folded into the weight rows at
 //     export), ADD residual, ReLU, and a channel-offset store (CONCAT without a
 //     copy).
 //
 // GEMM view: D[M = N*Ho*Wo pixels][cout] = A[M][K] * B[cout][K]^T, K = taps*cpad.
-// Tile 128 pixels x block_n channels (block_n <= 256, multiple of 16, runtime).
+// Tile 128 pixels x block_n channels (block_n <= 256, runtime).
 //
-// Persistent, warp-specialised, one CTA per SM; tiles are strided over the grid.
-//   warp 0      TMA producer (A: 2-D tiled or im2col; B: weights)
+// Data movement is chosen by measurement (tools/tma_probe.cu on B200): a TMA
+// LOAD costs ~10 SM cycles per box row (<= 128 B rows), capping 128-byte-row
+// loads near 3.7 TB/s chip-wide, while cp.async from 8 producer warps and TMA
+// STORES (~6.4 cycles/row) keep up with HBM.  So operands and the residual
+// come in by cp.async (completion tracked on mbarriers), outputs leave by TMA
+// bulk tensor store.
+//
+// Persistent, warp-specialised, one CTA (512 threads) per SM:
 //   warp 1      MMA issuer: tcgen05.mma into one of TWO TMEM accumulators, so the
 //               epilogue of tile i overlaps the mainloop of tile i+1
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: TMEM -> regs (+bias, +residual, ReLU) -> swizzled smem
-//               -> TMA bulk store; the residual tile arrives by TMA load,
-//               double-buffered one 32-channel chunk ahead
-//   warps 8-11  gather producers (GATHER mode only)
+//               -> TMA store (residual prefetched by cp.async two chunks ahead)
+//   warps 8-15  producers: A (tiled / im2col / gathered / fp32 stem) and B tiles
 #include <mutex>
 
 #include "ub_common.cuh"
@@ -32,12 +37,19 @@
 
 namespace ub {
 
-enum AMode : int { A_TILED = 0, A_IM2COL = 1, A_GATHER = 2 };
+enum AMode : int { A_TILED = 0, A_IM2COL = 1, A_GATHER = 2, A_STEM = 3 };
+// register-path producers (2-byte gathers, fp32 casts) arrive explicitly per warp as well
+__host__ __device__ constexpr bool reg_mode(int m) { return m == A_GATHER || m == A_STEM; }
 
 constexpr int BLOCK_M = 128;
-constexpr int EPI_CHUNK = 32;                // output channels per epilogue chunk
-constexpr int EPI_BUF = 32 * EPI_CHUNK * 2;  // one warp's 32 rows x 32 ch bf16 staging buffer
+constexpr int NUM_THREADS = 512;
+constexpr int PRODUCERS = 256;                // warps 8-15
+constexpr int EPI_CHUNK = 64;                 // output channels per epilogue chunk (128-byte rows)
+constexpr int EPI_SLOT = 32 * EPI_CHUNK * 2;  // one warp's 32 rows x 64 ch bf16 (4 KB)
+constexpr int EPI_SLOTS = 4;                  // per warp: residual lands / output leaves in place
 constexpr int MAX_BLOCK_N = 256;
+constexpr int BAR_BYTES = 512;   // mbarriers + TMEM slot region
+constexpr int MAX_STEM_K = 512;  // dense-K stem: taps * channels, padded to 64
 
 struct ConvKParams {
   int M;        // output pixels (GEMM M)
@@ -47,21 +59,27 @@ struct ConvKParams {
   int cchunks;  // channel chunks per tap
   int kw;       // filter width
   int cpad;     // per-tap weight K
+  int K_total;  // weight row length
+  int cin_eff;  // channels readable in the A source (slice length + lead)
   int H, W, Ho, Wo, stride, pad;
   int stages;
   int m_tiles, n_tiles;
   uint32_t tmem_cols, acc_stride;
-  // fused gather source
-  const uint16_t* x;
-  int x_cstride, x_coff;
+  const uint16_t* x;  // A source (bf16 NHWC), offset to the 8-aligned slice base / gather base
+  int x_cstride;
+  const uint16_t* w;  // B: bf16 [cout][K_total]
+  // fused gather
   const int32_t* gidx;
   int n_gather;
+  // fused stem: fp32 NCHW model input, dense K = taps * n_gather
+  const float* xf;
+  int C_in, k_real;
   // epilogue
   const float* bias;
   int has_res, relu, epi_tma;
-  const __nv_bfloat16* res;  // direct-store fallback only
-  int res_cstride, res_coff;
-  void* y;
+  const uint16_t* res;  // residual, offset to its channel base
+  int res_cstride;
+  void* y;  // direct-store fallback only
   int y_cstride, y_coff, y_f32;
 };
 
@@ -69,34 +87,39 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// Byte offset of 16-byte chunk j of row r in a 64-byte-row SWIZZLE_64B buffer.
-__device__ __forceinline__ uint32_t swz64(uint32_t r, uint32_t j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
+// Byte offset of 16-byte chunk j of row r in a swizzled K-major tile with BK-element rows
+// (SWIZZLE_128B / 64B / 32B: the chunk index is XORed with address bits [7, 10)).
+template <int BK>
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t j) {
+  if constexpr (BK == 64) return r * 128 + ((j ^ (r & 7)) << 4);
+  else if constexpr (BK == 32) return r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+  else return r * 32 + ((j ^ ((r >> 2) & 1)) << 4);
+}
 
 template <int AMODE, int BK>
-__global__ void __launch_bounds__(AMODE == A_GATHER ? 384 : 256, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
-                   const ConvKParams p) {
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const ConvKParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  constexpr uint32_t A_BYTES = BLOCK_M * BK * 2;
   constexpr uint32_t ROW_BYTES = BK * 2;
+  constexpr int CPR = ROW_BYTES / 16;  // 16-byte chunks per operand row
+  constexpr uint32_t A_BYTES = BLOCK_M * ROW_BYTES;
   constexpr uint32_t SBO = 8 * ROW_BYTES;
-  constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 6u;  // SWIZZLE_128B : SWIZZLE_32B
+  constexpr uint32_t LAYOUT = (BK == 64) ? 2u : (BK == 32 ? 4u : 6u);  // SWIZZLE_128B / 64B / 32B
   const uint32_t b_bytes = static_cast<uint32_t>(p.block_n) * ROW_BYTES;
   const uint32_t b_stride = (b_bytes + 1023u) & ~1023u;
   const int stages = p.stages;
 
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_BYTES;
-  uint8_t* sE = sB + stages * b_stride;                           // 4 warps x 2 x EPI_BUF (1024-aligned)
-  float* sBias = reinterpret_cast<float*>(sE + 4 * 2 * EPI_BUF);  // 4 warps x MAX_BLOCK_N
+  uint8_t* sE = sB + stages * b_stride;                                    // 4 warps x EPI_SLOTS x 4 KB
+  float* sBias = reinterpret_cast<float*>(sE + 4 * EPI_SLOTS * EPI_SLOT);  // 4 warps x MAX_BLOCK_N
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + 4 * MAX_BLOCK_N);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint64_t* rbar = tempty + 2;       // [4 warps][2 buffers]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int4* stem_tab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // A_STEM only
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -104,81 +127,52 @@ __global__ void __launch_bounds__(AMODE == A_GATHER ? 384 : 256, 1)
   const int nk = p.num_kb;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    if (p.epi_tma) {
-      tma_prefetch_desc(&tmY);
-      if (p.has_res) tma_prefetch_desc(&tmR);
-    }
+    if (p.epi_tma) tma_prefetch_desc(&tmY);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], AMODE == A_GATHER ? 1 + 4 : 1);
+      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PRODUCERS / 32 : 0));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&rbar[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  if constexpr (AMODE == A_STEM) {
+    // k -> (input offset relative to the window origin, filter row r, filter col s); k >= k_real: r = -1
+    for (int k = threadIdx.x; k < p.num_kb * 64; k += blockDim.x) {
+      int4 e = make_int4(0, -1, 0, 0);
+      if (k < p.k_real) {
+        const int t = k / p.n_gather;
+        const int c = k - t * p.n_gather;
+        const int r = t / p.kw;
+        const int sc = t - r * p.kw;
+        e = make_int4((__ldg(p.gidx + c) * p.H + r) * p.W + sc, r, sc, 0);
+      }
+      stem_tab[k] = e;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      // ================= TMA producer
-      int g = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_tile = t / p.n_tiles;
-        const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
-        const int m0 = m_tile * BLOCK_M;
-        int w_start = 0, h_start = 0, n_img = 0;
-        if (AMODE == A_IM2COL) {
-          const int hw = p.Ho * p.Wo;
-          n_img = m0 / hw;
-          const int rem = m0 - n_img * hw;
-          const int ho = rem / p.Wo;
-          w_start = (rem - ho * p.Wo) * p.stride - p.pad;
-          h_start = ho * p.stride - p.pad;
-        }
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % stages;
-          const uint32_t ph = (g / stages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], b_bytes + (AMODE == A_GATHER ? 0u : A_BYTES));
-          int kcoord = kb * BK;
-          if (AMODE == A_TILED) {
-            tma_load_2d(&tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
-          } else if (AMODE == A_IM2COL) {
-            const int tap = kb / p.cchunks;
-            const int cc = kb - tap * p.cchunks;
-            const int r = tap / p.kw;
-            tma_load_im2col_4d(&tmA, &full[s], sA + s * A_BYTES, cc * BK, w_start, h_start, n_img,
-                               static_cast<uint16_t>(tap - r * p.kw), static_cast<uint16_t>(r));
-            kcoord = tap * p.cpad + cc * BK;
-          }
-          tma_load_2d(&tmB, &full[s], sB + s * b_stride, kcoord, n0);
-        }
-      }
-    }
-  } else if (warp == 1) {
+  if (warp == 1) {
     if (lane == 0) {
       // ================= MMA issuer
       const uint32_t idesc = make_idesc_bf16(BLOCK_M, static_cast<uint32_t>(p.block_n));
-      int g = 0, it = 0;
+      int s = 0, it = 0;
+      uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * p.acc_stride;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % stages;
-          const uint32_t ph = (g / stages) & 1;
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          fence_proxy_async_smem();  // generic-proxy (cp.async / st.shared) writes -> tensor-core reads
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           const uint32_t b_base = smem_u32(sB + s * b_stride);
 #pragma unroll
@@ -187,22 +181,61 @@ __global__ void __launch_bounds__(AMODE == A_GATHER ? 384 : 256, 1)
                       (kb | k) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[s]);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         umma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 8) {
-    if constexpr (AMODE == A_GATHER) {
-      // ================= gather producers: implicit im2col over gathered channels
-      // A[row][j] of tap (r, s) = x[pixel(row) + (r, s)][x_coff + gidx[cc*64 + j]], 0 outside.
-      const int qg = warp - 8;
-      const int hw = p.Ho * p.Wo;
-      int g = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t / p.n_tiles) * BLOCK_M;
-        int g_img = 0, g_hb = -(1 << 28), g_wb = 0;  // lane owns row qg*32 + lane
-        {
-          const int m = m0 + qg * 32 + lane;
+    // ================= producers (256 threads): fill stage s with A and B, then arrive on full[s]
+    // Addresses are precomputed per tile so the per-k-block work is one add + one cp.async per
+    // 16-byte chunk; smem destinations are constant for the whole kernel.
+    const int pt = threadIdx.x - 256;  // 0..255
+    const int pw = pt >> 5;            // producer warp 0..7
+    const int hw = p.Ho * p.Wo;
+    constexpr int A_PER_THREAD = BLOCK_M * CPR / PRODUCERS;  // 4 / 2 / 1 for BK 64 / 32 / 16
+    constexpr int ROW_STEP = PRODUCERS / CPR;                // rows between a thread's chunks
+    const int row0 = pt / CPR;
+    const int cj = pt % CPR;  // this thread's 16-byte chunk within an operand row
+    const uint32_t dst0 = swz<BK>(row0, cj);  // + i * ROW_STEP * ROW_BYTES for chunk i (swizzle-invariant)
+    const int nb_pieces = (p.block_n + ROW_STEP - 1) / ROW_STEP;  // B chunks per thread (upper bound)
+    const size_t b_row_stride = static_cast<size_t>(ROW_STEP) * p.K_total;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m_tile = t / p.n_tiles;
+      const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
+      const int m0 = m_tile * BLOCK_M;
+      // A geometry of this thread's rows: pixel base pointer + top-left window coordinate
+      const uint16_t* a_base[A_PER_THREAD];
+      int a_hb[A_PER_THREAD], a_wb[A_PER_THREAD];
+#pragma unroll
+      for (int i = 0; i < A_PER_THREAD; ++i) {
+        const int m = m0 + row0 + i * ROW_STEP;
+        a_base[i] = p.x;
+        a_hb[i] = -(1 << 28);
+        a_wb[i] = 0;
+        if ((AMODE == A_TILED || AMODE == A_IM2COL) && m < p.M) {
+          const int img = m / hw;
+          const int rem = m - img * hw;
+          const int ho = rem / p.Wo;
+          a_hb[i] = ho * p.stride - p.pad;
+          a_wb[i] = (rem - ho * p.Wo) * p.stride - p.pad;
+          a_base[i] = p.x + ((static_cast<ptrdiff_t>(img) * p.H + a_hb[i]) * p.W + a_wb[i]) * p.x_cstride + cj * 8;
+        }
+      }
+      const uint16_t* b_base = p.w + static_cast<size_t>(n0 + row0) * p.K_total + cj * 8;
+      const int b_valid = min(p.block_n, p.cout - n0);  // rows beyond are zero-filled
+      // register-path geometry: gather -> warp pw owns rows 16*pw..16*pw+15 (lane = channel pair);
+      // stem -> thread owns row pt & 127 and k half pt >> 7
+      int g_img = 0, g_hb = -(1 << 28), g_wb = 0;
+      const float* stem_base = p.xf;
+      if constexpr (AMODE == A_GATHER) {
+        if (lane < 16) {
+          const int m = m0 + pw * 16 + lane;
           if (m < p.M) {
             g_img = m / hw;
             const int rem = m - g_img * hw;
@@ -211,53 +244,142 @@ __global__ void __launch_bounds__(AMODE == A_GATHER ? 384 : 256, 1)
             g_wb = (rem - ho * p.Wo) * p.stride - p.pad;
           }
         }
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % stages;
-          const uint32_t ph = (g / stages) & 1;
-          const int tap = kb / p.cchunks;
-          const int cc = kb - tap * p.cchunks;
-          const int fr = tap / p.kw;
-          const int fs = tap - fr * p.kw;
+      }
+      if constexpr (AMODE == A_STEM) {
+        const int m = m0 + (pt & 127);
+        if (m < p.M) {
+          const int img = m / hw;
+          const int rem = m - img * hw;
+          const int ho = rem / p.Wo;
+          g_hb = ho * p.stride - p.pad;
+          g_wb = (rem - ho * p.Wo) * p.stride - p.pad;
+          stem_base =
+              p.xf + static_cast<size_t>(img) * p.C_in * p.H * p.W + static_cast<ptrdiff_t>(g_hb) * p.W + g_wb;
+        }
+      }
+      int cc = 0, fs = 0, fr = 0;  // channel chunk, filter column, filter row of k-block kb
+      for (int kb = 0; kb < nk; ++kb) {
+        const int kcoord = kb * BK;  // weights are [cout][taps][cpad]: k-block kb starts at kb*BK
+        // register paths: issue the global loads before waiting for the slot
+        uint16_t la[16], lb[16];
+        uint32_t okm = 0;
+        int i0 = -1, i1 = -1;
+        float fv[32];
+        if constexpr (AMODE == A_GATHER) {
           const int j = cc * 64 + lane * 2;
-          const int i0 = j < p.n_gather ? __ldg(p.gidx + j) : -1;
-          const int i1 = (j + 1) < p.n_gather ? __ldg(p.gidx + j + 1) : -1;
-          uint32_t vals[32];
+          i0 = j < p.n_gather ? __ldg(p.gidx + j) : -1;
+          i1 = (j + 1) < p.n_gather ? __ldg(p.gidx + j + 1) : -1;
+          const int c0 = i0 < 0 ? 0 : i0;
+          const int c1 = i1 < 0 ? 0 : i1;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {  // all 64 loads of this lane in flight before any store
+          for (int u = 0; u < 16; ++u) {
             const int img = __shfl_sync(0xffffffffu, g_img, u);
             const int hi = __shfl_sync(0xffffffffu, g_hb, u) + fr;
             const int wi = __shfl_sync(0xffffffffu, g_wb, u) + fs;
-            uint32_t a = 0, b = 0;
-            if (hi >= 0 && hi < p.H && wi >= 0 && wi < p.W) {
-              const uint16_t* xr =
-                  p.x + ((static_cast<size_t>(img) * p.H + hi) * p.W + wi) * p.x_cstride + p.x_coff;
-              if (i0 >= 0) a = __ldg(xr + i0);
-              if (i1 >= 0) b = __ldg(xr + i1);
-            }
-            vals[u] = a | (b << 16);
+            const bool ok = hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            okm |= static_cast<uint32_t>(ok) << u;
+            const size_t pix = ok ? (static_cast<size_t>(img) * p.H + hi) * p.W + wi : 0;
+            const uint16_t* xr = p.x + pix * p.x_cstride;
+            la[u] = __ldg(xr + c0);
+            lb[u] = __ldg(xr + c1);
           }
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* tile = sA + s * A_BYTES;
+        }
+        if constexpr (AMODE == A_STEM) {
+          const int kh0 = kb * 64 + (pt >> 7) * 32;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int row = qg * 32 + u;
-            const uint32_t off = row * 128 + ((((lane >> 2) ^ (row & 7)) << 4)) + ((lane & 3) << 2);
-            *reinterpret_cast<uint32_t*>(tile + off) = vals[u];
+          for (int kk = 0; kk < 32; ++kk) {
+            const int4 e = stem_tab[kh0 + kk];  // warp-uniform -> smem broadcast
+            const int hi = g_hb + e.y;
+            const int wi = g_wb + e.z;
+            const bool ok = e.y >= 0 && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            fv[kk] = ok ? __ldg(stem_base + e.x) : 0.f;
           }
+        }
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t tileA = smem_u32(sA + s * A_BYTES);
+        const uint32_t tileB = smem_u32(sB + s * b_stride);
+        // ---- A
+        if constexpr (AMODE == A_TILED || AMODE == A_IM2COL) {
+          const bool ch_ok = cc * BK + cj * 8 < p.cin_eff;
+          const ptrdiff_t toff = (static_cast<ptrdiff_t>(fr) * p.W + fs) * p.x_cstride + cc * BK;
+#pragma unroll
+          for (int i = 0; i < A_PER_THREAD; ++i) {
+            const int hi = a_hb[i] + fr;
+            const int wi = a_wb[i] + fs;
+            const bool ok = ch_ok && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            const uint16_t* src = ok ? a_base[i] + toff : p.x;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileA + dst0 + i * ROW_STEP * ROW_BYTES),
+                         "l"(src), "r"(ok ? 16u : 0u)
+                         : "memory");
+          }
+        } else if constexpr (AMODE == A_GATHER) {
+          uint8_t* tA = sA + s * A_BYTES;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const bool ok = (okm >> u) & 1u;
+            const uint32_t a = (ok && i0 >= 0) ? la[u] : 0u;
+            const uint32_t b = (ok && i1 >= 0) ? lb[u] : 0u;
+            const int row = pw * 16 + u;
+            *reinterpret_cast<uint32_t*>(tA + swz<64>(row, lane >> 2) + ((lane & 3) << 2)) = a | (b << 16);
+          }
+        } else {  // A_STEM
+          uint8_t* tA = sA + s * A_BYTES;
+          const int row = pt & 127;
+          const int j0 = (pt >> 7) * 4;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            uint4 o;
+            o.x = pack_bf16x2(fv[jj * 8 + 0], fv[jj * 8 + 1]);
+            o.y = pack_bf16x2(fv[jj * 8 + 2], fv[jj * 8 + 3]);
+            o.z = pack_bf16x2(fv[jj * 8 + 4], fv[jj * 8 + 5]);
+            o.w = pack_bf16x2(fv[jj * 8 + 6], fv[jj * 8 + 7]);
+            *reinterpret_cast<uint4*>(tA + swz<64>(row, j0 + jj)) = o;
+          }
+        }
+        // ---- B (weights [cout][K_total]): rows row0 + i * ROW_STEP, chunk cj
+        {
+          const uint16_t* src = b_base + kcoord;
+          for (int i = 0; i < nb_pieces; ++i, src += b_row_stride) {
+            const int n = row0 + i * ROW_STEP;
+            if (n >= p.block_n) break;
+            const bool ok = n < b_valid;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileB + dst0 + i * ROW_STEP * ROW_BYTES),
+                         "l"(ok ? src : p.w), "r"(ok ? 16u : 0u)
+                         : "memory");
+          }
+        }
+        if constexpr (reg_mode(AMODE)) {  // st.shared part: fence, then one arrival per warp
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[s]);
         }
+        cp_async_arrive_noinc(&full[s]);
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++cc == p.cchunks) {
+          cc = 0;
+          if (++fs == p.kw) {
+            fs = 0;
+            ++fr;
+          }
+        }
       }
     }
+    cp_async_wait<0>();
   } else if (warp >= 4) {
     // ================= epilogue
+    // Warp q owns rows q*32..q*32+31 of the tile and walks 64-channel chunks.  The residual
+    // chunk lands by cp.async (two chunks ahead, the first ones during the mainloop) in a
+    // slot of a 4-slot ring; the output is written back into the same slot and leaves by
+    // TMA store, whose read-completion frees the slot four chunks later.
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint8_t* ebuf = sE + q * 2 * EPI_BUF;
+    uint8_t* slots = sE + q * EPI_SLOTS * EPI_SLOT;
     float* sb = sBias + q * MAX_BLOCK_N;
-    uint64_t* rb = rbar + q * 2;
-    uint32_t ec = 0;
+    uint32_t ec = 0;  // chunks processed by this warp so far (= TMA stores committed)
     int it = 0;
+    const bool tma = p.epi_tma;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
@@ -267,105 +389,128 @@ __global__ void __launch_bounds__(AMODE == A_GATHER ? 384 : 256, 1)
       const int nchunks = (ncols + EPI_CHUNK - 1) / EPI_CHUNK;
       __syncwarp();
       for (int i = lane; i < nchunks * EPI_CHUNK; i += 32) sb[i] = (p.bias && i < ncols) ? __ldg(p.bias + n0 + i) : 0.f;
-      __syncwarp();
-      if (p.epi_tma && p.has_res && lane == 0) {  // residual chunk 0, in flight during the mainloop
-        bulk_wait_read<0>();
-        mbar_arrive_expect_tx(&rb[ec & 1], EPI_BUF);
-        tma_load_2d(&tmR, &rb[ec & 1], ebuf + (ec & 1) * EPI_BUF, n0, rows0);
+      const bool res_tma = tma && p.has_res;
+      auto prefetch_res = [&](uint32_t e, int n_ch) {
+        uint8_t* slot = slots + (e % EPI_SLOTS) * EPI_SLOT;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // 32 rows x 8 chunks = 256 pieces, 8 per lane
+          const int row = (lane >> 3) + 4 * i;
+          const int j = lane & 7;
+          const int m = rows0 + row;
+          const bool ok = m < p.M && n_ch + j * 8 < p.cout;
+          const uint16_t* src = ok ? p.res + static_cast<size_t>(m) * p.res_cstride + n_ch + j * 8 : p.res;
+          cp_async16(slot + swz<64>(row, j), src, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+      };
+      if (res_tma) {  // chunks 0 and 1 fly while the mainloop runs
+        if (lane == 0) bulk_wait_read<2>();  // slots of chunks ec-4 / ec-3 were read by their stores
+        __syncwarp();
+        for (int c = 0; c < 2 && c < nchunks; ++c) prefetch_res(ec + c, n0 + c * EPI_CHUNK);
       }
+      __syncwarp();
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c, ++ec) {
-        const uint32_t b = ec & 1;
-        uint32_t r[32];
-        tmem_ld32(taddr + c * EPI_CHUNK, r);
-        tmem_ld_wait();
-        if (c == nchunks - 1) {  // accumulator drained: MMA may start the tile after next
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + sb[c * EPI_CHUNK + i];
-        if (p.epi_tma) {
-          uint8_t* buf = ebuf + b * EPI_BUF;
-          if (p.has_res) {
-            if (lane == 0 && c + 1 < nchunks) {
-              bulk_wait_read<0>();  // the other buffer's last store has read smem
-              mbar_arrive_expect_tx(&rb[b ^ 1], EPI_BUF);
-              tma_load_2d(&tmR, &rb[b ^ 1], ebuf + (b ^ 1) * EPI_BUF, n0 + (c + 1) * EPI_CHUNK, rows0);
-            }
-            mbar_wait(&rb[b], (ec >> 1) & 1);
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const uint4 u = *reinterpret_cast<const uint4*>(buf + swz64(lane, jj));
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float2 f = unpack_bf16x2(w4[h]);
-                v[jj * 8 + 2 * h] += f.x;
-                v[jj * 8 + 2 * h + 1] += f.y;
-              }
-            }
-          } else {
-            if (lane == 0) bulk_wait_read<1>();  // this buffer's store from two chunks ago has read smem
+        uint8_t* slot = slots + (ec % EPI_SLOTS) * EPI_SLOT;
+        if (res_tma) {
+          if (c + 1 < nchunks) cp_async_wait<1>();
+          else cp_async_wait<0>();
+          __syncwarp();  // every lane's pieces of this chunk are visible
+          if (c + 2 < nchunks) {
+            if (lane == 0) bulk_wait_read<1>();  // slot of chunk ec-2 has been read by its store
             __syncwarp();
+            prefetch_res(ec + 2, n0 + (c + 2) * EPI_CHUNK);
           }
-          if (p.relu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            uint4 o;
-            o.x = pack_bf16x2(v[jj * 8 + 0], v[jj * 8 + 1]);
-            o.y = pack_bf16x2(v[jj * 8 + 2], v[jj * 8 + 3]);
-            o.z = pack_bf16x2(v[jj * 8 + 4], v[jj * 8 + 5]);
-            o.w = pack_bf16x2(v[jj * 8 + 6], v[jj * 8 + 7]);
-            *reinterpret_cast<uint4*>(buf + swz64(lane, jj)) = o;
-          }
-          fence_proxy_async_smem();
+        } else if (tma) {
+          if (lane == 0) bulk_wait_read<3>();  // slot of chunk ec-4 has been read by its store
           __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmY, buf, n0 + c * EPI_CHUNK, rows0);
-            bulk_commit();
-          }
-        } else {
-          // direct-store fallback (fp32 logits / unaligned views)
-          const int m = rows0 + lane;
-          const int nb = n0 + c * EPI_CHUNK;
-          const int nv = min(EPI_CHUNK, p.cout - nb);
-          if (m < p.M) {
-            if (p.has_res) {
-              const __nv_bfloat16* rp = p.res + static_cast<size_t>(m) * p.res_cstride + p.res_coff + nb;
+        }
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < nv) v[i] += __bfloat162float(rp[i]);
+        for (int h = 0; h < 2; ++h) {  // two 32-column halves
+          uint32_t r[32];
+          tmem_ld32(taddr + c * EPI_CHUNK + h * 32, r);
+          tmem_ld_wait();
+          if (c == nchunks - 1 && h == 1) {  // accumulator drained: the MMA may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + sb[c * EPI_CHUNK + h * 32 + i];
+          if (tma) {
+            if (res_tma) {
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const uint4 u = *reinterpret_cast<const uint4*>(slot + swz<64>(lane, h * 4 + jj));
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                  const float2 f = unpack_bf16x2(w4[e2]);
+                  v[jj * 8 + 2 * e2] += f.x;
+                  v[jj * 8 + 2 * e2 + 1] += f.y;
+                }
+              }
             }
             if (p.relu) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
             }
-            const size_t yo = static_cast<size_t>(m) * p.y_cstride + p.y_coff + nb;
-            if (p.y_f32) {
-              float* yp = reinterpret_cast<float*>(p.y) + yo;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < nv) yp[i] = v[i];
-            } else {
-              __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(p.y) + yo;
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < nv) yp[i] = __float2bfloat16_rn(v[i]);
+            for (int jj = 0; jj < 4; ++jj) {
+              uint4 o;
+              o.x = pack_bf16x2(v[jj * 8 + 0], v[jj * 8 + 1]);
+              o.y = pack_bf16x2(v[jj * 8 + 2], v[jj * 8 + 3]);
+              o.z = pack_bf16x2(v[jj * 8 + 4], v[jj * 8 + 5]);
+              o.w = pack_bf16x2(v[jj * 8 + 6], v[jj * 8 + 7]);
+              *reinterpret_cast<uint4*>(slot + swz<64>(lane, h * 4 + jj)) = o;
             }
+          } else {
+            // direct-store fallback (fp32 logits / unaligned views)
+            const int m = rows0 + lane;
+            const int nb = n0 + c * EPI_CHUNK + h * 32;
+            const int nv = min(32, p.cout - nb);
+            if (m < p.M && nv > 0) {
+              if (p.has_res) {
+                const __nv_bfloat16* rp =
+                    reinterpret_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * p.res_cstride + nb;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < nv) v[i] += __bfloat162float(rp[i]);
+              }
+              if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+              }
+              const size_t yo = static_cast<size_t>(m) * p.y_cstride + p.y_coff + nb;
+              if (p.y_f32) {
+                float* yp = reinterpret_cast<float*>(p.y) + yo;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < nv) yp[i] = v[i];
+              } else {
+                __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(p.y) + yo;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < nv) yp[i] = __float2bfloat16_rn(v[i]);
+              }
+            }
+          }
+        }
+        if (tma) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, slot, n0 + c * EPI_CHUNK, rows0);
+            bulk_commit();
           }
         }
       }
     }
-    if (p.epi_tma && lane == 0) bulk_wait_all();
+    if (tma && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -403,8 +548,7 @@ int num_sms() {
 }
 
 template <int AMODE, int BK>
-int launch_conv(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmY, const CUtensorMap& tmR,
-                const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
+int launch_conv(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -412,27 +556,12 @@ int launch_conv(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMa
                                     227 * 1024);
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  const int threads = AMODE == A_GATHER ? 384 : 256;
-  conv_tc_kernel<AMODE, BK><<<grid, threads, smem, stream>>>(tmA, tmB, tmY, tmR, p);
+  conv_tc_kernel<AMODE, BK><<<grid, NUM_THREADS, smem, stream>>>(tmY, p);
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
 }
 
-int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : 64; }
-
-int encode_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                   uint32_t box_inner, uint32_t box_outer, int swizzle_bytes, const char* what) {
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(swizzle_bytes),
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode %s tensor map failed (%d)", what, (int)r);
-  apply_small_tensor_quirk(map, static_cast<size_t>(outer) * row_bytes);
-  return UB_OK;
-}
+int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : (cin_eff <= 32 ? 32 : 64); }
 
 }  // namespace
 }  // namespace ub
@@ -449,6 +578,8 @@ extern "C" int ub_conv_weight_layout(int cin, int coff, int gather, int* lead, i
   return UB_OK;
 }
 
+extern "C" int ub_conv_stem_kpad(int cin, int kh, int kw) { return (kh * kw * cin + 63) / 64 * 64; }
+
 extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   if (!d) return fail(UB_EINVAL, "ub_conv_fwd: null descriptor");
   if (!d->x || !d->w || !d->y) return fail(UB_EINVAL, "ub_conv_fwd: null x/w/y");
@@ -457,7 +588,8 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     return fail(UB_EINVAL, "ub_conv_fwd: bad geometry");
   if (d->Ho != (d->H + 2 * d->pad - d->kh) / d->stride + 1 || d->Wo != (d->W + 2 * d->pad - d->kw) / d->stride + 1)
     return fail(UB_EINVAL, "ub_conv_fwd: Ho/Wo inconsistent with kernel/stride/pad");
-  if (d->x_cstride % 8 || d->x_coff < 0 || (!d->gather_idx && d->x_coff + d->cin > d->x_cstride))
+  if (!d->x_nchw_f32 &&
+      (d->x_cstride % 8 || d->x_coff < 0 || (!d->gather_idx && d->x_coff + d->cin > d->x_cstride)))
     return fail(UB_EINVAL, "ub_conv_fwd: x channel stride must be a multiple of 8 and cover the read");
   if (!aligned16(d->x) || !aligned16(d->w) || !aligned16(d->y))
     return fail(UB_EINVAL, "ub_conv_fwd: x/w/y must be 16-byte aligned");
@@ -468,131 +600,123 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     return fail(UB_EINVAL, "ub_conv_fwd: residual channels exceed res_cstride");
   if (d->kh > 64 || d->kw > 64) return fail(UB_EUNSUPPORTED, "ub_conv_fwd: filter too large");
 
-  const bool gather = d->gather_idx != nullptr;
-  const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
+  const bool stem = d->x_nchw_f32 != 0;
+  const bool gather = d->gather_idx != nullptr && !stem;
   if (gather && d->x_coff % 8) return fail(UB_EINVAL, "ub_conv_fwd: gather base must be 8-aligned");
+  const int taps = d->kh * d->kw;
 
   int lead = 0, cpad = 0;
-  ub_conv_weight_layout(d->cin, d->x_coff, gather ? 1 : 0, &lead, &cpad);
+  if (stem) {
+    if (!d->gather_idx || d->x_channels < 1 || d->x_coff != 0)
+      return fail(UB_EINVAL, "ub_conv_fwd: stem mode needs gather_idx over x_channels input planes");
+    cpad = ub_conv_stem_kpad(d->cin, d->kh, d->kw);
+    if (cpad > MAX_STEM_K) return fail(UB_EUNSUPPORTED, "ub_conv_fwd: stem K %d > %d", cpad, MAX_STEM_K);
+  } else {
+    ub_conv_weight_layout(d->cin, d->x_coff, gather ? 1 : 0, &lead, &cpad);
+  }
   if (d->w_lead != lead || d->w_cpad != cpad)
     return fail(UB_EINVAL, "ub_conv_fwd: weight layout (lead %d, cpad %d) != expected (lead %d, cpad %d)", d->w_lead,
                 d->w_cpad, lead, cpad);
   const int cin_eff = d->cin + lead;
-  const int bk = gather ? 64 : pick_bk(cin_eff);
-  const int taps = d->kh * d->kw;
-  const int K_total = taps * cpad;
-  if (!encode_tiled_fn() || !encode_im2col_fn())
-    return fail(UB_ECUDA, "ub_conv_fwd: cannot resolve cuTensorMapEncode* entry points");
+  const int bk = (gather || stem) ? 64 : pick_bk(cin_eff);
 
   ConvKParams p{};
   p.M = d->N * d->Ho * d->Wo;
   p.cout = d->cout;
-  p.n_tiles = (d->cout + MAX_BLOCK_N - 1) / MAX_BLOCK_N;
-  // Multi-tile N: round to the epilogue's 32-channel chunk so a tile's last chunk never
-  // spills into the next tile's channels (the TMA store only clips at cout).
-  const int n_gran = p.n_tiles > 1 ? EPI_CHUNK : 16;
-  p.block_n = (((d->cout + p.n_tiles - 1) / p.n_tiles) + n_gran - 1) / n_gran * n_gran;
   p.m_tiles = (p.M + BLOCK_M - 1) / BLOCK_M;
-  p.cchunks = cpad / bk;
-  p.num_kb = taps * p.cchunks;
+  // N tiling: the widest tile (<= 256) unless that leaves SMs idle; then split N into
+  // more tiles until the grid fills.  Multi-tile N rounds to the epilogue's 64-channel
+  // chunk so a tile's last chunk never spills into the next tile's channels (the TMA
+  // store only clips at cout).
+  p.n_tiles = (d->cout + MAX_BLOCK_N - 1) / MAX_BLOCK_N;
+  while (static_cast<long long>(p.m_tiles) * p.n_tiles < num_sms() &&
+         (d->cout + p.n_tiles) / (p.n_tiles + 1) >= EPI_CHUNK)
+    ++p.n_tiles;
+  {
+    const int n_gran = p.n_tiles > 1 ? EPI_CHUNK : 16;
+    p.block_n = (((d->cout + p.n_tiles - 1) / p.n_tiles) + n_gran - 1) / n_gran * n_gran;
+    if (p.block_n > MAX_BLOCK_N) p.block_n = MAX_BLOCK_N;
+    p.n_tiles = (d->cout + p.block_n - 1) / p.block_n;
+  }
+  p.cchunks = stem ? 1 : cpad / bk;
+  p.num_kb = stem ? cpad / 64 : taps * p.cchunks;
   p.kw = d->kw;
   p.cpad = cpad;
+  p.K_total = stem ? cpad : taps * cpad;
+  p.cin_eff = cin_eff;
   p.H = d->H;
   p.W = d->W;
   p.Ho = d->Ho;
   p.Wo = d->Wo;
   p.stride = d->stride;
   p.pad = d->pad;
-  // two accumulators, each wide enough for the epilogue's 32-column chunks
-  const uint32_t acc_cols = (static_cast<uint32_t>(p.block_n) + 31u) & ~31u;
+  // two accumulators, each a whole number of 64-column epilogue chunks wide
+  const uint32_t acc_cols = (static_cast<uint32_t>(p.block_n) + EPI_CHUNK - 1) / EPI_CHUNK * EPI_CHUNK;
   uint32_t tc = 32;
   while (tc < 2u * acc_cols) tc <<= 1;
   p.tmem_cols = tc;
   p.acc_stride = tc / 2;
-  p.x = reinterpret_cast<const uint16_t*>(d->x);
+  p.x = stem ? nullptr : reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
   p.x_cstride = d->x_cstride;
-  p.x_coff = d->x_coff;
+  p.w = reinterpret_cast<const uint16_t*>(d->w);
   p.gidx = d->gather_idx;
-  p.n_gather = gather ? d->cin : 0;
+  p.n_gather = (gather || stem) ? d->cin : 0;
+  p.xf = stem ? static_cast<const float*>(d->x) : nullptr;
+  p.C_in = stem ? d->x_channels : 0;
+  p.k_real = stem ? taps * d->cin : 0;
   p.bias = d->bias;
   p.has_res = d->residual != nullptr;
   p.relu = d->relu;
-  p.res = reinterpret_cast<const __nv_bfloat16*>(d->residual);
+  p.res = reinterpret_cast<const uint16_t*>(d->residual) + (d->residual ? d->res_coff : 0);
   p.res_cstride = d->res_cstride;
-  p.res_coff = d->res_coff;
   p.y = d->y;
   p.y_cstride = d->y_cstride;
   p.y_coff = d->y_coff;
   p.y_f32 = d->y_dtype == UB_F32;
 
   const uint16_t* ybase = reinterpret_cast<const uint16_t*>(d->y) + d->y_coff;
-  const uint16_t* rbase = reinterpret_cast<const uint16_t*>(d->residual) + d->res_coff;
   p.epi_tma = !p.y_f32 && d->y_cstride % 8 == 0 && aligned16(ybase) &&
-              (!p.has_res || (d->res_cstride % 8 == 0 && aligned16(rbase)));
+              (!p.has_res || (d->res_cstride % 8 == 0 && aligned16(p.res)));
 
   const uint32_t a_bytes = BLOCK_M * bk * 2;
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
   const uint32_t stage_bytes = a_bytes + b_stride;
-  const uint32_t fixed = 1024 + 4 * 2 * EPI_BUF + 4 * MAX_BLOCK_N * 4 + 256;
+  const uint32_t fixed = 1024 + 4 * EPI_SLOTS * EPI_SLOT + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
+                         (stem ? MAX_STEM_K * sizeof(int4) : 0);
   const uint32_t budget = 226u * 1024u - fixed;
   int stages = static_cast<int>(budget / stage_bytes);
   stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
+  if (fixed + static_cast<size_t>(stages) * stage_bytes > 227u * 1024u)
+    return fail(UB_EUNSUPPORTED, "ub_conv_fwd: shared memory plan does not fit");
   p.stages = stages;
   const size_t smem = fixed + static_cast<size_t>(stages) * stage_bytes;
 
-  CUtensorMap tmA{}, tmB{}, tmY{}, tmR{};
-  int rc = encode_2d_bf16(&tmB, d->w, K_total, d->cout, static_cast<uint64_t>(K_total) * 2, bk, p.block_n, bk * 2,
-                          "B (weights)");
-  if (rc) return rc;
+  if (!encode_tiled_fn()) return fail(UB_ECUDA, "ub_conv_fwd: cannot resolve cuTensorMapEncodeTiled");
+  CUtensorMap tmY{};
   if (p.epi_tma) {
-    rc = encode_2d_bf16(&tmY, ybase, d->cout, p.M, static_cast<uint64_t>(d->y_cstride) * 2, EPI_CHUNK, 32, 64, "Y");
-    if (rc) return rc;
-    if (p.has_res) {
-      rc = encode_2d_bf16(&tmR, rbase, d->cout, p.M, static_cast<uint64_t>(d->res_cstride) * 2, EPI_CHUNK, 32, 64,
-                          "residual");
-      if (rc) return rc;
-    } else {
-      tmR = tmY;
-    }
-  } else {
-    tmY = tmB;
-    tmR = tmB;
-  }
-  const uint16_t* xbase = reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
-  const size_t x_footprint = static_cast<size_t>(d->N) * d->H * d->W * d->x_cstride * 2;
-  int amode;
-  if (gather) {
-    amode = A_GATHER;
-    tmA = tmB;  // unused by the kernel in gather mode
-  } else if (pointwise) {
-    amode = A_TILED;
-    rc = encode_2d_bf16(&tmA, xbase, cin_eff, p.M, static_cast<uint64_t>(d->x_cstride) * 2, bk, BLOCK_M, bk * 2,
-                        "A (tiled)");
-    if (rc) return rc;
-    apply_small_tensor_quirk(&tmA, x_footprint);
-  } else {
-    amode = A_IM2COL;
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(cin_eff), static_cast<cuuint64_t>(d->W),
-                          static_cast<cuuint64_t>(d->H), static_cast<cuuint64_t>(d->N)};
-    const cuuint64_t cs = static_cast<cuuint64_t>(d->x_cstride) * 2;
-    cuuint64_t strides[3] = {cs, cs * d->W, cs * d->W * d->H};
-    int lower[2] = {-d->pad, -d->pad};
-    int upper[2] = {d->pad - (d->kw - 1), d->pad - (d->kh - 1)};
-    cuuint32_t es[4] = {1, static_cast<cuuint32_t>(d->stride), static_cast<cuuint32_t>(d->stride), 1};
-    CUresult r = encode_im2col_fn()(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(xbase), dims,
-                                    strides, lower, upper, static_cast<cuuint32_t>(bk), BLOCK_M, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(bk * 2),
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode A (im2col) tensor map failed (%d)", (int)r);
-    apply_small_tensor_quirk(&tmA, x_footprint);
+    // output: [M][cout] view at y + y_coff, row pitch y_cstride; box 64 channels x 32 rows
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(d->cout), static_cast<cuuint64_t>(p.M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(d->y_cstride) * 2};
+    cuuint32_t box[2] = {EPI_CHUNK, 32};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_tiled_fn()(&tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(ybase), dims,
+                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode output tensor map failed (%d)", (int)r);
+    apply_small_tensor_quirk(&tmY, static_cast<size_t>(p.M) * d->y_cstride * 2);
   }
 
   const int num_tiles = p.m_tiles * p.n_tiles;
   const int grid = num_tiles < num_sms() ? num_tiles : num_sms();
-  if (amode == A_GATHER) return launch_conv<A_GATHER, 64>(tmA, tmB, tmY, tmR, p, grid, smem, stream);
-  if (amode == A_TILED)
-    return bk == 64 ? launch_conv<A_TILED, 64>(tmA, tmB, tmY, tmR, p, grid, smem, stream)
-                    : launch_conv<A_TILED, 16>(tmA, tmB, tmY, tmR, p, grid, smem, stream);
-  return bk == 64 ? launch_conv<A_IM2COL, 64>(tmA, tmB, tmY, tmR, p, grid, smem, stream)
-                  : launch_conv<A_IM2COL, 16>(tmA, tmB, tmY, tmR, p, grid, smem, stream);
+  if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream);
+  if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream);
+  const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
+  if (pointwise) {
+    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, p, grid, smem, stream);
+    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, p, grid, smem, stream);
+    return launch_conv<A_TILED, 16>(tmY, p, grid, smem, stream);
+  }
+  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, p, grid, smem, stream);
+  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, p, grid, smem, stream);
+  return launch_conv<A_IM2COL, 16>(tmY, p, grid, smem, stream);
 }

@@ -40,6 +40,12 @@ __global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps
       long long rc = e / taps;
       c = static_cast<int>(rc % n_cols);
       r = static_cast<int>(rc / n_cols);
+    } else if (LAYOUT == UB_LAYOUT_GEMM_DENSE) {  // [r][k], k = t * n_cols + c
+      const int k = static_cast<int>(e % cpad);
+      r = static_cast<int>(e / cpad);
+      t = k / n_cols;
+      c = k - t * n_cols;
+      inside = t < taps;
     } else {  // [r][t][k], column c at k = lead + c
       const int k = static_cast<int>(e % cpad);
       long long rt = e / cpad;
@@ -69,15 +75,19 @@ template <typename TI, typename TO>
 int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows, int n_rows, const int32_t* cols,
                             int n_cols, const float* scale, int layout, int lead, int cpad, void* out,
                             cudaStream_t s) {
-  const long long total = layout == UB_LAYOUT_OIHW ? (long long)n_rows * n_cols * taps
-                                                   : (long long)n_rows * taps * cpad;
+  const long long total = layout == UB_LAYOUT_OIHW    ? (long long)n_rows * n_cols * taps
+                          : layout == UB_LAYOUT_GEMM ? (long long)n_rows * taps * cpad
+                                                     : (long long)n_rows * cpad;
   const int block = 256;
   const int grid = grid_for(total, block, 4);
   if (layout == UB_LAYOUT_OIHW)
     permute_weights_kernel<TI, TO, UB_LAYOUT_OIHW><<<grid, block, 0, s>>>(
         static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
-  else
+  else if (layout == UB_LAYOUT_GEMM)
     permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM><<<grid, block, 0, s>>>(
+        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+  else
+    permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM_DENSE><<<grid, block, 0, s>>>(
         static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   count_launch();
   return cuda_status(cudaGetLastError(), "permute_weights_kernel");
@@ -152,15 +162,14 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H
                                int x_coff, int k, int stride, int pad, int Ho, int Wo, __nv_bfloat16* __restrict__ y,
                                int y_cstride, int y_coff, bool vec) {
   const int groups = (C + 7) / 8;
-  const long long total = (long long)N * Ho * Wo * groups;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int g = static_cast<int>(e % groups);
-    long long pix = e / groups;
-    const int wo = static_cast<int>(pix % Wo);
-    const long long t = pix / Wo;
-    const int ho = static_cast<int>(t % Ho);
-    const long long img = t / Ho;
+  const int total = N * Ho * Wo * groups;  // < 2^31 (checked by the host)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int g = e % groups;
+    const int pix = e / groups;
+    const int wo = pix % Wo;
+    const int t = pix / Wo;
+    const int ho = t % Ho;
+    const int img = t / Ho;
     const int c0 = g * 8;
     const int nc = min(8, C - c0);
     float m[8];
@@ -172,7 +181,7 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H
       for (int s = 0; s < k; ++s) {
         const int wi = wo * stride - pad + s;
         if (wi < 0 || wi >= W) continue;
-        const __nv_bfloat16* xp = x + ((img * H + hi) * W + wi) * x_cstride + x_coff + c0;
+        const __nv_bfloat16* xp = x + (static_cast<size_t>(img * H + hi) * W + wi) * x_cstride + x_coff + c0;
         if (vec && nc == 8) {
           const uint4 u = __ldg(reinterpret_cast<const uint4*>(xp));
           const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
@@ -187,7 +196,7 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H
         }
       }
     }
-    __nv_bfloat16* yp = y + pix * y_cstride + y_coff + c0;
+    __nv_bfloat16* yp = y + static_cast<size_t>(pix) * y_cstride + y_coff + c0;
     if (vec && nc == 8) {
       uint4 o;
       o.x = pack_bf16x2(m[0], m[1]);
@@ -245,7 +254,10 @@ extern "C" int ub_permute_weights(const void* W, int dtype_in, int O, int I, int
   if (!W || !rows || !cols || !out) return fail(UB_EINVAL, "ub_permute_weights: null pointer");
   if (O < 1 || I < 1 || kh < 1 || kw < 1 || n_rows < 1 || n_cols < 1)
     return fail(UB_EINVAL, "ub_permute_weights: bad sizes");
-  if (layout != UB_LAYOUT_OIHW && layout != UB_LAYOUT_GEMM) return fail(UB_EINVAL, "ub_permute_weights: layout");
+  if (layout != UB_LAYOUT_OIHW && layout != UB_LAYOUT_GEMM && layout != UB_LAYOUT_GEMM_DENSE)
+    return fail(UB_EINVAL, "ub_permute_weights: layout");
+  if (layout == UB_LAYOUT_GEMM_DENSE && kh * kw * n_cols > cpad)
+    return fail(UB_EINVAL, "ub_permute_weights: dense K %d > cpad %d", kh * kw * n_cols, cpad);
   if (layout == UB_LAYOUT_GEMM && (lead < 0 || lead + n_cols > cpad))
     return fail(UB_EINVAL, "ub_permute_weights: lead + n_cols > cpad");
   const int taps = kh * kw;
@@ -313,6 +325,7 @@ extern "C" int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cst
   const bool vec = aligned16(x) && aligned16(y) && (x_cstride % 8 == 0) && (x_coff % 8 == 0) &&
                    (y_cstride % 8 == 0) && (y_coff % 8 == 0);
   const long long total = (long long)N * Ho * Wo * ((C + 7) / 8);
+  if (total >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_maxpool2d: tensor too large");
   maxpool_kernel<<<grid_for(total, 256), 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(x), N, H, W, C, x_cstride, x_coff, k, stride, pad, Ho, Wo,
       static_cast<__nv_bfloat16*>(y), y_cstride, y_coff, vec);

@@ -178,3 +178,21 @@ UB_DEVI void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "memory");
 }
 }  // namespace ub
+
+namespace ub {
+// ---------------------------------------------------------------- cp.async (LSU) producers
+// 16-byte async copy global -> shared; src_bytes = 0 zero-fills the destination.
+UB_DEVI void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+UB_DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+UB_DEVI void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Arrive on `bar` once all prior cp.async of this thread have landed (no pending-count increment).
+UB_DEVI void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+}  // namespace ub

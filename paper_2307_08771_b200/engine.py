@@ -60,8 +60,9 @@ class Engine:
     """
 
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
-                 input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused"):
+                 input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True):
         assert gather_mode in ("fused", "copy")
+        self.fuse_stem = fuse_stem
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -184,6 +185,22 @@ class Engine:
                 succ = g.successors(lid)
                 idx = None
                 out = lid
+                # fused stem: the only reader of the model input is one spatial conv (directly or
+                # through its GATHER read) -> im2col from the fp32 input inside the conv kernel
+                stem_op = None
+                for op in ops:
+                    if op.kind == "conv" and op.info["src"] == lid and self.specs[op.anchor].op == "conv":
+                        stem_op = op
+                if stem_op is not None and len(succ) == 1 and self.fuse_stem:
+                    rd = stem_op.info["read"]
+                    if rd is not None and kinds[rd] is LayerKind.GATHER:
+                        stem_op.info["stem_idx"] = g.layer(rd).params
+                    elif rd is None:
+                        stem_op.info["stem_idx"] = tuple(range(g.layer(lid).out_channels))
+                    if "stem_idx" in stem_op.info:
+                        stem_op.info["read"] = None
+                        stem_op.inputs = []
+                        continue
                 if len(succ) == 1 and kinds[succ[0]] is LayerKind.GATHER:
                     idx = g.layer(succ[0]).params
                     out = succ[0]
@@ -336,6 +353,8 @@ class Engine:
         lid = info["conv"]
         spec = self.specs[lid]
         lay = self.graph.layer(lid)
+        if "stem_idx" in info:
+            return self._bind_stem(op, ws, vs, output_feed)
         x = self._value(info["src"])
         read = info["read"]
         gather_idx = None
@@ -379,6 +398,39 @@ class Engine:
         byts = 2.0 * (cin * x.H * x.W + cout * ho * wo) + (2.0 * cout * cin * kk * kk) / self.batch
         if residual is not None:
             byts += 2.0 * cout * ho * wo
+        self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
+
+    def _bind_stem(self, op, ws, vs, output_feed):
+        info = op.info
+        lid = info["conv"]
+        spec = self.specs[lid]
+        lay = self.graph.layer(lid)
+        idx = info["stem_idx"]
+        idx_dev = self._i32(idx)
+        cin = len(idx)
+        assert cin == lay.in_channels
+        kpad = _lib.conv_stem_kpad(cin, spec.kernel, spec.kernel)
+        W, rows, cols = ws(lid)
+        scale = bias = None
+        if info["bn"] is not None:
+            vec, perm = vs(info["bn"])
+            scale, bias = self._affine(info["bn"], vec, perm)
+            if self.specs[info["bn"]].op != "bn":
+                scale = None
+        O, I = W.shape[0], W.shape[1]
+        rows = rows if rows is not None else range(O)
+        cols = cols if cols is not None else range(I)
+        wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=kpad, out_dtype=torch.bfloat16)
+        self._keep.append(wg)
+        assert info.get("residual") is None and info["out"] not in output_feed
+        y = self._alloc(info["out"], lay.out_channels)
+        relu = info["relu"] is not None
+        x = self.input_buf
+        cout, kk, st, pd = lay.out_channels, spec.kernel, spec.stride, spec.pad
+        op.launch = lambda: K.conv_stem(x, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
+        ci, hi, wi = self.input_chw
+        flops = 2.0 * cout * cin * kk * kk * y.H * y.W
+        byts = 4.0 * ci * hi * wi + 2.0 * cout * y.H * y.W + (2.0 * cout * kpad) / self.batch
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
     # ------------------------------------------------------------------ execution

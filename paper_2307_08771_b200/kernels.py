@@ -87,6 +87,9 @@ def permute_weights(W: torch.Tensor, rows, cols, row_scale: torch.Tensor | None 
     if layout == "oihw":
         out = torch.empty((nr, nc, kh, kw), dtype=out_dtype, device=W.device)
         lay = _lib.UB_LAYOUT_OIHW
+    elif layout == "dense":
+        out = torch.empty((nr, cpad), dtype=out_dtype, device=W.device)
+        lay = _lib.UB_LAYOUT_GEMM_DENSE
     else:
         out = torch.empty((nr, kh * kw, cpad), dtype=out_dtype, device=W.device)
         lay = _lib.UB_LAYOUT_GEMM
@@ -132,6 +135,30 @@ def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: 
     d.relu = int(relu)
     d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
     d.y_dtype = _lib.UB_F32 if y_fp32 else _lib.UB_BF16
+    _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
+
+
+def conv_stem(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, kpad: int, cout: int, k: int,
+              stride: int, pad: int, y: Act, bias: torch.Tensor | None = None, relu: bool = False) -> None:
+    """Fused stem: im2col straight from the fp32 NCHW model input with the INPUT
+    node's GATHER (idx_dev) applied on the fly; w is UB_LAYOUT_GEMM_DENSE."""
+    N, C, H, W = x_nchw.shape
+    Ho = (H + 2 * pad - k) // stride + 1
+    Wo = (W + 2 * pad - k) // stride + 1
+    assert y.N == N and y.H == Ho and y.W == Wo, "output geometry mismatch"
+    d = _lib.ConvDesc()
+    d.N, d.H, d.W = N, H, W
+    d.cin = idx_dev.numel()
+    d.cout = cout
+    d.kh, d.kw, d.stride, d.pad, d.Ho, d.Wo = k, k, stride, pad, Ho, Wo
+    d.x, d.x_cstride, d.x_coff = x_nchw.data_ptr(), 0, 0
+    d.gather_idx = idx_dev.data_ptr()
+    d.w, d.w_lead, d.w_cpad = w.data_ptr(), 0, kpad
+    d.bias = bias.data_ptr() if bias is not None else None
+    d.relu = int(relu)
+    d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
+    d.y_dtype = _lib.UB_BF16
+    d.x_nchw_f32, d.x_channels = 1, C
     _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
 
 

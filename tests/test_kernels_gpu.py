@@ -103,6 +103,26 @@ def test_conv_matches_torch(case):
         assert torch.isnan(y.buf[:, :16].float()).all()
 
 
+@pytest.mark.parametrize("N,cin,idx", [(1, 2, [2, 0]), (3, 3, [0, 1, 2]), (2, 1, [1])])
+def test_stem_matches_torch(N, cin, idx):
+    """Fused stem: fp32 NCHW input, channel GATHER, 7x7/s2 im2col in the producer warps."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(N * 10 + cin)
+    x = torch.randn(N, 3, 224, 224, generator=g)
+    Wt = torch.randn(64, cin, 7, 7, generator=g) / (cin * 49) ** 0.5
+    bias = torch.randn(64, generator=g)
+    kpad = _lib.conv_stem_kpad(cin, 7, 7)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(64)), list(range(cin)), layout="dense", cpad=kpad,
+                           out_dtype=torch.bfloat16)
+    y = K.empty_act(N, 112, 112, 64, dev)
+    K.conv_stem(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), wg, kpad, 64, 7, 2, 3, y,
+                bias=bias.to(dev), relu=True)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(_bf(x[:, idx]), _bf(Wt), stride=2, padding=3) + bias.view(1, -1, 1, 1)
+    ref = ref.clamp_min(0)
+    assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
 def test_permute_weights_bit_exact():
     dev = "cuda"
     g = torch.Generator().manual_seed(0)
