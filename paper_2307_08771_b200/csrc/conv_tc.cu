@@ -10,26 +10,30 @@
 //     layer's tensor into swizzled shared memory -- the copy the baseline
 //     export materialises never touches HBM;
 //   * PER_CHANNEL bias (BN shift; the scale is folded into the weight rows at
-//     export), ADD residual, ReLU, and a channel-offset store (CONCAT without a
-//     copy).
+//     export): written into the TMEM accumulator before the first MMA;
+//   * ADD residual (interp.py:64-65): extra "identity" K-blocks -- the residual
+//     tile is the A operand and a 64x64 identity the B operand, so the tensor
+//     core adds it exactly in fp32;
+//   * ReLU (interp.py:68-69): folded into the fp32 -> bf16x2 conversion;
+//   * channel-offset store: CONCAT without a copy (interp.py:66-67).
 //
 // GEMM view: D[M = N*Ho*Wo pixels][cout] = A[M][K] * B[cout][K]^T, K = taps*cpad.
 // Tile 128 pixels x block_n channels (block_n <= 256, runtime).
 //
-// Data movement is chosen by measurement (tools/tma_probe.cu on B200): a TMA
-// LOAD costs ~10 SM cycles per box row (<= 128 B rows), capping 128-byte-row
-// loads near 3.7 TB/s chip-wide, while cp.async from 8 producer warps and TMA
-// STORES (~6.4 cycles/row) keep up with HBM.  So operands and the residual
-// come in by cp.async (completion tracked on mbarriers), outputs leave by TMA
-// bulk tensor store.
+// Data movement follows measurements on B200 (tools/tma_probe.cu): TMA LOADS
+// cost ~10 SM cycles per box row, so operands come in by cp.async from the
+// producer warps (completion tracked on mbarriers); TMA STORES (~6 cycles per
+// 128-byte row) carry the output.  The epilogue does ~0.7 instructions per
+// output element: TMEM load, one cvt(+relu) per pair, 16-byte smem stores.
 //
 // Persistent, warp-specialised, one CTA (512 threads) per SM:
 //   warp 1      MMA issuer: tcgen05.mma into one of TWO TMEM accumulators, so the
 //               epilogue of tile i overlaps the mainloop of tile i+1
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: TMEM -> regs (+bias, +residual, ReLU) -> swizzled smem
-//               -> TMA store (residual prefetched by cp.async two chunks ahead)
-//   warps 8-15  producers: A (tiled / im2col / gathered / fp32 stem) and B tiles
+//   warps 4-7   epilogue: TMEM -> regs -> cvt(+relu) -> swizzled smem -> TMA store;
+//               re-arms the drained accumulator with the bias of tile i+2
+//   warps 8-15  producers: A (tiled / im2col / gathered / fp32 stem / residual), B
+#include <cstdlib>
 #include <mutex>
 
 #include "ub_common.cuh"
@@ -46,7 +50,8 @@ constexpr int NUM_THREADS = 512;
 constexpr int PRODUCERS = 256;                // warps 8-15
 constexpr int EPI_CHUNK = 64;                 // output channels per epilogue chunk (128-byte rows)
 constexpr int EPI_SLOT = 32 * EPI_CHUNK * 2;  // one warp's 32 rows x 64 ch bf16 (4 KB)
-constexpr int EPI_SLOTS = 4;                  // per warp: residual lands / output leaves in place
+constexpr int EPI_WARP_BYTES = 2 * EPI_SLOT;  // two output slots per epilogue warp
+constexpr int IDENT_BYTES = 64 * 128;         // 64x64 bf16 identity (SWIZZLE_128B, K-major)
 constexpr int MAX_BLOCK_N = 256;
 constexpr int BAR_BYTES = 512;   // mbarriers + TMEM slot region
 constexpr int MAX_STEM_K = 512;  // dense-K stem: taps * channels, padded to 64
@@ -55,7 +60,7 @@ struct ConvKParams {
   int M;        // output pixels (GEMM M)
   int cout;     // output channels (GEMM N)
   int block_n;  // N tile
-  int num_kb;   // k-blocks per tile
+  int num_kb;   // main k-blocks per tile
   int cchunks;  // channel chunks per tap
   int kw;       // filter width
   int cpad;     // per-tap weight K
@@ -81,6 +86,7 @@ struct ConvKParams {
   int res_cstride;
   void* y;  // direct-store fallback only
   int y_cstride, y_coff, y_f32;
+  int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -96,6 +102,10 @@ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t j) {
   else return r * 32 + ((j ^ ((r >> 2) & 1)) << 4);
 }
 
+__device__ __forceinline__ int tile_res_chunks(const ConvKParams& p, int n0) {
+  return p.has_res ? (min(p.block_n, p.cout - n0) + EPI_CHUNK - 1) / EPI_CHUNK : 0;
+}
+
 template <int AMODE, int BK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const ConvKParams p) {
@@ -103,7 +113,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = align1024(smem_raw);
   constexpr uint32_t ROW_BYTES = BK * 2;
   constexpr int CPR = ROW_BYTES / 16;  // 16-byte chunks per operand row
-  constexpr uint32_t A_BYTES = BLOCK_M * ROW_BYTES;
+  // A stages are sized for max(BK, 64) columns: residual k-blocks are always 64 wide
+  constexpr uint32_t A_BYTES = BLOCK_M * 128;
   constexpr uint32_t SBO = 8 * ROW_BYTES;
   constexpr uint32_t LAYOUT = (BK == 64) ? 2u : (BK == 32 ? 4u : 6u);  // SWIZZLE_128B / 64B / 32B
   const uint32_t b_bytes = static_cast<uint32_t>(p.block_n) * ROW_BYTES;
@@ -112,8 +123,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_BYTES;
-  uint8_t* sE = sB + stages * b_stride;                                    // 4 warps x EPI_SLOTS x 4 KB
-  float* sBias = reinterpret_cast<float*>(sE + 4 * EPI_SLOTS * EPI_SLOT);  // 4 warps x MAX_BLOCK_N
+  uint8_t* sI = sB + stages * b_stride;                         // identity 64x64 (8 KB)
+  uint8_t* sE = sI + IDENT_BYTES;                               // 4 warps x 2 output slots
+  float* sBias = reinterpret_cast<float*>(sE + 4 * EPI_WARP_BYTES);  // 4 warps x MAX_BLOCK_N
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + 4 * MAX_BLOCK_N);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // [2]
@@ -139,6 +151,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 3) {  // identity B operand for the residual k-blocks: row n has 1.0 in column n
+    for (int i = lane; i < IDENT_BYTES / 16; i += 32) {
+      const int r = i >> 3, j = i & 7;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if ((r >> 3) == j) {
+        const uint32_t one = 0x3F80u << (16 * (r & 1));  // bf16 1.0 in the right half
+        const int word = (r & 7) >> 1;
+        if (word == 0) v.x = one;
+        else if (word == 1) v.y = one;
+        else if (word == 2) v.z = one;
+        else v.w = one;
+      }
+      *reinterpret_cast<uint4*>(sI + swz<64>(r, j)) = v;
+    }
+    fence_proxy_async_smem();
+  }
   if constexpr (AMODE == A_STEM) {
     // k -> (input offset relative to the window origin, filter row r, filter col s); k >= k_real: r = -1
     for (int k = threadIdx.x; k < p.num_kb * 64; k += blockDim.x) {
@@ -160,25 +188,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 1) {
     if (lane == 0) {
-      // ================= MMA issuer
+      // ================= MMA issuer (accumulators arrive pre-loaded with the bias)
       const uint32_t idesc = make_idesc_bf16(BLOCK_M, static_cast<uint32_t>(p.block_n));
+      const uint32_t idesc_res = make_idesc_bf16(BLOCK_M, EPI_CHUNK);
+      const uint32_t i_base = smem_u32(sI);
       int s = 0, it = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
-        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        const int n0 = (t % p.n_tiles) * p.block_n;
+        const int nres = tile_res_chunks(p, n0);
+        mbar_wait(&tempty[acc], (it >> 1) & 1);  // drained and re-armed with this tile's bias
         tc_fence_after();
         const uint32_t d = tmem_base + acc * p.acc_stride;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = 0; kb < nk + nres; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           fence_proxy_async_smem();  // generic-proxy (cp.async / st.shared) writes -> tensor-core reads
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-          const uint32_t b_base = smem_u32(sB + s * b_stride);
+          if (!(p.dbg & 4)) {
+            if (kb < nk) {
+              const uint32_t b_base = smem_u32(sB + s * b_stride);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT), idesc,
-                      (kb | k) != 0 ? 1u : 0u);
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT),
+                          idesc, 1u);
+            } else {  // residual chunk rc: D[:, rc*64 : rc*64+64] += R_rc * I
+              const uint32_t dc = d + (kb - nk) * EPI_CHUNK;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                umma_bf16(dc, make_sdesc(a_base + k * 32, 1024, 2), make_sdesc(i_base + k * 32, 1024, 2), idesc_res,
+                          1u);
+            }
           }
           umma_commit(&empty[s]);
           if (++s == stages) {
@@ -203,12 +244,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t dst0 = swz<BK>(row0, cj);  // + i * ROW_STEP * ROW_BYTES for chunk i (swizzle-invariant)
     const int nb_pieces = (p.block_n + ROW_STEP - 1) / ROW_STEP;  // B chunks per thread (upper bound)
     const size_t b_row_stride = static_cast<size_t>(ROW_STEP) * p.K_total;
+    // residual k-blocks: 64-channel rows; this thread owns rows pt/8 + 32 i, chunk pt%8
+    const int rrow0 = pt >> 3, rj = pt & 7;
+    const uint32_t rdst0 = swz<64>(rrow0, rj);
     int s = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
       const int m0 = m_tile * BLOCK_M;
+      const int nres = tile_res_chunks(p, n0);
       // A geometry of this thread's rows: pixel base pointer + top-left window coordinate
       const uint16_t* a_base[A_PER_THREAD];
       int a_hb[A_PER_THREAD], a_wb[A_PER_THREAD];
@@ -366,20 +411,78 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      // ---- residual k-blocks: A = residual[m0 : m0+128, n0 + rc*64 : +64], B = identity
+      for (int rc = 0; rc < nres; ++rc) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t tileA = smem_u32(sA + s * A_BYTES);
+        const int ch = n0 + rc * EPI_CHUNK + rj * 8;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int m = m0 + rrow0 + 32 * i;
+          const bool ok = m < p.M && ch < p.cout;
+          const uint16_t* src = ok ? p.res + static_cast<size_t>(m) * p.res_cstride + ch : p.res;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileA + rdst0 + i * 32 * 128), "l"(src),
+                       "r"(ok ? 16u : 0u)
+                       : "memory");
+        }
+        if constexpr (reg_mode(AMODE)) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
+        }
+        cp_async_arrive_noinc(&full[s]);
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
     }
     cp_async_wait<0>();
   } else if (warp >= 4) {
     // ================= epilogue
-    // Warp q owns rows q*32..q*32+31 of the tile and walks 64-channel chunks.  The residual
-    // chunk lands by cp.async (two chunks ahead, the first ones during the mainloop) in a
-    // slot of a 4-slot ring; the output is written back into the same slot and leaves by
-    // TMA store, whose read-completion frees the slot four chunks later.
+    // Warp q owns TMEM lanes / tile rows q*32..q*32+31 and walks 64-channel chunks.  After
+    // draining a 32-column half it re-arms those accumulator columns with the bias of the
+    // tile that will use this accumulator next (tile i+2).
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint8_t* slots = sE + q * EPI_SLOTS * EPI_SLOT;
+    uint8_t* oslots = sE + q * EPI_WARP_BYTES;
     float* sb = sBias + q * MAX_BLOCK_N;
-    uint32_t ec = 0;  // chunks processed by this warp so far (= TMA stores committed)
-    int it = 0;
     const bool tma = p.epi_tma;
+    uint32_t ec = 0;  // chunks processed by this warp (= TMA stores committed)
+    // bias of tile tt -> sb (zero past cout), columns [0, width)
+    auto stage_bias = [&](int tt) {
+      const int nn0 = (tt % p.n_tiles) * p.block_n;
+      const int width = static_cast<int>(p.acc_stride);
+      __syncwarp();
+      for (int i = lane; i < width; i += 32)
+        sb[i] = (p.bias && i < p.block_n && nn0 + i < p.cout) ? __ldg(p.bias + nn0 + i) : 0.f;
+      __syncwarp();
+    };
+    // write sb[col0 .. col0+32) into TMEM columns (all 32 lanes of this warp's quarter)
+    auto arm32 = [&](uint32_t taddr, int col0) {
+      uint32_t bv[32];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 f = *reinterpret_cast<const float4*>(sb + col0 + i);
+        bv[i] = __float_as_uint(f.x);
+        bv[i + 1] = __float_as_uint(f.y);
+        bv[i + 2] = __float_as_uint(f.z);
+        bv[i + 3] = __float_as_uint(f.w);
+      }
+      tmem_st32(taddr, bv);
+    };
+    // initial arming of both accumulators (tiles blockIdx.x and blockIdx.x + gridDim.x)
+    for (int a = 0; a < 2; ++a) {
+      const int tt = blockIdx.x + a * gridDim.x;
+      if (tt < num_tiles) {
+        stage_bias(tt);
+        const uint32_t ta = tmem_base + a * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+        for (int col = 0; col < static_cast<int>(p.acc_stride); col += 32) arm32(ta + col, col);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+    int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
@@ -387,104 +490,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int rows0 = m0 + q * 32;
       const int ncols = min(p.block_n, p.cout - n0);
       const int nchunks = (ncols + EPI_CHUNK - 1) / EPI_CHUNK;
-      __syncwarp();
-      for (int i = lane; i < nchunks * EPI_CHUNK; i += 32) sb[i] = (p.bias && i < ncols) ? __ldg(p.bias + n0 + i) : 0.f;
-      const bool res_tma = tma && p.has_res;
-      auto prefetch_res = [&](uint32_t e, int n_ch) {
-        uint8_t* slot = slots + (e % EPI_SLOTS) * EPI_SLOT;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {  // 32 rows x 8 chunks = 256 pieces, 8 per lane
-          const int row = (lane >> 3) + 4 * i;
-          const int j = lane & 7;
-          const int m = rows0 + row;
-          const bool ok = m < p.M && n_ch + j * 8 < p.cout;
-          const uint16_t* src = ok ? p.res + static_cast<size_t>(m) * p.res_cstride + n_ch + j * 8 : p.res;
-          cp_async16(slot + swz<64>(row, j), src, ok ? 16u : 0u);
-        }
-        cp_async_commit();
-      };
-      if (res_tma) {  // chunks 0 and 1 fly while the mainloop runs
-        if (lane == 0) bulk_wait_read<2>();  // slots of chunks ec-4 / ec-3 were read by their stores
-        __syncwarp();
-        for (int c = 0; c < 2 && c < nchunks; ++c) prefetch_res(ec + c, n0 + c * EPI_CHUNK);
-      }
-      __syncwarp();
+      const int t_next = t + 2 * gridDim.x;  // next user of this accumulator
+      const bool rearm = t_next < num_tiles;
+      if (rearm) stage_bias(t_next);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c, ++ec) {
-        uint8_t* slot = slots + (ec % EPI_SLOTS) * EPI_SLOT;
-        if (res_tma) {
-          if (c + 1 < nchunks) cp_async_wait<1>();
-          else cp_async_wait<0>();
-          __syncwarp();  // every lane's pieces of this chunk are visible
-          if (c + 2 < nchunks) {
-            if (lane == 0) bulk_wait_read<1>();  // slot of chunk ec-2 has been read by its store
-            __syncwarp();
-            prefetch_res(ec + 2, n0 + (c + 2) * EPI_CHUNK);
-          }
-        } else if (tma) {
-          if (lane == 0) bulk_wait_read<3>();  // slot of chunk ec-4 has been read by its store
-          __syncwarp();
-        }
+        uint8_t* oslot = oslots + (ec & 1) * EPI_SLOT;
+        if (tma && lane == 0) bulk_wait_read<1>();  // this slot's store from 2 chunks ago has read it
+        __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // two 32-column halves
+          const int col = c * EPI_CHUNK + h * 32;
           uint32_t r[32];
-          tmem_ld32(taddr + c * EPI_CHUNK + h * 32, r);
+          tmem_ld32(taddr + col, r);
           tmem_ld_wait();
-          if (c == nchunks - 1 && h == 1) {  // accumulator drained: the MMA may reuse it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) + sb[c * EPI_CHUNK + h * 32 + i];
+          if (rearm) arm32(taddr + col, col);
           if (tma) {
-            if (res_tma) {
+            if (!(p.dbg & 2)) {
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) {
-                const uint4 u = *reinterpret_cast<const uint4*>(slot + swz<64>(lane, h * 4 + jj));
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                  const float2 f = unpack_bf16x2(w4[e2]);
-                  v[jj * 8 + 2 * e2] += f.x;
-                  v[jj * 8 + 2 * e2 + 1] += f.y;
+                uint4 o;
+                const float* f = reinterpret_cast<const float*>(r) + jj * 8;
+                if (p.relu) {
+                  o.x = cvt_relu_bf16x2(f[0], f[1]);
+                  o.y = cvt_relu_bf16x2(f[2], f[3]);
+                  o.z = cvt_relu_bf16x2(f[4], f[5]);
+                  o.w = cvt_relu_bf16x2(f[6], f[7]);
+                } else {
+                  o.x = cvt_bf16x2(f[0], f[1]);
+                  o.y = cvt_bf16x2(f[2], f[3]);
+                  o.z = cvt_bf16x2(f[4], f[5]);
+                  o.w = cvt_bf16x2(f[6], f[7]);
                 }
+                *reinterpret_cast<uint4*>(oslot + swz<64>(lane, h * 4 + jj)) = o;
               }
-            }
-            if (p.relu) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-            }
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              uint4 o;
-              o.x = pack_bf16x2(v[jj * 8 + 0], v[jj * 8 + 1]);
-              o.y = pack_bf16x2(v[jj * 8 + 2], v[jj * 8 + 3]);
-              o.z = pack_bf16x2(v[jj * 8 + 4], v[jj * 8 + 5]);
-              o.w = pack_bf16x2(v[jj * 8 + 6], v[jj * 8 + 7]);
-              *reinterpret_cast<uint4*>(slot + swz<64>(lane, h * 4 + jj)) = o;
             }
           } else {
-            // direct-store fallback (fp32 logits / unaligned views)
+            // direct-store fallback (fp32 logits / unaligned views); bias and residual are
+            // already in the accumulator
             const int m = rows0 + lane;
-            const int nb = n0 + c * EPI_CHUNK + h * 32;
+            const int nb = n0 + col;
             const int nv = min(32, p.cout - nb);
             if (m < p.M && nv > 0) {
-              if (p.has_res) {
-                const __nv_bfloat16* rp =
-                    reinterpret_cast<const __nv_bfloat16*>(p.res) + static_cast<size_t>(m) * p.res_cstride + nb;
+              float v[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (i < nv) v[i] += __bfloat162float(rp[i]);
-              }
-              if (p.relu) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-              }
+              for (int i = 0; i < 32; ++i) v[i] = p.relu ? fmaxf(__uint_as_float(r[i]), 0.f) : __uint_as_float(r[i]);
               const size_t yo = static_cast<size_t>(m) * p.y_cstride + p.y_coff + nb;
               if (p.y_f32) {
                 float* yp = reinterpret_cast<float*>(p.y) + yo;
@@ -503,12 +556,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (tma) {
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmY, slot, n0 + c * EPI_CHUNK, rows0);
+          if (lane == 0 && !(p.dbg & 1)) {
+            tma_store_2d(&tmY, oslot, n0 + c * EPI_CHUNK, rows0);
             bulk_commit();
           }
         }
       }
+      // re-arm the columns past this tile's last chunk (the next user may be wider)
+      if (rearm)
+        for (int col = nchunks * EPI_CHUNK; col < static_cast<int>(p.acc_stride); col += 32) arm32(taddr + col, col);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // drained (and re-armed): the MMA may reuse it
     }
     if (tma && lane == 0) bulk_wait_all();
   }
@@ -673,15 +733,24 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   p.y_cstride = d->y_cstride;
   p.y_coff = d->y_coff;
   p.y_f32 = d->y_dtype == UB_F32;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("UB_DEBUG_FLAGS");
+      dbg = e ? atoi(e) : 0;
+    }
+    p.dbg = dbg;
+  }
 
   const uint16_t* ybase = reinterpret_cast<const uint16_t*>(d->y) + d->y_coff;
-  p.epi_tma = !p.y_f32 && d->y_cstride % 8 == 0 && aligned16(ybase) &&
-              (!p.has_res || (d->res_cstride % 8 == 0 && aligned16(p.res)));
+  if (p.has_res && (d->res_cstride % 8 || !aligned16(p.res)))
+    return fail(UB_EINVAL, "ub_conv_fwd: residual rows must be 16-byte aligned (res_cstride, res_coff multiples of 8)");
+  p.epi_tma = !p.y_f32 && d->y_cstride % 8 == 0 && aligned16(ybase);
 
-  const uint32_t a_bytes = BLOCK_M * bk * 2;
+  const uint32_t a_bytes = BLOCK_M * 128;  // sized for 64-wide residual k-blocks
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
   const uint32_t stage_bytes = a_bytes + b_stride;
-  const uint32_t fixed = 1024 + 4 * EPI_SLOTS * EPI_SLOT + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
+  const uint32_t fixed = 1024 + IDENT_BYTES + 4 * EPI_WARP_BYTES + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
                          (stem ? MAX_STEM_K * sizeof(int4) : 0);
   const uint32_t budget = 226u * 1024u - fixed;
   int stages = static_cast<int>(budget / stage_bytes);

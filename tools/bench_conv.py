@@ -29,6 +29,7 @@ CASES = {
     "l4_1x1s1_c390": (4, 7, 7, 232, 64, 128, 390, 1, 1, 0, 0, False, False),
     "l4_1x1s1_c416": (4, 7, 7, 232, 64, 128, 416, 1, 1, 0, 0, False, False),
     "l4_1x1s1_c390_big": (64, 7, 7, 232, 64, 128, 390, 1, 1, 0, 0, False, False),
+    "l1_conv3_nores": (256, 56, 56, 32, 0, 32, 256, 1, 1, 0, 0, False, True),
     "small_gather_multi": (8, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, True, True),
     "small_3x3_res_multi": (8, 56, 56, 64, 0, 64, 64, 3, 1, 1, 0, True, True),
     "small_stem_multi": (4, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),

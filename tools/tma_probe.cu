@@ -40,21 +40,22 @@ __global__ void __launch_bounds__(128, 1) probe_load(const __grid_constant__ CUt
 }
 
 // LSU streaming: each warp copies rows of `row_bytes` (16 B per lane-slot) with cp.async into smem.
-__global__ void __launch_bounds__(256, 1) probe_cpasync(const uint8_t* src, long long rows_total, int pitch, int row_bytes,
+template <int DEPTH>
+__global__ void __launch_bounds__(512, 1) probe_cpasync(const uint8_t* src, long long rows_total, int pitch, int row_bytes,
                                                          int iters, unsigned long long* sink) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int per_row = row_bytes / 16;
-  const int rows_per_iter = 256 / per_row;  // one 16-B piece per thread per iteration
+  const int rows_per_iter = blockDim.x / per_row;  // one 16-B piece per thread per iteration
   const int tid = threadIdx.x;
   long long row = (long long)blockIdx.x * rows_per_iter;
   const long long stride = (long long)gridDim.x * rows_per_iter;
   for (int i = 0; i < iters; ++i) {
     const long long r = (row + tid / per_row) % rows_total;
     const uint8_t* g = src + r * pitch + (tid % per_row) * 16;
-    uint32_t d = smem_u32(smem + ((i & 7) * 256 + tid) * 16);
+    uint32_t d = smem_u32(smem + ((i % (DEPTH + 1)) * blockDim.x + tid) * 16);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 6;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
     row += stride;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -139,21 +140,29 @@ int main() {
                  store ? "STORE" : "LOAD ", S, row_bytes, rows, moved / ms / 1e6, ms * 1e-3 * 1.9e9 / req);
         }
       }
-  cudaFuncSetAttribute(probe_cpasync, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  for (int rb : {64, 128, 256, 512}) {
+  cudaFuncSetAttribute(probe_cpasync<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(probe_cpasync<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(probe_cpasync<22>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int thr : {256, 512})
+  for (int depth : {6, 14, 22})
+  for (int rb : {128, 512}) {
     const int pitch = 512;
     const long long rows_total = (long long)(bytes / pitch);
-    const int per_iter_bytes = 256 * 16;
+    const int per_iter_bytes = thr * 16;
     const int iters = (int)((256ll << 20) / per_iter_bytes / 148);
     float ms = 0;
+    const size_t sm = (size_t)(depth + 1) * thr * 16;
+    if (sm > 200 * 1024) continue;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      probe_cpasync<<<148, 256, 8 * 256 * 16>>>(reinterpret_cast<const uint8_t*>(buf), rows_total, pitch, rb, iters, sink);
+      if (depth == 6) probe_cpasync<6><<<148, thr, sm>>>(reinterpret_cast<const uint8_t*>(buf), rows_total, pitch, rb, iters, sink);
+      if (depth == 14) probe_cpasync<14><<<148, thr, sm>>>(reinterpret_cast<const uint8_t*>(buf), rows_total, pitch, rb, iters, sink);
+      if (depth == 22) probe_cpasync<22><<<148, thr, sm>>>(reinterpret_cast<const uint8_t*>(buf), rows_total, pitch, rb, iters, sink);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
     }
     cudaEventElapsedTime(&ms, e0, e1);
-    printf("CPASYNC row %4d B (16 B/thread, 256 thr, 7 groups in flight): %7.1f GB/s total\n", rb,
+    printf("CPASYNC row %4d B, %d thr, %2d groups in flight (%6zu B/SM): %7.1f GB/s total\n", rb, thr, depth, (size_t)depth * thr * 16,
            (double)iters * 148 * per_iter_bytes / ms / 1e6);
   }
   cudaError_t err = cudaDeviceSynchronize();
