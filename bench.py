@@ -189,6 +189,7 @@ def main():
 
     from paper_2307_08771_b200 import _lib, api, engine as EN, export as E, plans as P
     from paper_2307_08771_b200.configs import CONFIGS, build_spatial_model
+    from paper_2307_08771_b200.driver import ReplicaDriver
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -213,13 +214,13 @@ def main():
     x = torch.randn(B, 3, 224, 224, generator=torch.Generator().manual_seed(rank)).to(dev)
     eng.input_buf.copy_(x)
     logits = eng.output_tensor()
-    gathered = torch.empty((world * B, logits.shape[1]), dtype=torch.float32, device=dev) if world > 1 else None
+    driver = ReplicaDriver(lambda: eng.output_tensor(), equal_shards=True)
     stream = torch.cuda.current_stream()
 
     def step():
         eng._graph_exec.replay()
         if world > 1:
-            dist.all_gather_into_tensor(gathered, eng.output_tensor().contiguous())
+            driver.gather(driver.run_local())  # the one exchange: NCCL all-gather of the logits
 
     def barrier():
         if world > 1:

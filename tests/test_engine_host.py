@@ -1,0 +1,71 @@
+"""Engine compilation (fusion + schedule) without a GPU: kernels are stubbed,
+the graph analysis is the real one."""
+
+import pytest
+import torch
+
+from paper_2307_08771_b200 import _lib, engine as EN, export as E, kernels as K, plans as P
+from paper_2307_08771_b200.configs import CONFIGS, build_spatial_model
+
+
+@pytest.fixture
+def stub_kernels(monkeypatch):
+    monkeypatch.setattr(K, "permute_weights", lambda W, rows, cols, **kw: torch.zeros(1))
+    monkeypatch.setattr(_lib, "conv_weight_layout", lambda cin, coff, g: (0 if g else coff & 7, 64))
+    monkeypatch.setattr(_lib, "conv_stem_kpad", lambda cin, kh, kw: 128)
+
+
+@pytest.fixture(scope="module")
+def r50():
+    return build_spatial_model(CONFIGS["resnet50_s50"])
+
+
+def _engine(sm, strategy, gather_mode, batch=2):
+    cfg = CONFIGS["resnet50_s50"]
+    plans = P.load_plans(cfg.asset_dir / f"plans_{strategy}.json")
+    eg = E.export_graph(sm.graph, plans)
+    return EN.from_plans(sm, eg, E.compose_maps(sm.graph, plans), batch=batch, device="cpu",
+                         gather_mode=gather_mode), eg
+
+
+@pytest.mark.parametrize("strategy,gather_mode,n_gather_ops", [
+    ("reorder", "fused", 0), ("reorder", "copy", 11), ("baseline", "fused", 0), ("baseline", "copy", 21)])
+def test_resnet50_schedule(stub_kernels, r50, strategy, gather_mode, n_gather_ops):
+    eng, eg = _engine(r50, strategy, gather_mode)
+    kinds = [op.kind for op in eng.ops]
+    assert kinds.count("conv") == 54
+    assert kinds.count("gather") == n_gather_ops  # the input GATHER is fused into the stem
+    assert kinds.count("maxpool") == 1 and kinds.count("avgpool") == 1
+    assert "stage" not in kinds and "eltwise" not in kinds  # BN/ADD/ReLU all absorbed
+    # every residual ADD is fused into a conv epilogue; each conv absorbs its BN
+    convs = [op for op in eng.ops if op.kind == "conv"]
+    assert sum(1 for op in convs if op.info.get("residual")) == 16
+    assert all(op.info["bn"] is not None for op in convs)
+    # schedule respects data dependencies
+    produced = set()
+    alias = eng._alias
+
+    def base(v):
+        while v in alias:
+            v = alias[v][0]
+        return v
+
+    for op in eng.ops:
+        for i in op.inputs:
+            assert base(i) in produced or base(i) == "x", (op.output, i)
+        produced.add(op.output)
+    assert eng.output_value.C == 1000
+
+
+def test_slices_are_views_not_copies(stub_kernels, r50):
+    eng, eg = _engine(r50, "reorder", "fused")
+    slices = [lay for lay in eg.layers if lay.kind.value == "slice"]
+    assert len(slices) == 10
+    for op in eng.ops:
+        assert op.output not in {s.id for s in slices}
+
+
+def test_conv_stats_match_survey_flops(stub_kernels, r50):
+    eng, _ = _engine(r50, "reorder", "fused")
+    flops, _ = eng.per_image_work()
+    assert 2.55e9 < flops < 2.75e9  # 2.644 GFLOP/img (reorder, per-layer)
