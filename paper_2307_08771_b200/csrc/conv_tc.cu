@@ -316,6 +316,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           i1 = (j + 1) < p.n_gather ? __ldg(p.gidx + j + 1) : -1;
           const int c0 = i0 < 0 ? 0 : i0;
           const int c1 = i1 < 0 ? 0 : i1;
+          // sorted gather lists make adjacent pairs common: one aligned 32-bit load for both
+          const bool pair = i0 >= 0 && i1 == i0 + 1 && !(i0 & 1);
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int img = __shfl_sync(0xffffffffu, g_img, u);
@@ -325,8 +327,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             okm |= static_cast<uint32_t>(ok) << u;
             const size_t pix = ok ? (static_cast<size_t>(img) * p.H + hi) * p.W + wi : 0;
             const uint16_t* xr = p.x + pix * p.x_cstride;
-            la[u] = __ldg(xr + c0);
-            lb[u] = __ldg(xr + c1);
+            if (pair) {
+              const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(xr + c0));
+              la[u] = static_cast<uint16_t>(v);
+              lb[u] = static_cast<uint16_t>(v >> 16);
+            } else {
+              la[u] = __ldg(xr + c0);
+              lb[u] = __ldg(xr + c1);
+            }
           }
         }
         if constexpr (AMODE == A_STEM) {

@@ -364,7 +364,12 @@ class Engine:
                 s, n = rl.params
                 x = x.view(s, n)
             else:
-                gather_idx = self._i32(rl.params)
+                # Internal K order: the gathered channels sorted by source position, so each
+                # 64-wide k-block reads a narrow window of the producer's rows.  The weight
+                # columns follow the same order (a GEMM is invariant to a consistent K
+                # permutation); the exported (perm, indices) stay the reference's.
+                k_order = sorted(range(len(rl.params)), key=lambda k: (rl.params[k], k))
+                gather_idx = self._i32([rl.params[k] for k in k_order])
         cin = gather_idx.numel() if gather_idx is not None else x.C
         assert cin == lay.in_channels, f"{lid}: reads {cin} channels, layer has {lay.in_channels}"
         cout = lay.out_channels
@@ -382,6 +387,8 @@ class Engine:
         O, I = W.shape[0], W.shape[1]
         rows = rows if rows is not None else range(O)
         cols = cols if cols is not None else range(I)
+        if gather_idx is not None:
+            cols = [list(cols)[k] for k in k_order]
         wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="gemm", lead=lead, cpad=cpad,
                                out_dtype=torch.bfloat16)
         self._keep.append(wg)

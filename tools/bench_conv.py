@@ -45,7 +45,7 @@ def run(name, check=True, iters=20, once=False):
     nin = ng if ng else cin
     Wt = (torch.randn(cout, nin, k, k, device=dev, generator=g) / (nin * k * k) ** 0.5).contiguous()
     if ng:
-        idx = torch.randperm(cin, device=dev, generator=g)[:ng].to(torch.int32)
+        idx = torch.randperm(cin, device=dev, generator=g)[:ng].sort().values.to(torch.int32)
         xa, lead, cpad = x, *_lib.conv_weight_layout(ng, 0, True)
     else:
         idx = None
