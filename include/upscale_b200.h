@@ -46,7 +46,7 @@ extern "C" {
 const char* ub_last_error(void);
 
 /* ABI version (bumped on any signature change). */
-int ub_abi_version(void); /* 2 */
+int ub_abi_version(void); /* 3 */
 
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (used by bench.py's gpu_launches claim). */
@@ -120,6 +120,7 @@ typedef struct {
                                   [N][x_channels][H][W]; gather_idx selects the cin planes
                                   (the INPUT node's GATHER), weights UB_LAYOUT_GEMM_DENSE */
   int x_channels;
+  int variant;                 /* 0: heuristic; 1: 256 producer threads; 2: 512 (autotuned by the engine) */
 } ub_conv_desc;
 
 /* Dense-K padding (multiple of 64) of the fused-stem weight operand. */

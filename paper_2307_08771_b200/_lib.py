@@ -48,6 +48,7 @@ class ConvDesc(ctypes.Structure):
         ("y", c_vp), ("y_cstride", c_int), ("y_coff", c_int),
         ("y_dtype", c_int),
         ("x_nchw_f32", c_int), ("x_channels", c_int),
+        ("variant", c_int),
     ]
 
 

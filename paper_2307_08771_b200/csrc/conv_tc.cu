@@ -46,8 +46,9 @@ enum AMode : int { A_TILED = 0, A_IM2COL = 1, A_GATHER = 2, A_STEM = 3 };
 __host__ __device__ constexpr bool reg_mode(int m) { return m == A_GATHER || m == A_STEM; }
 
 constexpr int BLOCK_M = 128;
-constexpr int NUM_THREADS = 512;
-constexpr int PRODUCERS = 256;                // warps 8-15
+// Producer warp count is a template parameter (256 or 512 threads): cp.async throughput scales
+// with issuing warps, but more warps also take issue slots and registers from the epilogue, so
+// the engine autotunes it per layer (ConvDesc.variant).
 constexpr int EPI_CHUNK = 64;                 // output channels per epilogue chunk (128-byte rows)
 constexpr int EPI_SLOT = 32 * EPI_CHUNK * 2;  // one warp's 32 rows x 64 ch bf16 (4 KB)
 constexpr int EPI_WARP_BYTES = 2 * EPI_SLOT;  // two output slots per epilogue warp
@@ -106,9 +107,12 @@ __device__ __forceinline__ int tile_res_chunks(const ConvKParams& p, int n0) {
   return p.has_res ? (min(p.block_n, p.cout - n0) + EPI_CHUNK - 1) / EPI_CHUNK : 0;
 }
 
-template <int AMODE, int BK>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int AMODE, int BK, int PRODUCERS>
+__global__ void __launch_bounds__(256 + PRODUCERS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const ConvKParams p) {
+  constexpr int PWARPS = PRODUCERS / 32;
+  constexpr int GROWS = BLOCK_M / PWARPS;       // gather mode: rows per producer warp
+  constexpr int STEM_K = 64 * 128 / PRODUCERS;  // stem mode: k values per producer thread per k-block
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   constexpr uint32_t ROW_BYTES = BK * 2;
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     if (p.epi_tma) tma_prefetch_desc(&tmY);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PRODUCERS / 32 : 0));
+      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -234,17 +238,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ================= producers (256 threads): fill stage s with A and B, then arrive on full[s]
     // Addresses are precomputed per tile so the per-k-block work is one add + one cp.async per
     // 16-byte chunk; smem destinations are constant for the whole kernel.
-    const int pt = threadIdx.x - 256;  // 0..255
-    const int pw = pt >> 5;            // producer warp 0..7
+    const int pt = threadIdx.x - 256;  // 0..PRODUCERS-1
+    const int pw = pt >> 5;            // producer warp 0..PWARPS-1
     const int hw = p.Ho * p.Wo;
-    constexpr int A_PER_THREAD = BLOCK_M * CPR / PRODUCERS;  // 4 / 2 / 1 for BK 64 / 32 / 16
+    // cp.async modes: this thread owns A rows row0 + i * ROW_STEP (i < A_PER_THREAD), chunk cj;
+    // with fewer chunks than threads (BK 16) the upper threads own none
+    constexpr int A_PIECES = BLOCK_M * CPR;
+    constexpr int A_PER_THREAD = A_PIECES >= PRODUCERS ? A_PIECES / PRODUCERS : 1;
     constexpr int ROW_STEP = PRODUCERS / CPR;                // rows between a thread's chunks
+    const bool a_owner = pt < A_PIECES;
     const int row0 = pt / CPR;
     const int cj = pt % CPR;  // this thread's 16-byte chunk within an operand row
     const uint32_t dst0 = swz<BK>(row0, cj);  // + i * ROW_STEP * ROW_BYTES for chunk i (swizzle-invariant)
     const int nb_pieces = (p.block_n + ROW_STEP - 1) / ROW_STEP;  // B chunks per thread (upper bound)
     const size_t b_row_stride = static_cast<size_t>(ROW_STEP) * p.K_total;
     // residual k-blocks: 64-channel rows; this thread owns rows pt/8 + 32 i, chunk pt%8
+    constexpr int R_PER_THREAD = BLOCK_M * 8 / PRODUCERS;  // residual 16-byte chunks per thread
     const int rrow0 = pt >> 3, rj = pt & 7;
     const uint32_t rdst0 = swz<64>(rrow0, rj);
     int s = 0;
@@ -275,12 +284,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint16_t* b_base = p.w + static_cast<size_t>(n0 + row0) * p.K_total + cj * 8;
       const int b_valid = min(p.block_n, p.cout - n0);  // rows beyond are zero-filled
       // register-path geometry: gather -> warp pw owns rows 16*pw..16*pw+15 (lane = channel pair);
-      // stem -> thread owns row pt & 127 and k half pt >> 7
+      // stem -> thread owns row pt & 127 and k slice pt >> 7
       int g_img = 0, g_hb = -(1 << 28), g_wb = 0;
       const float* stem_base = p.xf;
       if constexpr (AMODE == A_GATHER) {
-        if (lane < 16) {
-          const int m = m0 + pw * 16 + lane;
+        if (lane < GROWS) {
+          const int m = m0 + pw * GROWS + lane;
           if (m < p.M) {
             g_img = m / hw;
             const int rem = m - g_img * hw;
@@ -306,20 +315,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         const int kcoord = kb * BK;  // weights are [cout][taps][cpad]: k-block kb starts at kb*BK
         // register paths: issue the global loads before waiting for the slot
-        uint16_t la[16], lb[16];
+        uint16_t la[GROWS], lb[GROWS];
         uint32_t okm = 0;
         int i0 = -1, i1 = -1;
-        float fv[32];
+        float fv[STEM_K];
         if constexpr (AMODE == A_GATHER) {
           const int j = cc * 64 + lane * 2;
           i0 = j < p.n_gather ? __ldg(p.gidx + j) : -1;
           i1 = (j + 1) < p.n_gather ? __ldg(p.gidx + j + 1) : -1;
           const int c0 = i0 < 0 ? 0 : i0;
           const int c1 = i1 < 0 ? 0 : i1;
-          // sorted gather lists make adjacent pairs common: one aligned 32-bit load for both
-          const bool pair = i0 >= 0 && i1 == i0 + 1 && !(i0 & 1);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
+          for (int u = 0; u < GROWS; ++u) {
             const int img = __shfl_sync(0xffffffffu, g_img, u);
             const int hi = __shfl_sync(0xffffffffu, g_hb, u) + fr;
             const int wi = __shfl_sync(0xffffffffu, g_wb, u) + fs;
@@ -327,20 +334,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             okm |= static_cast<uint32_t>(ok) << u;
             const size_t pix = ok ? (static_cast<size_t>(img) * p.H + hi) * p.W + wi : 0;
             const uint16_t* xr = p.x + pix * p.x_cstride;
-            if (pair) {
-              const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(xr + c0));
-              la[u] = static_cast<uint16_t>(v);
-              lb[u] = static_cast<uint16_t>(v >> 16);
-            } else {
-              la[u] = __ldg(xr + c0);
-              lb[u] = __ldg(xr + c1);
-            }
+            la[u] = __ldg(xr + c0);
+            lb[u] = __ldg(xr + c1);
           }
         }
         if constexpr (AMODE == A_STEM) {
-          const int kh0 = kb * 64 + (pt >> 7) * 32;
+          const int kh0 = kb * 64 + (pt >> 7) * STEM_K;
 #pragma unroll
-          for (int kk = 0; kk < 32; ++kk) {
+          for (int kk = 0; kk < STEM_K; ++kk) {
             const int4 e = stem_tab[kh0 + kk];  // warp-uniform -> smem broadcast
             const int hi = g_hb + e.y;
             const int wi = g_wb + e.z;
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const ptrdiff_t toff = (static_cast<ptrdiff_t>(fr) * p.W + fs) * p.x_cstride + cc * BK;
 #pragma unroll
           for (int i = 0; i < A_PER_THREAD; ++i) {
+            if (!a_owner) break;
             const int hi = a_hb[i] + fr;
             const int wi = a_wb[i] + fs;
             const bool ok = ch_ok && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
@@ -368,19 +370,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else if constexpr (AMODE == A_GATHER) {
           uint8_t* tA = sA + s * A_BYTES;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
+          for (int u = 0; u < GROWS; ++u) {
             const bool ok = (okm >> u) & 1u;
             const uint32_t a = (ok && i0 >= 0) ? la[u] : 0u;
             const uint32_t b = (ok && i1 >= 0) ? lb[u] : 0u;
-            const int row = pw * 16 + u;
+            const int row = pw * GROWS + u;
             *reinterpret_cast<uint32_t*>(tA + swz<64>(row, lane >> 2) + ((lane & 3) << 2)) = a | (b << 16);
           }
         } else {  // A_STEM
           uint8_t* tA = sA + s * A_BYTES;
           const int row = pt & 127;
-          const int j0 = (pt >> 7) * 4;
+          const int j0 = (pt >> 7) * (STEM_K / 8);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
+          for (int jj = 0; jj < STEM_K / 8; ++jj) {
             uint4 o;
             o.x = pack_bf16x2(fv[jj * 8 + 0], fv[jj * 8 + 1]);
             o.y = pack_bf16x2(fv[jj * 8 + 2], fv[jj * 8 + 3]);
@@ -425,11 +427,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t tileA = smem_u32(sA + s * A_BYTES);
         const int ch = n0 + rc * EPI_CHUNK + rj * 8;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int m = m0 + rrow0 + 32 * i;
+        for (int i = 0; i < R_PER_THREAD; ++i) {
+          const int m = m0 + rrow0 + (PRODUCERS / 8) * i;
           const bool ok = m < p.M && ch < p.cout;
           const uint16_t* src = ok ? p.res + static_cast<size_t>(m) * p.res_cstride + ch : p.res;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileA + rdst0 + i * 32 * 128), "l"(src),
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileA + rdst0 + i * (PRODUCERS / 8) * 128), "l"(src),
                        "r"(ok ? 16u : 0u)
                        : "memory");
         }
@@ -615,18 +617,25 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int AMODE, int BK>
-int launch_conv(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
+template <int AMODE, int BK, int PRODUCERS>
+int launch_conv_p(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(conv_tc_kernel<AMODE, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024);
+    attr_err = cudaFuncSetAttribute(conv_tc_kernel<AMODE, BK, PRODUCERS>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  conv_tc_kernel<AMODE, BK><<<grid, NUM_THREADS, smem, stream>>>(tmY, p);
+  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, p);
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
+}
+
+template <int AMODE, int BK>
+int launch_conv(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream,
+                int wide) {
+  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, p, grid, smem, stream)
+              : launch_conv_p<AMODE, BK, 256>(tmY, p, grid, smem, stream);
 }
 
 int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : (cin_eff <= 32 ? 32 : 64); }
@@ -785,15 +794,18 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
 
   const int num_tiles = p.m_tiles * p.n_tiles;
   const int grid = num_tiles < num_sms() ? num_tiles : num_sms();
-  if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream);
-  if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream);
+  // producer width: explicit variant from the caller (engine autotune), else a heuristic
+  int wide = d->variant == 2 ? 1 : (d->variant == 1 ? 0 : (p.has_res ? 0 : 1));
+  if (stem) wide = 0;
+  if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream, wide);
+  if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   if (pointwise) {
-    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, p, grid, smem, stream);
-    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, p, grid, smem, stream);
-    return launch_conv<A_TILED, 16>(tmY, p, grid, smem, stream);
+    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, p, grid, smem, stream, wide);
+    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, p, grid, smem, stream, wide);
+    return launch_conv<A_TILED, 16>(tmY, p, grid, smem, stream, wide);
   }
-  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, p, grid, smem, stream);
-  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, p, grid, smem, stream);
-  return launch_conv<A_IM2COL, 16>(tmY, p, grid, smem, stream);
+  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, p, grid, smem, stream, wide);
+  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, p, grid, smem, stream, wide);
+  return launch_conv<A_IM2COL, 16>(tmY, p, grid, smem, stream, wide);
 }

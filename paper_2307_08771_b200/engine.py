@@ -396,8 +396,9 @@ class Engine:
         fp32_out = info["out"] in output_feed
         y = self._alloc(info["out"], cout, fp32=fp32_out)
         relu = info["relu"] is not None
+        op.info["variant"] = 0  # producer width: 0 = library heuristic; set by autotune()
         op.launch = lambda: K.conv(x, wg, lead, cpad, cout, kk, kk, st, pd, y, gather_idx=gather_idx, bias=bias,
-                                   residual=residual, relu=relu, y_fp32=fp32_out)
+                                   residual=residual, relu=relu, y_fp32=fp32_out, variant=op.info["variant"])
         # roofline bookkeeping (per image)
         _, hi, wi = self._shapes[info["src"]] if info["src"] in self._shapes else (0, x.H, x.W)
         ho, wo = y.H, y.W
@@ -461,8 +462,36 @@ class Engine:
             t = t.reshape(o.N, o.H, o.W, o.C).permute(0, 3, 1, 2)
         return t.float()
 
-    def capture(self) -> None:
-        """Capture the launch sequence in a CUDA graph (static buffers)."""
+    def autotune(self, reps: int = 3) -> dict[str, int]:
+        """Pick the conv kernel's producer width (256 vs 512 cp.async threads) per layer by
+        timing both on this engine's own buffers (CUDA events, after a warm-up)."""
+        picks = {}
+        for op in self.ops:
+            if op.kind != "conv" or "stem_idx" in op.info:
+                continue
+            best = None
+            for v in (1, 2):
+                op.info["variant"] = v
+                op.launch()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(reps):
+                    op.launch()
+                b.record()
+                b.synchronize()
+                t = a.elapsed_time(b)
+                if best is None or t < best[0]:
+                    best = (t, v)
+            op.info["variant"] = best[1]
+            picks[op.info["conv"]] = best[1]
+        return picks
+
+    def capture(self, autotune: bool = True) -> None:
+        """Capture the launch sequence in a CUDA graph (static buffers); optionally
+        autotune the conv variants first."""
+        if autotune and self.batch >= 16:
+            self.launch_all()
+            self.autotune()
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):

@@ -117,7 +117,7 @@ def channel_gather(x: Act, idx_dev: torch.Tensor, y: Act) -> None:
 
 def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: int, stride: int, pad: int,
          y: Act, gather_idx: torch.Tensor | None = None, bias: torch.Tensor | None = None,
-         residual: Act | None = None, relu: bool = False, y_fp32: bool = False) -> None:
+         residual: Act | None = None, relu: bool = False, y_fp32: bool = False, variant: int = 0) -> None:
     Ho = (x.H + 2 * pad - kh) // stride + 1
     Wo = (x.W + 2 * pad - kw) // stride + 1
     assert y.N == x.N and y.H == Ho and y.W == Wo, "output geometry mismatch"
@@ -135,6 +135,7 @@ def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: 
     d.relu = int(relu)
     d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
     d.y_dtype = _lib.UB_F32 if y_fp32 else _lib.UB_BF16
+    d.variant = variant
     _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
 
 
