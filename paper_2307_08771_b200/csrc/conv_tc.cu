@@ -90,8 +90,11 @@ struct ConvKParams {
   int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
 };
 
+// Align the dynamic smem base to 1024 B by pointer arithmetic on the __shared__ pointer itself
+// (a round trip through uintptr_t would make every derived pointer generic and turn all
+// shared-memory accesses into generic LD/ST).
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 // Byte offset of 16-byte chunk j of row r in a swizzled K-major tile with BK-element rows
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       // register-path geometry: gather -> warp pw owns rows 16*pw..16*pw+15 (lane = channel pair);
       // stem -> thread owns row pt & 127 and k slice pt >> 7
       int g_img = 0, g_hb = -(1 << 28), g_wb = 0;
+      uint32_t s_rok = 0, s_cok = 0;  // stem: in-image filter rows / columns of this pixel's window
       const float* stem_base = p.xf;
       if constexpr (AMODE == A_GATHER) {
         if (lane < GROWS) {
@@ -307,6 +311,10 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           const int ho = rem / p.Wo;
           g_hb = ho * p.stride - p.pad;
           g_wb = (rem - ho * p.Wo) * p.stride - p.pad;
+          for (int r = 0; r < p.kw; ++r) {
+            s_rok |= static_cast<uint32_t>(g_hb + r >= 0 && g_hb + r < p.H) << r;
+            s_cok |= static_cast<uint32_t>(g_wb + r >= 0 && g_wb + r < p.W) << r;
+          }
           stem_base =
               p.xf + static_cast<size_t>(img) * p.C_in * p.H * p.W + static_cast<ptrdiff_t>(g_hb) * p.W + g_wb;
         }
@@ -342,10 +350,8 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           const int kh0 = kb * 64 + (pt >> 7) * STEM_K;
 #pragma unroll
           for (int kk = 0; kk < STEM_K; ++kk) {
-            const int4 e = stem_tab[kh0 + kk];  // warp-uniform -> smem broadcast
-            const int hi = g_hb + e.y;
-            const int wi = g_wb + e.z;
-            const bool ok = e.y >= 0 && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            const int4 e = stem_tab[kh0 + kk];  // warp-uniform -> smem broadcast; e.y = -1 past k_real
+            const bool ok = ((s_rok >> (e.y & 31)) & (s_cok >> e.z) & 1u) && e.y >= 0;
             fv[kk] = ok ? __ldg(stem_base + e.x) : 0.f;
           }
         }
@@ -796,7 +802,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int grid = num_tiles < num_sms() ? num_tiles : num_sms();
   // producer width: explicit variant from the caller (engine autotune), else a heuristic
   int wide = d->variant == 2 ? 1 : (d->variant == 1 ? 0 : (p.has_res ? 0 : 1));
-  if (stem) wide = 0;
+  if (stem) wide = 1;
   if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream, wide);
   if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;

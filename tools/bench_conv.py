@@ -94,7 +94,33 @@ def run(name, check=True, iters=20, once=False):
           f"{flops/us/1e6:7.1f} TF/s  roof {roof:7.1f} us  frac {roof/us:.2f}", flush=True)
 
 
+def run_stem(N=256, cin_idx=(2, 0), iters=10):
+    dev = "cuda"
+    x = torch.randn(N, 3, 224, 224, device=dev)
+    cin = len(cin_idx)
+    Wt = torch.randn(64, cin, 7, 7, device=dev) / (cin * 49) ** 0.5
+    kpad = _lib.conv_stem_kpad(cin, 7, 7)
+    wg = K.permute_weights(Wt.contiguous(), list(range(64)), list(range(cin)), layout="dense", cpad=kpad,
+                           out_dtype=torch.bfloat16)
+    idx = torch.tensor(cin_idx, dtype=torch.int32, device=dev)
+    y = K.empty_act(N, 112, 112, 64, dev)
+    for _ in range(3):
+        K.conv_stem(x, idx, wg, kpad, 64, 7, 2, 3, y, relu=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        K.conv_stem(x, idx, wg, kpad, 64, 7, 2, 3, y, relu=True)
+    b.record()
+    torch.cuda.synchronize()
+    us = a.elapsed_time(b) / iters * 1e3
+    byts = N * (3 * 224 * 224 * 4 + 64 * 112 * 112 * 2)
+    print(f"stem N={N} cin={cin}: {us:.1f} us, {byts/us/1e3:.0f} GB/s (fp32 input read once + bf16 output)", flush=True)
+
+
 if __name__ == "__main__":
+    if "--stem" in sys.argv:
+        run_stem(iters=1 if "--once" in sys.argv else 10)
+        sys.exit(0)
     torch.backends.cudnn.allow_tf32 = False
     once = "--once" in sys.argv
     names = [a for a in sys.argv[1:] if not a.startswith("--")]
