@@ -41,12 +41,15 @@ extern "C" {
                             column c of tap t at (lead + c); zeros elsewhere */
 #define UB_LAYOUT_GEMM_DENSE 2 /* [n_rows][cpad]: dense-K operand of the fused stem,
                                   column c of tap t at t*n_cols + c; zeros beyond */
+#define UB_LAYOUT_S2D 3 /* [n_rows][kq][kq][8], kq = ceil(kw/2): operand of ub_conv_s2d,
+                           element (dy, dx, (py*2+px)*n_cols + c) = W[.][c][2dy+py][2dx+px]
+                           (0 past the filter); kh == kw, n_cols <= 2, lead/cpad ignored */
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* ub_last_error(void);
 
 /* ABI version (bumped on any signature change). */
-int ub_abi_version(void); /* 3 */
+int ub_abi_version(void); /* 4 */
 
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (used by bench.py's gpu_launches claim). */
@@ -90,6 +93,10 @@ int ub_channel_gather(const void* x, int x_cstride, int x_coff, const int32_t* i
  * `lead` weight columns are zero).  gather != 0: fused-gather read (lead 0). */
 int ub_conv_weight_layout(int cin, int coff, int gather, int* lead, int* cpad);
 
+/* Same for a kh x kw filter: small-channel k x k reads (cin + lead <= 32) use a packed
+ * per-tap K of 8/16/32 (several taps per 64-wide K-block); otherwise as above. */
+int ub_conv_weight_layout2(int cin, int coff, int gather, int kh, int kw, int* lead, int* cpad);
+
 /* One convolution (CHANNEL_MIX over a spatial tensor; interp.py:57-63) with its
  * read node and epilogue fused:
  *   read:      SLICE  -> x + x_coff view (interp.py:72-74), or
@@ -127,6 +134,25 @@ typedef struct {
 int ub_conv_stem_kpad(int cin, int kh, int kw);
 
 int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream);
+
+/*
+ * Space-to-depth stem (the stride-2 k x k first conv when its input GATHER keeps
+ * <= 2 channels).  Same op as ub_conv_fwd with x_nchw_f32 = 1, split in two launches:
+ *   ub_stem_s2d_pack:  x fp32 NCHW [N][C][H][W] -> s, bf16 rows of 8:
+ *                      s[(n*Hs + Y)*Ws + X][(py*2+px)*cin + c] = x[n][idx[c]][2Y+py-pad][2X+px-pad]
+ *                      (0 outside the image); the tail rows past N*Hs*Ws are read by the
+ *                      conv but never written here -- allocate s zeroed once;
+ *   ub_conv_s2d:       y = act(conv(s, w) + bias) with w in UB_LAYOUT_S2D, on tcgen05 (the
+ *                      2x2-folded conv is stride 1, so every filter tap of a 128-pixel tile
+ *                      is a shifted view of ONE contiguous block of s).
+ * ub_stem_s2d_geometry gives Hs, Ws and the byte size of s.  cout <= 128; y_cstride and
+ * y_coff multiples of 8.  Replaces the same reference nodes as ub_conv_fwd's stem.
+ */
+int ub_stem_s2d_geometry(int N, int H, int W, int k, int pad, int* Hs, int* Ws, long long* bytes);
+int ub_stem_s2d_pack(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, int k, int pad,
+                     void* s, cudaStream_t stream);
+int ub_conv_s2d(const void* s, int N, int H, int W, int k, int pad, const void* w, int cout,
+                const float* bias, int relu, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
 /* Model-input staging: NCHW fp32 -> NHWC bf16 [N*H*W][y_cstride], channels
  * idx[0..n) (a GATHER on the INPUT node, fused; idx == NULL: identity over C). */

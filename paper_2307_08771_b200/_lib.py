@@ -18,7 +18,7 @@ UB_EUNSUPPORTED = -2
 UB_ECUDA = -3
 
 UB_F32, UB_F64, UB_BF16 = 0, 1, 2
-UB_LAYOUT_OIHW, UB_LAYOUT_GEMM, UB_LAYOUT_GEMM_DENSE = 0, 1, 2
+UB_LAYOUT_OIHW, UB_LAYOUT_GEMM, UB_LAYOUT_GEMM_DENSE, UB_LAYOUT_S2D = 0, 1, 2, 3
 
 c_int, c_ll, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p
 
@@ -63,8 +63,15 @@ SIGNATURES = {
     "ub_permute_vector": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp]),
     "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
+                                       ctypes.POINTER(c_int)]),
     "ub_conv_fwd": (c_int, [ctypes.POINTER(ConvDesc), c_vp]),
     "ub_conv_stem_kpad": (c_int, [c_int, c_int, c_int]),
+    "ub_stem_s2d_geometry": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
+                                     ctypes.POINTER(c_int), ctypes.POINTER(c_ll)]),
+    "ub_stem_s2d_pack": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+    "ub_conv_s2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_int,
+                            c_int, c_vp]),
     "ub_stage_input": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp]),
     "ub_maxpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                              c_int, c_int, c_vp, c_int, c_int, c_vp]),
@@ -120,7 +127,14 @@ def conv_stem_kpad(cin: int, kh: int, kw: int) -> int:
     return int(load().ub_conv_stem_kpad(cin, kh, kw))
 
 
-def conv_weight_layout(cin: int, coff: int, gather: bool) -> tuple[int, int]:
+def stem_s2d_geometry(N: int, H: int, W: int, k: int, pad: int) -> tuple[int, int, int]:
+    """(Hs, Ws, bytes) of the space-to-depth stem input buffer."""
+    hs, ws, nb = c_int(), c_int(), c_ll()
+    check(load().ub_stem_s2d_geometry(N, H, W, k, pad, ctypes.byref(hs), ctypes.byref(ws), ctypes.byref(nb)))
+    return hs.value, ws.value, nb.value
+
+
+def conv_weight_layout(cin: int, coff: int, gather: bool, kh: int = 1, kw: int = 1) -> tuple[int, int]:
     lead, cpad = c_int(), c_int()
-    check(load().ub_conv_weight_layout(cin, coff, int(gather), ctypes.byref(lead), ctypes.byref(cpad)))
+    check(load().ub_conv_weight_layout2(cin, coff, int(gather), kh, kw, ctypes.byref(lead), ctypes.byref(cpad)))
     return lead.value, cpad.value

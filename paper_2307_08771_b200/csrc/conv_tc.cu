@@ -41,7 +41,9 @@
 
 namespace ub {
 
-enum AMode : int { A_TILED = 0, A_IM2COL = 1, A_GATHER = 2, A_STEM = 3 };
+enum AMode : int { A_TILED = 0, A_IM2COL = 1, A_GATHER = 2, A_STEM = 3, A_PACKED = 4 };
+// A_PACKED: im2col for small-channel k x k convs -- several taps share one 64-wide k-block
+// (cpad per tap 8/16/32), so every operand row is a full 128-byte SWIZZLE_128B row.
 // register-path producers (2-byte gathers, fp32 casts) arrive explicitly per warp as well
 __host__ __device__ constexpr bool reg_mode(int m) { return m == A_GATHER || m == A_STEM; }
 
@@ -80,6 +82,7 @@ struct ConvKParams {
   // fused stem: fp32 NCHW model input, dense K = taps * n_gather
   const float* xf;
   int C_in, k_real;
+  int taps, tpk;  // A_PACKED: filter taps, taps per k-block
   // epilogue
   const float* bias;
   int has_res, relu, epi_tma;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   uint64_t* tfull = empty + stages;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int4* stem_tab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // A_STEM only
+  int4* stem_tab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // A_STEM / A_PACKED
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -174,6 +177,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     }
     fence_proxy_async_smem();
   }
+  if constexpr (AMODE == A_PACKED) {  // tap -> (filter row, filter col, element offset in the input)
+    for (int t = threadIdx.x; t < p.taps; t += blockDim.x) {
+      const int r = t / p.kw, c = t - (t / p.kw) * p.kw;
+      stem_tab[t] = make_int4(r, c, (r * p.W + c) * p.x_cstride, 0);
+    }
+  }
   if constexpr (AMODE == A_STEM) {
     // k -> (input offset relative to the window origin, filter row r, filter col s); k >= k_real: r = -1
     for (int k = threadIdx.x; k < p.num_kb * 64; k += blockDim.x) {
@@ -194,8 +203,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer (accumulators arrive pre-loaded with the bias)
+    {
+      // ================= MMA issuer (accumulators arrive pre-loaded with the bias); the whole
+      // warp runs the loop and one elected lane issues (umma_*_warp)
       const uint32_t idesc = make_idesc_bf16(BLOCK_M, static_cast<uint32_t>(p.block_n));
       const uint32_t idesc_res = make_idesc_bf16(BLOCK_M, EPI_CHUNK);
       const uint32_t i_base = smem_u32(sI);
@@ -206,10 +216,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         const int n0 = (t % p.n_tiles) * p.block_n;
         const int nres = tile_res_chunks(p, n0);
         mbar_wait(&tempty[acc], (it >> 1) & 1);  // drained and re-armed with this tile's bias
+        __syncwarp();
         tc_fence_after();
         const uint32_t d = tmem_base + acc * p.acc_stride;
         for (int kb = 0; kb < nk + nres; ++kb) {
           mbar_wait(&full[s], ph);
+          __syncwarp();
           tc_fence_after();
           fence_proxy_async_smem();  // generic-proxy (cp.async / st.shared) writes -> tensor-core reads
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
@@ -218,23 +230,23 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
               const uint32_t b_base = smem_u32(sB + s * b_stride);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
-                umma_bf16(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT),
+                umma_bf16_warp(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT),
                           idesc, 1u);
             } else {  // residual chunk rc: D[:, rc*64 : rc*64+64] += R_rc * I
               const uint32_t dc = d + (kb - nk) * EPI_CHUNK;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                umma_bf16(dc, make_sdesc(a_base + k * 32, 1024, 2), make_sdesc(i_base + k * 32, 1024, 2), idesc_res,
+                umma_bf16_warp(dc, make_sdesc(a_base + k * 32, 1024, 2), make_sdesc(i_base + k * 32, 1024, 2), idesc_res,
                           1u);
             }
           }
-          umma_commit(&empty[s]);
+          umma_commit_warp(&empty[s]);
           if (++s == stages) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        umma_commit_warp(&tfull[acc]);
       }
     }
   } else if (warp >= 8) {
@@ -275,13 +287,14 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         a_base[i] = p.x;
         a_hb[i] = -(1 << 28);
         a_wb[i] = 0;
-        if ((AMODE == A_TILED || AMODE == A_IM2COL) && m < p.M) {
+        if ((AMODE == A_TILED || AMODE == A_IM2COL || AMODE == A_PACKED) && m < p.M) {
           const int img = m / hw;
           const int rem = m - img * hw;
           const int ho = rem / p.Wo;
           a_hb[i] = ho * p.stride - p.pad;
           a_wb[i] = (rem - ho * p.Wo) * p.stride - p.pad;
-          a_base[i] = p.x + ((static_cast<ptrdiff_t>(img) * p.H + a_hb[i]) * p.W + a_wb[i]) * p.x_cstride + cj * 8;
+          a_base[i] = p.x + ((static_cast<ptrdiff_t>(img) * p.H + a_hb[i]) * p.W + a_wb[i]) * p.x_cstride +
+                      (AMODE == A_PACKED ? 0 : cj * 8);
         }
       }
       const uint16_t* b_base = p.w + static_cast<size_t>(n0 + row0) * p.K_total + cj * 8;
@@ -359,7 +372,23 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         const uint32_t tileA = smem_u32(sA + s * A_BYTES);
         const uint32_t tileB = smem_u32(sB + s * b_stride);
         // ---- A
-        if constexpr (AMODE == A_TILED || AMODE == A_IM2COL) {
+        if constexpr (AMODE == A_PACKED) {
+          const int cpt8 = p.cpad >> 3;  // 16-byte chunks per tap
+          const int tap = kb * p.tpk + cj / cpt8;
+          const int cjt = cj - (cj / cpt8) * cpt8;
+          const int4 te = stem_tab[tap < p.taps ? tap : 0];
+          const bool tap_ok = tap < p.taps && cjt * 8 < p.cin_eff;
+#pragma unroll
+          for (int i = 0; i < A_PER_THREAD; ++i) {
+            const int hi = a_hb[i] + te.x;
+            const int wi = a_wb[i] + te.y;
+            const bool ok = tap_ok && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            const uint16_t* src = ok ? a_base[i] + te.z + cjt * 8 : p.x;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileA + dst0 + i * ROW_STEP * ROW_BYTES),
+                         "l"(src), "r"(ok ? 16u : 0u)
+                         : "memory");
+          }
+        } else if constexpr (AMODE == A_TILED || AMODE == A_IM2COL) {
           const bool ch_ok = cc * BK + cj * 8 < p.cin_eff;
           const ptrdiff_t toff = (static_cast<ptrdiff_t>(fr) * p.W + fs) * p.x_cstride + cc * BK;
 #pragma unroll
@@ -400,10 +429,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         // ---- B (weights [cout][K_total]): rows row0 + i * ROW_STEP, chunk cj
         {
           const uint16_t* src = b_base + kcoord;
+          const bool k_ok = AMODE != A_PACKED || kcoord + cj * 8 < p.K_total;  // packed: last k-block ragged
           for (int i = 0; i < nb_pieces; ++i, src += b_row_stride) {
             const int n = row0 + i * ROW_STEP;
             if (n >= p.block_n) break;
-            const bool ok = n < b_valid;
+            const bool ok = n < b_valid && k_ok;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileB + dst0 + i * ROW_STEP * ROW_BYTES),
                          "l"(ok ? src : p.w), "r"(ok ? 16u : 0u)
                          : "memory");
@@ -597,8 +627,6 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
 
 // ------------------------------------------------------------------ host side
 
-namespace {
-
 int g_driver_version = -1;
 int g_num_sms = -1;
 
@@ -622,6 +650,8 @@ int num_sms() {
   }
   return g_num_sms;
 }
+
+namespace {
 
 template <int AMODE, int BK, int PRODUCERS>
 int launch_conv_p(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
@@ -661,6 +691,19 @@ extern "C" int ub_conv_weight_layout(int cin, int coff, int gather, int* lead, i
   return UB_OK;
 }
 
+extern "C" int ub_conv_weight_layout2(int cin, int coff, int gather, int kh, int kw, int* lead, int* cpad) {
+  if (cin < 1 || coff < 0 || kh < 1 || kw < 1 || !lead || !cpad)
+    return fail(UB_EINVAL, "ub_conv_weight_layout2: bad arguments");
+  const int ld = gather ? 0 : (coff & 7);
+  const int ce = cin + ld;
+  if (!gather && kh * kw > 1 && ce <= 32) {  // packed taps: per-tap K of 8/16/32
+    *lead = ld;
+    *cpad = ce <= 8 ? 8 : (ce <= 16 ? 16 : 32);
+    return UB_OK;
+  }
+  return ub_conv_weight_layout(cin, coff, gather, lead, cpad);
+}
+
 extern "C" int ub_conv_stem_kpad(int cin, int kh, int kw) { return (kh * kw * cin + 63) / 64 * 64; }
 
 extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
@@ -695,13 +738,14 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     cpad = ub_conv_stem_kpad(d->cin, d->kh, d->kw);
     if (cpad > MAX_STEM_K) return fail(UB_EUNSUPPORTED, "ub_conv_fwd: stem K %d > %d", cpad, MAX_STEM_K);
   } else {
-    ub_conv_weight_layout(d->cin, d->x_coff, gather ? 1 : 0, &lead, &cpad);
+    ub_conv_weight_layout2(d->cin, d->x_coff, gather ? 1 : 0, d->kh, d->kw, &lead, &cpad);
   }
+  const bool packed = !stem && !gather && taps > 1 && cpad < 64;
   if (d->w_lead != lead || d->w_cpad != cpad)
     return fail(UB_EINVAL, "ub_conv_fwd: weight layout (lead %d, cpad %d) != expected (lead %d, cpad %d)", d->w_lead,
                 d->w_cpad, lead, cpad);
   const int cin_eff = d->cin + lead;
-  const int bk = (gather || stem) ? 64 : pick_bk(cin_eff);
+  const int bk = (gather || stem || packed) ? 64 : pick_bk(cin_eff);
 
   ConvKParams p{};
   p.M = d->N * d->Ho * d->Wo;
@@ -721,8 +765,10 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     if (p.block_n > MAX_BLOCK_N) p.block_n = MAX_BLOCK_N;
     p.n_tiles = (d->cout + p.block_n - 1) / p.block_n;
   }
-  p.cchunks = stem ? 1 : cpad / bk;
-  p.num_kb = stem ? cpad / 64 : taps * p.cchunks;
+  p.cchunks = (stem || packed) ? 1 : cpad / bk;
+  p.taps = taps;
+  p.tpk = packed ? 64 / cpad : 1;
+  p.num_kb = stem ? cpad / 64 : (packed ? (taps + p.tpk - 1) / p.tpk : taps * p.cchunks);
   p.kw = d->kw;
   p.cpad = cpad;
   p.K_total = stem ? cpad : taps * cpad;
@@ -774,7 +820,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
   const uint32_t stage_bytes = a_bytes + b_stride;
   const uint32_t fixed = 1024 + IDENT_BYTES + 4 * EPI_WARP_BYTES + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
-                         (stem ? MAX_STEM_K * sizeof(int4) : 0);
+                         ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
   const uint32_t budget = 226u * 1024u - fixed;
   int stages = static_cast<int>(budget / stage_bytes);
   stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
@@ -804,6 +850,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   int wide = d->variant == 2 ? 1 : (d->variant == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
   if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream, wide);
+  if (packed) return launch_conv<A_PACKED, 64>(tmY, p, grid, smem, stream, wide);
   if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   if (pointwise) {

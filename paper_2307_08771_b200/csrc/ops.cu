@@ -10,15 +10,7 @@
 namespace ub {
 namespace {
 
-constexpr int kSMs = 148;
 
-inline int grid_for(long long work, int block, int per_thread = 1) {
-  long long g = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
-  const long long cap = (long long)kSMs * 16;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  return static_cast<int>(g);
-}
 
 template <typename T>
 __device__ __forceinline__ float to_f(T v) { return static_cast<float>(v); }
@@ -40,6 +32,17 @@ __global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps
       long long rc = e / taps;
       c = static_cast<int>(rc % n_cols);
       r = static_cast<int>(rc / n_cols);
+    } else if (LAYOUT == UB_LAYOUT_S2D) {  // [r][dy][dx][(py*2+px)*n_cols + c], kw passed as `lead`
+      const int kw = lead, kq = (lead + 1) / 2;
+      const int k = static_cast<int>(e % cpad);
+      r = static_cast<int>(e / cpad);
+      const int tq = k >> 3, slot = k & 7;
+      const int dy = tq / kq, dx = tq - (tq / kq) * kq;
+      const int q = slot / n_cols;
+      c = slot - q * n_cols;
+      const int fr = 2 * dy + (q >> 1), fs = 2 * dx + (q & 1);
+      inside = q < 4 && fr < taps / kw && fs < kw;
+      t = fr * kw + fs;
     } else if (LAYOUT == UB_LAYOUT_GEMM_DENSE) {  // [r][k], k = t * n_cols + c
       const int k = static_cast<int>(e % cpad);
       r = static_cast<int>(e / cpad);
@@ -77,7 +80,7 @@ int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows,
                             cudaStream_t s) {
   const long long total = layout == UB_LAYOUT_OIHW    ? (long long)n_rows * n_cols * taps
                           : layout == UB_LAYOUT_GEMM ? (long long)n_rows * taps * cpad
-                                                     : (long long)n_rows * cpad;
+                                                     : (long long)n_rows * cpad;  // DENSE, S2D
   const int block = 256;
   const int grid = grid_for(total, block, 4);
   if (layout == UB_LAYOUT_OIHW)
@@ -85,6 +88,9 @@ int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows,
         static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   else if (layout == UB_LAYOUT_GEMM)
     permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM><<<grid, block, 0, s>>>(
+        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+  else if (layout == UB_LAYOUT_S2D)
+    permute_weights_kernel<TI, TO, UB_LAYOUT_S2D><<<grid, block, 0, s>>>(
         static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   else
     permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM_DENSE><<<grid, block, 0, s>>>(
@@ -254,8 +260,15 @@ extern "C" int ub_permute_weights(const void* W, int dtype_in, int O, int I, int
   if (!W || !rows || !cols || !out) return fail(UB_EINVAL, "ub_permute_weights: null pointer");
   if (O < 1 || I < 1 || kh < 1 || kw < 1 || n_rows < 1 || n_cols < 1)
     return fail(UB_EINVAL, "ub_permute_weights: bad sizes");
-  if (layout != UB_LAYOUT_OIHW && layout != UB_LAYOUT_GEMM && layout != UB_LAYOUT_GEMM_DENSE)
+  if (layout != UB_LAYOUT_OIHW && layout != UB_LAYOUT_GEMM && layout != UB_LAYOUT_GEMM_DENSE &&
+      layout != UB_LAYOUT_S2D)
     return fail(UB_EINVAL, "ub_permute_weights: layout");
+  if (layout == UB_LAYOUT_S2D) {
+    if (kh != kw || kw < 2 || 4 * n_cols > 8)
+      return fail(UB_EUNSUPPORTED, "ub_permute_weights: S2D needs a square filter and n_cols <= 2");
+    lead = kw;  // the kernel decomposes k with the filter width
+    cpad = (kw + 1) / 2 * ((kw + 1) / 2) * 8;
+  }
   if (layout == UB_LAYOUT_GEMM_DENSE && kh * kw * n_cols > cpad)
     return fail(UB_EINVAL, "ub_permute_weights: dense K %d > cpad %d", kh * kw * n_cols, cpad);
   if (layout == UB_LAYOUT_GEMM && (lead < 0 || lead + n_cols > cpad))

@@ -19,6 +19,9 @@ void count_launch();
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn();
 PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn();
+// Clear the descriptor bit CUTLASS clears for small tensors on drivers <= 13.1.
+void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes);
+int num_sms();  // multiprocessors of the current device
 
 // Swizzle span in bytes -> CUtensorMapSwizzle.
 inline CUtensorMapSwizzle swizzle_of(int bytes) {
@@ -28,6 +31,17 @@ inline CUtensorMapSwizzle swizzle_of(int bytes) {
     case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
     default: return CU_TENSOR_MAP_SWIZZLE_NONE;
   }
+}
+
+constexpr int kSMs = 148;
+
+// Grid for a grid-stride loop over `work` items: at most 16 CTAs per SM.
+inline int grid_for(long long work, int block, int per_thread = 1) {
+  long long g = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
+  const long long cap = (long long)kSMs * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -60,9 +60,11 @@ class Engine:
     """
 
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
-                 input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True):
+                 input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
+                 stem_s2d: bool = True):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
+        self.stem_s2d = stem_s2d
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -376,7 +378,7 @@ class Engine:
         kk = spec.kernel if spec.op == "conv" else 1
         st = spec.stride if spec.op == "conv" else 1
         pd = spec.pad if spec.op == "conv" else 0
-        lead, cpad = _lib.conv_weight_layout(cin, x.coff, gather_idx is not None)
+        lead, cpad = _lib.conv_weight_layout(cin, x.coff, gather_idx is not None, kk, kk)
         W, rows, cols = ws(lid)
         scale = bias = None
         if info["bn"] is not None:
@@ -417,7 +419,6 @@ class Engine:
         idx_dev = self._i32(idx)
         cin = len(idx)
         assert cin == lay.in_channels
-        kpad = _lib.conv_stem_kpad(cin, spec.kernel, spec.kernel)
         W, rows, cols = ws(lid)
         scale = bias = None
         if info["bn"] is not None:
@@ -428,17 +429,33 @@ class Engine:
         O, I = W.shape[0], W.shape[1]
         rows = rows if rows is not None else range(O)
         cols = cols if cols is not None else range(I)
-        wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=kpad, out_dtype=torch.bfloat16)
-        self._keep.append(wg)
         assert info.get("residual") is None and info["out"] not in output_feed
         y = self._alloc(info["out"], lay.out_channels)
         relu = info["relu"] is not None
         x = self.input_buf
         cout, kk, st, pd = lay.out_channels, spec.kernel, spec.stride, spec.pad
-        op.launch = lambda: K.conv_stem(x, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
         ci, hi, wi = self.input_chw
+        # space-to-depth stem when the folded 2x2 pixel fits 16 bytes (ub_conv_s2d); else the
+        # single-launch im2col stem
+        s2d = (self.stem_s2d and st == 2 and kk >= 2 and 4 * cin <= 8 and cout <= 128
+               and y.cstride % 8 == 0 and y.coff % 8 == 0)
+        if s2d:
+            wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
+            sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
+            self._keep += [wg, sbuf]
+            op.launch = lambda: K.stem_s2d(x, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias, relu=relu)
+            op.info["stem_kind"] = "s2d"
+            wbytes = 2.0 * wg.numel()
+        else:
+            kpad = _lib.conv_stem_kpad(cin, kk, kk)
+            wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=kpad,
+                                   out_dtype=torch.bfloat16)
+            self._keep.append(wg)
+            op.launch = lambda: K.conv_stem(x, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
+            op.info["stem_kind"] = "im2col"
+            wbytes = 2.0 * cout * kpad
         flops = 2.0 * cout * cin * kk * kk * y.H * y.W
-        byts = 4.0 * ci * hi * wi + 2.0 * cout * y.H * y.W + (2.0 * cout * kpad) / self.batch
+        byts = 4.0 * ci * hi * wi + 2.0 * cout * y.H * y.W + wbytes / self.batch
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
     # ------------------------------------------------------------------ execution

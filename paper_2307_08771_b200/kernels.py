@@ -90,6 +90,10 @@ def permute_weights(W: torch.Tensor, rows, cols, row_scale: torch.Tensor | None 
     elif layout == "dense":
         out = torch.empty((nr, cpad), dtype=out_dtype, device=W.device)
         lay = _lib.UB_LAYOUT_GEMM_DENSE
+    elif layout == "s2d":  # [rows][kq][kq][8] (ub_conv_s2d)
+        kq = (kw + 1) // 2
+        out = torch.empty((nr, kq * kq * 8), dtype=out_dtype, device=W.device)
+        lay = _lib.UB_LAYOUT_S2D
     else:
         out = torch.empty((nr, kh * kw, cpad), dtype=out_dtype, device=W.device)
         lay = _lib.UB_LAYOUT_GEMM
@@ -161,6 +165,24 @@ def conv_stem(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, kpad
     d.y_dtype = _lib.UB_BF16
     d.x_nchw_f32, d.x_channels = 1, C
     _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
+
+
+def s2d_buffer(N: int, H: int, W: int, k: int, pad: int, device) -> torch.Tensor:
+    """Zeroed staging buffer of the space-to-depth stem (bf16 rows of 8)."""
+    _, _, nbytes = _lib.stem_s2d_geometry(N, H, W, k, pad)
+    return torch.zeros(nbytes // 2, dtype=torch.bfloat16, device=device)
+
+
+def stem_s2d(x_nchw: torch.Tensor, idx_dev: torch.Tensor, s_buf: torch.Tensor, w: torch.Tensor, cout: int, k: int,
+             pad: int, y: Act, bias: torch.Tensor | None = None, relu: bool = False) -> None:
+    """Stride-2 stem as pack (fp32 NCHW + GATHER -> 2x2-folded bf16) + stride-1 tcgen05 conv;
+    w is UB_LAYOUT_S2D."""
+    N, C, H, W = x_nchw.shape
+    lib = _lib.load()
+    _lib.check(lib.ub_stem_s2d_pack(_p(x_nchw), N, C, H, W, _p(idx_dev), idx_dev.numel(), k, pad, _p(s_buf),
+                                    _stream()))
+    _lib.check(lib.ub_conv_s2d(_p(s_buf), N, H, W, k, pad, _p(w), cout, _p(bias), int(relu), _p(y.buf), y.cstride,
+                               y.coff, _stream()))
 
 
 def stage_input(x: torch.Tensor, y: Act, idx_dev: torch.Tensor | None = None) -> None:

@@ -11,7 +11,7 @@ from paper_2307_08771_b200.configs import CONFIGS, build_spatial_model
 @pytest.fixture
 def stub_kernels(monkeypatch):
     monkeypatch.setattr(K, "permute_weights", lambda W, rows, cols, **kw: torch.zeros(1))
-    monkeypatch.setattr(_lib, "conv_weight_layout", lambda cin, coff, g: (0 if g else coff & 7, 64))
+    monkeypatch.setattr(_lib, "conv_weight_layout", lambda cin, coff, g, kh=1, kw=1: (0 if g else coff & 7, 64))
     monkeypatch.setattr(_lib, "conv_stem_kpad", lambda cin, kh, kw: 128)
 
 

@@ -47,6 +47,12 @@ CASES = [
     ("two_ntiles_unaligned_390", 4, 14, 14, 232, 66, 128, 390, 1, 2, 0, 0, True, True, True, False),
     ("three_ntiles_700_gather", 2, 7, 7, 512, 0, 512, 700, 1, 1, 0, 300, True, False, False, False),
     ("1x1_s2_misaligned", 2, 56, 56, 56, 17, 32, 256, 1, 2, 0, 0, True, False, False, False),
+    # packed taps (cin + lead <= 32): several filter taps per 64-wide K-block
+    ("packed_3x3_c16", 2, 28, 28, 16, 0, 16, 64, 3, 1, 1, 0, True, False, True, False),
+    ("packed_3x3_c24_lead5", 2, 20, 20, 64, 5, 24, 40, 3, 1, 1, 0, True, True, True, False),
+    ("packed_3x3_s2_c8", 2, 30, 30, 8, 0, 8, 96, 3, 2, 1, 0, False, False, False, False),
+    ("packed_5x5_c3_ragged", 2, 17, 19, 8, 0, 3, 32, 5, 1, 2, 0, True, False, False, False),
+    ("packed_4x4_s1_p0_c8", 2, 115, 115, 8, 0, 8, 64, 4, 1, 0, 0, True, False, True, False),
 ]
 
 
@@ -64,12 +70,12 @@ def test_conv_matches_torch(case):
         xin = xfull[:, idx.long()]
         xa = x
         idx_dev = idx.to(dev)
-        lead, cpad = _lib.conv_weight_layout(ng, 0, True)
+        lead, cpad = _lib.conv_weight_layout(ng, 0, True, k, k)
     else:
         xa = x.view(coff, cin)
         xin = xfull[:, coff:coff + cin]
         idx_dev = None
-        lead, cpad = _lib.conv_weight_layout(cin, coff, False)
+        lead, cpad = _lib.conv_weight_layout(cin, coff, False, k, k)
     nin = Wt.shape[1]
     wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(nin)),
                            layout="gemm", lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
@@ -121,6 +127,35 @@ def test_stem_matches_torch(N, cin, idx):
     ref = torch.nn.functional.conv2d(_bf(x[:, idx]), _bf(Wt), stride=2, padding=3) + bias.view(1, -1, 1, 1)
     ref = ref.clamp_min(0)
     assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,k,pad,idx,cout", [(2, 224, 7, 3, [2, 0], 64), (3, 224, 7, 3, [1], 32),
+                                                (2, 37, 5, 2, [0, 2], 40), (1, 20, 3, 1, [1, 0], 16),
+                                                (1, 300, 7, 3, [0, 1], 128), (2, 64, 7, 3, [2, 1], 60)])
+def test_stem_s2d_matches_torch(N, H, k, pad, idx, cout):
+    """Space-to-depth stem: pack (fp32 NCHW + GATHER -> 2x2-folded rows) + stride-1 tcgen05 conv."""
+    dev = "cuda"
+    cin = len(idx)
+    g = torch.Generator().manual_seed(N * 100 + H + k)
+    x = torch.randn(N, 3, H, H, generator=g)
+    Wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
+    bias = torch.randn(cout, generator=g)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)), layout="s2d",
+                           out_dtype=torch.bfloat16)
+    Ho = (H + 2 * pad - k) // 2 + 1
+    y = K.empty_act(N, Ho, Ho, cout + 8, dev)
+    y.buf.fill_(float("nan"))
+    y = y.view(8, cout)
+    sbuf = K.s2d_buffer(N, H, H, k, pad, dev)
+    K.stem_s2d(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), sbuf, wg, cout, k, pad, y,
+               bias=bias.to(dev), relu=True)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(_bf(x[:, idx]), _bf(Wt), stride=2, padding=pad) + bias.view(1, -1, 1, 1)
+    ref = ref.clamp_min(0)
+    out = y.buf[:, 8:8 + cout].float().reshape(N, Ho, Ho, cout).permute(0, 3, 1, 2).cpu()
+    assert torch.isfinite(out).all()
+    assert _rel(out, ref) < 1e-2
+    assert torch.isnan(y.buf[:, :8].float()).all()
 
 
 def test_permute_weights_bit_exact():

@@ -43,11 +43,16 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_host_only_helpers(lib):
-    assert lib.ub_abi_version() == 3
+    assert lib.ub_abi_version() == 4
     assert _lib.conv_weight_layout(100, 13, False) == (5, 128)   # misaligned slice: lead 5, 105 -> 128
     assert _lib.conv_weight_layout(12, 0, False) == (0, 16)      # BK 16
     assert _lib.conv_weight_layout(32, 0, False) == (0, 32)      # BK 32
     assert _lib.conv_weight_layout(128, 7, True) == (0, 128)     # gather: no lead
+    assert _lib.conv_weight_layout(16, 0, False, 3, 3) == (0, 16)   # packed taps: 4 per K-block
+    assert _lib.conv_weight_layout(24, 5, False, 3, 3) == (5, 32)   # 29 -> 32: 2 taps per K-block
+    assert _lib.conv_weight_layout(2, 0, False, 7, 7) == (0, 8)
+    assert _lib.conv_weight_layout(48, 0, False, 3, 3) == (0, 64)   # too wide to pack
+    assert _lib.conv_weight_layout(16, 0, True, 3, 3) == (0, 64)    # gather reads never pack
     assert _lib.conv_stem_kpad(2, 7, 7) == 128
     with pytest.raises(_lib.UBError):
         _lib.conv_weight_layout(0, 0, False)

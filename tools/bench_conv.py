@@ -33,6 +33,8 @@ CASES = {
     "small_gather_multi": (8, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, True, True),
     "small_3x3_res_multi": (8, 56, 56, 64, 0, 64, 64, 3, 1, 1, 0, True, True),
     "small_stem_multi": (4, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),
+    "stem_s2d_4x4": (256, 115, 115, 8, 0, 8, 64, 4, 1, 0, 0, False, True),
+    "l1_conv2_c16": (256, 56, 56, 16, 0, 16, 64, 3, 1, 1, 0, False, True),
 }
 
 
@@ -46,11 +48,11 @@ def run(name, check=True, iters=20, once=False):
     Wt = (torch.randn(cout, nin, k, k, device=dev, generator=g) / (nin * k * k) ** 0.5).contiguous()
     if ng:
         idx = torch.randperm(cin, device=dev, generator=g)[:ng].sort().values.to(torch.int32)
-        xa, lead, cpad = x, *_lib.conv_weight_layout(ng, 0, True)
+        xa, lead, cpad = x, *_lib.conv_weight_layout(ng, 0, True, k, k)
     else:
         idx = None
         xa = x.view(coff, cin)
-        lead, cpad = _lib.conv_weight_layout(cin, coff, False)
+        lead, cpad = _lib.conv_weight_layout(cin, coff, False, k, k)
     wg = K.permute_weights(Wt, list(range(cout)), list(range(nin)), layout="gemm", lead=lead, cpad=cpad,
                            out_dtype=torch.bfloat16)
     Ho = (H + 2 * pad - k) // st + 1
