@@ -61,10 +61,11 @@ class Engine:
 
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
-                 stem_s2d: bool = True):
+                 stem_s2d: bool = True, cover_ratio: float = 2.5):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
+        self.cover_ratio = cover_ratio
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -359,26 +360,20 @@ class Engine:
             return self._bind_stem(op, ws, vs, output_feed)
         x = self._value(info["src"])
         read = info["read"]
-        gather_idx = None
+        gather = None  # reference GATHER params (channel indices into x)
         if read is not None:
             rl = self.graph.layer(read)
             if rl.kind is LayerKind.SLICE:
-                s, n = rl.params
-                x = x.view(s, n)
+                s0, n = rl.params
+                x = x.view(s0, n)
             else:
-                # Internal K order: the gathered channels sorted by source position, so each
-                # 64-wide k-block reads a narrow window of the producer's rows.  The weight
-                # columns follow the same order (a GEMM is invariant to a consistent K
-                # permutation); the exported (perm, indices) stay the reference's.
-                k_order = sorted(range(len(rl.params)), key=lambda k: (rl.params[k], k))
-                gather_idx = self._i32([rl.params[k] for k in k_order])
-        cin = gather_idx.numel() if gather_idx is not None else x.C
+                gather = list(rl.params)
+        cin = len(gather) if gather is not None else x.C
         assert cin == lay.in_channels, f"{lid}: reads {cin} channels, layer has {lay.in_channels}"
         cout = lay.out_channels
         kk = spec.kernel if spec.op == "conv" else 1
         st = spec.stride if spec.op == "conv" else 1
         pd = spec.pad if spec.op == "conv" else 0
-        lead, cpad = _lib.conv_weight_layout(cin, x.coff, gather_idx is not None, kk, kk)
         W, rows, cols = ws(lid)
         scale = bias = None
         if info["bn"] is not None:
@@ -387,20 +382,56 @@ class Engine:
             if self.specs[info["bn"]].op != "bn":
                 scale = None
         O, I = W.shape[0], W.shape[1]
-        rows = rows if rows is not None else range(O)
-        cols = cols if cols is not None else range(I)
-        if gather_idx is not None:
-            cols = [list(cols)[k] for k in k_order]
-        wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="gemm", lead=lead, cpad=cpad,
-                               out_dtype=torch.bfloat16)
-        self._keep.append(wg)
+        rows = list(rows if rows is not None else range(O))
+        cols = list(cols if cols is not None else range(I))
+
+        # Read plans for this layer's input (autotune() times them):
+        #   ("slice", ...)  contiguous window -- zero-copy view (UPSCALE's contiguous read)
+        #   ("gather", ...) fused gather: producer warps gather the channels; internal K order is
+        #                   the gathered channels sorted by source position (a GEMM is invariant to
+        #                   a consistent K permutation), the exported (perm, indices) stay the
+        #                   reference's
+        #   ("cover", ...)  the gather's covering window read as a slice, with zero weight columns
+        #                   for the channels the gather drops (same result; cp.async operand path)
+        plans = []
+
+        def add_plan(kind, xv, gidx, wcols, width):
+            lead, cpad = _lib.conv_weight_layout(width, xv.coff, gidx is not None, kk, kk)
+            wg = K.permute_weights(W, rows, wcols, row_scale=scale, layout="gemm", lead=lead, cpad=cpad,
+                                   out_dtype=torch.bfloat16)
+            self._keep.append(wg)
+            plans.append((kind, xv, gidx, lead, cpad, wg))
+
+        if gather is None:
+            add_plan("slice", x, None, cols, cin)
+        else:
+            k_order = sorted(range(cin), key=lambda k: (gather[k], k))
+            add_plan("gather", x, self._i32([gather[k] for k in k_order]), [cols[k] for k in k_order], cin)
+            lo, hi = min(gather), max(gather)
+            width = hi - lo + 1
+            if (self.gather_mode == "fused" and lo >= 0 and len(set(gather)) == cin
+                    and width <= self.cover_ratio * cin):
+                pos = {c: k for k, c in enumerate(gather)}
+                wcols = [cols[pos[lo + j]] if (lo + j) in pos else -1 for j in range(width)]
+                add_plan("cover", x.view(lo, width), None, wcols, width)
         residual = self._value(info["residual"]) if info.get("residual") else None
         fp32_out = info["out"] in output_feed
         y = self._alloc(info["out"], cout, fp32=fp32_out)
         relu = info["relu"] is not None
-        op.info["variant"] = 0  # producer width: 0 = library heuristic; set by autotune()
-        op.launch = lambda: K.conv(x, wg, lead, cpad, cout, kk, kk, st, pd, y, gather_idx=gather_idx, bias=bias,
-                                   residual=residual, relu=relu, y_fp32=fp32_out, variant=op.info["variant"])
+        # variant = (plan index, producer width: 0 = library heuristic, 1 = 256, 2 = 512 threads)
+        op.info["variants"] = [(pi, pw) for pi in range(len(plans)) for pw in (1, 2)]
+        op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
+        op.info["plans"] = [pl[0] for pl in plans]
+
+        def launch():
+            pi, pw = op.info["variant"]
+            _, xv, gidx, lead, cpad, wg = plans[pi]
+            K.conv(xv, wg, lead, cpad, cout, kk, kk, st, pd, y, gather_idx=gidx, bias=bias, residual=residual,
+                   relu=relu, y_fp32=fp32_out, variant=pw)
+
+        op.launch = launch
+        op.info["desc"] = (f"{kk}x{kk}s{st} {cin}->{cout} {x.H}x{x.W}"
+                           f"{' gather' if gather is not None else ''}{' +res' if residual is not None else ''}")
         # roofline bookkeeping (per image)
         _, hi, wi = self._shapes[info["src"]] if info["src"] in self._shapes else (0, x.H, x.W)
         ho, wo = y.H, y.W
@@ -479,15 +510,16 @@ class Engine:
             t = t.reshape(o.N, o.H, o.W, o.C).permute(0, 3, 1, 2)
         return t.float()
 
-    def autotune(self, reps: int = 3) -> dict[str, int]:
-        """Pick the conv kernel's producer width (256 vs 512 cp.async threads) per layer by
-        timing both on this engine's own buffers (CUDA events, after a warm-up)."""
+    def autotune(self, reps: int = 3) -> dict[str, tuple]:
+        """Pick, per conv layer, the read plan (fused gather vs covering slice) and the
+        producer width (256 vs 512 cp.async threads) by timing every combination on this
+        engine's own buffers (CUDA events, after a warm-up)."""
         picks = {}
         for op in self.ops:
             if op.kind != "conv" or "stem_idx" in op.info:
                 continue
             best = None
-            for v in (1, 2):
+            for v in op.info["variants"]:
                 op.info["variant"] = v
                 op.launch()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

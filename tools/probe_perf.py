@@ -55,14 +55,27 @@ def main():
         f = st.flops * N if st else 0.0
         b = (st.bytes + st.gather_bytes) * N if st else 0.0
         troof = max(f / PEAKS["tc"], b / PEAKS["hbm"]) * 1e3
-        rows.append((op.kind, name, t, f / 1e9, b / 1e6, troof))
+        rows.append((op.kind, name, t, f / 1e9, b / 1e6, troof, op.info.get("desc", "")))
     tot = sum(r[2] for r in rows)
     troof = sum(r[5] for r in rows)
-    for r in sorted(rows, key=lambda r: -r[2])[:25]:
-        print(f"{r[0]:8s} {r[1]:28s} {r[2]*1e3:8.1f} us  {r[3]:8.2f} GF {r[4]:8.1f} MB  roof {r[5]*1e3:7.1f} us  "
-              f"frac {r[5]/max(r[2],1e-9):.2f}")
+    for r in sorted(rows, key=lambda r: -r[2])[:int(sys.argv[5]) if len(sys.argv) > 5 else 25]:
+        print(f"{r[0]:8s} {r[1]:24s} {r[2]*1e3:7.1f} us {r[3]:6.2f} GF {r[4]:6.1f} MB roof {r[5]*1e3:6.1f} us "
+              f"frac {r[5]/max(r[2],1e-9):.2f}  {r[6]}")
+    cats = {}
+    for r in rows:
+        d = r[6]
+        key = r[0] if not d else (d.split()[0] + (" gather" if "gather" in d else ""))
+        c = cats.setdefault(key, [0.0, 0.0, 0])
+        c[0] += r[2]
+        c[1] += r[5]
+        c[2] += 1
+    for k, (t, tr, n) in sorted(cats.items(), key=lambda kv: -kv[1][0]):
+        print(f"  {k:16s} x{n:2d} {t*1e3:8.1f} us  roof {tr*1e3:7.1f} us  frac {tr/max(t,1e-9):.2f}")
     print(f"eager sum {tot:.3f} ms, roofline {troof:.3f} ms, frac {troof/tot:.3f}")
     eng.capture()
+    for op in eng.ops:
+        if "plans" in op.info and len(op.info["plans"]) > 1:
+            print("  pick", op.info["conv"], op.info["plans"][op.info["variant"][0]], op.info["variant"][1])
     for _ in range(3):
         eng._graph_exec.replay()
     torch.cuda.synchronize()
