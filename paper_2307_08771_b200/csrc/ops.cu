@@ -332,6 +332,92 @@ extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const 
   return cuda_status(cudaGetLastError(), "stage_input_kernel");
 }
 
+// Row-staged max pool for the 3x3 / stride-2 window (ResNet's): one CTA per band of ROWS
+// output rows of one image.  Each thread owns fixed 16-byte pieces (w, channel group) of the
+// input rows; per output row it loads input rows 2h and 2h+1 and carries row 2h-1 from the
+// previous output row in registers, so every input row is read once per band (bf16 max is
+// exact: __hmax2 on packed pairs).  The vertical maxima go to a shared [W][groups] row and
+// each output pixel then takes the horizontal window of that row.
+constexpr int MP_ROWS = 4;     // output rows per CTA
+constexpr int MP_PER_T = 4;    // 16-byte pieces per thread per input row (W*groups <= 4*blockDim)
+__global__ void maxpool3s2_rows_kernel(const uint4* __restrict__ x, int H, int W, int groups, int x_cs16,
+                                       int x_co16, int Ho, int Wo, uint4* __restrict__ y, int y_cs16, int y_co16) {
+  extern __shared__ uint4 vrow[];  // [W][groups]
+  const int bands = (Ho + MP_ROWS - 1) / MP_ROWS;
+  const int img = blockIdx.x / bands;
+  const int ho0 = (blockIdx.x - img * bands) * MP_ROWS;
+  const int total = W * groups;
+  const __nv_bfloat162 ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+  uint4 ninf4;
+  {
+    __nv_bfloat162* v = reinterpret_cast<__nv_bfloat162*>(&ninf4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = ninf;
+  }
+  size_t off[MP_PER_T];
+#pragma unroll
+  for (int b = 0; b < MP_PER_T; ++b) {
+    const int e = threadIdx.x + b * blockDim.x;
+    const int wi = e / groups, g = e - (e / groups) * groups;
+    off[b] = static_cast<size_t>(wi) * x_cs16 + x_co16 + g;
+  }
+  const uint4* ximg = x + static_cast<size_t>(img) * H * W * x_cs16;
+  uint4 carry[MP_PER_T];
+  {
+    const int r = 2 * ho0 - 1;
+#pragma unroll
+    for (int b = 0; b < MP_PER_T; ++b) {
+      const int e = threadIdx.x + b * blockDim.x;
+      carry[b] = (r >= 0 && r < H && e < total) ? __ldg(ximg + static_cast<size_t>(r) * W * x_cs16 + off[b]) : ninf4;
+    }
+  }
+  const int ho1 = min(ho0 + MP_ROWS, Ho);
+  for (int ho = ho0; ho < ho1; ++ho) {
+    const int ra = 2 * ho, rb = 2 * ho + 1;
+    uint4 a[MP_PER_T], c[MP_PER_T];
+#pragma unroll
+    for (int b = 0; b < MP_PER_T; ++b) {
+      const int e = threadIdx.x + b * blockDim.x;
+      a[b] = (ra < H && e < total) ? __ldg(ximg + static_cast<size_t>(ra) * W * x_cs16 + off[b]) : ninf4;
+      c[b] = (rb < H && e < total) ? __ldg(ximg + static_cast<size_t>(rb) * W * x_cs16 + off[b]) : ninf4;
+    }
+    if (ho > ho0) __syncthreads();  // previous row's horizontal pass is done with vrow
+#pragma unroll
+    for (int b = 0; b < MP_PER_T; ++b) {
+      const int e = threadIdx.x + b * blockDim.x;
+      uint4 m = carry[b];
+      __nv_bfloat162* mv = reinterpret_cast<__nv_bfloat162*>(&m);
+      const __nv_bfloat162* av = reinterpret_cast<const __nv_bfloat162*>(&a[b]);
+      const __nv_bfloat162* cv = reinterpret_cast<const __nv_bfloat162*>(&c[b]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], __hmax2(av[i], cv[i]));
+      if (e < total) vrow[e] = m;
+      carry[b] = c[b];
+    }
+    __syncthreads();
+    uint4* yrow = y + static_cast<size_t>(img * Ho + ho) * Wo * y_cs16 + y_co16;
+    for (int e = threadIdx.x; e < Wo * groups; e += blockDim.x) {
+      const int wo = e / groups, g = e - (e / groups) * groups;
+      const int w0 = 2 * wo - 1;
+      uint4 m = vrow[(2 * wo) * groups + g];
+      __nv_bfloat162* mv = reinterpret_cast<__nv_bfloat162*>(&m);
+      if (w0 >= 0) {
+        const uint4 u = vrow[w0 * groups + g];
+        const __nv_bfloat162* uv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], uv[i]);
+      }
+      if (w0 + 2 < W) {
+        const uint4 u = vrow[(w0 + 2) * groups + g];
+        const __nv_bfloat162* uv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], uv[i]);
+      }
+      yrow[static_cast<size_t>(wo) * y_cs16 + g] = m;
+    }
+  }
+}
+
 extern "C" int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int stride,
                             int pad, int Ho, int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream) {
   if (!x || !y || N < 1 || C < 1 || k < 1 || stride < 1) return fail(UB_EINVAL, "ub_maxpool2d: bad arguments");
@@ -339,6 +425,21 @@ extern "C" int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cst
                    (y_cstride % 8 == 0) && (y_coff % 8 == 0);
   const long long total = (long long)N * Ho * Wo * ((C + 7) / 8);
   if (total >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_maxpool2d: tensor too large");
+  const int groups = (C + 7) / 8;
+  const size_t row_smem = static_cast<size_t>(W) * groups * 16;
+  // whole 16-byte groups; a ragged last group is allowed when it is the tail of both rows
+  // (the padding channels of y get the max of x's padding channels)
+  const bool whole = C % 8 == 0 || (y_coff + groups * 8 == y_cstride && x_coff + groups * 8 <= x_cstride);
+  const int block = 256;
+  if (vec && whole && k == 3 && stride == 2 && pad == 1 && W * groups <= MP_PER_T * block &&
+      row_smem <= 48 * 1024 && (long long)N * ((Ho + MP_ROWS - 1) / MP_ROWS) < (1ll << 31)) {
+    const int grid = N * ((Ho + MP_ROWS - 1) / MP_ROWS);
+    maxpool3s2_rows_kernel<<<grid, block, row_smem, stream>>>(static_cast<const uint4*>(x), H, W, groups,
+                                                              x_cstride / 8, x_coff / 8, Ho, Wo,
+                                                              static_cast<uint4*>(y), y_cstride / 8, y_coff / 8);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "maxpool3s2_rows_kernel");
+  }
   maxpool_kernel<<<grid_for(total, 256), 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(x), N, H, W, C, x_cstride, x_coff, k, stride, pad, Ho, Wo,
       static_cast<__nv_bfloat16*>(y), y_cstride, y_coff, vec);

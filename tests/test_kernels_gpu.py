@@ -199,6 +199,25 @@ def test_channel_gather_and_pools():
     assert _rel(ya.to_nchw().cpu().reshape(2, 40), refa) < 1e-2
 
 
+@pytest.mark.parametrize("H,C,coff,k,st,pd", [(112, 64, 0, 3, 2, 1), (57, 48, 16, 3, 2, 1), (20, 24, 8, 2, 2, 0),
+                                             (30, 60, 0, 3, 2, 1)])
+def test_maxpool_rows_matches_torch(H, C, coff, k, st, pd):
+    """Row-staged max pool (bit-exact: max of bf16 values); C = 60 is the ragged-tail case."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(H + C)
+    ragged = C % 8 != 0
+    x = torch.randn(3, C + coff + (0 if ragged else 8), H, H + 3, generator=g)
+    xa = K.act_from_nchw(x.to(dev)).view(coff, C)
+    Ho = (H + 2 * pd - k) // st + 1
+    Wo = (H + 3 + 2 * pd - k) // st + 1
+    yp = K.empty_act(3, Ho, Wo, C if ragged else C + 8, dev)
+    yp = yp if ragged else yp.view(8, C)
+    K.maxpool(xa, k, st, pd, yp)
+    torch.cuda.synchronize()
+    refp = torch.nn.functional.max_pool2d(_bf(x[:, coff:coff + C]), k, st, pd)
+    assert torch.equal(yp.to_nchw().cpu(), refp)
+
+
 def test_stage_input_gathers_channels():
     dev = "cuda"
     x = torch.randn(2, 3, 8, 8)
