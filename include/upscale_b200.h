@@ -127,7 +127,8 @@ typedef struct {
                                   [N][x_channels][H][W]; gather_idx selects the cin planes
                                   (the INPUT node's GATHER), weights UB_LAYOUT_GEMM_DENSE */
   int x_channels;
-  int variant;                 /* 0: heuristic; 1: 256 producer threads; 2: 512 (autotuned by the engine) */
+  int variant;                 /* bits 0-1 producer width (0 heuristic, 1: 256, 2: 512 threads);
+                                  bit 2: re-load weights per tile (no weight-stationary B) */
 } ub_conv_desc;
 
 /* Dense-K padding (multiple of 64) of the fused-stem weight operand. */

@@ -91,6 +91,7 @@ struct ConvKParams {
   void* y;  // direct-store fallback only
   int y_cstride, y_coff, y_f32;
   int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
+  int b_res;  // weights of this CTA's N tile stay resident in smem (loaded once; grid % n_tiles == 0)
 };
 
 // Align the dynamic smem base to 1024 B by pointer arithmetic on the __shared__ pointer itself
@@ -132,8 +133,8 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   const int stages = p.stages;
 
   uint8_t* sA = smem;
-  uint8_t* sB = sA + stages * A_BYTES;
-  uint8_t* sI = sB + stages * b_stride;                         // identity 64x64 (8 KB)
+  uint8_t* sB = sA + stages * A_BYTES;  // per-stage B, or all k-blocks of B when resident
+  uint8_t* sI = sB + (p.b_res ? p.num_kb : stages) * b_stride;  // identity 64x64 (8 KB)
   uint8_t* sE = sI + IDENT_BYTES;                               // 4 warps x 2 output slots
   float* sBias = reinterpret_cast<float*>(sE + 4 * EPI_WARP_BYTES);  // 4 warps x MAX_BLOCK_N
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + 4 * MAX_BLOCK_N);
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   uint64_t* tfull = empty + stages;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres = tempty + 3;  // resident B landed (PRODUCERS cp.async arrivals)
   int4* stem_tab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // A_STEM / A_PACKED
 
   const int warp = threadIdx.x >> 5;
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    mbar_init(bres, PRODUCERS);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       const uint32_t i_base = smem_u32(sI);
       int s = 0, it = 0;
       uint32_t ph = 0;
+      if (p.b_res) mbar_wait(bres, 0);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         const int n0 = (t % p.n_tiles) * p.block_n;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           if (!(p.dbg & 4)) {
             if (kb < nk) {
-              const uint32_t b_base = smem_u32(sB + s * b_stride);
+              const uint32_t b_base = smem_u32(sB + (p.b_res ? kb : s) * b_stride);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
                 umma_bf16_warp(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT),
@@ -273,6 +277,26 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     const uint32_t rdst0 = swz<64>(rrow0, rj);
     int s = 0;
     uint32_t ph = 0;
+    if (p.b_res) {  // all k-blocks of this CTA's N tile, once
+      const int n0 = (blockIdx.x % p.n_tiles) * p.block_n;
+      const int b_valid = min(p.block_n, p.cout - n0);
+      const uint16_t* b_base = p.w + static_cast<size_t>(n0 + row0) * p.K_total + cj * 8;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int kcoord = kb * BK;
+        const uint32_t tileB = smem_u32(sB + kb * b_stride);
+        const uint16_t* src = b_base + kcoord;
+        const bool k_ok = AMODE != A_PACKED || kcoord + cj * 8 < p.K_total;
+        for (int i = 0; i < nb_pieces; ++i, src += b_row_stride) {
+          const int n = row0 + i * ROW_STEP;
+          if (n >= p.block_n) break;
+          const bool ok = n < b_valid && k_ok;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tileB + dst0 + i * ROW_STEP * ROW_BYTES),
+                       "l"(ok ? src : p.w), "r"(ok ? 16u : 0u)
+                       : "memory");
+        }
+      }
+      cp_async_arrive_noinc(bres);
+    }
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
@@ -427,7 +451,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           }
         }
         // ---- B (weights [cout][K_total]): rows row0 + i * ROW_STEP, chunk cj
-        {
+        if (!p.b_res) {
           const uint16_t* src = b_base + kcoord;
           const bool k_ok = AMODE != A_PACKED || kcoord + cj * 8 < p.K_total;  // packed: last k-block ragged
           for (int i = 0; i < nb_pieces; ++i, src += b_row_stride) {
@@ -818,9 +842,15 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
 
   const uint32_t a_bytes = BLOCK_M * 128;  // sized for 64-wide residual k-blocks
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
-  const uint32_t stage_bytes = a_bytes + b_stride;
-  const uint32_t fixed = 1024 + IDENT_BYTES + 4 * EPI_WARP_BYTES + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
-                         ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
+  uint32_t fixed = 1024 + IDENT_BYTES + 4 * EPI_WARP_BYTES + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
+                   ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
+  // Weight-stationary B: when all k-blocks of one N tile fit next to >= 4 A stages, each CTA
+  // keeps its N tile's weights in smem (grid a multiple of n_tiles, so a CTA's tiles share
+  // one N tile) instead of re-loading B for every tile.
+  const uint32_t b_res_bytes = static_cast<uint32_t>(p.num_kb) * b_stride;
+  p.b_res = !(d->variant & 4) && p.n_tiles <= num_sms() && fixed + b_res_bytes + 4 * a_bytes <= 226u * 1024u;
+  if (p.b_res) fixed += b_res_bytes;
+  const uint32_t stage_bytes = a_bytes + (p.b_res ? 0u : b_stride);
   const uint32_t budget = 226u * 1024u - fixed;
   int stages = static_cast<int>(budget / stage_bytes);
   stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
@@ -845,9 +875,11 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   }
 
   const int num_tiles = p.m_tiles * p.n_tiles;
-  const int grid = num_tiles < num_sms() ? num_tiles : num_sms();
+  int grid = num_tiles < num_sms() ? num_tiles : num_sms();
+  if (p.b_res && grid % p.n_tiles) grid = grid / p.n_tiles * p.n_tiles;
   // producer width: explicit variant from the caller (engine autotune), else a heuristic
-  int wide = d->variant == 2 ? 1 : (d->variant == 1 ? 0 : (p.has_res ? 0 : 1));
+  const int pw = d->variant & 3;
+  int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
   if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream, wide);
   if (packed) return launch_conv<A_PACKED, 64>(tmY, p, grid, smem, stream, wide);

@@ -418,8 +418,10 @@ class Engine:
         fp32_out = info["out"] in output_feed
         y = self._alloc(info["out"], cout, fp32=fp32_out)
         relu = info["relu"] is not None
-        # variant = (plan index, producer width: 0 = library heuristic, 1 = 256, 2 = 512 threads)
-        op.info["variants"] = [(pi, pw) for pi in range(len(plans)) for pw in (1, 2)]
+        # variant = (plan index, kernel variant bits: producer width 0 = library heuristic,
+        # 1 = 256, 2 = 512 threads; +4 = re-load the weights per tile instead of keeping them
+        # resident in shared memory)
+        op.info["variants"] = [(pi, pw | nb) for pi in range(len(plans)) for pw in (1, 2) for nb in (0, 4)]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
 
@@ -431,7 +433,9 @@ class Engine:
 
         op.launch = launch
         op.info["desc"] = (f"{kk}x{kk}s{st} {cin}->{cout} {x.H}x{x.W}"
-                           f"{' gather' if gather is not None else ''}{' +res' if residual is not None else ''}")
+                           f"{' gather' if gather is not None else ''}{' +res' if residual is not None else ''}"
+                           f" [coff {plans[-1][1].coff} cs {plans[-1][1].cstride} lead {plans[-1][3]}"
+                           f" cpad {plans[-1][4]}]")
         # roofline bookkeeping (per image)
         _, hi, wi = self._shapes[info["src"]] if info["src"] in self._shapes else (0, x.H, x.W)
         ho, wo = y.H, y.W

@@ -34,6 +34,7 @@ def main():
     for _ in range(3):
         eng.launch_all()
     torch.cuda.synchronize()
+    eng.autotune()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in eng.ops]
     reps = 5
     times = [0.0] * len(eng.ops)
@@ -72,7 +73,7 @@ def main():
     for k, (t, tr, n) in sorted(cats.items(), key=lambda kv: -kv[1][0]):
         print(f"  {k:16s} x{n:2d} {t*1e3:8.1f} us  roof {tr*1e3:7.1f} us  frac {tr/max(t,1e-9):.2f}")
     print(f"eager sum {tot:.3f} ms, roofline {troof:.3f} ms, frac {troof/tot:.3f}")
-    eng.capture()
+    eng.capture(autotune=False)
     for op in eng.ops:
         if "plans" in op.info and len(op.info["plans"]) > 1:
             print("  pick", op.info["conv"], op.info["plans"][op.info["variant"][0]], op.info["variant"][1])

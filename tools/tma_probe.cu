@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ub_common.cuh"
@@ -78,11 +79,11 @@ __global__ void __launch_bounds__(128, 1) probe_store(const __grid_constant__ CU
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
-  const size_t bytes = 1ull << 30;
+  const size_t bytes = (argc > 1 ? atoll(argv[1]) : 1024ll) << 20;
   void* buf;
   cudaMalloc(&buf, bytes);
   cudaMemset(buf, 0, bytes);
