@@ -1,0 +1,347 @@
+// Halo-tile implicit GEMM for stride-1 3x3 convolutions on tcgen05 tensor cores.
+//
+// The im2col operand of a 3x3 conv re-reads every input pixel 9 times; streamed from L2 by
+// cp.async that is the bound of the generic kernel (conv_tc.cu) for the bottleneck convs.
+// Here a tile is R whole output rows of one image, and its input -- the R + 2 rows of the
+// window, each laid out over a padded width Wp (a power of two >= W + 2, zeros outside the
+// image) -- is staged ONCE in shared memory as channel planes:
+//     plane p (channels 8p .. 8p+7) = [position q][8 bf16], q = row * Wp + col.
+// Output position r = j * Wp + x (tile row j) reads input position r + dy * Wp + dx for tap
+// (dy, dx), so the A operand of a tap is the plane block shifted by dy * Wp + dx: 128
+// consecutive 16-byte rows -- a no-swizzle K-major UMMA operand (8-row core matrices,
+// SBO = 128 B) whose two K halves are consecutive planes (LBO = plane stride).  Every tap's
+// MMAs read the same staged block; nothing is copied per tap.  Positions with x >= W (or
+// rows past H) are computed and dropped by the output TMA store's bounds clipping.
+//
+// The weights of all taps stay resident in shared memory (SWIZZLE_128B, one 128-byte row
+// per output channel and tap), loaded once per CTA.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warps 0-3   epilogue: TMEM -> regs, +bias, ReLU, bf16 -> SW128 smem -> 4-D TMA store
+//               (box 64 channels x BX pixels x BY rows of the output)
+//   warp 4      MMA issuer (two TMEM accumulators; one elected lane issues)
+//   warp 5      TMEM allocator
+//   warps 6-13  producers: halo planes by cp.async (zero-fill outside the image)
+#include <cstdlib>
+
+#include "ub_common.cuh"
+#include "ub_host.h"
+
+#include "upscale_b200.h"
+
+namespace ub {
+namespace {
+
+constexpr int HALO_PRODUCERS = 256;
+constexpr int HALO_THREADS = 192 + HALO_PRODUCERS;
+constexpr int HALO_SLOT = 32 * 128;  // one epilogue warp's 32 rows x 64 channels bf16
+
+struct HaloParams {
+  const uint16_t* x;  // at channel (coff - lead)
+  int x_cstride, H, W;
+  int R, Wp, wp_shift, n_pos, planes;
+  uint32_t plane_stride, a_stage_bytes;
+  int a_stages;
+  int tiles, tiles_per_img;
+  int cout, np, acc_cols;
+  uint32_t b_block_bytes;  // np * 128: one tap's weights
+  const uint16_t* w;       // [cout][9][cpad]
+  int cpad;
+  const float* bias;
+  int relu;
+  int bx;  // output box width (pixels); box height = 32 / bx rows
+};
+
+UB_DEVI uint64_t sdesc_plain(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  return d;  // SWIZZLE_NONE
+}
+
+UB_DEVI void tma_store_4d(const void* map, const void* smem, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(HALO_THREADS, 1)
+    conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
+  constexpr int TAPS = 9;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sB = base;                                   // [tap][np rows][128 B], SW128
+  uint8_t* sE = sB + TAPS * p.b_block_bytes;            // 4 warps x 2 slots x 4 KB (1024-aligned)
+  uint8_t* sA = sE + 4 * 2 * HALO_SLOT;                 // a_stages x a_stage_bytes
+  float* sBias = reinterpret_cast<float*>(sA + p.a_stages * p.a_stage_bytes);  // 256 floats
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sBias + 256);
+  uint64_t* aempty = afull + 8;
+  uint64_t* tfull = aempty + 8;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 4 && lane == 0) {
+    for (int s = 0; s < p.a_stages; ++s) {
+      mbar_init(&afull[s], HALO_PRODUCERS);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    mbar_init(bres, HALO_PRODUCERS);
+    fence_mbar_init();
+  }
+  if (warp == 0) tma_prefetch_desc(&tmY);
+  if (warp == 5) tmem_alloc(tmem_slot, 2 * p.acc_cols);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sBias[i] = (p.bias && i < p.cout) ? p.bias[i] : 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp >= 6) {
+    // ================= producers
+    const int pt = threadIdx.x - 192;
+    // resident weights: tap t, row n, 16-byte chunk j (K = 8j .. 8j+7 of the tap) -> SW128
+    const int cp8 = p.cpad >> 3;
+    for (int e = pt; e < TAPS * p.np * cp8; e += HALO_PRODUCERS) {
+      const int t = e / (p.np * cp8);
+      const int rem = e - t * (p.np * cp8);
+      const int n = rem / cp8, j = rem - (rem / cp8) * cp8;
+      const bool ok = n < p.cout;
+      const uint16_t* src = ok ? p.w + (static_cast<size_t>(n) * TAPS + t) * p.cpad + j * 8 : p.w;
+      const uint32_t dst = smem_u32(sB + t * p.b_block_bytes + n * 128 + ((j ^ (n & 7)) << 4));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16u : 0u)
+                   : "memory");
+    }
+    cp_async_arrive_noinc(bres);
+    // halo planes: this thread always fills plane pp of positions q0 + i * qstep
+    const int pp = pt % p.planes;
+    const int q0 = pt / p.planes;
+    const int qstep = HALO_PRODUCERS / p.planes;
+    const int wmask = p.Wp - 1;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      const int img = t / p.tiles_per_img;
+      const int y0 = (t - img * p.tiles_per_img) * p.R - 1;  // first staged input row (pad 1)
+      const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + pp * 8;
+      mbar_wait(&aempty[s], ph ^ 1);
+      const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * p.plane_stride);
+      for (int q = q0; q < p.n_pos; q += qstep) {
+        const int yy = y0 + (q >> p.wp_shift);
+        const int xx = (q & wmask) - 1;
+        const bool ok = yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
+        const uint16_t* src = ok ? ximg + (static_cast<size_t>(yy) * p.W + xx) * p.x_cstride : p.x;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + q * 16), "l"(src),
+                     "r"(ok ? 16u : 0u)
+                     : "memory");
+      }
+      cp_async_arrive_noinc(&afull[s]);
+      if (++s == p.a_stages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == 4) {
+    // ================= MMA issuer (whole warp; one elected lane issues)
+    const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
+    const uint32_t b0 = smem_u32(sB);
+    const int kpairs = p.planes >> 1;
+    mbar_wait(bres, 0);
+    __syncwarp();
+    tc_fence_after();
+    fence_proxy_async_smem();
+    int s = 0, it = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&afull[s], ph);
+      __syncwarp();
+      tc_fence_after();
+      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+      const uint32_t a0 = smem_u32(sA + s * p.a_stage_bytes);
+      const uint32_t d = tmem_base + acc * p.acc_cols;
+#pragma unroll
+      for (int tap = 0; tap < TAPS; ++tap) {
+        const int dy = tap / 3, dx = tap - (tap / 3) * 3;
+        const uint32_t ashift = a0 + ((dy << p.wp_shift) + dx) * 16;
+        for (int j = 0; j < kpairs; ++j)
+          umma_bf16_warp(d, sdesc_plain(ashift + 2 * j * p.plane_stride, p.plane_stride, 128),
+                         make_sdesc(b0 + tap * p.b_block_bytes + j * 32, 1024, 2), idesc,
+                         (tap | j) ? 1u : 0u);
+      }
+      umma_commit_warp(&aempty[s]);
+      umma_commit_warp(&tfull[acc]);
+      if (++s == p.a_stages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp < 4) {
+    // ================= epilogue: warp q owns TMEM lanes / tile rows 32q .. 32q+31
+    const int q = warp;
+    uint8_t* slots = sE + q * 2 * HALO_SLOT;
+    const int by = 32 / p.bx;
+    const int nchunks = (p.np + 63) >> 6;
+    uint32_t ec = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
+      const int img = t / p.tiles_per_img;
+      const int y0 = (t - img * p.tiles_per_img) * p.R;
+      const int r0 = q * 32;
+      const int oy = y0 + (r0 >> p.wp_shift);
+      const int ox = r0 & (p.Wp - 1);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * p.acc_cols + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c = 0; c < nchunks; ++c, ++ec) {
+        uint8_t* slot = slots + (ec & 1) * HALO_SLOT;
+        if (lane == 0) bulk_wait_read<1>();  // this slot's store from two chunks ago has read it
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c * 64 + h * 32;
+          if (col >= p.np) break;
+          uint32_t v[32];
+          if (col + 32 <= p.np) {
+            tmem_ld32(taddr + col, v);
+          } else {
+            tmem_ld16(taddr + col, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+#pragma unroll
+            for (int i = 16; i < 32; ++i) v[i] = 0;
+          }
+          tmem_ld_wait();
+          const float4* bq = reinterpret_cast<const float4*>(sBias + col);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {  // 16-byte chunk jj of this half = channels col + 8jj ..
+            const float4 b0 = bq[2 * jj], b1 = bq[2 * jj + 1];
+            const float2 s0 = add_f32x2(make_float2(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1])),
+                                        make_float2(b0.x, b0.y));
+            const float2 s1 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3])),
+                                        make_float2(b0.z, b0.w));
+            const float2 s2 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 4]), __uint_as_float(v[8 * jj + 5])),
+                                        make_float2(b1.x, b1.y));
+            const float2 s3 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])),
+                                        make_float2(b1.z, b1.w));
+            uint4 o;
+            if (p.relu) {
+              o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y), cvt_relu_bf16x2(s2.x, s2.y),
+                             cvt_relu_bf16x2(s3.x, s3.y));
+            } else {
+              o = make_uint4(cvt_bf16x2(s0.x, s0.y), cvt_bf16x2(s1.x, s1.y), cvt_bf16x2(s2.x, s2.y),
+                             cvt_bf16x2(s3.x, s3.y));
+            }
+            const int chunk = h * 4 + jj;
+            *reinterpret_cast<uint4*>(slot + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o;
+          }
+        }
+        if (c + 1 == nchunks) {  // accumulator drained: hand it back before the store
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmY, slot, c * 64, ox, oy, img);
+          bulk_commit();
+        }
+        (void)by;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * p.acc_cols);
+  }
+}
+
+}  // namespace
+
+// Returns UB_OK with *handled = true when the halo kernel ran; *handled = false (and UB_OK)
+// when the layer is outside its scope (the caller then uses the generic kernel).
+int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
+  *handled = false;
+  if (d->kh != 3 || d->kw != 3 || d->stride != 1 || d->pad != 1 || d->x_nchw_f32 || d->gather_idx ||
+      d->residual || d->y_dtype != UB_BF16 || (d->variant & 8))
+    return UB_OK;
+  if (cpad != 16 && cpad != 32 && cpad != 64) return UB_OK;
+  if (d->cout > 256 || d->y_cstride % 8 || d->y_coff % 8) return UB_OK;
+  int Wp = 8;
+  while (Wp < d->W + 2) Wp <<= 1;
+  if (Wp > 64) return UB_OK;
+  HaloParams p{};
+  p.x = reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
+  p.x_cstride = d->x_cstride;
+  p.H = d->H;
+  p.W = d->W;
+  p.Wp = Wp;
+  p.wp_shift = __builtin_ctz(Wp);
+  p.R = 128 / Wp;
+  p.planes = cpad / 8;
+  p.n_pos = ((p.R + 2) * Wp + 2 + 7) / 8 * 8;
+  p.plane_stride = p.n_pos * 16 + 16;  // odd number of 16-byte units: planes land on different banks
+  p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
+  p.tiles_per_img = (d->H + p.R - 1) / p.R;
+  const long long tiles = static_cast<long long>(d->N) * p.tiles_per_img;
+  if (tiles >= (1ll << 31)) return UB_OK;
+  p.tiles = static_cast<int>(tiles);
+  p.cout = d->cout;
+  p.np = (d->cout + 15) / 16 * 16;
+  p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
+  p.b_block_bytes = static_cast<uint32_t>((p.np + 7) / 8 * 8) * 128;
+  p.w = reinterpret_cast<const uint16_t*>(d->w);
+  p.cpad = cpad;
+  p.bias = d->bias;
+  p.relu = d->relu;
+  p.bx = Wp < 32 ? Wp : 32;
+  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + 4 * 2 * HALO_SLOT + 256 * 4 + 256;
+  const size_t budget = 227 * 1024;
+  if (fixed + 2 * p.a_stage_bytes > budget) return UB_OK;
+  int stages = static_cast<int>((budget - fixed) / p.a_stage_bytes);
+  p.a_stages = stages > 6 ? 6 : stages;
+  const size_t smem = fixed + static_cast<size_t>(p.a_stages) * p.a_stage_bytes;
+
+  if (!encode_tiled_fn()) return fail(UB_ECUDA, "ub_conv_fwd: cannot resolve cuTensorMapEncodeTiled");
+  CUtensorMap tm{};
+  const cuuint64_t cs = static_cast<cuuint64_t>(d->y_cstride) * 2;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d->cout), static_cast<cuuint64_t>(d->Wo),
+                        static_cast<cuuint64_t>(d->Ho), static_cast<cuuint64_t>(d->N)};
+  cuuint64_t strides[3] = {cs, cs * d->Wo, cs * d->Wo * d->Ho};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(p.bx), static_cast<cuuint32_t>(32 / p.bx), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_tiled_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                                 reinterpret_cast<uint16_t*>(d->y) + d->y_coff, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo output tensor map failed (%d)", (int)r);
+  apply_small_tensor_quirk(&tm, static_cast<size_t>(d->N) * d->Ho * d->Wo * d->y_cstride * 2);
+
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_halo3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
+  conv_halo3_kernel<<<grid, HALO_THREADS, smem, stream>>>(tm, p);
+  count_launch();
+  *handled = true;
+  return cuda_status(cudaGetLastError(), "conv_halo3_kernel");
+}
+
+}  // namespace ub

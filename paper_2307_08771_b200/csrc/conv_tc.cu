@@ -768,6 +768,11 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   if (d->w_lead != lead || d->w_cpad != cpad)
     return fail(UB_EINVAL, "ub_conv_fwd: weight layout (lead %d, cpad %d) != expected (lead %d, cpad %d)", d->w_lead,
                 d->w_cpad, lead, cpad);
+  {  // stride-1 3x3 convs: halo-tile kernel when in scope
+    bool handled = false;
+    const int rc = conv_halo_fwd(d, lead, cpad, stream, &handled);
+    if (rc != UB_OK || handled) return rc;
+  }
   const int cin_eff = d->cin + lead;
   const int bk = (gather || stem || packed) ? 64 : pick_bk(cin_eff);
 

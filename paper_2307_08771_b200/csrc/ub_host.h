@@ -22,6 +22,9 @@ PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn();
 // Clear the descriptor bit CUTLASS clears for small tensors on drivers <= 13.1.
 void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes);
 int num_sms();  // multiprocessors of the current device
+// Stride-1 3x3 halo-tile kernel (conv_halo.cu); *handled = false when the layer is outside
+// its scope and the generic kernel should run instead.
+int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled);
 
 // Swizzle span in bytes -> CUtensorMapSwizzle.
 inline CUtensorMapSwizzle swizzle_of(int bytes) {

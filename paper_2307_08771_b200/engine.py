@@ -548,7 +548,9 @@ class Engine:
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
+            _lib.reset_launch_count()
             self.launch_all()  # warm-up (first-launch attribute setup)
+            self._launches = _lib.launch_count()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -558,7 +560,12 @@ class Engine:
 
     @property
     def n_launches(self) -> int:
-        return len(self.ops)
+        """Library kernel launches per forward, counted by the C ABI (ub_launch_count) over
+        one eager pass; before any pass, the op count (one launch per op, two for the
+        space-to-depth stem)."""
+        if getattr(self, "_launches", None) is None:
+            return sum(2 if op.info.get("stem_kind") == "s2d" else 1 for op in self.ops)
+        return self._launches
 
     def per_image_work(self) -> tuple[float, float]:
         f = sum(c.flops for c in self.conv_stats)

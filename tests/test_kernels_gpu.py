@@ -53,6 +53,13 @@ CASES = [
     ("packed_3x3_s2_c8", 2, 30, 30, 8, 0, 8, 96, 3, 2, 1, 0, False, False, False, False),
     ("packed_5x5_c3_ragged", 2, 17, 19, 8, 0, 3, 32, 5, 1, 2, 0, True, False, False, False),
     ("packed_4x4_s1_p0_c8", 2, 115, 115, 8, 0, 8, 64, 4, 1, 0, 0, True, False, True, False),
+    # halo-tile kernel (stride-1 3x3, cpad 16/32/64): padded widths 64 / 32 / 16 / 8, ragged rows
+    ("halo_c32_w56", 2, 56, 56, 32, 0, 32, 32, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c64_w28_cout48", 3, 28, 28, 64, 0, 64, 48, 3, 1, 1, 0, True, False, False, False),
+    ("halo_c64_w14_slice", 2, 14, 14, 96, 24, 64, 64, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c16_w7_cout256", 2, 7, 7, 16, 0, 16, 256, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c32_lead_h13_w5", 3, 13, 5, 48, 11, 20, 40, 3, 1, 1, 0, False, False, False, False),
+    ("halo_c64_w30_cout16", 2, 17, 30, 64, 0, 64, 16, 3, 1, 1, 0, True, False, True, False),
 ]
 
 

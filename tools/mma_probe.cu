@@ -48,8 +48,13 @@ __global__ void __launch_bounds__(128, 1) probe_mma(int n, int mode, int iters, 
     uint64_t ad[4], bd[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      ad[k] = sdesc(a0 + k * 32, 16, 1024, 2);
-      bd[k] = sdesc(b0 + k * 32, 16, 1024, 2);
+      if (commit_every == 1) {  // no-swizzle planes: A rows 16 B apart, K core matrices 4 KB apart
+        ad[k] = sdesc(a0 + k * 16 * 3, 4096, 128, 0);
+        bd[k] = sdesc(b0, n * 16, 128, 0);
+      } else {
+        ad[k] = sdesc(a0 + k * 32, 16, 1024, 2);
+        bd[k] = sdesc(b0 + k * 32, 16, 1024, 2);
+      }
     }
     __syncwarp();
     const long long t0 = clock64();
@@ -132,9 +137,9 @@ int main() {
   cudaFuncSetAttribute(probe_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const int iters = 4096;
   const char* names[6] = {"sw128", "noswz", "noswz-lbo16", "sw128-pre", "sw128-pre-c", "warp-elect"};
-  for (int mode = 3; mode < 6; ++mode) {
+  for (int mode = 5; mode < 6; ++mode) {
     for (int n : {32, 64, 128, 256}) {
-      for (int ce : {0, 8}) {
+      for (int ce : {0, 1}) {
         for (int grid : {1, 148}) {
           probe_mma<<<grid, 128, 64 * 1024>>>(n, mode, iters, ce, dout);
           cudaError_t e = cudaDeviceSynchronize();
