@@ -68,9 +68,19 @@ UB_DEVI void tma_store_4d(const void* map, const void* smem, int c0, int c1, int
                : "memory");
 }
 
+// Compile-time halo geometry: padded width WP, rows per tile, staged positions, plane stride.
+template <int WP>
+struct HaloGeom {
+  static constexpr int R = 128 / WP;
+  static constexpr int N_POS = ((R + 2) * WP + 2 + 7) / 8 * 8;
+  static constexpr uint32_t PLANE_STRIDE = N_POS * 16 + 16;  // odd # of 16-B units: planes on different banks
+};
+
+template <int WP, int PLANES>
 __global__ void __launch_bounds__(HALO_THREADS, 1)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
   constexpr int TAPS = 9;
+  using G = HaloGeom<WP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = base;                                   // [tap][np rows][128 B], SW128
@@ -124,20 +134,21 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     }
     cp_async_arrive_noinc(bres);
     // halo planes: this thread always fills plane pp of positions q0 + i * qstep
-    const int pp = pt % p.planes;
-    const int q0 = pt / p.planes;
-    const int qstep = HALO_PRODUCERS / p.planes;
-    const int wmask = p.Wp - 1;
+    const int pp = pt % PLANES;
+    const int q0 = pt / PLANES;
+    constexpr int qstep = HALO_PRODUCERS / PLANES;
+    constexpr int wmask = WP - 1;
+    constexpr int wp_shift = __builtin_ctz(WP);
     int s = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * p.R - 1;  // first staged input row (pad 1)
+      const int y0 = (t - img * p.tiles_per_img) * G::R - 1;  // first staged input row (pad 1)
       const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + pp * 8;
       mbar_wait(&aempty[s], ph ^ 1);
-      const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * p.plane_stride);
-      for (int q = q0; q < p.n_pos; q += qstep) {
-        const int yy = y0 + (q >> p.wp_shift);
+      const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * G::PLANE_STRIDE);
+      for (int q = q0; q < G::N_POS; q += qstep) {
+        const int yy = y0 + (q >> wp_shift);
         const int xx = (q & wmask) - 1;
         const bool ok = yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
         const uint16_t* src = ok ? ximg + (static_cast<size_t>(yy) * p.W + xx) * p.x_cstride : p.x;
@@ -156,7 +167,11 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     // ================= MMA issuer (whole warp; one elected lane issues)
     const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
     const uint32_t b0 = smem_u32(sB);
-    const int kpairs = p.planes >> 1;
+    uint64_t bdesc[TAPS];
+#pragma unroll
+    for (int tap = 0; tap < TAPS; ++tap) bdesc[tap] = make_sdesc(b0 + tap * p.b_block_bytes, 1024, 2);
+    const uint64_t adesc0 = sdesc_plain(smem_u32(sA), G::PLANE_STRIDE, 128);
+    const uint32_t stage_units = p.a_stage_bytes >> 4;
     mbar_wait(bres, 0);
     __syncwarp();
     tc_fence_after();
@@ -170,16 +185,16 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
       __syncwarp();
       tc_fence_after();
       fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
-      const uint32_t a0 = smem_u32(sA + s * p.a_stage_bytes);
+      const uint64_t ad = adesc0 + s * stage_units;
       const uint32_t d = tmem_base + acc * p.acc_cols;
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap) {
-        const int dy = tap / 3, dx = tap - (tap / 3) * 3;
-        const uint32_t ashift = a0 + ((dy << p.wp_shift) + dx) * 16;
-        for (int j = 0; j < kpairs; ++j)
-          umma_bf16_warp(d, sdesc_plain(ashift + 2 * j * p.plane_stride, p.plane_stride, 128),
-                         make_sdesc(b0 + tap * p.b_block_bytes + j * 32, 1024, 2), idesc,
-                         (tap | j) ? 1u : 0u);
+#pragma unroll
+        for (int j = 0; j < PLANES / 2; ++j) {
+          // A: planes 2j, 2j+1 shifted by tap (dy, dx); B: K step j (32 B) of the tap's row
+          const uint32_t aoff = (((tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
+          umma_bf16_warp(d, ad + aoff, bdesc[tap] + 2 * j, idesc, (tap | j) ? 1u : 0u);
+        }
       }
       umma_commit_warp(&aempty[s]);
       umma_commit_warp(&tfull[acc]);
@@ -198,10 +213,10 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
       const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * p.R;
+      const int y0 = (t - img * p.tiles_per_img) * G::R;
       const int r0 = q * 32;
-      const int oy = y0 + (r0 >> p.wp_shift);
-      const int ox = r0 & (p.Wp - 1);
+      const int oy = y0 + r0 / WP;
+      const int ox = r0 % WP;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -294,8 +309,8 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   p.wp_shift = __builtin_ctz(Wp);
   p.R = 128 / Wp;
   p.planes = cpad / 8;
-  p.n_pos = ((p.R + 2) * Wp + 2 + 7) / 8 * 8;
-  p.plane_stride = p.n_pos * 16 + 16;  // odd number of 16-byte units: planes land on different banks
+  p.n_pos = ((p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp>::N_POS
+  p.plane_stride = p.n_pos * 16 + 16;          // == HaloGeom<Wp>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
   p.tiles_per_img = (d->H + p.R - 1) / p.R;
   const long long tiles = static_cast<long long>(d->N) * p.tiles_per_img;
@@ -332,13 +347,18 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo output tensor map failed (%d)", (int)r);
   apply_small_tensor_quirk(&tm, static_cast<size_t>(d->N) * d->Ho * d->Wo * d->y_cstride * 2);
 
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv_halo3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
   const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
-  conv_halo3_kernel<<<grid, HALO_THREADS, smem, stream>>>(tm, p);
+  void (*kern)(const CUtensorMap, const HaloParams) = nullptr;
+#define UB_HALO_CASE(WPV, PL) \
+  if (Wp == WPV && p.planes == PL) kern = conv_halo3_kernel<WPV, PL>;
+  UB_HALO_CASE(8, 2) UB_HALO_CASE(8, 4) UB_HALO_CASE(8, 8)
+  UB_HALO_CASE(16, 2) UB_HALO_CASE(16, 4) UB_HALO_CASE(16, 8)
+  UB_HALO_CASE(32, 2) UB_HALO_CASE(32, 4) UB_HALO_CASE(32, 8)
+  UB_HALO_CASE(64, 2) UB_HALO_CASE(64, 4) UB_HALO_CASE(64, 8)
+#undef UB_HALO_CASE
+  if (!kern) return UB_OK;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  kern<<<grid, HALO_THREADS, smem, stream>>>(tm, p);
   count_launch();
   *handled = true;
   return cuda_status(cudaGetLastError(), "conv_halo3_kernel");
