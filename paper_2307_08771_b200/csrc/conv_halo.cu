@@ -17,11 +17,12 @@
 // per output channel and tap), loaded once per CTA.
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warps 0-3   epilogue: TMEM -> regs, +bias, ReLU, bf16 -> SW128 smem -> 4-D TMA store
+//   warps 0-7   epilogue, two groups of four taking alternate tiles: TMEM -> regs, +bias,
+//               ReLU, bf16 -> SW128 smem -> 4-D TMA store
 //               (box 64 channels x BX pixels x BY rows of the output)
-//   warp 4      MMA issuer (two TMEM accumulators; one elected lane issues)
-//   warp 5      TMEM allocator
-//   warps 6-13  producers: halo planes by cp.async (zero-fill outside the image)
+//   warp 8      MMA issuer (2-4 TMEM accumulators; one elected lane issues)
+//   warp 9      TMEM allocator
+//   warps 10-13 producers: halo planes by cp.async (zero-fill outside the image)
 #include <cstdlib>
 
 #include "ub_common.cuh"
@@ -32,8 +33,10 @@
 namespace ub {
 namespace {
 
-constexpr int HALO_PRODUCERS = 256;
-constexpr int HALO_THREADS = 192 + HALO_PRODUCERS;
+constexpr int HALO_PRODUCERS = 128;
+constexpr int HALO_EPI_WARPS = 8;                      // two groups of four, alternate tiles
+constexpr int HALO_PROD_WARP0 = HALO_EPI_WARPS + 2;    // after the MMA and TMEM-alloc warps
+constexpr int HALO_THREADS = 32 * HALO_PROD_WARP0 + HALO_PRODUCERS;
 constexpr int HALO_SLOT = 32 * 128;  // one epilogue warp's 32 rows x 64 channels bf16
 
 struct HaloParams {
@@ -43,13 +46,16 @@ struct HaloParams {
   uint32_t plane_stride, a_stage_bytes;
   int a_stages;
   int tiles, tiles_per_img;
-  int cout, np, acc_cols;
+  int cout, np, acc_cols, nacc;
   uint32_t b_block_bytes;  // np * 128: one tap's weights
   const uint16_t* w;       // [cout][9][cpad]
   int cpad;
   const float* bias;
   int relu;
   int bx;  // output box width (pixels); box height = 32 / bx rows
+  long long* trace;  // profiling (UB_HALO_TRACE): CTA 0 event clocks, [tile][8]
+  int dbg;           // profiling ablations (UB_HALO_DBG): 1 no halo loads, 2 no output, 4 no TMEM reads,
+                     // 8 no TMA store, 16 no slot wait (races; timing only)
 };
 
 UB_DEVI uint64_t sdesc_plain(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -69,57 +75,59 @@ UB_DEVI void tma_store_4d(const void* map, const void* smem, int c0, int c1, int
 }
 
 // Compile-time halo geometry: padded width WP, rows per tile, staged positions, plane stride.
-template <int WP>
+template <int WP, int MT>
 struct HaloGeom {
-  static constexpr int R = 128 / WP;
-  static constexpr int N_POS = ((R + 2) * WP + 2 + 7) / 8 * 8;
+  static constexpr int R = 128 / WP;    // output rows per 128-position MMA tile
+  static constexpr int RT = MT * R;     // output rows per staged tile (MT MMA tiles)
+  static constexpr int N_POS = ((RT + 2) * WP + 2 + 7) / 8 * 8;
   static constexpr uint32_t PLANE_STRIDE = N_POS * 16 + 16;  // odd # of 16-B units: planes on different banks
 };
 
-template <int WP, int PLANES>
+template <int WP, int PLANES, int MT>
 __global__ void __launch_bounds__(HALO_THREADS, 1)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
   constexpr int TAPS = 9;
-  using G = HaloGeom<WP>;
+  using G = HaloGeom<WP, MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = base;                                   // [tap][np rows][128 B], SW128
-  uint8_t* sE = sB + TAPS * p.b_block_bytes;            // 4 warps x 2 slots x 4 KB (1024-aligned)
-  uint8_t* sA = sE + 4 * 2 * HALO_SLOT;                 // a_stages x a_stage_bytes
+  uint8_t* sE = sB + TAPS * p.b_block_bytes;            // 8 warps x 2 slots x 4 KB (1024-aligned)
+  uint8_t* sA = sE + HALO_EPI_WARPS * 2 * HALO_SLOT;    // a_stages x a_stage_bytes
   float* sBias = reinterpret_cast<float*>(sA + p.a_stages * p.a_stage_bytes);  // 256 floats
   uint64_t* afull = reinterpret_cast<uint64_t*>(sBias + 256);
   uint64_t* aempty = afull + 8;
   uint64_t* tfull = aempty + 8;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bres = tempty + 2;
+  uint64_t* tempty = tfull + 4;
+  uint64_t* bres = tempty + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  if (warp == 4 && lane == 0) {
+  constexpr int MMA_WARP = HALO_EPI_WARPS, ALLOC_WARP = HALO_EPI_WARPS + 1;
+  if (warp == MMA_WARP && lane == 0) {
     for (int s = 0; s < p.a_stages; ++s) {
       mbar_init(&afull[s], HALO_PRODUCERS);
       mbar_init(&aempty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < p.nacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4);  // the four warps of the group draining it
     }
     mbar_init(bres, HALO_PRODUCERS);
     fence_mbar_init();
   }
   if (warp == 0) tma_prefetch_desc(&tmY);
-  if (warp == 5) tmem_alloc(tmem_slot, 2 * p.acc_cols);
+  if (warp == ALLOC_WARP) tmem_alloc(tmem_slot, p.nacc * MT * p.acc_cols);
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sBias[i] = (p.bias && i < p.cout) ? p.bias[i] : 0.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp >= 6) {
+  if (warp >= HALO_PROD_WARP0) {
     // ================= producers
-    const int pt = threadIdx.x - 192;
+    const int pt = threadIdx.x - 32 * HALO_PROD_WARP0;
     // resident weights: tap t, row n, 16-byte chunk j (K = 8j .. 8j+7 of the tap) -> SW128
     const int cp8 = p.cpad >> 3;
     for (int e = pt; e < TAPS * p.np * cp8; e += HALO_PRODUCERS) {
@@ -143,11 +151,15 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * G::R - 1;  // first staged input row (pad 1)
+      const int y0 = (t - img * p.tiles_per_img) * G::RT - 1;  // first staged input row (pad 1)
       const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + pp * 8;
       mbar_wait(&aempty[s], ph ^ 1);
+      if (p.trace && blockIdx.x == 0 && pt == 0) {
+        const int itp = (t - blockIdx.x) / gridDim.x;
+        if (itp < 64) p.trace[itp * 8 + 7] = clock64();
+      }
       const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * G::PLANE_STRIDE);
-      for (int q = q0; q < G::N_POS; q += qstep) {
+      for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
         const int yy = y0 + (q >> wp_shift);
         const int xx = (q & wmask) - 1;
         const bool ok = yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
       }
     }
     cp_async_wait<0>();
-  } else if (warp == 4) {
+  } else if (warp == MMA_WARP) {
     // ================= MMA issuer (whole warp; one elected lane issues)
     const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
     const uint32_t b0 = smem_u32(sB);
@@ -179,69 +191,94 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     int s = 0, it = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      const int acc = it % p.nacc;
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 0] = clock64();
+      mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 1] = clock64();
       mbar_wait(&afull[s], ph);
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 2] = clock64();
       __syncwarp();
       tc_fence_after();
       fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
       const uint64_t ad = adesc0 + s * stage_units;
-      const uint32_t d = tmem_base + acc * p.acc_cols;
 #pragma unroll
-      for (int tap = 0; tap < TAPS; ++tap) {
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint32_t d = tmem_base + (acc * MT + mt) * p.acc_cols;
 #pragma unroll
-        for (int j = 0; j < PLANES / 2; ++j) {
-          // A: planes 2j, 2j+1 shifted by tap (dy, dx); B: K step j (32 B) of the tap's row
-          const uint32_t aoff = (((tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
-          umma_bf16_warp(d, ad + aoff, bdesc[tap] + 2 * j, idesc, (tap | j) ? 1u : 0u);
+        for (int tap = 0; tap < TAPS; ++tap) {
+#pragma unroll
+          for (int j = 0; j < PLANES / 2; ++j) {
+            // A: planes 2j, 2j+1 of MMA tile mt shifted by tap (dy, dx); B: K step j of the tap
+            const uint32_t aoff =
+                ((mt * G::R * WP + (tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
+            umma_bf16_warp(d, ad + aoff, bdesc[tap] + 2 * j, idesc, (tap | j) ? 1u : 0u);
+          }
         }
       }
       umma_commit_warp(&aempty[s]);
       umma_commit_warp(&tfull[acc]);
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 3] = clock64();
       if (++s == p.a_stages) {
         s = 0;
         ph ^= 1;
       }
     }
-  } else if (warp < 4) {
-    // ================= epilogue: warp q owns TMEM lanes / tile rows 32q .. 32q+31
-    const int q = warp;
-    uint8_t* slots = sE + q * 2 * HALO_SLOT;
-    const int by = 32 / p.bx;
+  } else if (warp < HALO_EPI_WARPS) {
+    // ================= epilogue: group g = warp / 4 drains the tiles it % 2 == g; warp q = warp % 4
+    // owns TMEM lanes / tile rows 32q .. 32q+31
+    const int grp = warp >> 2;
+    const int q = warp & 3;
+    uint8_t* slots = sE + warp * 2 * HALO_SLOT;
     const int nchunks = (p.np + 63) >> 6;
     uint32_t ec = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
+      if ((it & 1) != grp) continue;
       const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * G::R;
+      const int y0 = (t - img * p.tiles_per_img) * G::RT;
       const int r0 = q * 32;
-      const int oy = y0 + r0 / WP;
       const int ox = r0 % WP;
-      const int acc = it & 1;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      const int acc = it % p.nacc;
+      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 4] = clock64();
+      mbar_wait(&tfull[acc], (it / p.nacc) & 1);
+      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 5] = clock64();
       tc_fence_after();
-      const uint32_t taddr = tmem_base + acc * p.acc_cols + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < nchunks; ++c, ++ec) {
+      for (int cm = 0; cm < MT * nchunks; ++cm, ++ec) {
+        const int mt = cm / nchunks, c = cm - mt * nchunks;
+        const int oy = y0 + mt * G::R + r0 / WP;
+        const uint32_t taddr =
+            tmem_base + (acc * MT + mt) * p.acc_cols + (static_cast<uint32_t>(q * 32) << 16);
         uint8_t* slot = slots + (ec & 1) * HALO_SLOT;
-        if (lane == 0) bulk_wait_read<1>();  // this slot's store from two chunks ago has read it
-        __syncwarp();
+        // both 32-column halves of the chunk in flight before one wait
+        uint32_t v0[32], v1[32];
+        const int col0 = c * 64;
+        if (p.dbg & 4) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = c * 64 + h * 32;
-          if (col >= p.np) break;
-          uint32_t v[32];
-          if (col + 32 <= p.np) {
-            tmem_ld32(taddr + col, v);
-          } else {
-            tmem_ld16(taddr + col, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-#pragma unroll
-            for (int i = 16; i < 32; ++i) v[i] = 0;
-          }
+          for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0;
+        } else {
+          if (col0 + 32 <= p.np) tmem_ld32(taddr + col0, v0);
+          else tmem_ld16_lo(taddr + col0, v0);
+          if (col0 + 64 <= p.np) tmem_ld32(taddr + col0 + 32, v1);
+          else if (col0 + 32 < p.np) tmem_ld16_lo(taddr + col0 + 32, v1);
           tmem_ld_wait();
-          const float4* bq = reinterpret_cast<const float4*>(sBias + col);
+        }
+        if (cm + 1 == MT * nchunks) {  // accumulators drained: hand them back before the math and store
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 6] = clock64();
+        }
+        if (p.dbg & 2) continue;
+        if (lane == 0 && !(p.dbg & 16)) bulk_wait_read<1>();  // this slot's store from two chunks ago has read it
+        __syncwarp();
+        // 16-byte chunk k (channels col0 + 8k ..) of row `lane`, SW128 position k ^ (lane & 7)
+        auto emit = [&](const uint32_t (&v)[32], int half) {
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {  // 16-byte chunk jj of this half = channels col + 8jj ..
-            const float4 b0 = bq[2 * jj], b1 = bq[2 * jj + 1];
+          for (int jj = 0; jj < 4; ++jj) {
+            const int col = col0 + half * 32 + 8 * jj;
+            if (col >= p.np) break;
+            const float4 b0 = *reinterpret_cast<const float4*>(sBias + col);
+            const float4 b1 = *reinterpret_cast<const float4*>(sBias + col + 4);
             const float2 s0 = add_f32x2(make_float2(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1])),
                                         make_float2(b0.x, b0.y));
             const float2 s1 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3])),
@@ -258,31 +295,27 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
               o = make_uint4(cvt_bf16x2(s0.x, s0.y), cvt_bf16x2(s1.x, s1.y), cvt_bf16x2(s2.x, s2.y),
                              cvt_bf16x2(s3.x, s3.y));
             }
-            const int chunk = h * 4 + jj;
+            const int chunk = half * 4 + jj;
             *reinterpret_cast<uint4*>(slot + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o;
           }
-        }
-        if (c + 1 == nchunks) {  // accumulator drained: hand it back before the store
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        fence_proxy_async_smem();
+        };
+        emit(v0, 0);
+        emit(v1, 1);
+        if (!(p.dbg & 32)) fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          tma_store_4d(&tmY, slot, c * 64, ox, oy, img);
+        if (lane == 0 && !(p.dbg & 8)) {
+          tma_store_4d(&tmY, slot, col0, ox, oy, img);
           bulk_commit();
         }
-        (void)by;
       }
     }
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == ALLOC_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * p.acc_cols);
+    tmem_dealloc(tmem_base, p.nacc * MT * p.acc_cols);
   }
 }
 
@@ -290,6 +323,8 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
 
 // Returns UB_OK with *handled = true when the halo kernel ran; *handled = false (and UB_OK)
 // when the layer is outside its scope (the caller then uses the generic kernel).
+long long* g_halo_trace = nullptr;
+
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
   *handled = false;
   if (d->kh != 3 || d->kw != 3 || d->stride != 1 || d->pad != 1 || d->x_nchw_f32 || d->gather_idx ||
@@ -309,23 +344,37 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   p.wp_shift = __builtin_ctz(Wp);
   p.R = 128 / Wp;
   p.planes = cpad / 8;
-  p.n_pos = ((p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp>::N_POS
-  p.plane_stride = p.n_pos * 16 + 16;          // == HaloGeom<Wp>::PLANE_STRIDE
+  p.np = (d->cout + 15) / 16 * 16;
+  p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
+  // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
+  const int mt = (d->H > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
+  p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
+  p.n_pos = ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp, mt>::N_POS
+  p.plane_stride = p.n_pos * 16 + 16;               // == HaloGeom<Wp, mt>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
-  p.tiles_per_img = (d->H + p.R - 1) / p.R;
+  p.tiles_per_img = (d->H + mt * p.R - 1) / (mt * p.R);
   const long long tiles = static_cast<long long>(d->N) * p.tiles_per_img;
   if (tiles >= (1ll << 31)) return UB_OK;
   p.tiles = static_cast<int>(tiles);
   p.cout = d->cout;
-  p.np = (d->cout + 15) / 16 * 16;
-  p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
   p.b_block_bytes = static_cast<uint32_t>((p.np + 7) / 8 * 8) * 128;
   p.w = reinterpret_cast<const uint16_t*>(d->w);
   p.cpad = cpad;
   p.bias = d->bias;
   p.relu = d->relu;
   p.bx = Wp < 32 ? Wp : 32;
-  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + 4 * 2 * HALO_SLOT + 256 * 4 + 256;
+  {
+    static long long* trace = nullptr;
+    static int want = -1;
+    if (want < 0) want = getenv("UB_HALO_TRACE") ? 1 : 0;
+    if (want && !trace) cudaMalloc(&trace, 64 * 8 * sizeof(long long));
+    p.trace = trace;
+    g_halo_trace = trace;
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("UB_HALO_DBG") ? atoi(getenv("UB_HALO_DBG")) : 0;
+    p.dbg = dbg;
+  }
+  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + HALO_EPI_WARPS * 2 * HALO_SLOT + 256 * 4 + 256;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * p.a_stage_bytes > budget) return UB_OK;
   int stages = static_cast<int>((budget - fixed) / p.a_stage_bytes);
@@ -349,8 +398,9 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
 
   const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
   void (*kern)(const CUtensorMap, const HaloParams) = nullptr;
-#define UB_HALO_CASE(WPV, PL) \
-  if (Wp == WPV && p.planes == PL) kern = conv_halo3_kernel<WPV, PL>;
+#define UB_HALO_CASE(WPV, PL)                                                     \
+  if (Wp == WPV && p.planes == PL) kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2> \
+                                                  : conv_halo3_kernel<WPV, PL, 1>;
   UB_HALO_CASE(8, 2) UB_HALO_CASE(8, 4) UB_HALO_CASE(8, 8)
   UB_HALO_CASE(16, 2) UB_HALO_CASE(16, 4) UB_HALO_CASE(16, 8)
   UB_HALO_CASE(32, 2) UB_HALO_CASE(32, 4) UB_HALO_CASE(32, 8)
@@ -365,3 +415,5 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
 }
 
 }  // namespace ub
+
+extern "C" long long* ub_debug_halo_trace() { return ub::g_halo_trace; }
