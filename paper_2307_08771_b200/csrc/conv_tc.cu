@@ -92,7 +92,12 @@ struct ConvKParams {
   int y_cstride, y_coff, y_f32;
   int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
   int b_res;  // weights of this CTA's N tile stay resident in smem (loaded once; grid % n_tiles == 0)
+  long long* trace;  // profiling (UB_CONV_TRACE): CTA 0 per-tile event clocks [tile][8]
 };
+#define UB_TRACE(slot)                                                                  \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && it < 64) p.trace[it * 8 + (slot)] = clock64(); \
+  } while (0)
 
 // Align the dynamic smem base to 1024 B by pointer arithmetic on the __shared__ pointer itself
 // (a round trip through uintptr_t would make every derived pointer generic and turn all
@@ -219,7 +224,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         const int acc = it & 1;
         const int n0 = (t % p.n_tiles) * p.block_n;
         const int nres = tile_res_chunks(p, n0);
+        UB_TRACE(0);
         mbar_wait(&tempty[acc], (it >> 1) & 1);  // drained and re-armed with this tile's bias
+        UB_TRACE(1);
         __syncwarp();
         tc_fence_after();
         const uint32_t d = tmem_base + acc * p.acc_stride;
@@ -251,6 +258,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           }
         }
         umma_commit_warp(&tfull[acc]);
+        UB_TRACE(2);
       }
     }
   } else if (warp >= 8) {
@@ -298,6 +306,8 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       cp_async_arrive_noinc(bres);
     }
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int it = (t - blockIdx.x) / gridDim.x;
+      if (pt == 0) UB_TRACE(6);
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
       const int m0 = m_tile * BLOCK_M;
@@ -505,6 +515,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           ph ^= 1;
         }
       }
+      if (pt == 0) UB_TRACE(7);
     }
     cp_async_wait<0>();
   } else if (warp >= 4) {
@@ -564,7 +575,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       const bool rearm = t_next < num_tiles;
       if (rearm) stage_bias(t_next);
       const int acc = it & 1;
+      if (q == 0) UB_TRACE(3);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
+      if (q == 0) UB_TRACE(4);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < nchunks; ++c, ++ec) {
@@ -639,6 +652,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);  // drained (and re-armed): the MMA may reuse it
+      if (q == 0) UB_TRACE(5);
     }
     if (tma && lane == 0) bulk_wait_all();
   }
@@ -652,6 +666,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
 // ------------------------------------------------------------------ host side
 
 int g_driver_version = -1;
+long long* g_conv_trace = nullptr;
 int g_num_sms = -1;
 
 void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes) {
@@ -840,6 +855,14 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     p.dbg = dbg;
   }
 
+  {
+    static long long* trace = nullptr;
+    static int want = -1;
+    if (want < 0) want = getenv("UB_CONV_TRACE") ? 1 : 0;
+    if (want && !trace) cudaMalloc(&trace, 64 * 8 * sizeof(long long));
+    p.trace = trace;
+    g_conv_trace = trace;
+  }
   const uint16_t* ybase = reinterpret_cast<const uint16_t*>(d->y) + d->y_coff;
   if (p.has_res && (d->res_cstride % 8 || !aligned16(p.res)))
     return fail(UB_EINVAL, "ub_conv_fwd: residual rows must be 16-byte aligned (res_cstride, res_coff multiples of 8)");
@@ -899,3 +922,5 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, p, grid, smem, stream, wide);
   return launch_conv<A_IM2COL, 16>(tmY, p, grid, smem, stream, wide);
 }
+
+extern "C" long long* ub_debug_conv_trace() { return ub::g_conv_trace; }

@@ -16,6 +16,9 @@ from paper_2307_08771_b200 import _lib, kernels as K  # noqa: E402
 # name: (N, H, W, cstride, coff, cin, cout, k, stride, pad, n_gather, res, relu)
 CASES = {
     "l1_conv3": (256, 56, 56, 32, 0, 32, 256, 1, 1, 0, 0, True, True),
+    "l2_conv3_502": (256, 28, 28, 64, 0, 64, 502, 1, 1, 0, 0, True, True),
+    "l3_conv3_1016": (256, 14, 14, 128, 0, 128, 1016, 1, 1, 0, 0, True, True),
+    "l4_conv1_1024": (256, 7, 7, 1816, 0, 1024, 256, 1, 1, 0, 0, False, True),
     "l1_conv1_gather": (256, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, False, True),
     "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv2_3x3": (256, 56, 56, 64, 0, 32, 64, 3, 1, 1, 0, False, True),

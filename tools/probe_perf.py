@@ -62,6 +62,10 @@ def main():
     for r in sorted(rows, key=lambda r: -r[2])[:int(sys.argv[5]) if len(sys.argv) > 5 else 25]:
         print(f"{r[0]:8s} {r[1]:24s} {r[2]*1e3:7.1f} us {r[3]:6.2f} GF {r[4]:6.1f} MB roof {r[5]*1e3:6.1f} us "
               f"frac {r[5]/max(r[2],1e-9):.2f}  {r[6]}")
+    if len(sys.argv) > 6 and sys.argv[6] == "gap":
+        print("--- by gap to roofline")
+        for r in sorted(rows, key=lambda r: -(r[2] - r[5]))[:40]:
+            print(f"{r[1]:24s} {r[2]*1e3:7.1f} us roof {r[5]*1e3:6.1f} gap {(r[2]-r[5])*1e3:6.1f}  {r[6]}")
     cats = {}
     for r in rows:
         d = r[6]
