@@ -300,20 +300,25 @@ def main():
         runner = api.Runner(ex, gather_mode=args.gather, device=dev)
         runner._engines[B] = eng
         host_x = x.cpu().pin_memory()
-        for _ in range(2):
-            runner.run(host_x)
+        for _ in runner.run_many([host_x] * 3):
+            pass
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k2 = max(5, args.steps // 5)
+        k2 = max(10, args.steps // 2)
         a.record(stream)
-        for _ in range(k2):
-            out_np = runner.run(host_x)
+        outs = 0
+        for out_np in runner.run_many(host_x for _ in range(k2)):
+            outs += 1
         b.record(stream)
         torch.cuda.synchronize()
+        assert outs == k2
         e2e_ms = a.elapsed_time(b) / k2
-        e2e = {"value": round(B / (e2e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": host_x.numel() * 4,
+        e2e = {"value": round(B / (e2e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": runner.h2d_bytes,
                "d2h_bytes_per_step": int(out_np.nbytes), "ms_per_step": round(e2e_ms, 4),
-               "path": "api.Runner.run: pinned host fp32 -> H2D -> CUDA-graph forward -> D2H logits"}
+               "steps": k2,
+               "path": "api.Runner.run_many: pinned host NCHW fp32 -> H2D of the channels the INPUT GATHER "
+                       "keeps (copy stream, overlapped with the previous batch's forward) -> CUDA-graph "
+                       "forward -> D2H logits -> host numpy, every step"}
         # ---- batch-1 latency
         eng1 = EN.from_plans(sm, eg, maps, batch=1, device=dev, gather_mode=args.gather)
         eng1.capture()

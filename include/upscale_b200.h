@@ -161,6 +161,14 @@ int ub_conv_s2d(const void* s, int N, int H, int W, int k, int pad, const void* 
 int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n,
                    void* y, int y_cstride, cudaStream_t stream);
 
+/* Host -> device copy of the model input restricted to the channels the INPUT node's
+ * GATHER keeps (planner.py:774-783): for each c in channels[0..n) (HOST array), plane c of
+ * every image of the pinned host NCHW fp32 batch goes to the same place in the device NCHW
+ * buffer (one strided cudaMemcpy2DAsync per channel); dropped channels never cross PCIe.
+ * *bytes (optional) receives the bytes copied. */
+int ub_h2d_input_channels(const float* host_nchw, int N, int C, int HW, const int32_t* channels, int n,
+                          float* dev_nchw, long long* bytes, cudaStream_t stream);
+
 /* Max pool (PASS_THROUGH lowering of nn.MaxPool2d), NHWC bf16, -inf padding. */
 int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff,
                  int k, int stride, int pad, int Ho, int Wo,

@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 from . import engine as EN
+from . import kernels as K
 from . import export as E
 from . import ir
 from . import plans as P
@@ -73,37 +74,98 @@ def export_model(model: SpatialModel, masks: ir.ChannelMask, mode: str = "input"
 
 
 class Runner:
-    """Compiled engine cache keyed by batch size (one CUDA graph per size)."""
+    """Compiled engine cache keyed by batch size (CUDA graphs per size).
+
+    The host side of interp.run for batches: the H2D copy carries only the input
+    channels the exported model reads (the INPUT node's GATHER, applied to the copy:
+    ub_h2d_input_channels), and run_many() pipelines consecutive batches -- the copy
+    of batch i+1 runs on its own stream while the forward of batch i replays its
+    graph (two input buffers, one graph each)."""
 
     def __init__(self, exported: Exported, gather_mode: str = "fused", device="cuda"):
         self.exported = exported
         self.gather_mode = gather_mode
         self.device = device
         self._engines: dict[int, EN.Engine] = {}
-        self._host_out: dict[int, torch.Tensor] = {}
+        self._host_out: dict[tuple, torch.Tensor] = {}
+        self._copy_stream = None
+        self.h2d_bytes = 0  # bytes moved host -> device by the last run / run_many step
 
     def engine(self, batch: int) -> EN.Engine:
         if batch not in self._engines:
             ex = self.exported
             eng = EN.from_plans(ex.model, ex.graph, ex.maps, batch, device=self.device, gather_mode=self.gather_mode)
-            eng.capture()
+            eng.capture(n_inputs=2)
             self._engines[batch] = eng
-        return self._engines[batch]
+        eng = self._engines[batch]
+        if len(eng._graphs) < 2:  # an engine captured elsewhere with one input buffer
+            eng.capture(autotune=False, n_inputs=2)
+        return eng
+
+    def _pinned_out(self, eng, slot):
+        key = (eng.batch, slot)
+        if key not in self._host_out:
+            o = eng.output_tensor()
+            self._host_out[key] = torch.empty(o.shape, dtype=torch.float32, pin_memory=True)
+        return self._host_out[key]
+
+    def _h2d(self, eng, xt, slot) -> int:
+        if xt.is_pinned() and xt.is_contiguous():
+            return K.h2d_input_channels(xt, eng.input_bufs[slot], eng.kept_input_channels())
+        eng.input_bufs[slot].copy_(xt, non_blocking=True)
+        return xt.numel() * 4
 
     def run(self, x) -> np.ndarray:
         """x: host array/tensor [N, C, H, W] float32 -> logits [N, classes] (host).
-        Pinned host tensors are copied asynchronously; the D2H lands in a
-        pinned buffer and the call returns after the stream drains."""
+        Pinned host tensors are copied asynchronously (kept channels only); the D2H
+        lands in a pinned buffer and the call returns after the stream drains."""
         xt = torch.as_tensor(x, dtype=torch.float32)
         eng = self.engine(xt.shape[0])
-        out = eng.forward(xt)  # H2D into the engine's static input buffer
-        host = self._host_out.get(eng.batch)
-        if host is None or host.shape != out.shape:
-            host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
-            self._host_out[eng.batch] = host
-        host.copy_(out, non_blocking=True)
+        self.h2d_bytes = self._h2d(eng, xt, 0)
+        eng.replay(0)
+        host = self._pinned_out(eng, 0)
+        host.copy_(eng.output_tensor(), non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return host.numpy().copy()
+
+    def run_many(self, batches):
+        """Pipelined run over an iterable of equally-sized pinned host batches; yields
+        the logits of each batch (host numpy) in order.  Batch i+1's H2D overlaps batch
+        i's forward; every batch still crosses PCIe and every result comes back."""
+        compute = torch.cuda.current_stream()
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        copy = self._copy_stream
+        eng = None
+        consumed = [None, None]  # event: the forward that read input buffer k finished
+        pending = None           # (event, host buffer) of the previous batch's D2H
+        for i, x in enumerate(batches):
+            xt = torch.as_tensor(x, dtype=torch.float32)
+            if eng is None:
+                eng = self.engine(xt.shape[0])
+            slot = i & 1
+            with torch.cuda.stream(copy):
+                if consumed[slot] is not None:
+                    copy.wait_event(consumed[slot])
+                self.h2d_bytes = self._h2d(eng, xt, slot)
+                landed = torch.cuda.Event()
+                landed.record(copy)
+            compute.wait_event(landed)
+            eng.replay(slot)
+            done = torch.cuda.Event()
+            done.record(compute)
+            consumed[slot] = done
+            host = self._pinned_out(eng, slot)
+            host.copy_(eng.output_tensor(), non_blocking=True)
+            d2h = torch.cuda.Event()
+            d2h.record(compute)
+            if pending is not None:
+                pending[0].synchronize()
+                yield pending[1].numpy().copy()
+            pending = (d2h, host)
+        if pending is not None:
+            pending[0].synchronize()
+            yield pending[1].numpy().copy()
 
 
 def run(exported: Exported, x, gather_mode: str = "fused") -> np.ndarray:

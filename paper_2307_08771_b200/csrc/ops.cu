@@ -332,6 +332,24 @@ extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const 
   return cuda_status(cudaGetLastError(), "stage_input_kernel");
 }
 
+extern "C" int ub_h2d_input_channels(const float* host_nchw, int N, int C, int HW, const int32_t* channels, int n,
+                                     float* dev_nchw, long long* bytes, cudaStream_t stream) {
+  if (!host_nchw || !dev_nchw || !channels || N < 1 || C < 1 || HW < 1 || n < 1 || n > C)
+    return fail(UB_EINVAL, "ub_h2d_input_channels: bad arguments");
+  const size_t plane = static_cast<size_t>(HW) * sizeof(float);
+  const size_t pitch = plane * C;
+  for (int i = 0; i < n; ++i) {
+    const int c = channels[i];
+    if (c < 0 || c >= C) return fail(UB_EINVAL, "ub_h2d_input_channels: channel %d out of range", c);
+    const cudaError_t e = cudaMemcpy2DAsync(reinterpret_cast<char*>(dev_nchw) + c * plane, pitch,
+                                            reinterpret_cast<const char*>(host_nchw) + c * plane, pitch, plane, N,
+                                            cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_status(e, "ub_h2d_input_channels");
+  }
+  if (bytes) *bytes = static_cast<long long>(n) * N * plane;
+  return UB_OK;
+}
+
 // Row-staged max pool for the 3x3 / stride-2 window (ResNet's): one CTA per band of ROWS
 // output rows of one image.  Each thread owns fixed 16-byte pieces (w, channel group) of the
 // input rows; per output row it loads input rows 2h and 2h+1 and carries row 2h-1 from the

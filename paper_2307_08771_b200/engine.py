@@ -271,6 +271,8 @@ class Engine:
 
         # --- allocate + bind launches -------------------------------------------
         self.input_buf = torch.zeros((self.batch, *self.input_chw), dtype=torch.float32, device=self.device)
+        self.input_bufs = [self.input_buf]
+        self._graphs: list = []
         for op in self.ops:
             getattr(self, f"_bind_{op.kind}")(op, weight_source, vector_source, output_feed)
         out_id = next(lid for lid in topo if kinds[lid] is LayerKind.OUTPUT)
@@ -293,8 +295,9 @@ class Engine:
         C = len(idx) if idx is not None else self.input_chw[0]
         y = self._alloc(op.output, C)
         idx_dev = self._i32(idx) if idx is not None else None
-        x = self.input_buf
-        op.launch = lambda: K.stage_input(x, y, idx_dev)
+        # the model input is read through self.input_buf at launch time (capture() records
+        # one graph per input buffer for the pipelined Runner)
+        op.launch = lambda: K.stage_input(self.input_buf, y, idx_dev)
 
     def _bind_maxpool(self, op, ws, vs, output_feed):
         sp = op.info["spec"]
@@ -467,7 +470,6 @@ class Engine:
         assert info.get("residual") is None and info["out"] not in output_feed
         y = self._alloc(info["out"], lay.out_channels)
         relu = info["relu"] is not None
-        x = self.input_buf
         cout, kk, st, pd = lay.out_channels, spec.kernel, spec.stride, spec.pad
         ci, hi, wi = self.input_chw
         # space-to-depth stem when the folded 2x2 pixel fits 16 bytes (ub_conv_s2d); else the
@@ -478,7 +480,7 @@ class Engine:
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
             sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
             self._keep += [wg, sbuf]
-            op.launch = lambda: K.stem_s2d(x, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias, relu=relu)
+            op.launch = lambda: K.stem_s2d(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias, relu=relu)
             op.info["stem_kind"] = "s2d"
             wbytes = 2.0 * wg.numel()
         else:
@@ -486,7 +488,7 @@ class Engine:
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=kpad,
                                    out_dtype=torch.bfloat16)
             self._keep.append(wg)
-            op.launch = lambda: K.conv_stem(x, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
+            op.launch = lambda: K.conv_stem(self.input_buf, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
             op.info["stem_kind"] = "im2col"
             wbytes = 2.0 * cout * kpad
         flops = 2.0 * cout * cin * kk * kk * y.H * y.W
@@ -506,6 +508,21 @@ class Engine:
         else:
             self.launch_all()
         return self.output_tensor()
+
+    def kept_input_channels(self) -> list[int]:
+        """Input channels any op reads (the INPUT node's GATHER; all when none)."""
+        kept = set()
+        for op in self.ops:
+            if "stem_idx" in op.info:
+                kept.update(op.info["stem_idx"])
+            elif op.kind == "stage":
+                idx = op.info["idx"]
+                kept.update(idx if idx is not None else range(self.input_chw[0]))
+        return sorted(kept) if kept else list(range(self.input_chw[0]))
+
+    def replay(self, slot: int = 0) -> None:
+        """Run the captured forward that reads input buffer `slot`."""
+        self._graphs[slot].replay()
 
     def output_tensor(self) -> torch.Tensor:
         o = self.output_value
@@ -539,9 +556,11 @@ class Engine:
             picks[op.info["conv"]] = best[1]
         return picks
 
-    def capture(self, autotune: bool = True) -> None:
+    def capture(self, autotune: bool = True, n_inputs: int = 1) -> None:
         """Capture the launch sequence in a CUDA graph (static buffers); optionally
-        autotune the conv variants first."""
+        autotune the conv variants first.  n_inputs > 1 allocates that many input
+        buffers and captures one graph per buffer (double-buffered input for the
+        pipelined Runner.run_many)."""
         if autotune and self.batch >= 16:
             self.launch_all()
             self.autotune()
@@ -553,10 +572,17 @@ class Engine:
             self._launches = _lib.launch_count()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.launch_all()
-        self._graph_exec = g
+        while len(self.input_bufs) < n_inputs:
+            self.input_bufs.append(torch.zeros_like(self.input_bufs[0]))
+        self._graphs = []
+        for k in range(max(n_inputs, 1)):
+            self.input_buf = self.input_bufs[k]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.launch_all()
+            self._graphs.append(g)
+        self.input_buf = self.input_bufs[0]
+        self._graph_exec = self._graphs[0]
 
     @property
     def n_launches(self) -> int:

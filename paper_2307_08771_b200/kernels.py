@@ -185,6 +185,18 @@ def stem_s2d(x_nchw: torch.Tensor, idx_dev: torch.Tensor, s_buf: torch.Tensor, w
                                y.coff, _stream()))
 
 
+def h2d_input_channels(host: torch.Tensor, dev: torch.Tensor, channels) -> int:
+    """Pinned host NCHW fp32 -> device NCHW fp32, only `channels` (the INPUT GATHER's
+    kept planes; the others are left untouched). Returns the bytes copied."""
+    assert host.is_pinned() and host.is_contiguous() and dev.is_contiguous() and host.shape == dev.shape
+    N, C, H, W = host.shape
+    ch = (ctypes.c_int32 * len(channels))(*channels)
+    nbytes = ctypes.c_longlong()
+    _lib.call("ub_h2d_input_channels", _p(host), N, C, H * W, ch, len(channels), _p(dev), ctypes.byref(nbytes),
+              _stream())
+    return nbytes.value
+
+
 def stage_input(x: torch.Tensor, y: Act, idx_dev: torch.Tensor | None = None) -> None:
     N, C, H, W = x.shape
     n = idx_dev.numel() if idx_dev is not None else C

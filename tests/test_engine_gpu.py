@@ -73,3 +73,27 @@ def test_export_model_weights_bit_exact_vs_oracle():
         for n, t in named.items():
             assert torch.equal(res.weights.vec[uid][n].cpu(), t), (uid, n)
     assert ir.graph_to_dict(res.graph) == ir.graph_to_dict(eg)
+
+
+def test_runner_pipelined_matches_single_runs():
+    """api.Runner: the kept-channel H2D (INPUT GATHER on the copy) and the pipelined
+    run_many (double-buffered input, copy stream) give the same logits as plain
+    engine forwards of the full batches."""
+    from paper_2307_08771_b200 import api
+
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    N = 4
+    xs = [torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(10 + i)).pin_memory()
+          for i in range(5)]
+    ex = api.Exported(E.ExportResult(eg, None, tuple(plans), P.copy_report(plans), ()), sm, maps)
+    runner = api.Runner(ex)
+    eng = runner.engine(N)
+    kept = eng.kept_input_channels()
+    assert len(kept) < 3  # resnet50_s50's INPUT GATHER drops an image channel
+    ref = [eng.forward(x.cuda()).cpu().numpy().copy() for x in xs]
+    single = [runner.run(x) for x in xs]
+    assert runner.h2d_bytes == N * len(kept) * 224 * 224 * 4
+    piped = list(runner.run_many(xs))
+    assert len(piped) == len(xs)
+    for r, a, b in zip(ref, single, piped):
+        assert (r == a).all() and (r == b).all()
