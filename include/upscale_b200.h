@@ -156,6 +156,16 @@ int ub_stem_s2d_pack(const float* x, int N, int C, int H, int W, const int32_t* 
 int ub_conv_s2d(const void* s, int N, int H, int W, int k, int pad, const void* w, int cout,
                 const float* bias, int relu, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
+/*
+ * ub_conv_s2d followed by the max pool that consumes it (PASS_THROUGH nn.MaxPool2d,
+ * kernel 3 / stride 2 / pad 1, -inf padding), fused: y is the POOLED output
+ * [N][Ho/2][Wo/2][y_cstride] bf16; the conv output never reaches memory.  cout <= 64,
+ * conv output Ho, Wo even with Wo <= 128.  Same result as ub_conv_s2d + ub_maxpool2d.
+ */
+int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, int pad, const void* w, int cout,
+                        const float* bias, int relu, int pool_k, int pool_stride, int pool_pad,
+                        void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
 /* Model-input staging: NCHW fp32 -> NHWC bf16 [N*H*W][y_cstride], channels
  * idx[0..n) (a GATHER on the INPUT node, fused; idx == NULL: identity over C). */
 int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n,

@@ -58,22 +58,6 @@ struct HaloParams {
                      // 8 no TMA store, 16 no slot wait (races; timing only)
 };
 
-UB_DEVI uint64_t sdesc_plain(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1u) << 46;
-  return d;  // SWIZZLE_NONE
-}
-
-UB_DEVI void tma_store_4d(const void* map, const void* smem, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-
 // Compile-time halo geometry: padded width WP, rows per tile, staged positions, plane stride.
 template <int WP, int MT>
 struct HaloGeom {

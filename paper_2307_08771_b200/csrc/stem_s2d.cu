@@ -56,35 +56,6 @@ struct S2DParams {
             // 32 no TMEM reads, 64 no proxy fence, 128 no group barriers
 };
 
-// no-swizzle K-major descriptor with explicit LBO/SBO
-UB_DEVI uint64_t sdesc_interleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1u) << 46;
-  return d;  // layout 0 = SWIZZLE_NONE
-}
-
-UB_DEVI void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem)),
-      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-UB_DEVI void tma_store_4d(const void* map, const void* smem, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-
-UB_DEVI void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
 UB_DEVI void spin_wait(uint64_t* bar, uint32_t parity, int dbg) {
   if (dbg & 512) {
     const uint32_t a = smem_u32(bar);
@@ -196,9 +167,9 @@ __global__ void __launch_bounds__(S2D_THREADS, 1)
     for (int j = 0; j < NMMA; ++j) {
       const int dy = j / PAIRS, dx = (j % PAIRS) * 2;
       aoff[j] = static_cast<uint32_t>(dy * p.Ws + dx);
-      bdesc[j] = sdesc_interleave(b0 + j * 2 * p.np * 16, p.np * 16, 128);
+      bdesc[j] = sdesc_plain(b0 + j * 2 * p.np * 16, p.np * 16, 128);
     }
-    uint64_t adesc0 = sdesc_interleave(smem_u32(sA), 16, 128);
+    uint64_t adesc0 = sdesc_plain(smem_u32(sA), 16, 128);
     if (KQ == 4 && (p.dbg & 8192)) {
 #pragma unroll
       for (int j = 0; j < NMMA; ++j) {
@@ -207,7 +178,7 @@ __global__ void __launch_bounds__(S2D_THREADS, 1)
       }
     }
     if (p.dbg & 2048) {  // timing probe: aligned, non-overlapping K core matrices
-      adesc0 = sdesc_interleave(smem_u32(sA), 2048, 128);
+      adesc0 = sdesc_plain(smem_u32(sA), 2048, 128);
 #pragma unroll
       for (int j = 0; j < NMMA; ++j) aoff[j] = 0;
     }

@@ -61,10 +61,11 @@ class Engine:
 
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
-                 stem_s2d: bool = True, cover_ratio: float = 2.5):
+                 stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
+        self.stem_pool = stem_pool
         self.cover_ratio = cover_ratio
         self.graph = graph
         self.specs = specs
@@ -245,13 +246,32 @@ class Engine:
                     op.inputs[0] = r
             ops.extend(extra)
 
-        # --- schedule: Kahn over value dependencies, ties by topological position
-        produced = {op.output: op for op in ops}
-
         def base(v):
             while v in alias:
                 v = alias[v][0]
             return v
+
+        # --- stem -> max pool fusion: when the space-to-depth stem's only reader is a
+        # 3x3/s2/p1 max pool, the pool runs in the stem's epilogue (ub_conv_s2d_maxpool)
+        if self.stem_pool:
+            for sop in [o for o in ops if o.kind == "conv" and "stem_idx" in o.info]:
+                readers = [o for o in ops if any(base(i) == sop.output for i in o.inputs)]
+                if len(readers) != 1 or readers[0].kind != "maxpool":
+                    continue
+                mp = readers[0]
+                sp, cs = mp.info["spec"], self.specs[sop.info["conv"]]
+                _, ho, wo = self._shapes[sop.output]
+                cout = g.layer(sop.info["conv"]).out_channels
+                if ((sp.kernel, sp.stride, sp.pad) == (3, 2, 1) and base(mp.inputs[0]) == sop.output
+                        and self._s2d_ok(len(sop.info["stem_idx"]), cs, cout) and cout <= 64
+                        and ho % 2 == 0 and wo % 2 == 0 and wo <= 128):
+                    sop.info["pool"] = sp
+                    sop.info["out"] = mp.output
+                    sop.output = mp.output
+                    ops.remove(mp)
+
+        # --- schedule: Kahn over value dependencies, ties by topological position
+        produced = {op.output: op for op in ops}
 
         deps = {id(op): {id(produced[base(i)]) for i in op.inputs if base(i) in produced} for op in ops}
         done: set[int] = set()
@@ -448,6 +468,11 @@ class Engine:
             byts += 2.0 * cout * ho * wo
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
+    def _s2d_ok(self, cin: int, spec, cout: int) -> bool:
+        """Stem shapes the space-to-depth kernel takes (the folded 2x2 pixel fits 16 bytes)."""
+        kk = spec.kernel
+        return self.stem_s2d and spec.stride == 2 and kk >= 2 and (kk + 1) // 2 <= 4 and 4 * cin <= 8 and cout <= 128
+
     def _bind_stem(self, op, ws, vs, output_feed):
         info = op.info
         lid = info["conv"]
@@ -473,10 +498,18 @@ class Engine:
         cout, kk, st, pd = lay.out_channels, spec.kernel, spec.stride, spec.pad
         ci, hi, wi = self.input_chw
         # space-to-depth stem when the folded 2x2 pixel fits 16 bytes (ub_conv_s2d); else the
-        # single-launch im2col stem
-        s2d = (self.stem_s2d and st == 2 and kk >= 2 and 4 * cin <= 8 and cout <= 128
-               and y.cstride % 8 == 0 and y.coff % 8 == 0)
-        if s2d:
+        # single-launch im2col stem.  info["pool"]: the following max pool is fused.
+        s2d = self._s2d_ok(cin, spec, cout) and y.cstride % 8 == 0 and y.coff % 8 == 0
+        if "pool" in info:
+            assert s2d, "stem/max-pool fusion needs the space-to-depth stem"
+            wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
+            sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
+            self._keep += [wg, sbuf]
+            op.launch = lambda: K.stem_s2d_maxpool(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias,
+                                                   relu=relu)
+            op.info["stem_kind"] = "s2d+maxpool"
+            wbytes = 2.0 * wg.numel()
+        elif s2d:
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
             sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
             self._keep += [wg, sbuf]
@@ -491,8 +524,10 @@ class Engine:
             op.launch = lambda: K.conv_stem(self.input_buf, idx_dev, wg, kpad, cout, kk, st, pd, y, bias=bias, relu=relu)
             op.info["stem_kind"] = "im2col"
             wbytes = 2.0 * cout * kpad
-        flops = 2.0 * cout * cin * kk * kk * y.H * y.W
-        byts = 4.0 * ci * hi * wi + 2.0 * cout * y.H * y.W + wbytes / self.batch
+        pooled = "pool" in info
+        ho, wo = (2 * y.H, 2 * y.W) if pooled else (y.H, y.W)  # conv output (the pool halves it)
+        flops = 2.0 * cout * cin * kk * kk * ho * wo
+        byts = 4.0 * cin * hi * wi + 2.0 * cout * y.H * y.W + wbytes / self.batch
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
     # ------------------------------------------------------------------ execution
@@ -590,7 +625,7 @@ class Engine:
         one eager pass; before any pass, the op count (one launch per op, two for the
         space-to-depth stem)."""
         if getattr(self, "_launches", None) is None:
-            return sum(2 if op.info.get("stem_kind") == "s2d" else 1 for op in self.ops)
+            return sum(2 if op.info.get("stem_kind", "").startswith("s2d") else 1 for op in self.ops)
         return self._launches
 
     def per_image_work(self) -> tuple[float, float]:
@@ -601,7 +636,7 @@ class Engine:
 
 # ---------------------------------------------------------------------- builders
 def from_plans(sm, exported_graph: ModelGraph, maps, batch: int, device="cuda", gather_mode="fused",
-               masks: Mapping[str, Sequence[int]] | None = None) -> Engine:
+               masks: Mapping[str, Sequence[int]] | None = None, **engine_opts) -> Engine:
     """One-pass export: original sidecar weights + composed plan maps -> GEMM operands.
     With `masks` and an identity export this runs the mask-simulated original
     (interp.py:59-60: masked input channels == zero weight columns)."""
@@ -621,7 +656,7 @@ def from_plans(sm, exported_graph: ModelGraph, maps, batch: int, device="cuda", 
     def vs(uid):
         return sm.vectors[uid], (maps.vec.get(uid) if maps is not None else None)
 
-    return Engine(exported_graph, sm.specs, ws, vs, batch, sm.input_chw, device, gather_mode)
+    return Engine(exported_graph, sm.specs, ws, vs, batch, sm.input_chw, device, gather_mode, **engine_opts)
 
 
 def from_export(sm, result, batch: int, device="cuda", gather_mode="fused") -> Engine:

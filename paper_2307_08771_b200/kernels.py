@@ -185,6 +185,19 @@ def stem_s2d(x_nchw: torch.Tensor, idx_dev: torch.Tensor, s_buf: torch.Tensor, w
                                y.coff, _stream()))
 
 
+def stem_s2d_maxpool(x_nchw: torch.Tensor, idx_dev: torch.Tensor, s_buf: torch.Tensor, w: torch.Tensor, cout: int,
+                     k: int, pad: int, y: Act, bias: torch.Tensor | None = None, relu: bool = False,
+                     pool=(3, 2, 1)) -> None:
+    """stem_s2d with the following 3x3/s2 max pool fused into the epilogue; y is the pooled
+    output."""
+    N, C, H, W = x_nchw.shape
+    lib = _lib.load()
+    _lib.check(lib.ub_stem_s2d_pack(_p(x_nchw), N, C, H, W, _p(idx_dev), idx_dev.numel(), k, pad, _p(s_buf),
+                                    _stream()))
+    _lib.check(lib.ub_conv_s2d_maxpool(_p(s_buf), N, H, W, k, pad, _p(w), cout, _p(bias), int(relu), *pool,
+                                       _p(y.buf), y.cstride, y.coff, _stream()))
+
+
 def h2d_input_channels(host: torch.Tensor, dev: torch.Tensor, channels) -> int:
     """Pinned host NCHW fp32 -> device NCHW fp32, only `channels` (the INPUT GATHER's
     kept planes; the others are left untouched). Returns the bytes copied."""

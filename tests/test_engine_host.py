@@ -35,7 +35,10 @@ def test_resnet50_schedule(stub_kernels, r50, strategy, gather_mode, n_gather_op
     kinds = [op.kind for op in eng.ops]
     assert kinds.count("conv") == 54
     assert kinds.count("gather") == n_gather_ops  # the input GATHER is fused into the stem
-    assert kinds.count("maxpool") == 1 and kinds.count("avgpool") == 1
+    # the max pool after the space-to-depth stem runs in the stem's epilogue
+    assert kinds.count("maxpool") == 0 and kinds.count("avgpool") == 1
+    stem = [op for op in eng.ops if "stem_idx" in op.info]
+    assert len(stem) == 1 and "pool" in stem[0].info
     assert "stage" not in kinds and "eltwise" not in kinds  # BN/ADD/ReLU all absorbed
     # every residual ADD is fused into a conv epilogue; each conv absorbs its BN
     convs = [op for op in eng.ops if op.kind == "conv"]

@@ -165,6 +165,36 @@ def test_stem_s2d_matches_torch(N, H, k, pad, idx, cout):
     assert torch.isnan(y.buf[:, :8].float()).all()
 
 
+@pytest.mark.parametrize("N,H,idx,cout", [(3, 224, [2, 0], 64), (5, 64, [1], 60), (2, 100, [0, 2], 32)])
+def test_stem_s2d_maxpool_matches_torch(N, H, idx, cout):
+    """Stem with the 3x3/s2/p1 max pool fused into its epilogue (bands of pooled rows,
+    halo pairs, hrow hand-over ring) == conv -> bias -> ReLU -> max_pool2d."""
+    dev = "cuda"
+    k, pad = 7, 3
+    cin = len(idx)
+    g = torch.Generator().manual_seed(N * 1000 + H + cout)
+    x = torch.randn(N, 3, H, H, generator=g)
+    Wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
+    bias = torch.randn(cout, generator=g)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)), layout="s2d",
+                           out_dtype=torch.bfloat16)
+    Ho = (H + 2 * pad - k) // 2 + 1
+    Hp = Ho // 2
+    y = K.empty_act(N, Hp, Hp, cout + 8, dev)
+    y.buf.fill_(float("nan"))
+    y = y.view(8, cout)
+    sbuf = K.s2d_buffer(N, H, H, k, pad, dev)
+    K.stem_s2d_maxpool(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), sbuf, wg, cout, k, pad, y,
+                       bias=bias.to(dev), relu=True)
+    torch.cuda.synchronize()
+    conv = torch.nn.functional.conv2d(_bf(x[:, idx]), _bf(Wt), stride=2, padding=pad) + bias.view(1, -1, 1, 1)
+    ref = torch.nn.functional.max_pool2d(_bf(conv.clamp_min(0)), 3, 2, 1)
+    out = y.buf[:, 8:8 + cout].float().reshape(N, Hp, Hp, cout).permute(0, 3, 1, 2).cpu()
+    assert torch.isfinite(out).all()
+    assert _rel(out, ref) < 1e-2
+    assert torch.isnan(y.buf[:, :8].float()).all()
+
+
 def test_permute_weights_bit_exact():
     dev = "cuda"
     g = torch.Generator().manual_seed(0)

@@ -6,6 +6,7 @@ around each launch, eager) with algorithmic bytes/FLOPs and roofline times.
 """
 
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -27,7 +28,12 @@ def main():
     plans = P.load_plans(cfg.asset_dir / f"plans_{strategy}.json")
     eg = E.export_graph(sm.graph, plans)
     maps = E.compose_maps(sm.graph, plans)
-    eng = EN.from_plans(sm, eg, maps, batch=N, gather_mode=gm)
+    opts = {}
+    for kv in os.environ.get("UB_ENGINE_OPTS", "").split(","):
+        if "=" in kv:
+            k, v = kv.split("=")
+            opts[k] = v == "1"
+    eng = EN.from_plans(sm, eg, maps, batch=N, gather_mode=gm, **opts)
     x = torch.randn(N, 3, 224, 224, device="cuda")
     eng.input_buf.copy_(x)
     # per-op eager timing
