@@ -93,6 +93,7 @@ struct ConvKParams {
   int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
   int b_res;  // weights of this CTA's N tile stay resident in smem (loaded once; grid % n_tiles == 0)
   long long* trace;  // profiling (UB_CONV_TRACE): CTA 0 per-tile event clocks [tile][8]
+  int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
 };
 #define UB_TRACE(slot)                                                                  \
   do {                                                                                  \
@@ -121,7 +122,8 @@ __device__ __forceinline__ int tile_res_chunks(const ConvKParams& p, int n0) {
 
 template <int AMODE, int BK, int PRODUCERS>
 __global__ void __launch_bounds__(256 + PRODUCERS, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const ConvKParams p) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmB,
+                   const ConvKParams p) {
   constexpr int PWARPS = PRODUCERS / 32;
   constexpr int GROWS = BLOCK_M / PWARPS;       // gather mode: rows per producer warp
   constexpr int STEM_K = 64 * 128 / PRODUCERS;  // stem mode: k values per producer thread per k-block
@@ -157,8 +159,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
 
   if (warp == 0 && lane == 0) {
     if (p.epi_tma) tma_prefetch_desc(&tmY);
+    if (p.b_tma) tma_prefetch_desc(&tmB);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0));
+      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0) + (p.b_tma ? 1 : 0));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -460,8 +463,13 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
             *reinterpret_cast<uint4*>(tA + swz<64>(row, j0 + jj)) = o;
           }
         }
-        // ---- B (weights [cout][K_total]): rows row0 + i * ROW_STEP, chunk cj
-        if (!p.b_res) {
+        // ---- B (weights [cout][K_total]): one TMA box, or rows row0 + i * ROW_STEP, chunk cj
+        if (p.b_tma) {
+          if (pt == 0) {
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(p.block_n) * ROW_BYTES);
+            tma_load_2d(&tmB, &full[s], sB + s * b_stride, kcoord, n0);
+          }
+        } else if (!p.b_res) {
           const uint16_t* src = b_base + kcoord;
           const bool k_ok = AMODE != A_PACKED || kcoord + cj * 8 < p.K_total;  // packed: last k-block ragged
           for (int i = 0; i < nb_pieces; ++i, src += b_row_stride) {
@@ -509,6 +517,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&full[s]);
         }
+        if (p.b_tma && pt == 0) mbar_arrive(&full[s]);  // no weight box in a residual k-block
         cp_async_arrive_noinc(&full[s]);
         if (++s == stages) {
           s = 0;
@@ -693,7 +702,8 @@ int num_sms() {
 namespace {
 
 template <int AMODE, int BK, int PRODUCERS>
-int launch_conv_p(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
+int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const ConvKParams& p, int grid, size_t smem,
+                  cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -701,16 +711,16 @@ int launch_conv_p(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, p);
+  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, tmB, p);
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
 }
 
 template <int AMODE, int BK>
-int launch_conv(const CUtensorMap& tmY, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream,
-                int wide) {
-  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, p, grid, smem, stream)
-              : launch_conv_p<AMODE, BK, 256>(tmY, p, grid, smem, stream);
+int launch_conv(const CUtensorMap& tmY, const CUtensorMap& tmB, const ConvKParams& p, int grid, size_t smem,
+                cudaStream_t stream, int wide) {
+  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, tmB, p, grid, smem, stream)
+              : launch_conv_p<AMODE, BK, 256>(tmY, tmB, p, grid, smem, stream);
 }
 
 int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : (cin_eff <= 32 ? 32 : 64); }
@@ -902,6 +912,20 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     apply_small_tensor_quirk(&tmY, static_cast<size_t>(p.M) * d->y_cstride * 2);
   }
 
+  // weights by TMA: one box (BK x block_n, the operand's swizzle) per k-block
+  CUtensorMap tmB{};
+  p.b_tma = !p.b_res && !(d->variant & 16);
+  if (p.b_tma) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.K_total), static_cast<cuuint64_t>(d->cout)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.K_total) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(p.block_n)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_tiled_fn()(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d->w), dims, strides,
+                                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(bk * 2),
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode weight tensor map failed (%d)", (int)r);
+    apply_small_tensor_quirk(&tmB, static_cast<size_t>(p.K_total) * d->cout * 2);
+  }
   const int num_tiles = p.m_tiles * p.n_tiles;
   int grid = num_tiles < num_sms() ? num_tiles : num_sms();
   if (p.b_res && grid % p.n_tiles) grid = grid / p.n_tiles * p.n_tiles;
@@ -909,18 +933,18 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int pw = d->variant & 3;
   int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
-  if (stem) return launch_conv<A_STEM, 64>(tmY, p, grid, smem, stream, wide);
-  if (packed) return launch_conv<A_PACKED, 64>(tmY, p, grid, smem, stream, wide);
-  if (gather) return launch_conv<A_GATHER, 64>(tmY, p, grid, smem, stream, wide);
+  if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, p, grid, smem, stream, wide);
+  if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, p, grid, smem, stream, wide);
+  if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   if (pointwise) {
-    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, p, grid, smem, stream, wide);
-    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, p, grid, smem, stream, wide);
-    return launch_conv<A_TILED, 16>(tmY, p, grid, smem, stream, wide);
+    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, tmB, p, grid, smem, stream, wide);
+    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, tmB, p, grid, smem, stream, wide);
+    return launch_conv<A_TILED, 16>(tmY, tmB, p, grid, smem, stream, wide);
   }
-  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, p, grid, smem, stream, wide);
-  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, p, grid, smem, stream, wide);
-  return launch_conv<A_IM2COL, 16>(tmY, p, grid, smem, stream, wide);
+  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, tmB, p, grid, smem, stream, wide);
+  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, tmB, p, grid, smem, stream, wide);
+  return launch_conv<A_IM2COL, 16>(tmY, tmB, p, grid, smem, stream, wide);
 }
 
 extern "C" long long* ub_debug_conv_trace() { return ub::g_conv_trace; }
