@@ -94,6 +94,7 @@ struct ConvKParams {
   int b_res;  // weights of this CTA's N tile stay resident in smem (loaded once; grid % n_tiles == 0)
   long long* trace;  // profiling (UB_CONV_TRACE): CTA 0 per-tile event clocks [tile][8]
   int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
+  int a_tma;         // tiled mode: A and residual k-blocks by TMA too (one producer thread)
 };
 #define UB_TRACE(slot)                                                                  \
   do {                                                                                  \
@@ -123,6 +124,7 @@ __device__ __forceinline__ int tile_res_chunks(const ConvKParams& p, int n0) {
 template <int AMODE, int BK, int PRODUCERS>
 __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
                    const ConvKParams p) {
   constexpr int PWARPS = PRODUCERS / 32;
   constexpr int GROWS = BLOCK_M / PWARPS;       // gather mode: rows per producer warp
@@ -160,8 +162,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   if (warp == 0 && lane == 0) {
     if (p.epi_tma) tma_prefetch_desc(&tmY);
     if (p.b_tma) tma_prefetch_desc(&tmB);
+    if (p.a_tma) {
+      tma_prefetch_desc(&tmA);
+      if (p.has_res) tma_prefetch_desc(&tmR);
+    }
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0) + (p.b_tma ? 1 : 0));
+      mbar_init(&full[s], p.a_tma ? 1 : PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0) + (p.b_tma ? 1 : 0));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -308,6 +314,38 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       }
       cp_async_arrive_noinc(bres);
     }
+    if (AMODE == A_TILED && p.a_tma) {
+      // every operand of a 1x1/s1 tile is a TMA box: one thread issues A (BK ch x 128 px),
+      // B (BK x block_n) and the residual chunks (64 ch x 128 px) per stage
+      if (pt == 0) {
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+          const int m_tile = t / p.n_tiles;
+          const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
+          const int m0 = m_tile * BLOCK_M;
+          const int nres = tile_res_chunks(p, n0);
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t bytes = BLOCK_M * ROW_BYTES + (p.b_tma ? static_cast<uint32_t>(p.block_n) * ROW_BYTES : 0u);
+            mbar_arrive_expect_tx(&full[s], bytes);
+            tma_load_2d(&tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
+            if (p.b_tma) tma_load_2d(&tmB, &full[s], sB + s * b_stride, kb * BK, n0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          for (int rc = 0; rc < nres; ++rc) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], BLOCK_M * 128);
+            tma_load_2d(&tmR, &full[s], sA + s * A_BYTES, n0 + rc * EPI_CHUNK, m0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    } else
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int it = (t - blockIdx.x) / gridDim.x;
       if (pt == 0) UB_TRACE(6);
@@ -702,8 +740,8 @@ int num_sms() {
 namespace {
 
 template <int AMODE, int BK, int PRODUCERS>
-int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const ConvKParams& p, int grid, size_t smem,
-                  cudaStream_t stream) {
+int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
+                  const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -711,16 +749,16 @@ int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const ConvKPar
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, tmB, p);
+  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, tmB, tmA, tmR, p);
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
 }
 
 template <int AMODE, int BK>
-int launch_conv(const CUtensorMap& tmY, const CUtensorMap& tmB, const ConvKParams& p, int grid, size_t smem,
-                cudaStream_t stream, int wide) {
-  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, tmB, p, grid, smem, stream)
-              : launch_conv_p<AMODE, BK, 256>(tmY, tmB, p, grid, smem, stream);
+int launch_conv(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
+                const ConvKParams& p, int grid, size_t smem, cudaStream_t stream, int wide) {
+  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, tmB, tmA, tmR, p, grid, smem, stream)
+              : launch_conv_p<AMODE, BK, 256>(tmY, tmB, tmA, tmR, p, grid, smem, stream);
 }
 
 int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : (cin_eff <= 32 ? 32 : 64); }
@@ -926,6 +964,28 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode weight tensor map failed (%d)", (int)r);
     apply_small_tensor_quirk(&tmB, static_cast<size_t>(p.K_total) * d->cout * 2);
   }
+  // 1x1/s1 (tiled) A and the residual by TMA as well
+  CUtensorMap tmA{}, tmR{};
+  const bool tiled = !stem && !packed && !gather && d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
+  p.a_tma = tiled && !(d->variant & 32);
+  if (p.a_tma) {
+    auto enc = [&](CUtensorMap* m, const void* base, int cstride, int cols, int box_c) -> CUresult {
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(p.M)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(cstride) * 2};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(box_c), BLOCK_M};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = encode_tiled_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(box_c * 2),
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      apply_small_tensor_quirk(m, static_cast<size_t>(p.M) * cstride * 2);
+      return r;
+    };
+    // A: channels [coff - lead, x_cstride) of every pixel row (beyond: zero fill)
+    if (enc(&tmA, p.x, d->x_cstride, d->x_cstride - (d->x_coff - lead), bk) != CUDA_SUCCESS)
+      return fail(UB_ECUDA, "ub_conv_fwd: encode activation tensor map failed");
+    if (p.has_res && enc(&tmR, p.res, d->res_cstride, d->res_cstride - d->res_coff, EPI_CHUNK) != CUDA_SUCCESS)
+      return fail(UB_ECUDA, "ub_conv_fwd: encode residual tensor map failed");
+  }
   const int num_tiles = p.m_tiles * p.n_tiles;
   int grid = num_tiles < num_sms() ? num_tiles : num_sms();
   if (p.b_res && grid % p.n_tiles) grid = grid / p.n_tiles * p.n_tiles;
@@ -933,18 +993,18 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int pw = d->variant & 3;
   int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
-  if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, p, grid, smem, stream, wide);
-  if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, p, grid, smem, stream, wide);
-  if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, p, grid, smem, stream, wide);
+  if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   if (pointwise) {
-    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, tmB, p, grid, smem, stream, wide);
-    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, tmB, p, grid, smem, stream, wide);
-    return launch_conv<A_TILED, 16>(tmY, tmB, p, grid, smem, stream, wide);
+    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+    return launch_conv<A_TILED, 16>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
   }
-  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, tmB, p, grid, smem, stream, wide);
-  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, tmB, p, grid, smem, stream, wide);
-  return launch_conv<A_IM2COL, 16>(tmY, tmB, p, grid, smem, stream, wide);
+  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  return launch_conv<A_IM2COL, 16>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
 }
 
 extern "C" long long* ub_debug_conv_trace() { return ub::g_conv_trace; }

@@ -441,10 +441,11 @@ class Engine:
         fp32_out = info["out"] in output_feed
         y = self._alloc(info["out"], cout, fp32=fp32_out)
         relu = info["relu"] is not None
-        # variant = (plan index, kernel variant bits: producer width 0 = library heuristic,
-        # 1 = 256, 2 = 512 threads; +4 = re-load the weights per tile instead of keeping them
-        # resident in shared memory)
-        op.info["variants"] = [(pi, pw | nb) for pi in range(len(plans)) for pw in (1, 2) for nb in (0, 4)]
+        # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
+        # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
+        # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA)
+        op.info["variants"] = [(pi, pw | nb | bt | at) for pi in range(len(plans)) for pw in (1, 2)
+                               for nb in (0, 4) for bt in (0, 16) for at in (0, 32)]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
 
