@@ -68,7 +68,7 @@ struct HaloGeom {
 };
 
 template <int WP, int PLANES, int MT>
-__global__ void __launch_bounds__(HALO_THREADS, 1)
+__global__ void __maxnreg__(144)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
   constexpr int TAPS = 9;
   using G = HaloGeom<WP, MT>;
@@ -137,10 +137,11 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
       const int img = t / p.tiles_per_img;
       const int y0 = (t - img * p.tiles_per_img) * G::RT - 1;  // first staged input row (pad 1)
       const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + pp * 8;
-      mbar_wait(&aempty[s], ph ^ 1);
+      if (p.dbg & 64) mbar_wait_sleep(&aempty[s], ph ^ 1, 2000);
+      else mbar_wait(&aempty[s], ph ^ 1);
       if (p.trace && blockIdx.x == 0 && pt == 0) {
         const int itp = (t - blockIdx.x) / gridDim.x;
-        if (itp < 64) p.trace[itp * 8 + 7] = clock64();
+        if (itp < 64) p.trace[itp * 16 + 7] = clock64();
       }
       const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * G::PLANE_STRIDE);
       for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
@@ -176,11 +177,11 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
       const int acc = it % p.nacc;
-      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 0] = clock64();
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 0] = clock64();
       mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
-      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 1] = clock64();
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 1] = clock64();
       mbar_wait(&afull[s], ph);
-      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 2] = clock64();
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 2] = clock64();
       __syncwarp();
       tc_fence_after();
       fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
       }
       umma_commit_warp(&aempty[s]);
       umma_commit_warp(&tfull[acc]);
-      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 8 + 3] = clock64();
+      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 3] = clock64();
       if (++s == p.a_stages) {
         s = 0;
         ph ^= 1;
@@ -223,46 +224,54 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
       const int r0 = q * 32;
       const int ox = r0 % WP;
       const int acc = it % p.nacc;
-      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 4] = clock64();
-      mbar_wait(&tfull[acc], (it / p.nacc) & 1);
-      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 5] = clock64();
+      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 16 + 4] = clock64();
+      if (p.dbg & 128) mbar_wait_sleep(&tfull[acc], (it / p.nacc) & 1, 2000);
+      else mbar_wait(&tfull[acc], (it / p.nacc) & 1);
+      if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 16 + 5] = clock64();
       tc_fence_after();
+#define HALO_T(k) \
+  if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && cm < 2) p.trace[it * 16 + 8 + cm * 4 + (k)] = clock64()
       for (int cm = 0; cm < MT * nchunks; ++cm, ++ec) {
         const int mt = cm / nchunks, c = cm - mt * nchunks;
         const int oy = y0 + mt * G::R + r0 / WP;
         const uint32_t taddr =
             tmem_base + (acc * MT + mt) * p.acc_cols + (static_cast<uint32_t>(q * 32) << 16);
         uint8_t* slot = slots + (ec & 1) * HALO_SLOT;
-        // both 32-column halves of the chunk in flight before one wait
-        uint32_t v0[32], v1[32];
         const int col0 = c * 64;
-        if (p.dbg & 4) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0;
-        } else {
-          if (col0 + 32 <= p.np) tmem_ld32(taddr + col0, v0);
-          else tmem_ld16_lo(taddr + col0, v0);
-          if (col0 + 64 <= p.np) tmem_ld32(taddr + col0 + 32, v1);
-          else if (col0 + 32 < p.np) tmem_ld16_lo(taddr + col0 + 32, v1);
-          tmem_ld_wait();
-        }
-        if (cm + 1 == MT * nchunks) {  // accumulators drained: hand them back before the math and store
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-          if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 8 + 6] = clock64();
-        }
-        if (p.dbg & 2) continue;
         if (lane == 0 && !(p.dbg & 16)) bulk_wait_read<1>();  // this slot's store from two chunks ago has read it
         __syncwarp();
-        // 16-byte chunk k (channels col0 + 8k ..) of row `lane`, SW128 position k ^ (lane & 7)
-        auto emit = [&](const uint32_t (&v)[32], int half) {
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {  // 32 columns per TMEM round trip (register budget)
+          const int colh = col0 + half * 32;
+          if (colh >= p.np) break;
+          uint32_t v[32];
+          if (p.dbg & 4) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0;
+          } else {
+            if (colh + 32 <= p.np) tmem_ld32(taddr + colh, v);
+            else tmem_ld16_lo(taddr + colh, v);
+            tmem_ld_wait();
+          }
+          HALO_T(half);
+          const bool last = cm + 1 == MT * nchunks && (half == 1 || colh + 32 >= p.np);
+          if (last) {  // accumulators drained: hand them back before the math and store
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 16 + 6] = clock64();
+          }
+          if (p.dbg & 2) continue;
+          // 16-byte chunk k (channels colh + 8k ..) of row `lane`, SW128 position (half*4+k) ^ (lane & 7)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
-            const int col = col0 + half * 32 + 8 * jj;
+            const int col = colh + 8 * jj;
             if (col >= p.np) break;
-            const float4 b0 = *reinterpret_cast<const float4*>(sBias + col);
-            const float4 b1 = *reinterpret_cast<const float4*>(sBias + col + 4);
+            float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+            if (!(p.dbg & 256)) {
+              b0 = *reinterpret_cast<const float4*>(sBias + col);
+              b1 = *reinterpret_cast<const float4*>(sBias + col + 4);
+            }
             const float2 s0 = add_f32x2(make_float2(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1])),
                                         make_float2(b0.x, b0.y));
             const float2 s1 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3])),
@@ -282,15 +291,16 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
             const int chunk = half * 4 + jj;
             *reinterpret_cast<uint4*>(slot + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o;
           }
-        };
-        emit(v0, 0);
-        emit(v1, 1);
+        }
+        HALO_T(2);
+        if (p.dbg & 2) continue;
         if (!(p.dbg & 32)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && !(p.dbg & 8)) {
           tma_store_4d(&tmY, slot, col0, ox, oy, img);
           bulk_commit();
         }
+        HALO_T(3);
       }
     }
     if (lane == 0) bulk_wait_all();
@@ -351,7 +361,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
     static long long* trace = nullptr;
     static int want = -1;
     if (want < 0) want = getenv("UB_HALO_TRACE") ? 1 : 0;
-    if (want && !trace) cudaMalloc(&trace, 64 * 8 * sizeof(long long));
+    if (want && !trace) cudaMalloc(&trace, 64 * 16 * sizeof(long long));
     p.trace = trace;
     g_halo_trace = trace;
     static int dbg = -1;

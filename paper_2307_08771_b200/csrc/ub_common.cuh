@@ -37,6 +37,29 @@ UB_DEVI bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint (ns): the thread sleeps in hardware until the phase
+// completes or the hint elapses -- for waiters that would otherwise spin for many
+// microseconds and steal issue slots from the warps doing the work.
+UB_DEVI bool mbar_try_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+UB_DEVI void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait_hint(a, parity, ns)) return;
+  long long t0 = clock64();
+  while (!mbar_try_wait_hint(a, parity, ns)) {
+    if (clock64() - t0 > (1ll << 33)) asm volatile("trap;");
+  }
+}
+
 // Bounded wait: a lost arrival traps (kernel error) instead of hanging the GPU.
 UB_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

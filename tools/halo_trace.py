@@ -25,13 +25,14 @@ def main():
     lib = _lib.load()
     lib.ub_debug_halo_trace.restype = ctypes.c_void_p
     ptr = lib.ub_debug_halo_trace()
-    t = torch.empty(64 * 8, dtype=torch.int64, device=dev)
+    t = torch.empty(64 * 16, dtype=torch.int64, device=dev)
     import cuda.bindings.runtime as rt
-    rt.cudaMemcpy(t.data_ptr(), ptr, 64 * 8 * 8, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+    rt.cudaMemcpy(t.data_ptr(), ptr, 64 * 16 * 8, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
     torch.cuda.synchronize()
-    v = t.cpu().view(64, 8).tolist()
+    v = t.cpu().view(64, 16).tolist()
     t0 = v[0][0]
-    print("tile  mma:start tempty_ok afull_ok issued | epi:start tfull_ok tempty_arr | prod:stage_free")
+    print("tile  mma:start tempty_ok afull_ok issued | epi:start tfull_ok tempty_arr | prod:stage_free |"
+          " epi warp0 per chunk: ld_done bulkwait_done emit_done store_issued (x2)")
     for i, r in enumerate(v[:40]):
         print(i, [x - t0 if x else None for x in r])
 
