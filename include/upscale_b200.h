@@ -131,7 +131,8 @@ typedef struct {
                                   bit 2: re-load weights per tile (no weight-stationary B);
                                   bit 3: no halo-tile kernel for stride-1 3x3 convs;
                                   bit 4: weights by cp.async instead of one TMA box per K-block;
-                                  bit 5: 1x1/s1 activations and residual by cp.async, not TMA */
+                                  bit 5: 1x1/s1 activations and residual by cp.async, not TMA;
+                                  bit 6: one epilogue warpgroup (not two) on the TMA-fed 1x1 path */
 } ub_conv_desc;
 
 /* Dense-K padding (multiple of 64) of the fused-stem weight operand. */

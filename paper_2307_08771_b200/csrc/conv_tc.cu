@@ -95,6 +95,7 @@ struct ConvKParams {
   long long* trace;  // profiling (UB_CONV_TRACE): CTA 0 per-tile event clocks [tile][8]
   int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
   int a_tma;         // tiled mode: A and residual k-blocks by TMA too (one producer thread)
+  int epi2;          // (a_tma only) idle producer warps 12-15 form a second epilogue group
 };
 #define UB_TRACE(slot)                                                                  \
   do {                                                                                  \
@@ -144,9 +145,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_BYTES;  // per-stage B, or all k-blocks of B when resident
   uint8_t* sI = sB + (p.b_res ? p.num_kb : stages) * b_stride;  // identity 64x64 (8 KB)
-  uint8_t* sE = sI + IDENT_BYTES;                               // 4 warps x 2 output slots
-  float* sBias = reinterpret_cast<float*>(sE + 4 * EPI_WARP_BYTES);  // 4 warps x MAX_BLOCK_N
-  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + 4 * MAX_BLOCK_N);
+  // epilogue warps: 4, or 8 when the producers are idle (TMA-fed 1x1): group 1 = warps 12-15
+  const int epi_warps = p.epi2 ? 8 : 4;
+  uint8_t* sE = sI + IDENT_BYTES;                                          // epi_warps x 2 output slots
+  float* sBias = reinterpret_cast<float*>(sE + epi_warps * EPI_WARP_BYTES);  // epi_warps x MAX_BLOCK_N
+  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + epi_warps * MAX_BLOCK_N);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
 
   if (warp == 0 && lane == 0) {
     if (p.epi_tma) tma_prefetch_desc(&tmY);
-    if (p.b_tma) tma_prefetch_desc(&tmB);
+    if (p.b_tma || p.a_tma) tma_prefetch_desc(&tmB);
     if (p.a_tma) {
       tma_prefetch_desc(&tmA);
       if (p.has_res) tma_prefetch_desc(&tmR);
@@ -172,9 +175,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], epi_warps);
     }
-    mbar_init(bres, PRODUCERS);
+    mbar_init(bres, p.a_tma ? 1 : PRODUCERS);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         UB_TRACE(2);
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && !(p.epi2 && warp >= 12 && warp < 16)) {
     // ================= producers (256 threads): fill stage s with A and B, then arrive on full[s]
     // Addresses are precomputed per tile so the per-k-block work is one add + one cp.async per
     // 16-byte chunk; smem destinations are constant for the whole kernel.
@@ -294,7 +297,13 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     const uint32_t rdst0 = swz<64>(rrow0, rj);
     int s = 0;
     uint32_t ph = 0;
-    if (p.b_res) {  // all k-blocks of this CTA's N tile, once
+    if (p.b_res && p.a_tma) {  // all k-blocks of this CTA's N tile, once, as TMA boxes
+      if (pt == 0) {
+        const int n0 = (blockIdx.x % p.n_tiles) * p.block_n;
+        mbar_arrive_expect_tx(bres, static_cast<uint32_t>(nk) * p.block_n * ROW_BYTES);
+        for (int kb = 0; kb < nk; ++kb) tma_load_2d(&tmB, bres, sB + kb * b_stride, kb * BK, n0);
+      }
+    } else if (p.b_res) {  // all k-blocks of this CTA's N tile, once
       const int n0 = (blockIdx.x % p.n_tiles) * p.block_n;
       const int b_valid = min(p.block_n, p.cout - n0);
       const uint16_t* b_base = p.w + static_cast<size_t>(n0 + row0) * p.K_total + cj * 8;
@@ -567,12 +576,16 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     cp_async_wait<0>();
   } else if (warp >= 4) {
     // ================= epilogue
-    // Warp q owns TMEM lanes / tile rows q*32..q*32+31 and walks 64-channel chunks.  After
-    // draining a 32-column half it re-arms those accumulator columns with the bias of the
-    // tile that will use this accumulator next (tile i+2).
-    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint8_t* oslots = sE + q * EPI_WARP_BYTES;
-    float* sb = sBias + q * MAX_BLOCK_N;
+    // Warp q owns TMEM lanes / tile rows q*32..q*32+31 and walks 64-channel chunks (with two
+    // groups: group eg takes the chunks c % 2 == eg).  After draining a 32-column half it
+    // re-arms those accumulator columns with the bias of the tile that uses this
+    // accumulator next (tile i+2).
+    const int q = warp & 3;  // TMEM lane quarter (warp % 4)
+    const int eg = warp >= 12 ? 1 : 0;
+    const int ngrp = epi_warps / 4;
+    const int ew = eg * 4 + q;  // epilogue warp index: slots and bias buffer
+    uint8_t* oslots = sE + ew * EPI_WARP_BYTES;
+    float* sb = sBias + ew * MAX_BLOCK_N;
     const bool tma = p.epi_tma;
     uint32_t ec = 0;  // chunks processed by this warp (= TMA stores committed)
     // bias of tile tt -> sb (zero past cout), columns [0, width)
@@ -603,7 +616,8 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       if (tt < num_tiles) {
         stage_bias(tt);
         const uint32_t ta = tmem_base + a * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-        for (int col = 0; col < static_cast<int>(p.acc_stride); col += 32) arm32(ta + col, col);
+        for (int col = 0; col < static_cast<int>(p.acc_stride); col += 32)
+          if ((col / EPI_CHUNK) % ngrp == eg) arm32(ta + col, col);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -622,12 +636,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       const bool rearm = t_next < num_tiles;
       if (rearm) stage_bias(t_next);
       const int acc = it & 1;
-      if (q == 0) UB_TRACE(3);
+      if (ew == 0) UB_TRACE(3);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
-      if (q == 0) UB_TRACE(4);
+      if (ew == 0) UB_TRACE(4);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < nchunks; ++c, ++ec) {
+      for (int c = eg; c < nchunks; c += ngrp, ++ec) {
         uint8_t* oslot = oslots + (ec & 1) * EPI_SLOT;
         if (tma && lane == 0) bulk_wait_read<1>();  // this slot's store from 2 chunks ago has read it
         __syncwarp();
@@ -694,12 +708,13 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       }
       // re-arm the columns past this tile's last chunk (the next user may be wider)
       if (rearm)
-        for (int col = nchunks * EPI_CHUNK; col < static_cast<int>(p.acc_stride); col += 32) arm32(taddr + col, col);
+        for (int col = nchunks * EPI_CHUNK; col < static_cast<int>(p.acc_stride); col += 32)
+          if ((col / EPI_CHUNK) % ngrp == eg) arm32(taddr + col, col);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);  // drained (and re-armed): the MMA may reuse it
-      if (q == 0) UB_TRACE(5);
+      if (ew == 0) UB_TRACE(5);
     }
     if (tma && lane == 0) bulk_wait_all();
   }
@@ -918,7 +933,11 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
 
   const uint32_t a_bytes = BLOCK_M * 128;  // sized for 64-wide residual k-blocks
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
-  uint32_t fixed = 1024 + IDENT_BYTES + 4 * EPI_WARP_BYTES + 4 * MAX_BLOCK_N * 4 + BAR_BYTES +
+  const bool tiled_1x1 = !stem && !packed && !gather && d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
+  p.a_tma = tiled_1x1 && !(d->variant & 32);
+  p.epi2 = p.a_tma && !(d->variant & 64);
+  const int epi_warps = p.epi2 ? 8 : 4;
+  uint32_t fixed = 1024 + IDENT_BYTES + epi_warps * EPI_WARP_BYTES + epi_warps * MAX_BLOCK_N * 4 + BAR_BYTES +
                    ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
   // Weight-stationary B: when all k-blocks of one N tile fit next to >= 4 A stages, each CTA
   // keeps its N tile's weights in smem (grid a multiple of n_tiles, so a CTA's tiles share
@@ -952,8 +971,8 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
 
   // weights by TMA: one box (BK x block_n, the operand's swizzle) per k-block
   CUtensorMap tmB{};
-  p.b_tma = !p.b_res && !(d->variant & 16);
-  if (p.b_tma) {
+  p.b_tma = !p.b_res && (p.a_tma || !(d->variant & 16));  // the TMA-fed 1x1 path has no cp.async B
+  if (p.b_tma || p.a_tma) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.K_total), static_cast<cuuint64_t>(d->cout)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.K_total) * 2};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(p.block_n)};
@@ -966,8 +985,6 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   }
   // 1x1/s1 (tiled) A and the residual by TMA as well
   CUtensorMap tmA{}, tmR{};
-  const bool tiled = !stem && !packed && !gather && d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
-  p.a_tma = tiled && !(d->variant & 32);
   if (p.a_tma) {
     auto enc = [&](CUtensorMap* m, const void* base, int cstride, int cols, int box_c) -> CUresult {
       cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(p.M)};

@@ -443,9 +443,12 @@ class Engine:
         relu = info["relu"] is not None
         # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
-        # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA)
-        op.info["variants"] = [(pi, pw | nb | bt | at) for pi in range(len(plans)) for pw in (1, 2)
-                               for nb in (0, 4) for bt in (0, 16) for at in (0, 32)]
+        # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
+        # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path)
+        tiled = kk == 1 and st == 1
+        op.info["variants"] = [(pi, pw | nb | bt | at | e1) for pi in range(len(plans)) for pw in (1, 2)
+                               for nb in (0, 4) for bt in (0, 16) for at in ((0, 32) if tiled else (32,))
+                               for e1 in ((0, 64) if tiled else (0,))]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
 
