@@ -43,6 +43,15 @@ int cuda_status(cudaError_t e, const char* what) {
 
 void count_launch() { ++g_launches; }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UB_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn() {
   std::call_once(g_once, resolve);
   return g_tiled;

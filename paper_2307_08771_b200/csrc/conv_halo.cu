@@ -108,6 +108,7 @@ __global__ void __maxnreg__(144)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
 
   if (warp >= HALO_PROD_WARP0) {
     // ================= producers
@@ -125,6 +126,7 @@ __global__ void __maxnreg__(144)
                    : "memory");
     }
     cp_async_arrive_noinc(bres);
+    griddep_wait();  // the input activations come from the previous kernel (PDL)
     // halo planes: this thread always fills plane pp of positions q0 + i * qstep
     const int pp = pt % PLANES;
     const int q0 = pt / PLANES;
@@ -402,10 +404,10 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
 #undef UB_HALO_CASE
   if (!kern) return UB_OK;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  kern<<<grid, HALO_THREADS, smem, stream>>>(tm, p);
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, p);
   count_launch();
   *handled = true;
-  return cuda_status(cudaGetLastError(), "conv_halo3_kernel");
+  return cuda_status(e, "conv_halo3_kernel");
 }
 
 }  // namespace ub

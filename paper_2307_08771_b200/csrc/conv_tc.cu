@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();  // the next kernel may start its prologue as SMs free up
 
   if (warp == 1) {
     {
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       }
       cp_async_arrive_noinc(bres);
     }
+    griddep_wait();  // activations / residual come from the previous kernel (PDL)
     if (AMODE == A_TILED && p.a_tma) {
       // every operand of a 1x1/s1 tile is a TMA box: one thread issues A (BK ch x 128 px),
       // B (BK x block_n) and the residual chunks (64 ch x 128 px) per stage
@@ -764,7 +766,9 @@ int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensor
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  conv_tc_kernel<AMODE, BK, PRODUCERS><<<grid, 256 + PRODUCERS, smem, stream>>>(tmY, tmB, tmA, tmR, p);
+  const cudaError_t e = launch_pdl(conv_tc_kernel<AMODE, BK, PRODUCERS>, dim3(grid), dim3(256 + PRODUCERS), smem,
+                                   stream, tmY, tmB, tmA, tmR, p);
+  if (e != cudaSuccess) return cuda_status(e, "conv_tc_kernel launch");
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
 }

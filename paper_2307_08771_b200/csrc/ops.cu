@@ -116,6 +116,8 @@ __global__ void permute_vector_kernel(const T* __restrict__ v, const int32_t* __
 __global__ void channel_gather_kernel(const uint16_t* __restrict__ x, int x_cstride, int x_coff,
                                       const int32_t* __restrict__ idx, int n, long long npix, uint16_t* __restrict__ y,
                                       int y_cstride, int y_coff) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (long long p = (long long)blockIdx.x * warps + (threadIdx.x >> 5); p < npix; p += (long long)gridDim.x * warps) {
@@ -167,6 +169,8 @@ __global__ void stage_input_kernel(const float* __restrict__ x, int N, int C, in
 __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_cstride,
                                int x_coff, int k, int stride, int pad, int Ho, int Wo, __nv_bfloat16* __restrict__ y,
                                int y_cstride, int y_coff, bool vec) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int groups = (C + 7) / 8;
   const int total = N * Ho * Wo * groups;  // < 2^31 (checked by the host)
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -220,6 +224,8 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, int N, int H
 // Block = one image x 256 channels; threads stride the HW positions per channel.
 __global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C, int x_cstride, int x_coff,
                                __nv_bfloat16* __restrict__ y, int y_cstride, int y_coff) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int img = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
@@ -314,10 +320,11 @@ extern "C" int ub_channel_gather(const void* x, int x_cstride, int x_coff, const
   if (y_coff + n > y_cstride) return fail(UB_EINVAL, "ub_channel_gather: output exceeds y_cstride");
   const int block = 256;
   const int grid = grid_for(npix, block / 32);
-  channel_gather_kernel<<<grid, block, 0, stream>>>(static_cast<const uint16_t*>(x), x_cstride, x_coff, idx, n, npix,
-                                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
+  const cudaError_t e = launch_pdl(channel_gather_kernel, dim3(grid), dim3(block), 0, stream,
+                                   static_cast<const uint16_t*>(x), x_cstride, x_coff, idx, n, npix,
+                                   static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
-  return cuda_status(cudaGetLastError(), "channel_gather_kernel");
+  return cuda_status(e, "channel_gather_kernel");
 }
 
 extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n, void* y,
@@ -360,6 +367,8 @@ constexpr int MP_ROWS = 4;     // output rows per CTA
 constexpr int MP_PER_T = 4;    // 16-byte pieces per thread per input row (W*groups <= 4*blockDim)
 __global__ void maxpool3s2_rows_kernel(const uint4* __restrict__ x, int H, int W, int groups, int x_cs16,
                                        int x_co16, int Ho, int Wo, uint4* __restrict__ y, int y_cs16, int y_co16) {
+  griddep_wait();
+  griddep_launch_dependents();
   extern __shared__ uint4 vrow[];  // [W][groups]
   const int bands = (Ho + MP_ROWS - 1) / MP_ROWS;
   const int img = blockIdx.x / bands;
@@ -452,11 +461,11 @@ extern "C" int ub_maxpool2d(const void* x, int N, int H, int W, int C, int x_cst
   if (vec && whole && k == 3 && stride == 2 && pad == 1 && W * groups <= MP_PER_T * block &&
       row_smem <= 48 * 1024 && (long long)N * ((Ho + MP_ROWS - 1) / MP_ROWS) < (1ll << 31)) {
     const int grid = N * ((Ho + MP_ROWS - 1) / MP_ROWS);
-    maxpool3s2_rows_kernel<<<grid, block, row_smem, stream>>>(static_cast<const uint4*>(x), H, W, groups,
-                                                              x_cstride / 8, x_coff / 8, Ho, Wo,
-                                                              static_cast<uint4*>(y), y_cstride / 8, y_coff / 8);
+    const cudaError_t e = launch_pdl(maxpool3s2_rows_kernel, dim3(grid), dim3(block), row_smem, stream,
+                                     static_cast<const uint4*>(x), H, W, groups, x_cstride / 8, x_coff / 8, Ho, Wo,
+                                     static_cast<uint4*>(y), y_cstride / 8, y_coff / 8);
     count_launch();
-    return cuda_status(cudaGetLastError(), "maxpool3s2_rows_kernel");
+    return cuda_status(e, "maxpool3s2_rows_kernel");
   }
   maxpool_kernel<<<grid_for(total, 256), 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(x), N, H, W, C, x_cstride, x_coff, k, stride, pad, Ho, Wo,
@@ -470,10 +479,10 @@ extern "C" int ub_avgpool_global(const void* x, int N, int HW, int C, int x_cstr
   if (!x || !y || N < 1 || HW < 1 || C < 1) return fail(UB_EINVAL, "ub_avgpool_global: bad arguments");
   if (N > 65535) return fail(UB_EUNSUPPORTED, "ub_avgpool_global: N too large");
   dim3 grid((C + 127) / 128, N);
-  avgpool_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(x), HW, C, x_cstride, x_coff,
-                                           static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);
+  const cudaError_t e = launch_pdl(avgpool_kernel, grid, dim3(128), 0, stream, static_cast<const __nv_bfloat16*>(x),
+                                   HW, C, x_cstride, x_coff, static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);
   count_launch();
-  return cuda_status(cudaGetLastError(), "avgpool_kernel");
+  return cuda_status(e, "avgpool_kernel");
 }
 
 extern "C" int ub_affine_add_relu(const void* a, int a_cstride, int a_coff, const float* scale, const float* shift,

@@ -131,12 +131,14 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  griddep_launch_dependents();
   TileIter ti;
   ti.u = blockIdx.x;
   if (ti.valid(p)) ti.start_band(p);
 
   if (warp == 0) {
     if (lane == 0) {  // ================= producer: conv rows 2yp, 2yp+1 in one bulk copy
+      griddep_wait();  // S comes from the pack kernel (PDL)
       int s = 0;
       uint32_t ph = 0;
       for (; ti.valid(p); ti.next(p)) {
@@ -333,7 +335,7 @@ void launch_pool(const CUtensorMap& tm, const PoolParams& p, int grid, size_t sm
     cudaFuncSetAttribute(stem_pool_kernel<KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  stem_pool_kernel<KQ><<<grid, SP_THREADS, smem, stream>>>(tm, p);
+  (void)launch_pdl(stem_pool_kernel<KQ>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, p);
 }
 
 }  // namespace

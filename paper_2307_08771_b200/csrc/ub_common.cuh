@@ -72,6 +72,14 @@ UB_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the forward are launched with programmatic stream serialisation (ub_host.h
+// launch_pdl): a kernel may start -- barrier init, TMEM alloc, resident weights -- while
+// its predecessor drains, and blocks in griddep_wait() before reading the predecessor's
+// output.  Both are no-ops for a normal launch.
+UB_DEVI void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+UB_DEVI void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- proxy fences
 UB_DEVI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
