@@ -126,7 +126,7 @@ def test_random_dags(rec):
             np.testing.assert_allclose(out.numpy().reshape(-1), _unhex(y1), rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("cfg_name", ["resnet18_s50", "resnet50_s50"])
+@pytest.mark.parametrize("cfg_name", ["resnet18_s50", "resnet50_s50", "resnet101_s50"])
 def test_resnet_assets_pin_lowering_and_apply(cfg_name):
     """Lowering is deterministic (proxy sha == reference run) and the oracle's
     apply_plan on the proxies reproduces the reference export bit-for-bit."""
