@@ -5,6 +5,7 @@ Each case: checks ub_conv_fwd against torch (bf16-rounded inputs, fp32 math) on
 the full output, then times it with CUDA events and prints algorithmic GB/s.
 """
 
+import os
 import sys
 from pathlib import Path
 
@@ -14,6 +15,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2307_08771_b200 import _lib, kernels as K  # noqa: E402
 
 # name: (N, H, W, cstride, coff, cin, cout, k, stride, pad, n_gather, res, relu)
+VARIANT = int(os.environ.get("UB_VARIANT", "0"))  # ub_conv_desc.variant bits
+
 CASES = {
     "l1_conv3": (256, 56, 56, 32, 0, 32, 256, 1, 1, 0, 0, True, True),
     "l2_conv3_502": (256, 28, 28, 64, 0, 64, 502, 1, 1, 0, 0, True, True),
@@ -21,6 +24,8 @@ CASES = {
     "l4_conv1_1024": (256, 7, 7, 1816, 0, 1024, 256, 1, 1, 0, 0, False, True),
     "l1_conv1_gather": (256, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, False, True),
     "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_dense": (256, 56, 56, 128, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_c32": (256, 56, 56, 240, 0, 128, 32, 1, 1, 0, 0, False, True),
     "l1_conv2_3x3": (256, 56, 56, 64, 0, 32, 64, 3, 1, 1, 0, False, True),
     "l2_down_gather_s2": (256, 56, 56, 240, 0, 237, 512, 1, 2, 0, 128, False, False),
     "l3_conv2_3x3s2": (256, 28, 28, 128, 0, 128, 256, 3, 2, 1, 0, False, True),
@@ -65,7 +70,7 @@ def run(name, check=True, iters=20, once=False):
     if res is not None:
         res.buf.normal_(generator=g)
     y = K.empty_act(N, Ho, Wo, cout, dev)
-    K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+    K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu, variant=VARIANT)
     torch.cuda.synchronize()
     if once:
         print(name, "launched once", flush=True)
@@ -85,10 +90,10 @@ def run(name, check=True, iters=20, once=False):
         del ref, xin
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(3):
-        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu, variant=VARIANT)
     a.record()
     for _ in range(iters):
-        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu)
+        K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu, variant=VARIANT)
     b.record()
     torch.cuda.synchronize()
     us = a.elapsed_time(b) / iters * 1e3
