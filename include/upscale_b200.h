@@ -130,6 +130,7 @@ typedef struct {
   int variant;                 /* bits 0-1 producer width (0 heuristic, 1: 256, 2: 512 threads);
                                   bit 2: re-load weights per tile (no weight-stationary B);
                                   bit 3: no halo-tile kernel for stride-1 3x3 convs;
+                                  bit 7: halo kernel with two epilogue groups (default: up to three);
                                   bit 4: weights by cp.async instead of one TMA box per K-block;
                                   bit 5: 1x1/s1 activations and residual by cp.async, not TMA;
                                   bit 6: one epilogue warpgroup (not two) on the TMA-fed 1x1 path */

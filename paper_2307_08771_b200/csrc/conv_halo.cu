@@ -34,7 +34,7 @@ namespace ub {
 namespace {
 
 constexpr int HALO_PRODUCERS = 128;
-constexpr int HALO_EPI_WARPS = 8;                      // two groups of four, alternate tiles
+constexpr int HALO_EPI_WARPS = 12;                     // up to three groups of four, round-robin tiles
 constexpr int HALO_PROD_WARP0 = HALO_EPI_WARPS + 2;    // after the MMA and TMEM-alloc warps
 constexpr int HALO_THREADS = 32 * HALO_PROD_WARP0 + HALO_PRODUCERS;
 constexpr int HALO_SLOT = 32 * 128;  // one epilogue warp's 32 rows x 64 channels bf16
@@ -46,7 +46,7 @@ struct HaloParams {
   uint32_t plane_stride, a_stage_bytes;
   int a_stages;
   int tiles, tiles_per_img;
-  int cout, np, acc_cols, nacc;
+  int cout, np, acc_cols, nacc, ngroups;
   uint32_t b_block_bytes;  // np * 128: one tap's weights
   const uint16_t* w;       // [cout][9][cpad]
   int cpad;
@@ -68,7 +68,7 @@ struct HaloGeom {
 };
 
 template <int WP, int PLANES, int MT>
-__global__ void __maxnreg__(144)
+__global__ void __maxnreg__(96)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
   constexpr int TAPS = 9;
   using G = HaloGeom<WP, MT>;
@@ -76,7 +76,7 @@ __global__ void __maxnreg__(144)
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = base;                                   // [tap][np rows][128 B], SW128
   uint8_t* sE = sB + TAPS * p.b_block_bytes;            // 8 warps x 2 slots x 4 KB (1024-aligned)
-  uint8_t* sA = sE + HALO_EPI_WARPS * 2 * HALO_SLOT;    // a_stages x a_stage_bytes
+  uint8_t* sA = sE + HALO_EPI_WARPS * HALO_SLOT;        // a_stages x a_stage_bytes
   float* sBias = reinterpret_cast<float*>(sA + p.a_stages * p.a_stage_bytes);  // 256 floats
   uint64_t* afull = reinterpret_cast<uint64_t*>(sBias + 256);
   uint64_t* aempty = afull + 8;
@@ -213,14 +213,14 @@ __global__ void __maxnreg__(144)
   } else if (warp < HALO_EPI_WARPS) {
     // ================= epilogue: group g = warp / 4 drains the tiles it % 2 == g; warp q = warp % 4
     // owns TMEM lanes / tile rows 32q .. 32q+31
-    const int grp = warp >> 2;
+    const int grp = warp >> 2;  // groups >= p.ngroups stay idle
     const int q = warp & 3;
-    uint8_t* slots = sE + warp * 2 * HALO_SLOT;
+    uint8_t* slot = sE + warp * HALO_SLOT;  // one store slot per warp (a group's tiles are far apart)
     const int nchunks = (p.np + 63) >> 6;
     uint32_t ec = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      if ((it & 1) != grp) continue;
+      if ((it % p.ngroups) != grp) continue;
       const int img = t / p.tiles_per_img;
       const int y0 = (t - img * p.tiles_per_img) * G::RT;
       const int r0 = q * 32;
@@ -238,9 +238,9 @@ __global__ void __maxnreg__(144)
         const int oy = y0 + mt * G::R + r0 / WP;
         const uint32_t taddr =
             tmem_base + (acc * MT + mt) * p.acc_cols + (static_cast<uint32_t>(q * 32) << 16);
-        uint8_t* slot = slots + (ec & 1) * HALO_SLOT;
+
         const int col0 = c * 64;
-        if (lane == 0 && !(p.dbg & 16)) bulk_wait_read<1>();  // this slot's store from two chunks ago has read it
+        if (lane == 0 && !(p.dbg & 16)) bulk_wait_read<0>();  // this warp's previous store has left the slot
         __syncwarp();
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {  // 32 columns per TMEM round trip (register budget)
@@ -345,6 +345,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
   const int mt = (d->H > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
   p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
+  p.ngroups = (d->variant & 128) ? 2 : (p.nacc < HALO_EPI_WARPS / 4 ? p.nacc : HALO_EPI_WARPS / 4);  // drainers
   p.n_pos = ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp, mt>::N_POS
   p.plane_stride = p.n_pos * 16 + 16;               // == HaloGeom<Wp, mt>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
@@ -370,7 +371,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
     if (dbg < 0) dbg = getenv("UB_HALO_DBG") ? atoi(getenv("UB_HALO_DBG")) : 0;
     p.dbg = dbg;
   }
-  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + HALO_EPI_WARPS * 2 * HALO_SLOT + 256 * 4 + 256;
+  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + HALO_EPI_WARPS * HALO_SLOT + 256 * 4 + 256;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * p.a_stage_bytes > budget) return UB_OK;
   int stages = static_cast<int>((budget - fixed) / p.a_stage_bytes);
@@ -407,7 +408,14 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, p);
   count_launch();
   *handled = true;
-  return cuda_status(e, "conv_halo3_kernel");
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    return fail(UB_ECUDA, "conv_halo3_kernel: %s (threads %d, max %d, regs %d, smem %zu, max dyn %d)",
+                cudaGetErrorString(e), HALO_THREADS, fa.maxThreadsPerBlock, fa.numRegs, smem,
+                fa.maxDynamicSharedSizeBytes);
+  }
+  return UB_OK;
 }
 
 }  // namespace ub

@@ -444,11 +444,15 @@ class Engine:
         # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
         # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
-        # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path)
+        # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path;
+        # +8 no halo-tile kernel for a stride-1 3x3; +128 halo kernel with two epilogue groups)
         tiled = kk == 1 and st == 1
-        op.info["variants"] = [(pi, pw | nb | bt | at | e1) for pi in range(len(plans)) for pw in (1, 2)
-                               for nb in (0, 4) for bt in (0, 16) for at in ((0, 32) if tiled else (32,))
-                               for e1 in ((0, 64) if tiled else (0,))]
+        halo = kk == 3 and st == 1 and pd == 1
+        gen = [pw | nb | bt | at | e1 for pw in (1, 2) for nb in (0, 4) for bt in (0, 16)
+               for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
+        if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
+            gen = [0, 128] + [v | 8 for v in gen]
+        op.info["variants"] = [(pi, v) for pi in range(len(plans)) for v in gen]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
 
