@@ -117,3 +117,19 @@ def test_runner_pipelined_matches_single_runs():
     assert len(piped) == len(xs)
     for r, a, b in zip(ref, single, piped):
         assert (r == a).all() and (r == b).all()
+
+
+def test_export_artifact_runs_like_the_live_export(tmp_path):
+    """8f-3: save the GPU export (graph, plans, specs, binary weights), load it back
+    without the original model and run it -- same logits as the live export."""
+    from paper_2307_08771_b200 import api, artifact
+
+    lc = api.load_config("resnet18_s50", randomize_bn=True)
+    plans = P.load_plans(lc.cfg.asset_dir / "plans_reorder.json")
+    ex = api.export_model(lc.model, lc.masks, plans=plans)
+    x = torch.randn(2, 3, 224, 224, generator=torch.Generator().manual_seed(5))
+    live = EN.from_export(lc.model, ex.result, batch=2).forward(x.cuda()).cpu()
+    artifact.save_export(ex.result, lc.model, tmp_path / "r18")
+    res, model = artifact.load_export(tmp_path / "r18")
+    back = EN.from_export(model, res, batch=2).forward(x.cuda()).cpu()
+    assert torch.equal(live, back)
