@@ -201,6 +201,21 @@ int ub_affine_add_relu(const void* a, int a_cstride, int a_coff,
                        long long npix, int C, void* y, int y_cstride, int y_coff,
                        cudaStream_t stream);
 
+/*
+ * Planner core (host only, no GPU): decompose one segment's reorder graph into maximum-
+ * reward paths and emit its channel order -- path_search.py:157-305 (solve_mrap with the
+ * lexicographic tie-break, the greedy fallback above 20 nodes, decompose_paths) and
+ * ordering.py:39-88 (order_channels), restated natively; the reference's plan_model uses
+ * it through paper_2307_08771_b200.native_planner.install().
+ *   n nodes sorted by id; node i retains channels[offsets[i] .. offsets[i+1]) (ascending,
+ *   non-empty, < channel_space).  Outputs: out_order[*n_order] (kept channels in the new
+ *   order; capacity channel_space), path_of[i] / path_pos[i] (path index; position on it,
+ *   -1 for an absorbed parent), path_reward[k] for k < *n_paths (capacity n).
+ */
+int ub_plan_order_segment(int n, const int32_t* offsets, const int32_t* channels, int channel_space,
+                          int32_t* out_order, int32_t* n_order, int32_t* path_of, int32_t* path_pos,
+                          int64_t* path_reward, int32_t* n_paths);
+
 #ifdef __cplusplus
 }
 #endif

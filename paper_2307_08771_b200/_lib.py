@@ -76,6 +76,7 @@ SIGNATURES = {
                                     c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_h2d_input_channels": (c_int, [c_vp, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_int32), c_int, c_vp,
                                       ctypes.POINTER(c_ll), c_vp]),
+    "ub_plan_order_segment": (c_int, [c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ub_stage_input": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp]),
     "ub_maxpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                              c_int, c_int, c_vp, c_int, c_int, c_vp]),
