@@ -13,16 +13,21 @@
 // MMAs read the same staged block; nothing is copied per tap.  Positions with x >= W (or
 // rows past H) are computed and dropped by the output TMA store's bounds clipping.
 //
-// The weights of all taps stay resident in shared memory (SWIZZLE_128B, one 128-byte row
-// per output channel and tap), loaded once per CTA.
+// Padded width: Wp >= W + 1 suffices -- column 0 of every staged row is zero and serves as the
+// right pad of the previous row.  Small images (H + 1) * Wp <= 64 are stacked, ipt per tile,
+// one zero row between them, so a 7x7 map fills 98 of the 128 MMA rows instead of 49.
+//
+// Weights (SWIZZLE_128B, one 128-byte row per output channel, tap and 64-channel group): for
+// cpad <= 64 all taps stay resident, loaded once per CTA; for cpad > 64 the input is staged per
+// 64-channel group and the (group, tap) weight blocks stream through a TMA ring (SB = true).
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warps 0-7   epilogue, two groups of four taking alternate tiles: TMEM -> regs, +bias,
-//               ReLU, bf16 -> SW128 smem -> 4-D TMA store
-//               (box 64 channels x BX pixels x BY rows of the output)
-//   warp 8      MMA issuer (2-4 TMEM accumulators; one elected lane issues)
-//   warp 9      TMEM allocator
-//   warps 10-13 producers: halo planes by cp.async (zero-fill outside the image)
+//   warps 0-11  epilogue, three groups of four (whole tiles round-robin, or each tile's 64-column
+//               chunks dealt to all groups): TMEM -> regs, +bias, ReLU, bf16 -> SW128 smem ->
+//               4-D TMA store (box 64 channels x BX pixels x BY rows of the output)
+//   warp 12     MMA issuer (2-4 TMEM accumulators; one elected lane issues)
+//   warp 13     TMEM allocator; lane 0 then streams the weight blocks (SB)
+//   warps 14-17 producers: halo planes by cp.async (zero-fill outside the image)
 #include <cstdlib>
 
 #include "ub_common.cuh"
@@ -41,18 +46,23 @@ constexpr int HALO_SLOT = 32 * 128;  // one epilogue warp's 32 rows x 64 channel
 
 struct HaloParams {
   const uint16_t* x;  // at channel (coff - lead)
-  int x_cstride, H, W;
+  int x_cstride, N, H, W;
   int R, Wp, wp_shift, n_pos, planes;
   uint32_t plane_stride, a_stage_bytes;
   int a_stages;
   int tiles, tiles_per_img;
   int cout, np, acc_cols, nacc, ngroups;
+  int drainers;  // groups draining each tile: 1 (whole tiles round-robin) or ngroups (chunks dealt out)
   uint32_t b_block_bytes;  // np * 128: one tap's weights
   const uint16_t* w;       // [cout][9][cpad]
   int cpad;
   const float* bias;
   int relu;
   int bx;  // output box width (pixels); box height = 32 / bx rows
+  int groups;    // 64-channel groups (1: all taps' weights resident; > 1: streamed per group x tap)
+  int b_stages;  // streamed weight ring depth
+  int kvalid;    // lead + cin: channels past it are not read (their weights are zero)
+  int ipt;       // images stacked per tile (small images): image i's row y at staged row 1 + i * (H + 1) + y
   long long* trace;  // profiling (UB_HALO_TRACE): CTA 0 event clocks, [tile][8]
   int dbg;           // profiling ablations (UB_HALO_DBG): 1 no halo loads, 2 no output, 4 no TMEM reads,
                      // 8 no TMA store, 16 no slot wait (races; timing only)
@@ -67,15 +77,19 @@ struct HaloGeom {
   static constexpr uint32_t PLANE_STRIDE = N_POS * 16 + 16;  // odd # of 16-B units: planes on different banks
 };
 
-template <int WP, int PLANES, int MT>
+// SB: weights streamed per (64-channel group, tap) through a TMA ring (cpad > 64); else resident.
+template <int WP, int PLANES, int MT, bool SB>
 __global__ void __maxnreg__(96)
-    conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const HaloParams p) {
+    conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmW,
+                      const HaloParams p) {
   constexpr int TAPS = 9;
   using G = HaloGeom<WP, MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sB = base;                                   // [tap][np rows][128 B], SW128
-  uint8_t* sE = sB + TAPS * p.b_block_bytes;            // 8 warps x 2 slots x 4 KB (1024-aligned)
+  // weights: resident [tap][np rows][128 B] (one group) or a ring of (group, tap) blocks; SW128
+  uint8_t* sB = base;
+  const int groups = SB ? p.groups : 1;
+  uint8_t* sE = sB + (SB ? p.b_stages : TAPS) * p.b_block_bytes;  // epilogue slots (1024-aligned)
   uint8_t* sA = sE + HALO_EPI_WARPS * HALO_SLOT;        // a_stages x a_stage_bytes
   float* sBias = reinterpret_cast<float*>(sA + p.a_stages * p.a_stage_bytes);  // 256 floats
   uint64_t* afull = reinterpret_cast<uint64_t*>(sBias + 256);
@@ -83,7 +97,9 @@ __global__ void __maxnreg__(96)
   uint64_t* tfull = aempty + 8;
   uint64_t* tempty = tfull + 4;
   uint64_t* bres = tempty + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+  uint64_t* bfull = bres + 1;
+  uint64_t* bempty = bfull + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -96,12 +112,19 @@ __global__ void __maxnreg__(96)
     }
     for (int a = 0; a < p.nacc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // the four warps of the group draining it
+      mbar_init(&tempty[a], 4 * p.drainers);  // every warp of the groups draining a tile
     }
     mbar_init(bres, HALO_PRODUCERS);
+    for (int b = 0; b < p.b_stages; ++b) {
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tma_prefetch_desc(&tmY);
+  if (warp == 0) {
+    tma_prefetch_desc(&tmY);
+    if (SB) tma_prefetch_desc(&tmW);
+  }
   if (warp == ALLOC_WARP) tmem_alloc(tmem_slot, p.nacc * MT * p.acc_cols);
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sBias[i] = (p.bias && i < p.cout) ? p.bias[i] : 0.f;
   tc_fence_before();
@@ -114,7 +137,7 @@ __global__ void __maxnreg__(96)
     // ================= producers
     const int pt = threadIdx.x - 32 * HALO_PROD_WARP0;
     // resident weights: tap t, row n, 16-byte chunk j (K = 8j .. 8j+7 of the tap) -> SW128
-    const int cp8 = p.cpad >> 3;
+    const int cp8 = SB ? 0 : p.cpad >> 3;
     for (int e = pt; e < TAPS * p.np * cp8; e += HALO_PRODUCERS) {
       const int t = e / (p.np * cp8);
       const int rem = e - t * (p.np * cp8);
@@ -135,10 +158,11 @@ __global__ void __maxnreg__(96)
     constexpr int wp_shift = __builtin_ctz(WP);
     int s = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-      const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * G::RT - 1;  // first staged input row (pad 1)
-      const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + pp * 8;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
+    for (int g = 0; g < groups; ++g) {
+      const int img = p.ipt > 1 ? t * p.ipt : t / p.tiles_per_img;
+      const int y0 = p.ipt > 1 ? -1 : (t - img * p.tiles_per_img) * G::RT - 1;  // first staged input row (pad 1)
+      const uint16_t* ximg = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + g * 64 + pp * 8;
       if (p.dbg & 64) mbar_wait_sleep(&aempty[s], ph ^ 1, 2000);
       else mbar_wait(&aempty[s], ph ^ 1);
       if (p.trace && blockIdx.x == 0 && pt == 0) {
@@ -146,14 +170,29 @@ __global__ void __maxnreg__(96)
         if (itp < 64) p.trace[itp * 16 + 7] = clock64();
       }
       const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * G::PLANE_STRIDE);
-      for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
-        const int yy = y0 + (q >> wp_shift);
-        const int xx = (q & wmask) - 1;
-        const bool ok = yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
-        const uint16_t* src = ok ? ximg + (static_cast<size_t>(yy) * p.W + xx) * p.x_cstride : p.x;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + q * 16), "l"(src),
-                     "r"(ok ? 16u : 0u)
-                     : "memory");
+      const bool kin = g * 64 + pp * 8 < p.kvalid;
+      if (p.ipt > 1) {  // stacked images: stack row r -> image i = r / (H + 1), its row r - i (H + 1)
+        for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
+          const int r = (q >> wp_shift) - 1;
+          const int xx = (q & wmask) - 1;
+          const int i = r / (p.H + 1);
+          const int y = r - i * (p.H + 1);
+          const bool ok = kin && r >= 0 && y < p.H && i < p.ipt && img + i < p.N && xx >= 0 && xx < p.W;
+          const uint16_t* src = ok ? ximg + (static_cast<size_t>(i * p.H + y) * p.W + xx) * p.x_cstride : p.x;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + q * 16), "l"(src),
+                       "r"(ok ? 16u : 0u)
+                       : "memory");
+        }
+      } else {
+        for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
+          const int yy = y0 + (q >> wp_shift);
+          const int xx = (q & wmask) - 1;
+          const bool ok = kin && yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
+          const uint16_t* src = ok ? ximg + (static_cast<size_t>(yy) * p.W + xx) * p.x_cstride : p.x;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + q * 16), "l"(src),
+                       "r"(ok ? 16u : 0u)
+                       : "memory");
+        }
       }
       cp_async_arrive_noinc(&afull[s]);
       if (++s == p.a_stages) {
@@ -166,49 +205,87 @@ __global__ void __maxnreg__(96)
     // ================= MMA issuer (whole warp; one elected lane issues)
     const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
     const uint32_t b0 = smem_u32(sB);
-    uint64_t bdesc[TAPS];
-#pragma unroll
-    for (int tap = 0; tap < TAPS; ++tap) bdesc[tap] = make_sdesc(b0 + tap * p.b_block_bytes, 1024, 2);
+    const uint64_t bdesc0 = make_sdesc(b0, 1024, 2);
+    const uint32_t b_units = p.b_block_bytes >> 4;
     const uint64_t adesc0 = sdesc_plain(smem_u32(sA), G::PLANE_STRIDE, 128);
     const uint32_t stage_units = p.a_stage_bytes >> 4;
-    mbar_wait(bres, 0);
+    if (!SB) mbar_wait(bres, 0);
     __syncwarp();
     tc_fence_after();
     fence_proxy_async_smem();
-    int s = 0, it = 0;
-    uint32_t ph = 0;
+    int s = 0, it = 0, bs = 0;
+    uint32_t ph = 0, bph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
       const int acc = it % p.nacc;
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 0] = clock64();
       mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 1] = clock64();
-      mbar_wait(&afull[s], ph);
-      if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 2] = clock64();
-      __syncwarp();
-      tc_fence_after();
-      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
-      const uint64_t ad = adesc0 + s * stage_units;
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const uint32_t d = tmem_base + (acc * MT + mt) * p.acc_cols;
+      for (int g = 0; g < groups; ++g) {
+        mbar_wait(&afull[s], ph);
+        if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64 && g == 0) p.trace[it * 16 + 2] = clock64();
+        __syncwarp();
+        tc_fence_after();
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+        const uint64_t ad = adesc0 + s * stage_units;
 #pragma unroll
         for (int tap = 0; tap < TAPS; ++tap) {
+          uint64_t bd;
+          if constexpr (!SB) {
+            bd = bdesc0 + tap * b_units;
+          } else {  // this (group, tap)'s weight block from the ring
+            mbar_wait(&bfull[bs], bph);
+            __syncwarp();
+            tc_fence_after();
+            bd = bdesc0 + bs * b_units;
+          }
 #pragma unroll
-          for (int j = 0; j < PLANES / 2; ++j) {
-            // A: planes 2j, 2j+1 of MMA tile mt shifted by tap (dy, dx); B: K step j of the tap
-            const uint32_t aoff =
-                ((mt * G::R * WP + (tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
-            umma_bf16_warp(d, ad + aoff, bdesc[tap] + 2 * j, idesc, (tap | j) ? 1u : 0u);
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint32_t d = tmem_base + (acc * MT + mt) * p.acc_cols;
+#pragma unroll
+            for (int j = 0; j < PLANES / 2; ++j) {
+              // A: planes 2j, 2j+1 of MMA tile mt shifted by tap (dy, dx); B: K step j of the tap
+              const uint32_t aoff =
+                  ((mt * G::R * WP + (tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
+              umma_bf16_warp(d, ad + aoff, bd + 2 * j, idesc, (g | tap | j) ? 1u : 0u);
+            }
+          }
+          if constexpr (SB) {
+            umma_commit_warp(&bempty[bs]);
+            if (++bs == p.b_stages) {
+              bs = 0;
+              bph ^= 1;
+            }
           }
         }
+        umma_commit_warp(&aempty[s]);
+        if (++s == p.a_stages) {
+          s = 0;
+          ph ^= 1;
+        }
       }
-      umma_commit_warp(&aempty[s]);
       umma_commit_warp(&tfull[acc]);
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 3] = clock64();
-      if (++s == p.a_stages) {
-        s = 0;
-        ph ^= 1;
-      }
+    }
+  } else if (SB && warp == ALLOC_WARP) {
+    // ================= streamed weights: one TMA box (64 K x np rows, SW128) per (group, tap)
+    if (lane == 0) {
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
+        for (int g = 0; g < groups; ++g)
+          for (int tap = 0; tap < TAPS; ++tap) {
+            mbar_wait(&bempty[bs], bph ^ 1);
+            if (p.dbg & 512) {  // ablation: no weight traffic
+              mbar_arrive(&bfull[bs]);
+            } else {
+              mbar_arrive_expect_tx(&bfull[bs], p.b_block_bytes);
+              tma_load_2d(&tmW, &bfull[bs], sB + bs * p.b_block_bytes, tap * p.cpad + g * 64, 0);
+            }
+            if (++bs == p.b_stages) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
     }
   } else if (warp < HALO_EPI_WARPS) {
     // ================= epilogue: group g = warp / 4 drains the tiles it % 2 == g; warp q = warp % 4
@@ -220,10 +297,22 @@ __global__ void __maxnreg__(96)
     uint32_t ec = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      if ((it % p.ngroups) != grp) continue;
-      const int img = t / p.tiles_per_img;
-      const int y0 = (t - img * p.tiles_per_img) * G::RT;
+      // drainers == 1: the group takes whole tiles, it % ngroups == grp.  Otherwise the tile's 64-column
+      // chunks cm = 0 .. MT * nchunks - 1 are dealt to all groups, rotated per tile: cm = first + k ngroups
+      const int cstep = p.drainers == 1 ? 1 : p.ngroups;
+      const int first = p.drainers == 1 ? ((it % p.ngroups) == grp ? 0 : MT * nchunks)
+                                        : ((grp - it) % p.ngroups + p.ngroups) % p.ngroups;
+      if (grp >= p.ngroups || first >= MT * nchunks) continue;
+      int img = t / p.tiles_per_img;
+      int y0 = (t - img * p.tiles_per_img) * G::RT;
       const int r0 = q * 32;
+      bool store_ok = true;
+      if (p.ipt > 1) {  // this warp's rows lie in stacked image i (host: H + 1 a multiple of the box rows)
+        const int i = (r0 / WP) / (p.H + 1);
+        img = t * p.ipt + i;
+        y0 = -i * (p.H + 1);
+        store_ok = i < p.ipt;
+      }
       const int ox = r0 % WP;
       const int acc = it % p.nacc;
       if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) p.trace[it * 16 + 4] = clock64();
@@ -233,7 +322,7 @@ __global__ void __maxnreg__(96)
       tc_fence_after();
 #define HALO_T(k) \
   if (p.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && cm < 2) p.trace[it * 16 + 8 + cm * 4 + (k)] = clock64()
-      for (int cm = 0; cm < MT * nchunks; ++cm, ++ec) {
+      for (int cm = first; cm < MT * nchunks; cm += cstep, ++ec) {
         const int mt = cm / nchunks, c = cm - mt * nchunks;
         const int oy = y0 + mt * G::R + r0 / WP;
         const uint32_t taddr =
@@ -256,7 +345,7 @@ __global__ void __maxnreg__(96)
             tmem_ld_wait();
           }
           HALO_T(half);
-          const bool last = cm + 1 == MT * nchunks && (half == 1 || colh + 32 >= p.np);
+          const bool last = cm + cstep >= MT * nchunks && (half == 1 || colh + 32 >= p.np);
           if (last) {  // accumulators drained: hand them back before the math and store
             tc_fence_before();
             __syncwarp();
@@ -298,7 +387,7 @@ __global__ void __maxnreg__(96)
         if (p.dbg & 2) continue;
         if (!(p.dbg & 32)) fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0 && !(p.dbg & 8)) {
+        if (lane == 0 && !(p.dbg & 8) && store_ok) {
           tma_store_4d(&tmY, slot, col0, ox, oy, img);
           bulk_commit();
         }
@@ -326,35 +415,47 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   if (d->kh != 3 || d->kw != 3 || d->stride != 1 || d->pad != 1 || d->x_nchw_f32 || d->gather_idx ||
       d->residual || d->y_dtype != UB_BF16 || (d->variant & 8))
     return UB_OK;
-  if (cpad != 16 && cpad != 32 && cpad != 64) return UB_OK;
+  if (cpad != 16 && cpad != 32 && cpad % 64 != 0) return UB_OK;
   if (d->cout > 256 || d->y_cstride % 8 || d->y_coff % 8) return UB_OK;
   int Wp = 8;
-  while (Wp < d->W + 2) Wp <<= 1;
+  while (Wp < d->W + 1) Wp <<= 1;  // one zero column: the right pad of a row is the left pad of the next
   if (Wp > 64) return UB_OK;
   HaloParams p{};
   p.x = reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
   p.x_cstride = d->x_cstride;
+  p.N = d->N;
   p.H = d->H;
   p.W = d->W;
   p.Wp = Wp;
   p.wp_shift = __builtin_ctz(Wp);
   p.R = 128 / Wp;
-  p.planes = cpad / 8;
+  p.groups = cpad > 64 ? cpad / 64 : 1;
+  p.planes = p.groups > 1 ? 8 : cpad / 8;
   p.np = (d->cout + 15) / 16 * 16;
   p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
   // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
   const int mt = (d->H > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
   p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
-  p.ngroups = (d->variant & 128) ? 2 : (p.nacc < HALO_EPI_WARPS / 4 ? p.nacc : HALO_EPI_WARPS / 4);  // drainers
+  p.ngroups = (d->variant & 128) ? 2 : HALO_EPI_WARPS / 4;
+  // chunks dealt to all groups when every group gets one (shorter drain per tile), else whole tiles
+  p.drainers = (mt * ((p.np + 63) / 64) >= p.ngroups && !(d->variant & 1024)) ? p.ngroups : 1;
+  if (p.drainers == 1 && p.ngroups > p.nacc) p.ngroups = p.nacc;
   p.n_pos = ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp, mt>::N_POS
   p.plane_stride = p.n_pos * 16 + 16;               // == HaloGeom<Wp, mt>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
   p.tiles_per_img = (d->H + mt * p.R - 1) / (mt * p.R);
-  const long long tiles = static_cast<long long>(d->N) * p.tiles_per_img;
+  // small images: stack ipt of them per 128-row tile, one zero row between (a store box stays in one image)
+  p.ipt = 1;
+  if (mt == 1 && (d->H + 1) * Wp <= 64 && (d->H + 1) % (32 / (Wp < 32 ? Wp : 32)) == 0 && !(d->variant & 256))
+    p.ipt = 128 / ((d->H + 1) * Wp);
+  const long long tiles =
+      p.ipt > 1 ? (d->N + p.ipt - 1) / p.ipt : static_cast<long long>(d->N) * p.tiles_per_img;
   if (tiles >= (1ll << 31)) return UB_OK;
   p.tiles = static_cast<int>(tiles);
   p.cout = d->cout;
   p.b_block_bytes = static_cast<uint32_t>((p.np + 7) / 8 * 8) * 128;
+  p.b_stages = p.groups > 1 ? 4 : 0;
+  p.kvalid = lead + d->cin;
   p.w = reinterpret_cast<const uint16_t*>(d->w);
   p.cpad = cpad;
   p.bias = d->bias;
@@ -371,7 +472,8 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
     if (dbg < 0) dbg = getenv("UB_HALO_DBG") ? atoi(getenv("UB_HALO_DBG")) : 0;
     p.dbg = dbg;
   }
-  const size_t fixed = 1024 + 9 * static_cast<size_t>(p.b_block_bytes) + HALO_EPI_WARPS * HALO_SLOT + 256 * 4 + 256;
+  const size_t fixed = 1024 + (p.groups == 1 ? 9 : p.b_stages) * static_cast<size_t>(p.b_block_bytes) +
+                      HALO_EPI_WARPS * HALO_SLOT + 256 * 4 + 512;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * p.a_stage_bytes > budget) return UB_OK;
   int stages = static_cast<int>((budget - fixed) / p.a_stage_bytes);
@@ -394,18 +496,30 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   apply_small_tensor_quirk(&tm, static_cast<size_t>(d->N) * d->Ho * d->Wo * d->y_cstride * 2);
 
   const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
-  void (*kern)(const CUtensorMap, const HaloParams) = nullptr;
-#define UB_HALO_CASE(WPV, PL)                                                     \
-  if (Wp == WPV && p.planes == PL) kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2> \
-                                                  : conv_halo3_kernel<WPV, PL, 1>;
-  UB_HALO_CASE(8, 2) UB_HALO_CASE(8, 4) UB_HALO_CASE(8, 8)
-  UB_HALO_CASE(16, 2) UB_HALO_CASE(16, 4) UB_HALO_CASE(16, 8)
-  UB_HALO_CASE(32, 2) UB_HALO_CASE(32, 4) UB_HALO_CASE(32, 8)
-  UB_HALO_CASE(64, 2) UB_HALO_CASE(64, 4) UB_HALO_CASE(64, 8)
+  void (*kern)(const CUtensorMap, const CUtensorMap, const HaloParams) = nullptr;
+  const bool sb = p.groups > 1;
+#define UB_HALO_CASE(WPV, PL, SBV)                                                                \
+  if (Wp == WPV && p.planes == PL && sb == SBV) kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV> \
+                                                               : conv_halo3_kernel<WPV, PL, 1, SBV>;
+  UB_HALO_CASE(8, 2, false) UB_HALO_CASE(8, 4, false) UB_HALO_CASE(8, 8, false) UB_HALO_CASE(8, 8, true)
+  UB_HALO_CASE(16, 2, false) UB_HALO_CASE(16, 4, false) UB_HALO_CASE(16, 8, false) UB_HALO_CASE(16, 8, true)
+  UB_HALO_CASE(32, 2, false) UB_HALO_CASE(32, 4, false) UB_HALO_CASE(32, 8, false) UB_HALO_CASE(32, 8, true)
+  UB_HALO_CASE(64, 2, false) UB_HALO_CASE(64, 4, false) UB_HALO_CASE(64, 8, false) UB_HALO_CASE(64, 8, true)
 #undef UB_HALO_CASE
   if (!kern) return UB_OK;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, p);
+  CUtensorMap tmw{};
+  if (p.groups > 1) {  // weights [cout][9 * cpad]: box 64 K x np rows
+    cuuint64_t wd[2] = {static_cast<cuuint64_t>(9 * cpad), static_cast<cuuint64_t>(d->cout)};
+    cuuint64_t ws[1] = {static_cast<cuuint64_t>(9 * cpad) * 2};
+    cuuint32_t wb[2] = {64, static_cast<cuuint32_t>(p.np)};
+    cuuint32_t we[2] = {1, 1};
+    CUresult rw = encode_tiled_fn()(&tmw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d->w), wd, ws, wb, we,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rw != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo weight tensor map failed (%d)", (int)rw);
+  }
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, tmw, p);
   count_launch();
   *handled = true;
   if (e != cudaSuccess) {

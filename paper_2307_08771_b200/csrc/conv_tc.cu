@@ -90,7 +90,8 @@ struct ConvKParams {
   int res_cstride;
   void* y;  // direct-store fallback only
   int y_cstride, y_coff, y_f32;
-  int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA
+  int dbg;  // ablation bits for profiling (UB_DEBUG_FLAGS): 1 no store, 2 no epilogue math, 4 no MMA,
+            // 8 no streamed weight loads
   int b_res;  // weights of this CTA's N tile stay resident in smem (loaded once; grid % n_tiles == 0)
   long long* trace;  // profiling (UB_CONV_TRACE): CTA 0 per-tile event clocks [tile][8]
   int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
@@ -336,10 +337,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           const int nres = tile_res_chunks(p, n0);
           for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
-            const uint32_t bytes = BLOCK_M * ROW_BYTES + (p.b_tma ? static_cast<uint32_t>(p.block_n) * ROW_BYTES : 0u);
+            const bool bload = p.b_tma && !(p.dbg & 8);
+            const uint32_t bytes = BLOCK_M * ROW_BYTES + (bload ? static_cast<uint32_t>(p.block_n) * ROW_BYTES : 0u);
             mbar_arrive_expect_tx(&full[s], bytes);
             tma_load_2d(&tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
-            if (p.b_tma) tma_load_2d(&tmB, &full[s], sB + s * b_stride, kb * BK, n0);
+            if (bload) tma_load_2d(&tmB, &full[s], sB + s * b_stride, kb * BK, n0);
             if (++s == stages) {
               s = 0;
               ph ^= 1;
@@ -515,8 +517,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         // ---- B (weights [cout][K_total]): one TMA box, or rows row0 + i * ROW_STEP, chunk cj
         if (p.b_tma) {
           if (pt == 0) {
-            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(p.block_n) * ROW_BYTES);
-            tma_load_2d(&tmB, &full[s], sB + s * b_stride, kcoord, n0);
+            if (p.dbg & 8) {  // profiling: weights not loaded (timing only)
+              mbar_arrive(&full[s]);
+            } else {
+              mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(p.block_n) * ROW_BYTES);
+              tma_load_2d(&tmB, &full[s], sB + s * b_stride, kcoord, n0);
+            }
           }
         } else if (!p.b_res) {
           const uint16_t* src = b_base + kcoord;

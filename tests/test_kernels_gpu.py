@@ -60,6 +60,15 @@ CASES = [
     ("halo_c16_w7_cout256", 2, 7, 7, 16, 0, 16, 256, 3, 1, 1, 0, True, False, True, False),
     ("halo_c32_lead_h13_w5", 3, 13, 5, 48, 11, 20, 40, 3, 1, 1, 0, False, False, False, False),
     ("halo_c64_w30_cout16", 2, 17, 30, 64, 0, 64, 16, 3, 1, 1, 0, True, False, True, False),
+    # halo with streamed weights (cpad > 64: 64-channel groups x taps through a TMA ring)
+    ("halo_c128_w14", 3, 14, 14, 128, 0, 128, 128, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c256_w7_cout256", 2, 7, 7, 256, 0, 256, 256, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c190_lead_w14_cout100", 3, 14, 14, 256, 37, 190, 100, 3, 1, 1, 0, True, False, False, False),
+    ("halo_c128_w28_ragged", 2, 19, 28, 136, 8, 128, 72, 3, 1, 1, 0, False, False, True, False),
+    # stacked small images (ipt images per 128-row tile), odd N
+    ("halo_c64_w7_stack_n3", 3, 7, 7, 64, 0, 64, 96, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c32_h3_w5_stack4_n5", 5, 3, 5, 32, 0, 32, 64, 3, 1, 1, 0, True, False, False, False),
+    ("halo_c256_w7_stack_n5", 5, 7, 7, 264, 8, 256, 200, 3, 1, 1, 0, True, False, True, False),
 ]
 
 

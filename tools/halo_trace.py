@@ -12,7 +12,12 @@ from paper_2307_08771_b200 import _lib, kernels as K  # noqa: E402
 
 
 def main():
-    N, H, W, cin, cout = 256, 56, 56, int(sys.argv[1]) if len(sys.argv) > 1 else 32, 64
+    # args: cin [H=W [cout [N]]]
+    a = [int(v) for v in sys.argv[1:]]
+    cin = a[0] if a else 32
+    H = W = a[1] if len(a) > 1 else 56
+    cout = a[2] if len(a) > 2 else 64
+    N = a[3] if len(a) > 3 else 256
     dev = "cuda"
     x = K.Act(torch.randn(N * H * W, cin, device=dev).to(torch.bfloat16), N, H, W, cin)
     lead, cpad = _lib.conv_weight_layout(cin, 0, False, 3, 3)

@@ -23,7 +23,7 @@ UB_DEVI uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layo
 // mode 2: no-swizzle A with LBO 16 (overlapping, shifted-row trick), B no-swizzle
 // commit_every: commit + wait after this many MMAs (0 = only at the end)
 __global__ void __launch_bounds__(128, 1) probe_mma(int n, int mode, int iters, int commit_every,
-                                                    unsigned long long* out) {
+                                                    unsigned long long* out, int shift = 48) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = smem + ((1024u - (smem_u32(smem) & 1023u)) & 1023u);
   uint8_t* sA = base;          // 16 KB
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(128, 1) probe_mma(int n, int mode, int iters, 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (commit_every == 1) {  // no-swizzle planes: A rows 16 B apart, K core matrices 4 KB apart
-        ad[k] = sdesc(a0 + k * 16 * 3, 4096, 128, 0);
+        ad[k] = sdesc(a0 + k * shift, 4096, 128, 0);
         bd[k] = sdesc(b0, n * 16, 128, 0);
       } else {
         ad[k] = sdesc(a0 + k * 32, 16, 1024, 2);
@@ -139,9 +139,10 @@ int main() {
   const char* names[6] = {"sw128", "noswz", "noswz-lbo16", "sw128-pre", "sw128-pre-c", "warp-elect"};
   for (int mode = 5; mode < 6; ++mode) {
     for (int n : {32, 64, 128, 256}) {
-      for (int ce : {0, 1}) {
-        for (int grid : {1, 148}) {
-          probe_mma<<<grid, 128, 64 * 1024>>>(n, mode, iters, ce, dout);
+      for (int sh : {-1, 0, 128, 256, 16, 48, 112}) {
+        const int ce = sh < 0 ? 0 : 1;
+        for (int grid : {148}) {
+          probe_mma<<<grid, 128, 64 * 1024>>>(n, mode, iters, ce, dout, sh);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) {
             printf("error %s\n", cudaGetErrorString(e));
@@ -149,7 +150,8 @@ int main() {
           }
           unsigned long long cyc = 0;
           cudaMemcpy(&cyc, dout, 8, cudaMemcpyDeviceToHost);
-          printf("%-12s N=%3d commit_every=%d grid=%3d: %6.1f cyc/MMA (ideal %5.1f)\n", names[mode], n, ce, grid,
+            printf("shift %4d ", sh);
+          printf("%-12s N=%3d planes=%d grid=%3d: %6.1f cyc/MMA (ideal %5.1f)\n", names[mode], n, ce, grid,
                  double(cyc) / iters, 128.0 * n / 256.0);
         }
       }
