@@ -1,25 +1,34 @@
 // Space-to-depth stem fused with the 3x3 / stride-2 / pad-1 max pool that follows it.
 //
-// Same tensor-core mainloop as stem_s2d.cu (the folded input S, one bulk copy per tile,
-// every filter tap a shifted view), but a tile is a PAIR of conv rows (2yp, 2yp+1) -- two
-// MMA tiles -- and the epilogue pools instead of storing the conv output:
-//   conv row -> bias, ReLU, bf16 (the reference's conv -> BN -> ReLU) -> smem row
-//   -> horizontal 3-window max at stride 2 ("hrow", Wo/2 pixels)
-//   pooled row yp = max(hrow(2yp-1), hrow(2yp), hrow(2yp+1)) -> TMA store.
-// Row 2yp-1 belongs to the previous pair: its hrow is handed over through a small ring in
-// shared memory (mbarriers hready/hfree per slot), so the 411 MB conv output of ResNet's
-// stem never reaches HBM and the pool never reads it back.  bf16 max is exact, and
-// max(relu(v)) = relu(max(v)), so the result equals conv -> BN -> ReLU -> MaxPool.
+// A tile is a PAIR of conv rows (2yp, 2yp+1) of one image, computed as ONE 128-row MMA with
+// the roles of the operands swapped: the accumulator's 128 TMEM lanes are (conv row r, output
+// channel c) = r * 64 + c and its columns are the conv pixels x.  So
+//   A (weights, resident): row r*64+c, K = (dy', dx, s) over dy' = 0..KQ -- the weights of
+//      tap (dy' - r, dx), zero outside the filter (the second conv row is the first shifted
+//      by one folded row, folded into the weights);
+//   B (folded input S, one bulk copy per tile): row x = S[2yp + dy'][x + dx], a shifted view
+//      (no-swizzle K-major, LBO 16 B: one K=16 MMA covers taps dx and dx+1) -- no im2col.
+// (KQ + 1) * ceil(KQ/2) MMAs of N = Wo per pair.
+//
+// The epilogue then pools in registers: a thread owns one (conv row, channel) and the
+// pixels run along its registers, so the horizontal 3-window / stride-2 max is register math
+// on the raw fp32 accumulators; bias, ReLU and the bf16 rounding follow the max (exact:
+// fl(v + b), ReLU and rounding are monotonic, so max commutes with them -- the result equals
+// conv -> BN -> ReLU -> MaxPool of the reference).  The vertical max takes the pair's two rows
+// and the previous pair's odd row, handed over through a ring in shared memory (hready /
+// hfree mbarriers); the pooled row is transposed to [pixel][channel] in shared memory and
+// TMA-stored.  ResNet's 411 MB conv output never exists.
 //
 // Work is split into bands of U pooled rows of one image; a band that does not start at
 // the top of the image first computes one extra "halo" pair (2*yp0-2, 2*yp0-1) whose
 // pooled row is not stored.  U is chosen on the host to balance bands over the SMs.
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warp 0      bulk-copy producer (both conv rows of a pair in one copy)
-//   warp 1      MMA issuer (4 accumulator pairs)
+//   warp 0      bulk-copy producer (the pair's S rows in one copy)
+//   warp 1      MMA issuer (4 accumulators of 128 columns)
 //   warp 2      TMEM allocator
-//   warps 4-19  epilogue, four groups of four (group g drains accumulator pair g)
+//   warps 4-19  epilogue, four groups of four (group g drains accumulator g): warps q = 0, 1
+//               own conv row 2yp (channels 32q ..), warps 2, 3 row 2yp+1
 #include <cstdlib>
 
 #include "ub_common.cuh"
@@ -30,23 +39,26 @@
 namespace ub {
 namespace {
 
-constexpr int SP_STAGES_MAX = 4;
-constexpr int SP_ACC = 4;         // accumulator pairs in flight
-constexpr int SP_GROUPS = SP_ACC;  // epilogue group g drains pair g (tiles it % 4 == g)
+constexpr int SP_STAGES_MAX = 6;
+constexpr int SP_ACC = 4;          // accumulators (tiles) in flight
+constexpr int SP_GROUPS = SP_ACC;  // epilogue group g drains accumulator g (tiles it % 4 == g)
 constexpr int SP_THREADS = 128 + 32 * 4 * SP_GROUPS;
-constexpr int SP_RING = 6;        // hrow hand-over slots (> SP_GROUPS)
+constexpr int SP_RING = 6;         // odd-row hand-over slots (> SP_GROUPS)
+constexpr int SP_COLS = 128;       // TMEM columns per accumulator (conv pixels, Wo <= 128)
 
 struct PoolParams {
   const uint16_t* s;  // folded input, 8 bf16 per row
   int n_img, Hs, Ws, Ho, Wo, Hp, Wp;
   int band, bands_per_img, n_bands;
-  int np, cout;
+  int n, cout;  // MMA N (Wo rounded up to 16), output channels (<= 64)
   uint32_t load_bytes, stage_bytes;
   int stages;
   const uint16_t* w;  // bf16 [cout][kq*kq*8]
   const float* bias;
   int relu;
-  uint32_t crow_bytes, hrow_bytes;  // Wo * 128, Wp * 128
+  int dbg;  // profiling ablations (UB_DEBUG_FLAGS): 4 no MMA, 16 no loads, 64 no pooled-row output
+  int sleep_ns;  // epilogue accumulator wait: suspend-time hint (0: spin)
+  int rw;  // ring words per channel (bf16 pairs of pooled pixels; rw / 4 odd: conflict-free rows)
 };
 
 // The CTA's tile sequence: bands u = blockIdx.x, +gridDim.x, ...; per band an optional halo
@@ -74,17 +86,17 @@ struct TileIter {
 template <int KQ>
 __global__ void __launch_bounds__(SP_THREADS, 1)
     stem_pool_kernel(const __grid_constant__ CUtensorMap tmY, const PoolParams p) {
-  constexpr int PAIRS = (KQ + 1) / 2, NMMA = KQ * PAIRS;
+  constexpr int PAIRS = (KQ + 1) / 2, NMMA = (KQ + 1) * PAIRS;
+  constexpr uint32_t A_BYTES = 128 * 32;  // one MMA's weights: 128 rows x K 16
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int b_bytes = (NMMA * 2 * p.np * 16 + 1023) & ~1023;
-  const uint32_t crow_sz = (p.crow_bytes + 1023) & ~1023u, hrow_sz = (p.hrow_bytes + 1023) & ~1023u;
-  const uint32_t grp_bytes = crow_sz + 2 * hrow_sz;
-  uint8_t* sB = base;
-  uint8_t* sG = sB + b_bytes;                      // per group: crow | hev | out (1024-aligned)
-  uint8_t* sRing = sG + SP_GROUPS * grp_bytes;     // SP_RING x hrow
-  uint8_t* sA = sRing + SP_RING * p.hrow_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sA + p.stages * p.stage_bytes);
+  const uint32_t out_sz = (static_cast<uint32_t>(p.Wp) * 128 + 1023) & ~1023u;
+  const uint32_t ring_sz = 64u * p.rw * 4;
+  uint8_t* sW = base;                                // NMMA x [khalf][128 rows][16 B]
+  uint8_t* sOut = sW + NMMA * A_BYTES;               // per group: pooled row [xp][64 ch] SW128
+  uint8_t* sRing = sOut + SP_GROUPS * out_sz;        // SP_RING x [64 ch][rw words]
+  uint8_t* sS = sRing + SP_RING * ring_sz;           // stages x folded rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(sS + p.stages * p.stage_bytes);
   uint64_t* empty = full + SP_STAGES_MAX;
   uint64_t* tfull = empty + SP_STAGES_MAX;
   uint64_t* tempty = tfull + SP_ACC;
@@ -104,25 +116,27 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     }
     for (int a = 0; a < SP_ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4);  // the group's four warps
     }
     for (int r = 0; r < SP_RING; ++r) {
-      mbar_init(&hready[r], 1);
-      mbar_init(&hfree[r], 1);
+      mbar_init(&hready[r], 2);  // the two odd-row warps of the writing tile
+      mbar_init(&hfree[r], 4);   // the even-row warps of the writing tile and of the next
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * SP_ACC * 64);
-  for (int i = threadIdx.x; i < NMMA * 2 * p.np; i += blockDim.x) {
-    const int n = i % p.np;
-    const int jh = i / p.np;
+  if (warp == 2) tmem_alloc(tmem_slot, SP_ACC * SP_COLS);
+  // weights: MMA j = dy' * PAIRS + pr, row m = r * 64 + c, K half h -> tap (dy' - r, 2 pr + h)
+  for (int i = threadIdx.x; i < NMMA * 2 * 128; i += blockDim.x) {
+    const int m = i & 127;
+    const int jh = i >> 7;
     const int j = jh >> 1, h = jh & 1;
-    const int dy = j / PAIRS;
-    const int dx = (j - dy * PAIRS) * 2 + h;
+    const int r = m >> 6, c = m & 63;
+    const int dy = j / PAIRS - r;
+    const int dx = (j % PAIRS) * 2 + h;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (n < p.cout && dx < KQ)
-      v = *reinterpret_cast<const uint4*>(p.w + static_cast<size_t>(n) * (KQ * KQ * 8) + (dy * KQ + dx) * 8);
-    *reinterpret_cast<uint4*>(sB + static_cast<size_t>(i) * 16) = v;
+    if (c < p.cout && dy >= 0 && dy < KQ && dx < KQ)
+      v = *reinterpret_cast<const uint4*>(p.w + static_cast<size_t>(c) * (KQ * KQ * 8) + (dy * KQ + dx) * 8);
+    *reinterpret_cast<uint4*>(sW + j * A_BYTES + h * 2048 + m * 16) = v;
   }
   for (int i = threadIdx.x; i < 64; i += blockDim.x) sBias[i] = (p.bias && i < p.cout) ? p.bias[i] : 0.f;
   fence_proxy_async_smem();
@@ -137,15 +151,19 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   if (ti.valid(p)) ti.start_band(p);
 
   if (warp == 0) {
-    if (lane == 0) {  // ================= producer: conv rows 2yp, 2yp+1 in one bulk copy
+    if (lane == 0) {  // ================= producer: the pair's folded rows in one bulk copy
       griddep_wait();  // S comes from the pack kernel (PDL)
       int s = 0;
       uint32_t ph = 0;
       for (; ti.valid(p); ti.next(p)) {
         const size_t R0 = (static_cast<size_t>(ti.n) * p.Hs + 2 * ti.yp()) * p.Ws;
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], p.load_bytes);
-        bulk_load(sA + s * p.stage_bytes, p.s + R0 * 8, p.load_bytes, &full[s]);
+        if (p.dbg & 16) {
+          mbar_arrive(&full[s]);
+        } else {
+          mbar_arrive_expect_tx(&full[s], p.load_bytes);
+          bulk_load(sS + s * p.stage_bytes, p.s + R0 * 8, p.load_bytes, &full[s]);
+        }
         if (++s == p.stages) {
           s = 0;
           ph ^= 1;
@@ -153,17 +171,15 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
       }
     }
   } else if (warp == 1) {  // ================= MMA issuer
-    const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
-    const uint32_t b0 = smem_u32(sB);
-    uint64_t bdesc[NMMA];
-    uint32_t aoff[NMMA];
+    const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.n));
+    uint64_t adesc[NMMA];
+    uint32_t boff[NMMA];
 #pragma unroll
     for (int j = 0; j < NMMA; ++j) {
-      const int dy = j / PAIRS, dx = (j % PAIRS) * 2;
-      aoff[j] = static_cast<uint32_t>(dy * p.Ws + dx);
-      bdesc[j] = sdesc_plain(b0 + j * 2 * p.np * 16, p.np * 16, 128);
+      adesc[j] = sdesc_plain(smem_u32(sW) + j * A_BYTES, 2048, 128);
+      boff[j] = static_cast<uint32_t>((j / PAIRS) * p.Ws + (j % PAIRS) * 2);
     }
-    const uint64_t adesc0 = sdesc_plain(smem_u32(sA), 16, 128);
+    const uint64_t bdesc0 = sdesc_plain(smem_u32(sS), 16, 128);
     const uint32_t stage_units = p.stage_bytes >> 4;
     int s = 0, a = 0;
     uint32_t sph = 0, aph = 0;
@@ -172,14 +188,11 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
       mbar_wait(&full[s], sph);
       __syncwarp();
       tc_fence_after();
-      const uint64_t ad = adesc0 + s * stage_units;
+      const uint64_t bd = bdesc0 + s * stage_units;
+      const uint32_t d = tmem_base + a * SP_COLS;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const uint32_t d = tmem_base + (a * 2 + mt) * 64;
-#pragma unroll
-        for (int j = 0; j < NMMA; ++j)
-          umma_bf16_warp(d, ad + aoff[j] + mt * p.Ws, bdesc[j], idesc, j > 0 ? 1u : 0u);
-      }
+      for (int j = 0; j < NMMA; ++j)
+        if (!(p.dbg & 4)) umma_bf16_warp(d, adesc[j], bd + boff[j], idesc, j > 0 ? 1u : 0u);
       umma_commit_warp(&empty[s]);
       umma_commit_warp(&tfull[a]);
       if (++s == p.stages) {
@@ -193,138 +206,112 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     }
   } else if (warp >= 4) {  // ================= epilogue
     const int grp = (warp - 4) >> 2;
-    const int quad = warp & 3;
-    const int gt = threadIdx.x - 128 - grp * 128;  // 0..127 within the group
-    const int r = quad * 32 + lane;                 // conv pixel x of this thread's TMEM lane
-    const bool leader = gt == 0;
-    uint8_t* crow = sG + grp * grp_bytes;
-    uint8_t* hev = crow + crow_sz;
-    uint8_t* out = hev + hrow_sz;  // 1024-aligned: TMA SWIZZLE_128B source
-    const __nv_bfloat162 ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
-    uint4 ninf4;
-    {
-      __nv_bfloat162* v = reinterpret_cast<__nv_bfloat162*>(&ninf4);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = ninf;
-    }
+    const int q = warp & 3;              // TMEM lane quarter: (conv row r, channels 32 (q & 1) ..)
+    const int r = q >> 1;
+    const int c = (q & 1) * 32 + lane;   // output channel of this thread
+    const bool leader = q == 0 && lane == 0;
+    const float bias = sBias[c];
+    uint8_t* out = sOut + grp * out_sz;  // 1024-aligned: TMA SWIZZLE_128B source
+    const int nw = (p.Wp + 1) >> 1;      // bf16x2 words of a pooled row (the last half-used if Wp is odd)
+    const int chunk8 = c >> 3;             // this channel's 16-byte chunk of a pooled pixel row
+    const uint32_t cbyte2 = (c & 7) * 2;
     int it = 0;
     for (; ti.valid(p); ti.next(p), ++it) {
       if ((it % SP_GROUPS) != grp) continue;
       const int a = it % SP_ACC;
       const int slot = it % SP_RING;
       const int prev = (it + SP_RING - 1) % SP_RING;
-      mbar_wait(&tfull[a], (it / SP_ACC) & 1);
+      if (p.sleep_ns) mbar_wait_sleep(&tfull[a], (it / SP_ACC) & 1, p.sleep_ns);
+      else mbar_wait(&tfull[a], (it / SP_ACC) & 1);
       tc_fence_after();
-      for (int mt = 0; mt < 2; ++mt) {
-        // ---- conv row 2yp+mt: TMEM -> bias, ReLU, bf16 -> crow[x] (SW128-style chunk swizzle)
-        uint32_t v0[32], v1[32];
-        const uint32_t taddr = tmem_base + (a * 2 + mt) * 64 + (static_cast<uint32_t>(quad * 32) << 16);
-        tmem_ld32(taddr, v0);
-        tmem_ld32(taddr + 32, v1);
+      // ---- horizontal 3-window / stride-2 max over this thread's conv row, 32 pixels per load
+      uint32_t h[SP_COLS / 4];  // bf16x2: pooled pixels (2i, 2i+1) after bias / ReLU / rounding
+      float carry = -INFINITY;  // pixel 32k - 1 (the left pad for k = 0)
+      const uint32_t taddr = tmem_base + a * SP_COLS + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+      for (int k = 0; k < SP_COLS / 32; ++k) {
+        if (32 * k >= p.Wo) break;
+        uint32_t v[32];
+        tmem_ld32(taddr + 32 * k, v);
         tmem_ld_wait();
-        if (mt == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[a]);
-        }
-        if (r < p.Wo) {
-          uint8_t* rowp = crow + r * 128;
-          auto emit = [&](const uint32_t (&v)[32], int half) {
+        float m[16];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int col = half * 32 + 8 * jj;
-              const float4 b0 = *reinterpret_cast<const float4*>(sBias + col);
-              const float4 b1 = *reinterpret_cast<const float4*>(sBias + col + 4);
-              const float2 s0 = add_f32x2(make_float2(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1])),
-                                          make_float2(b0.x, b0.y));
-              const float2 s1 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3])),
-                                          make_float2(b0.z, b0.w));
-              const float2 s2 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 4]), __uint_as_float(v[8 * jj + 5])),
-                                          make_float2(b1.x, b1.y));
-              const float2 s3 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])),
-                                          make_float2(b1.z, b1.w));
-              uint4 o;
-              if (p.relu) {
-                o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y),
-                               cvt_relu_bf16x2(s2.x, s2.y), cvt_relu_bf16x2(s3.x, s3.y));
-              } else {
-                o = make_uint4(cvt_bf16x2(s0.x, s0.y), cvt_bf16x2(s1.x, s1.y), cvt_bf16x2(s2.x, s2.y),
-                               cvt_bf16x2(s3.x, s3.y));
-              }
-              const int k = half * 4 + jj;
-              *reinterpret_cast<uint4*>(rowp + ((k ^ (r & 7)) << 4)) = o;
-            }
-          };
-          emit(v0, 0);
-          emit(v1, 1);
+        for (int i = 0; i < 16; ++i) {
+          const float left = i == 0 ? carry : __uint_as_float(v[2 * i - 1]);
+          m[i] = fmaxf(left, fmaxf(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])));
         }
-        if (mt == 1) {  // this tile's odd hrow goes to the ring: its previous reader must be done
-          if (leader) mbar_wait(&hfree[slot], ((it / SP_RING) & 1) ^ 1);
-        }
-        named_bar_sync(1 + grp, 128);
-        // ---- horizontal max: hrow[xp][k] = max(crow[2xp-1], crow[2xp], crow[2xp+1]) chunk k
-        uint8_t* hdst = mt == 0 ? hev : sRing + slot * p.hrow_bytes;
-        for (int e = gt; e < p.Wp * 8; e += 128) {
-          const int xp = e >> 3, k = e & 7;
-          const int x0 = 2 * xp - 1;
-          uint4 m = *reinterpret_cast<const uint4*>(crow + (x0 + 1) * 128 + ((k ^ ((x0 + 1) & 7)) << 4));
-          __nv_bfloat162* mv = reinterpret_cast<__nv_bfloat162*>(&m);
-          if (x0 >= 0) {
-            const uint4 u = *reinterpret_cast<const uint4*>(crow + x0 * 128 + ((k ^ (x0 & 7)) << 4));
-            const __nv_bfloat162* uv = reinterpret_cast<const __nv_bfloat162*>(&u);
+        carry = __uint_as_float(v[31]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], uv[i]);
-          }
-          if (x0 + 2 < p.Wo) {
-            const uint4 u = *reinterpret_cast<const uint4*>(crow + (x0 + 2) * 128 + ((k ^ ((x0 + 2) & 7)) << 4));
-            const __nv_bfloat162* uv = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], uv[i]);
-          }
-          *reinterpret_cast<uint4*>(hdst + e * 16) = m;
-        }
-        named_bar_sync(1 + grp, 128);  // crow free for the next row; hrow complete
-        if (mt == 1 && leader) mbar_arrive(&hready[slot]);
+        for (int i = 0; i < 8; ++i)
+          h[8 * k + i] = p.relu ? cvt_relu_bf16x2(m[2 * i] + bias, m[2 * i + 1] + bias)
+                                : cvt_bf16x2(m[2 * i] + bias, m[2 * i + 1] + bias);
       }
-      // ---- vertical max with the previous pair's odd hrow (row 2yp-1), then store
-      const int yp = ti.yp();
-      const bool has_prev = it > 0;
-      if (has_prev) mbar_wait(&hready[prev], ((it - 1) / SP_RING) & 1);
-      if (ti.emit()) {
-        if (leader) bulk_wait_read<0>();  // this group's previous pooled row has left `out`
-        named_bar_sync(1 + grp, 128);
-        const uint8_t* hodd = sRing + slot * p.hrow_bytes;
-        const uint8_t* hprv = sRing + prev * p.hrow_bytes;
-        for (int e = gt; e < p.Wp * 8; e += 128) {
-          const int xp = e >> 3, k = e & 7;
-          uint4 m = *reinterpret_cast<const uint4*>(hev + e * 16);
-          __nv_bfloat162* mv = reinterpret_cast<__nv_bfloat162*>(&m);
-          const uint4 u1 = *reinterpret_cast<const uint4*>(hodd + e * 16);
-          const __nv_bfloat162* v1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
-          const uint4 u0 = yp > 0 ? *reinterpret_cast<const uint4*>(hprv + e * 16) : ninf4;
-          const __nv_bfloat162* v0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);  // accumulator drained
+      uint32_t* ring_slot = reinterpret_cast<uint32_t*>(sRing + slot * ring_sz) + c * p.rw;
+      if (r == 1) {
+        // ---- odd conv row 2yp+1 -> ring slot (read by this pair and the next)
+        if (lane == 0) mbar_wait(&hfree[slot], ((it / SP_RING) & 1) ^ 1);
+        __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 4; ++i) mv[i] = __hmax2(mv[i], __hmax2(v0[i], v1[i]));
-          *reinterpret_cast<uint4*>(out + xp * 128 + ((k ^ (xp & 7)) << 4)) = m;
+        for (int i = 0; i < SP_COLS / 4; i += 4)
+          if (i < nw) *reinterpret_cast<uint4*>(ring_slot + i) = make_uint4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hready[slot]);
+        continue;
+      }
+      // ---- even conv row 2yp: pooled row yp = max(row 2yp-1 (previous pair), 2yp, 2yp+1)
+      if (ti.emit() && !(p.dbg & 64)) {
+        const int yp = ti.yp();
+        const bool has_prev = yp > 0;
+        mbar_wait(&hready[slot], (it / SP_RING) & 1);
+        if (has_prev) mbar_wait(&hready[prev], ((it - 1) / SP_RING) & 1);
+        const uint32_t* prv = reinterpret_cast<const uint32_t*>(sRing + prev * ring_sz) + c * p.rw;
+        if (leader) bulk_wait_read<0>();  // the group's previous pooled row has left `out`
+#pragma unroll
+        for (int i = 0; i < SP_COLS / 4; i += 4) {
+          if (i >= nw) break;
+          const uint4 o = *reinterpret_cast<const uint4*>(ring_slot + i);
+          uint4 pv = o;
+          if (has_prev) pv = *reinterpret_cast<const uint4*>(prv + i);
+          h[i] = bf16x2_max3(h[i], o.x, pv.x);
+          h[i + 1] = bf16x2_max3(h[i + 1], o.y, pv.y);
+          h[i + 2] = bf16x2_max3(h[i + 2], o.z, pv.z);
+          h[i + 3] = bf16x2_max3(h[i + 3], o.w, pv.w);
+        }
+        // [xp][64 ch] with SW128 chunk swizzle: this thread's channel, pixels 2i and 2i+1
+        named_bar_sync(1 + grp, 64);
+#pragma unroll
+        for (int i = 0; i < SP_COLS / 4; ++i) {
+          if (i >= nw) break;
+          const int x0 = 2 * i, x1 = 2 * i + 1;
+          *reinterpret_cast<uint16_t*>(out + x0 * 128 + ((chunk8 ^ (x0 & 7)) << 4) + cbyte2) =
+              static_cast<uint16_t>(h[i] & 0xffffu);
+          if (x1 < p.Wp)
+            *reinterpret_cast<uint16_t*>(out + x1 * 128 + ((chunk8 ^ (x1 & 7)) << 4) + cbyte2) =
+                static_cast<uint16_t>(h[i] >> 16);
         }
         fence_proxy_async_smem();
-        named_bar_sync(1 + grp, 128);
+        named_bar_sync(1 + grp, 64);
         if (leader) {
           tma_store_4d(&tmY, out, 0, 0, yp, ti.n);
           bulk_commit();
         }
-      } else {
-        named_bar_sync(1 + grp, 128);
       }
-      if (has_prev && leader) mbar_arrive(&hfree[prev]);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&hfree[slot]);              // this pair is done with its own odd row
+        if (it > 0) mbar_arrive(&hfree[prev]);  // and with the previous pair's
+      }
     }
-    if (leader) bulk_wait_all();
+    if (q == 0 && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * SP_ACC * 64);
+    tmem_dealloc(tmem_base, SP_ACC * SP_COLS);
   }
 }
 
@@ -370,17 +357,26 @@ extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, in
   p.Wo = Wo;
   p.Hp = Ho / 2;
   p.Wp = Wo / 2;
-  p.np = 64;
+  p.n = (Wo + 15) / 16 * 16;
+  {
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("UB_DEBUG_FLAGS") ? atoi(getenv("UB_DEBUG_FLAGS")) : 0;
+    p.dbg = dbg;
+    static int sl = -1;
+    if (sl < 0) sl = getenv("UB_SP_SLEEP") ? atoi(getenv("UB_SP_SLEEP")) : 0;
+    p.sleep_ns = sl;
+  }
   p.cout = cout;
+  p.rw = ((p.Wp + 1) / 2 + 3) / 4 * 4;
+  if (((p.rw / 4) & 1) == 0) p.rw += 4;
   p.w = static_cast<const uint16_t*>(w);
   p.bias = bias;
   p.relu = relu;
-  p.crow_bytes = static_cast<uint32_t>(Wo) * 128;
-  p.hrow_bytes = static_cast<uint32_t>(p.Wp) * 128;
-  // the pair's copy: rows R0 .. R0 + Ws + 128 + (kq-1)*Ws + 2*pairs - 1 of S; stays inside the
-  // buffer for the last pair since S holds Hs = Ho + kq - 1 rows per image plus its tail
+  // the pair's copy: S rows R0 .. R0 + kq*Ws + 2*pairs + N - 2 (folded rows 2yp .. 2yp + kq);
+  // stays inside the buffer for the last pair since S holds Hs = Ho + kq - 1 rows per image
+  // plus its tail
   const int pairs = (kq + 1) / 2;
-  const uint32_t load_rows = static_cast<uint32_t>(Ws + 128 + (kq - 1) * Ws + 2 * pairs - 1);
+  const uint32_t load_rows = static_cast<uint32_t>(kq * Ws + 2 * pairs + p.n - 1);
   const long long last_end = (static_cast<long long>(N - 1) * Hs + Ho - 2) * Ws + load_rows;
   if (last_end * 16 > sbytes) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: staging buffer too small");
   p.load_bytes = load_rows * 16;
@@ -404,9 +400,9 @@ extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, in
   const long long n_bands = static_cast<long long>(p.bands_per_img) * N;
   if (n_bands >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: too many bands");
   p.n_bands = static_cast<int>(n_bands);
-  const int b_bytes = (kq * pairs * 2 * p.np * 16 + 1023) & ~1023;
-  const size_t grp_bytes = ((p.crow_bytes + 1023) & ~1023u) + 2 * ((p.hrow_bytes + 1023) & ~1023u);
-  const size_t fixed = 1024 + b_bytes + SP_GROUPS * grp_bytes + SP_RING * p.hrow_bytes + 512 + 64 * 4;
+  const size_t w_bytes = static_cast<size_t>(kq + 1) * pairs * 128 * 32;
+  const size_t out_bytes = (static_cast<size_t>(p.Wp) * 128 + 1023) & ~static_cast<size_t>(1023);
+  const size_t fixed = 1024 + w_bytes + SP_GROUPS * out_bytes + SP_RING * 64 * p.rw * 4 + 512 + 64 * 4;
   int stages = static_cast<int>((227 * 1024 - fixed) / p.stage_bytes);
   if (stages < 2) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: shared memory");
   p.stages = stages > SP_STAGES_MAX ? SP_STAGES_MAX : stages;

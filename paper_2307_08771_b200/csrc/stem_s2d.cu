@@ -320,6 +320,64 @@ __global__ void stem_s2d_pack_kernel(const float* __restrict__ x, int C, int H, 
   s[static_cast<size_t>(n) * Hs * Ws + rem] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// Row-staged pack: one CTA per PACK_YB folded rows (n, Y .. Y + PACK_YB - 1).  The 2 * CIN
+// input rows of each are loaded with coalesced float4 loads into shared memory (zero margins of
+// `off` columns on the left and up to `sw` on the right stand in for the padding); then each
+// thread assembles folded pixels from shared memory.  Thread -> (row, float4 column) and
+// (row, pixel) maps are shifts, not divisions.  Needs W % 4 == 0 (16-byte row alignment).
+constexpr int PACK_YB = 4, PACK_THREADS = 256;
+
+template <int CIN>
+__global__ void __launch_bounds__(PACK_THREADS) stem_s2d_pack_rows_kernel(
+    const float* __restrict__ x, int C, int H, int W, const int32_t* __restrict__ idx, int pad, int Hs, int Ws,
+    int off, int sw, uint4* __restrict__ s) {
+  constexpr int NROWS = PACK_YB * 2 * CIN;  // staged rows: [yb][py][c]
+  extern __shared__ float4 srow4[];
+  const float* srow = reinterpret_cast<const float*>(srow4);
+  const int Y0 = blockIdx.x * PACK_YB, n = blockIdx.y;
+  const int w4 = W >> 2, sw4 = sw >> 2, off4 = off >> 2;
+  int ch[CIN];
+#pragma unroll
+  for (int c = 0; c < CIN; ++c) ch[c] = __ldg(idx + c);
+  // load: 64 threads per staged row, PACK_THREADS / 64 rows per pass
+  {
+    const int j0 = threadIdx.x & 63;
+#pragma unroll
+    for (int r0 = 0; r0 < NROWS; r0 += PACK_THREADS / 64) {
+      const int rr = r0 + (threadIdx.x >> 6);
+      const int yb = rr / (2 * CIN), py = (rr / CIN) & 1, c = rr % CIN;  // compile-time divisors
+      const int hi = 2 * (Y0 + yb) + py - pad;
+      const bool row_ok = Y0 + yb < Hs && hi >= 0 && hi < H;
+      const float4* src = reinterpret_cast<const float4*>(x + ((static_cast<size_t>(n) * C + ch[c]) * H + hi) * W);
+      for (int j = j0; j < sw4; j += 64) {
+        const int i4 = j - off4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row_ok && i4 >= 0 && i4 < w4) v = __ldg(src + i4);
+        srow4[rr * sw4 + j] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // assemble: 128 threads per folded row
+  for (int yb = threadIdx.x >> 7; yb < PACK_YB; yb += PACK_THREADS / 128) {
+    if (Y0 + yb >= Hs) break;
+    const float* rows = srow + yb * 2 * CIN * sw;
+    uint4* dst = s + (static_cast<size_t>(n) * Hs + Y0 + yb) * Ws;
+    for (int X = threadIdx.x & 127; X < Ws; X += 128) {
+      const int col = 2 * X - pad + off;  // in [0, sw - 1) by construction of off / sw
+      float f[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < CIN; ++c) f[q * CIN + c] = rows[((q >> 1) * CIN + c) * sw + col + (q & 1)];
+#pragma unroll
+      for (int i = 4 * CIN; i < 8; ++i) f[i] = 0.f;
+      dst[X] = make_uint4(cvt_bf16x2(f[0], f[1]), cvt_bf16x2(f[2], f[3]), cvt_bf16x2(f[4], f[5]),
+                          cvt_bf16x2(f[6], f[7]));
+    }
+  }
+}
+
 template <int KQ>
 void launch_s2d(const CUtensorMap& tm, const S2DParams& p, int grid, size_t smem, cudaStream_t stream) {
   static bool attr = false;
@@ -378,6 +436,23 @@ extern "C" int ub_stem_s2d_pack(const float* x, int N, int C, int H, int W, cons
   S2DGeom g;
   const int rc = s2d_geometry(N, H, W, k, pad, &g);
   if (rc) return rc;
+  if (W % 4 == 0 && !(reinterpret_cast<uintptr_t>(x) & 15) && g.Hs <= 65535 && N <= 65535) {
+    const int off = (pad + 3) & ~3;                       // left zero margin (>= pad, float4-aligned)
+    const int right = 2 * g.Ws + 1 - pad;                 // one past the last column read
+    const int sw = off + ((right > W ? right : W) + 3) / 4 * 4;
+    const size_t smem = static_cast<size_t>(PACK_YB) * 2 * cin * sw * sizeof(float);
+    if (smem <= 48 * 1024) {
+      const dim3 grid((g.Hs + PACK_YB - 1) / PACK_YB, N);
+      if (cin == 1)
+        stem_s2d_pack_rows_kernel<1><<<grid, PACK_THREADS, smem, stream>>>(x, C, H, W, idx, pad, g.Hs, g.Ws, off, sw,
+                                                                           static_cast<uint4*>(s));
+      else
+        stem_s2d_pack_rows_kernel<2><<<grid, PACK_THREADS, smem, stream>>>(x, C, H, W, idx, pad, g.Hs, g.Ws, off, sw,
+                                                                           static_cast<uint4*>(s));
+      count_launch();
+      return cuda_status(cudaGetLastError(), "stem_s2d_pack_rows_kernel");
+    }
+  }
   const int block = 256;
   const dim3 grid((g.Hs * g.Ws + block - 1) / block, N);
   stem_s2d_pack_kernel<<<grid, block, 0, stream>>>(x, C, H, W, idx, cin, pad, g.Hs, g.Ws, static_cast<uint4*>(s));

@@ -331,4 +331,12 @@ UB_DEVI uint32_t cvt_relu_bf16x2(float lo, float hi) {
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
 }
+// Lane-wise max of three packed bf16x2 (exact).
+UB_DEVI uint32_t bf16x2_max3(uint32_t a, uint32_t b, uint32_t c) {
+  __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
+  const __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
+  const __nv_bfloat162 z = *reinterpret_cast<__nv_bfloat162*>(&c);
+  x = __hmax2(x, __hmax2(y, z));
+  return *reinterpret_cast<uint32_t*>(&x);
+}
 }  // namespace ub

@@ -174,6 +174,33 @@ def test_stem_s2d_matches_torch(N, H, k, pad, idx, cout):
     assert torch.isnan(y.buf[:, :8].float()).all()
 
 
+@pytest.mark.parametrize("N,H,k,pad,idx", [(2, 224, 7, 3, [2, 0]), (1, 37, 5, 2, [1]), (2, 20, 3, 1, [0, 1]),
+                                            (1, 64, 7, 4, [1, 2])])
+def test_stem_s2d_pack_exact(N, H, k, pad, idx):
+    """The 2x2 fold is a pure relayout + bf16 rounding: bit-exact against a torch restatement."""
+    dev = "cuda"
+    cin = len(idx)
+    g = torch.Generator().manual_seed(N * 7 + H + k + pad)
+    x = torch.randn(N, 3, H, H, generator=g)
+    sbuf = K.s2d_buffer(N, H, H, k, pad, dev)
+    sbuf.fill_(12345)
+    lib = _lib.load()
+    xd, idxd = x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev)  # alive until the kernel ran
+    _lib.check(lib.ub_stem_s2d_pack(K._p(xd), N, 3, H, H, K._p(idxd), cin, k, pad, K._p(sbuf), K._stream()))
+    torch.cuda.synchronize()
+    Hs, Ws = _lib.stem_s2d_geometry(N, H, H, k, pad)[:2]
+    xp = torch.zeros(N, cin, 2 * Hs + 2, 2 * Ws + 2)
+    xp[:, :, pad:pad + H, pad:pad + H] = x[:, idx]
+    xp = xp[:, :, :2 * Hs, :2 * Ws].to(torch.bfloat16)
+    # S[n][Y][X][(py * 2 + px) * cin + c] = x[n][idx[c]][2Y + py - pad][2X + px - pad]
+    ref = xp.reshape(N, cin, Hs, 2, Ws, 2).permute(0, 2, 4, 3, 5, 1).reshape(N, Hs, Ws, 4 * cin)
+    full = torch.zeros(N, Hs, Ws, 8, dtype=torch.bfloat16)
+    full[..., :4 * cin] = ref
+    got = sbuf.view(torch.bfloat16)[:N * Hs * Ws * 8].reshape(N, Hs, Ws, 8).cpu()
+    bad = (got.view(torch.int16) != full.view(torch.int16)).nonzero()
+    assert bad.numel() == 0, (bad[:8].tolist(), got[tuple(bad[0])].item(), full[tuple(bad[0])].item())
+
+
 @pytest.mark.parametrize("N,H,idx,cout", [(3, 224, [2, 0], 64), (5, 64, [1], 60), (2, 100, [0, 2], 32)])
 def test_stem_s2d_maxpool_matches_torch(N, H, idx, cout):
     """Stem with the 3x3/s2/p1 max pool fused into its epilogue (bands of pooled rows,

@@ -35,7 +35,8 @@ def timeit(fn, reps=20):
 
 
 def main():
-    N = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    N = int(args[0]) if args else 256
     dev = "cuda"
     x = torch.randn(N, 3, 224, 224, device=dev)
     idx = torch.tensor([2, 0], dtype=torch.int32, device=dev)
@@ -54,6 +55,24 @@ def main():
         _lib.check(lib.ub_conv_s2d(K._p(sbuf), N, 224, 224, k, pad, K._p(wg), cout, K._p(bias), 1, K._p(y.buf),
                                    y.cstride, y.coff, K._stream()))
 
+    yp = K.empty_act(N, 56, 56, cout, dev)
+
+    def pool():
+        _lib.check(lib.ub_conv_s2d_maxpool(K._p(sbuf), N, 224, 224, k, pad, K._p(wg), cout, K._p(bias), 1, 3, 2, 1,
+                                           K._p(yp.buf), yp.cstride, yp.coff, K._stream()))
+
+    if "--pack-only" in sys.argv:
+        for _ in range(3):
+            pack()
+        torch.cuda.synchronize()
+        return
+    if "--pool-only" in sys.argv:
+        for _ in range(3):
+            pool()
+        torch.cuda.synchronize()
+        return
+    tpool = timeit(pool)
+    print(f"conv+maxpool {tpool:8.1f} us")
     tp, tc = timeit(pack), timeit(conv)
     out_b = N * 112 * 112 * cout * 2
     s_b = sbuf.numel() * 2
