@@ -46,7 +46,8 @@ constexpr int HALO_SLOT = 32 * 128;  // one epilogue warp's 32 rows x 64 channel
 
 struct HaloParams {
   const uint16_t* x;  // at channel (coff - lead)
-  int x_cstride, N, H, W;
+  int x_cstride, N, H, W;  // input
+  int Ho;                  // output rows per image (== H for stride 1)
   int R, Wp, wp_shift, n_pos, planes;
   uint32_t plane_stride, a_stage_bytes;
   int a_stages;
@@ -62,6 +63,7 @@ struct HaloParams {
   int groups;    // 64-channel groups (1: all taps' weights resident; > 1: streamed per group x tap)
   int b_stages;  // streamed weight ring depth
   int kvalid;    // lead + cin: channels past it are not read (their weights are zero)
+  uint32_t a_box_bytes;  // AT: bytes of one input box (one stacked image's box when ipt > 1)
   int ipt;       // images stacked per tile (small images): image i's row y at staged row 1 + i * (H + 1) + y
   long long* trace;  // profiling (UB_HALO_TRACE): CTA 0 event clocks, [tile][8]
   int dbg;           // profiling ablations (UB_HALO_DBG): 1 no halo loads, 2 no output, 4 no TMEM reads,
@@ -69,21 +71,35 @@ struct HaloParams {
 };
 
 // Compile-time halo geometry: padded width WP, rows per tile, staged positions, plane stride.
-template <int WP, int MT>
+// Stride 2 runs as a stride-1 2x2 conv over the 2x2-folded input (see conv_halo3_kernel): one
+// staged row fewer and no left pad column.
+template <int WP, int MT, int S>
 struct HaloGeom {
   static constexpr int R = 128 / WP;    // output rows per 128-position MMA tile
   static constexpr int RT = MT * R;     // output rows per staged tile (MT MMA tiles)
-  static constexpr int N_POS = ((RT + 2) * WP + 2 + 7) / 8 * 8;
+  static constexpr int N_POS = S == 1 ? ((RT + 2) * WP + 2 + 7) / 8 * 8 : ((RT + 1) * WP + 1 + 7) / 8 * 8;
   static constexpr uint32_t PLANE_STRIDE = N_POS * 16 + 16;  // odd # of 16-B units: planes on different banks
 };
 
 // SB: weights streamed per (64-channel group, tap) through a TMA ring (cpad > 64); else resident.
-template <int WP, int PLANES, int MT, bool SB>
+// S = 2: stride-2 3x3 conv as a 2x2 stride-1 conv over the input folded 2x2 with origin -1:
+// folded pixel (Y, X) quadrant (py, px) = input (2Y + py - 1, 2X + px - 1), so output (y, x)
+// reads folded (y + dy, x + dx), dy, dx < 2, with filter tap (ky, kx) = (2dy + py, 2dx + px)
+// (taps past 2 do not exist: 9 of the 16 (quadrant, shift) pairs).  Groups = quadrant x 64
+// input channels; the producer folds on the fly (a plane is 16 contiguous bytes of one input
+// pixel), so no folded copy is ever written.
+// AT: the input tile arrives by ONE 4-D TMA box per (tile, 64-channel group) -- positions
+// [row][Wp] x KB bytes (= PLANES * 16) with the 128-/64-byte swizzle, zero-filled outside the
+// image (negative coordinates; stride 2 through element strides 2 on W and H) -- and the tap
+// shifts are whole rows of that swizzled block.  Otherwise 128 producer threads cp.async the
+// 16-byte channel planes.
+template <int WP, int PLANES, int MT, bool SB, int S, bool AT>
 __global__ void __maxnreg__(96)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmW,
-                      const HaloParams p) {
+                      const __grid_constant__ CUtensorMap tmX, const HaloParams p) {
+  constexpr int KB = PLANES * 16;  // bytes of one staged position (AT)
   constexpr int TAPS = 9;
-  using G = HaloGeom<WP, MT>;
+  using G = HaloGeom<WP, MT, S>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // weights: resident [tap][np rows][128 B] (one group) or a ring of (group, tap) blocks; SW128
@@ -107,7 +123,7 @@ __global__ void __maxnreg__(96)
   constexpr int MMA_WARP = HALO_EPI_WARPS, ALLOC_WARP = HALO_EPI_WARPS + 1;
   if (warp == MMA_WARP && lane == 0) {
     for (int s = 0; s < p.a_stages; ++s) {
-      mbar_init(&afull[s], HALO_PRODUCERS);
+      mbar_init(&afull[s], AT ? 1 : HALO_PRODUCERS);
       mbar_init(&aempty[s], 1);
     }
     for (int a = 0; a < p.nacc; ++a) {
@@ -124,9 +140,18 @@ __global__ void __maxnreg__(96)
   if (warp == 0) {
     tma_prefetch_desc(&tmY);
     if (SB) tma_prefetch_desc(&tmW);
+    if (AT) tma_prefetch_desc(&tmX);
   }
   if (warp == ALLOC_WARP) tmem_alloc(tmem_slot, p.nacc * MT * p.acc_cols);
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sBias[i] = (p.bias && i < p.cout) ? p.bias[i] : 0.f;
+  if constexpr (AT) {
+    // positions no box covers read as zero: the right pad of a tile's (or the last stacked
+    // image's) last row wraps to the next row's column 0 (Wp = W + 1)
+    uint4* a4 = reinterpret_cast<uint4*>(sA);
+    for (int i = threadIdx.x; i < static_cast<int>(p.a_stages * p.a_stage_bytes / 16); i += blockDim.x)
+      a4[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -137,7 +162,8 @@ __global__ void __maxnreg__(96)
     // ================= producers
     const int pt = threadIdx.x - 32 * HALO_PROD_WARP0;
     // resident weights: tap t, row n, 16-byte chunk j (K = 8j .. 8j+7 of the tap) -> SW128
-    const int cp8 = SB ? 0 : p.cpad >> 3;
+    const int cp8 = p.cpad >> 3;
+    if constexpr (!SB)
     for (int e = pt; e < TAPS * p.np * cp8; e += HALO_PRODUCERS) {
       const int t = e / (p.np * cp8);
       const int rem = e - t * (p.np * cp8);
@@ -150,6 +176,42 @@ __global__ void __maxnreg__(96)
     }
     cp_async_arrive_noinc(bres);
     griddep_wait();  // the input activations come from the previous kernel (PDL)
+    if constexpr (AT) {
+      if (pt == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        const int ncb = p.cpad >> 6;
+        for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
+          for (int g = 0; g < groups; ++g) {
+            const int img = p.ipt > 1 ? t * p.ipt : t / p.tiles_per_img;
+            int c0 = g * 64, ox = -1, oy = -1;  // box origin: channel, column, row (input coordinates)
+            int img_rows = p.H + 1;             // staged rows per stacked image
+            if constexpr (S == 2) {
+              const int qd = g / ncb;
+              c0 = (g - qd * ncb) * 64;
+              ox = (qd & 1) - 1;
+              oy = (qd >> 1) - 1;
+              img_rows = p.Ho + 1;
+            }
+            mbar_wait(&aempty[s], ph ^ 1);
+            uint8_t* dst = sA + s * p.a_stage_bytes;
+            if (p.ipt > 1) {
+              const int n_i = p.N - img < p.ipt ? p.N - img : p.ipt;
+              mbar_arrive_expect_tx(&afull[s], n_i * p.a_box_bytes);
+              for (int i = 0; i < n_i; ++i)
+                tma_load_4d(&tmX, &afull[s], dst + i * img_rows * WP * KB, c0, ox, oy, img + i);
+            } else {
+              const int row0 = (t - img * p.tiles_per_img) * G::RT;  // first output row
+              mbar_arrive_expect_tx(&afull[s], p.a_box_bytes);
+              tma_load_4d(&tmX, &afull[s], dst, c0, ox, S * row0 + oy, img);
+            }
+            if (++s == p.a_stages) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+      }
+    } else {
     // halo planes: this thread always fills plane pp of positions q0 + i * qstep
     const int pp = pt % PLANES;
     const int q0 = pt / PLANES;
@@ -170,6 +232,29 @@ __global__ void __maxnreg__(96)
         if (itp < 64) p.trace[itp * 16 + 7] = clock64();
       }
       const uint32_t dst0 = smem_u32(sA + s * p.a_stage_bytes + pp * G::PLANE_STRIDE);
+      if constexpr (S == 2) {
+        const int ncb = p.cpad >> 6;
+        const int qd = g / ncb, cb = g - qd * ncb;
+        const int py = qd >> 1, px = qd & 1;
+        const uint16_t* xq = p.x + static_cast<size_t>(img) * p.H * p.W * p.x_cstride + cb * 64 + pp * 8;
+        const bool kin = cb * 64 + pp * 8 < p.kvalid;
+        const int ybase = p.ipt > 1 ? 0 : (t - img * p.tiles_per_img) * G::RT;  // first folded row
+        for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
+          int sr = ybase + (q >> wp_shift);
+          int i = 0;
+          if (p.ipt > 1) {  // stacked: image i's folded rows 0 .. Ho at stack rows i (Ho + 1) ..
+            i = sr / (p.Ho + 1);
+            sr -= i * (p.Ho + 1);
+          }
+          const int yy = 2 * sr + py - 1;
+          const int xx = 2 * (q & wmask) + px - 1;
+          const bool ok = kin && i < p.ipt && img + i < p.N && yy >= 0 && yy < p.H && xx >= 0 && xx < p.W;
+          const uint16_t* src = ok ? xq + (static_cast<size_t>(i * p.H + yy) * p.W + xx) * p.x_cstride : p.x;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + q * 16), "l"(src),
+                       "r"(ok ? 16u : 0u)
+                       : "memory");
+        }
+      } else {
       const bool kin = g * 64 + pp * 8 < p.kvalid;
       if (p.ipt > 1) {  // stacked images: stack row r -> image i = r / (H + 1), its row r - i (H + 1)
         for (int q = q0; q < G::N_POS && !(p.dbg & 1); q += qstep) {
@@ -194,6 +279,7 @@ __global__ void __maxnreg__(96)
                        : "memory");
         }
       }
+      }
       cp_async_arrive_noinc(&afull[s]);
       if (++s == p.a_stages) {
         s = 0;
@@ -201,13 +287,21 @@ __global__ void __maxnreg__(96)
       }
     }
     cp_async_wait<0>();
+    }
   } else if (warp == MMA_WARP) {
     // ================= MMA issuer (whole warp; one elected lane issues)
     const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(p.np));
     const uint32_t b0 = smem_u32(sB);
     const uint64_t bdesc0 = make_sdesc(b0, 1024, 2);
     const uint32_t b_units = p.b_block_bytes >> 4;
-    const uint64_t adesc0 = sdesc_plain(smem_u32(sA), G::PLANE_STRIDE, 128);
+    const uint64_t adesc0 = AT ? make_sdesc(smem_u32(sA), 8 * KB, KB == 128 ? 2 : 4)
+                               : sdesc_plain(smem_u32(sA), G::PLANE_STRIDE, 128);
+    // A operand of MMA tile mt, tap shift (dy, dx), K step j (16-byte units)
+    auto a_off = [&](int mt, int dy, int dx, int j) -> uint32_t {
+      const int pos = mt * G::R * WP + dy * WP + dx;
+      return AT ? static_cast<uint32_t>(pos * KB + 32 * j) >> 4
+                : static_cast<uint32_t>(pos * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
+    };
     const uint32_t stage_units = p.a_stage_bytes >> 4;
     if (!SB) mbar_wait(bres, 0);
     __syncwarp();
@@ -227,6 +321,30 @@ __global__ void __maxnreg__(96)
         tc_fence_after();
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
         const uint64_t ad = adesc0 + s * stage_units;
+        if constexpr (S == 2) {
+          const int qd = g / (p.cpad >> 6);
+          const int py = qd >> 1, px = qd & 1;
+          for (int dy = 0; dy < 2 - py; ++dy)
+            for (int dx = 0; dx < 2 - px; ++dx) {
+              mbar_wait(&bfull[bs], bph);
+              __syncwarp();
+              tc_fence_after();
+              const uint64_t bd = bdesc0 + bs * b_units;
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) {
+                const uint32_t d = tmem_base + (acc * MT + mt) * p.acc_cols;
+#pragma unroll
+                for (int j = 0; j < PLANES / 2; ++j) {
+                  umma_bf16_warp(d, ad + a_off(mt, dy, dx, j), bd + 2 * j, idesc, (g | dy | dx | j) ? 1u : 0u);
+                }
+              }
+              umma_commit_warp(&bempty[bs]);
+              if (++bs == p.b_stages) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+        } else
 #pragma unroll
         for (int tap = 0; tap < TAPS; ++tap) {
           uint64_t bd;
@@ -244,9 +362,7 @@ __global__ void __maxnreg__(96)
 #pragma unroll
             for (int j = 0; j < PLANES / 2; ++j) {
               // A: planes 2j, 2j+1 of MMA tile mt shifted by tap (dy, dx); B: K step j of the tap
-              const uint32_t aoff =
-                  ((mt * G::R * WP + (tap / 3) * WP + (tap % 3)) * 16 + 2 * j * G::PLANE_STRIDE) >> 4;
-              umma_bf16_warp(d, ad + aoff, bd + 2 * j, idesc, (g | tap | j) ? 1u : 0u);
+              umma_bf16_warp(d, ad + a_off(mt, tap / 3, tap % 3, j), bd + 2 * j, idesc, (g | tap | j) ? 1u : 0u);
             }
           }
           if constexpr (SB) {
@@ -271,15 +387,26 @@ __global__ void __maxnreg__(96)
     if (lane == 0) {
       int bs = 0;
       uint32_t bph = 0;
+      const int ncb = p.cpad >> 6;
       for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
         for (int g = 0; g < groups; ++g)
-          for (int tap = 0; tap < TAPS; ++tap) {
+          for (int k = 0; k < TAPS; ++k) {
+            int tap = k, cb = g;
+            if constexpr (S == 2) {  // the quadrant's taps (ky, kx) = (2dy + py, 2dx + px), MMA order
+              const int qd = g / ncb;
+              const int py = qd >> 1, px = qd & 1;
+              const int ndx = 2 - px;
+              if (k >= (2 - py) * ndx) break;
+              const int dy = k / ndx, dx = k - dy * ndx;
+              tap = (2 * dy + py) * 3 + 2 * dx + px;
+              cb = g - qd * ncb;
+            }
             mbar_wait(&bempty[bs], bph ^ 1);
             if (p.dbg & 512) {  // ablation: no weight traffic
               mbar_arrive(&bfull[bs]);
             } else {
               mbar_arrive_expect_tx(&bfull[bs], p.b_block_bytes);
-              tma_load_2d(&tmW, &bfull[bs], sB + bs * p.b_block_bytes, tap * p.cpad + g * 64, 0);
+              tma_load_2d(&tmW, &bfull[bs], sB + bs * p.b_block_bytes, tap * p.cpad + cb * 64, 0);
             }
             if (++bs == p.b_stages) {
               bs = 0;
@@ -308,9 +435,9 @@ __global__ void __maxnreg__(96)
       const int r0 = q * 32;
       bool store_ok = true;
       if (p.ipt > 1) {  // this warp's rows lie in stacked image i (host: H + 1 a multiple of the box rows)
-        const int i = (r0 / WP) / (p.H + 1);
+        const int i = (r0 / WP) / (p.Ho + 1);
         img = t * p.ipt + i;
-        y0 = -i * (p.H + 1);
+        y0 = -i * (p.Ho + 1);
         store_ok = i < p.ipt;
       }
       const int ox = r0 % WP;
@@ -412,13 +539,18 @@ long long* g_halo_trace = nullptr;
 
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
   *handled = false;
-  if (d->kh != 3 || d->kw != 3 || d->stride != 1 || d->pad != 1 || d->x_nchw_f32 || d->gather_idx ||
-      d->residual || d->y_dtype != UB_BF16 || (d->variant & 8))
+  if (d->kh != 3 || d->kw != 3 || (d->stride != 1 && d->stride != 2) || d->pad != 1 || d->x_nchw_f32 ||
+      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8))
     return UB_OK;
+  const int S = d->stride;
   if (cpad != 16 && cpad != 32 && cpad % 64 != 0) return UB_OK;
+  if (S == 2 && (cpad % 64 != 0 || lead != 0)) return UB_OK;  // a folded plane = 8 channels of one pixel
   if (d->cout > 256 || d->y_cstride % 8 || d->y_coff % 8) return UB_OK;
+  const int Ho = d->Ho;
   int Wp = 8;
-  while (Wp < d->W + 1) Wp <<= 1;  // one zero column: the right pad of a row is the left pad of the next
+  // stride 1: one zero column (the right pad of a row is the left pad of the next); stride 2:
+  // folded columns 0 .. Wo (origin -1)
+  while (Wp < d->Wo + 1) Wp <<= 1;
   if (Wp > 64) return UB_OK;
   HaloParams p{};
   p.x = reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
@@ -426,28 +558,37 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   p.N = d->N;
   p.H = d->H;
   p.W = d->W;
+  p.Ho = Ho;
   p.Wp = Wp;
   p.wp_shift = __builtin_ctz(Wp);
   p.R = 128 / Wp;
-  p.groups = cpad > 64 ? cpad / 64 : 1;
+  p.groups = S == 2 ? 4 * (cpad / 64) : (cpad > 64 ? cpad / 64 : 1);
   p.planes = p.groups > 1 ? 8 : cpad / 8;
   p.np = (d->cout + 15) / 16 * 16;
   p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
   // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
-  const int mt = (d->H > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
+  const int mt = (Ho > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
   p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
   p.ngroups = (d->variant & 128) ? 2 : HALO_EPI_WARPS / 4;
   // chunks dealt to all groups when every group gets one (shorter drain per tile), else whole tiles
   p.drainers = (mt * ((p.np + 63) / 64) >= p.ngroups && !(d->variant & 1024)) ? p.ngroups : 1;
   if (p.drainers == 1 && p.ngroups > p.nacc) p.ngroups = p.nacc;
-  p.n_pos = ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8;  // == HaloGeom<Wp, mt>::N_POS
+  p.n_pos = S == 1 ? ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8 : ((mt * p.R + 1) * Wp + 1 + 7) / 8 * 8;  // == N_POS
   p.plane_stride = p.n_pos * 16 + 16;               // == HaloGeom<Wp, mt>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
-  p.tiles_per_img = (d->H + mt * p.R - 1) / (mt * p.R);
+  // input by TMA boxes (AT) when a position's channels fill a 64- or 128-byte swizzle row
+  const bool at = (cpad == 32 || cpad % 64 == 0) && !(d->variant & 2048);
+  if (S == 2 && !at) return UB_OK;
+  const int kb = p.planes * 16;
+  if (at) {
+    const int staged_rows = S == 1 ? mt * p.R + 2 : mt * p.R + 1;
+    p.a_stage_bytes = static_cast<uint32_t>(((staged_rows * Wp + 8) * kb + 1023) & ~1023);
+  }
+  p.tiles_per_img = (Ho + mt * p.R - 1) / (mt * p.R);
   // small images: stack ipt of them per 128-row tile, one zero row between (a store box stays in one image)
   p.ipt = 1;
-  if (mt == 1 && (d->H + 1) * Wp <= 64 && (d->H + 1) % (32 / (Wp < 32 ? Wp : 32)) == 0 && !(d->variant & 256))
-    p.ipt = 128 / ((d->H + 1) * Wp);
+  if (mt == 1 && (Ho + 1) * Wp <= 64 && (Ho + 1) % (32 / (Wp < 32 ? Wp : 32)) == 0 && !(d->variant & 256))
+    p.ipt = 128 / ((Ho + 1) * Wp);
   const long long tiles =
       p.ipt > 1 ? (d->N + p.ipt - 1) / p.ipt : static_cast<long long>(d->N) * p.tiles_per_img;
   if (tiles >= (1ll << 31)) return UB_OK;
@@ -496,15 +637,18 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   apply_small_tensor_quirk(&tm, static_cast<size_t>(d->N) * d->Ho * d->Wo * d->y_cstride * 2);
 
   const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
-  void (*kern)(const CUtensorMap, const CUtensorMap, const HaloParams) = nullptr;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const HaloParams) = nullptr;
   const bool sb = p.groups > 1;
-#define UB_HALO_CASE(WPV, PL, SBV)                                                                \
-  if (Wp == WPV && p.planes == PL && sb == SBV) kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV> \
-                                                               : conv_halo3_kernel<WPV, PL, 1, SBV>;
-  UB_HALO_CASE(8, 2, false) UB_HALO_CASE(8, 4, false) UB_HALO_CASE(8, 8, false) UB_HALO_CASE(8, 8, true)
-  UB_HALO_CASE(16, 2, false) UB_HALO_CASE(16, 4, false) UB_HALO_CASE(16, 8, false) UB_HALO_CASE(16, 8, true)
-  UB_HALO_CASE(32, 2, false) UB_HALO_CASE(32, 4, false) UB_HALO_CASE(32, 8, false) UB_HALO_CASE(32, 8, true)
-  UB_HALO_CASE(64, 2, false) UB_HALO_CASE(64, 4, false) UB_HALO_CASE(64, 8, false) UB_HALO_CASE(64, 8, true)
+#define UB_HALO_CASE(WPV, PL, SBV, SV, ATV)                                                     \
+  if (Wp == WPV && p.planes == PL && sb == SBV && S == SV && at == ATV)                         \
+    kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV> : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV>;
+#define UB_HALO_WP(WPV)                                                                                    \
+  UB_HALO_CASE(WPV, 2, false, 1, false) UB_HALO_CASE(WPV, 4, false, 1, false)                              \
+  UB_HALO_CASE(WPV, 4, false, 1, true) UB_HALO_CASE(WPV, 8, false, 1, false)                               \
+  UB_HALO_CASE(WPV, 8, false, 1, true) UB_HALO_CASE(WPV, 8, true, 1, false) UB_HALO_CASE(WPV, 8, true, 1, true) \
+  UB_HALO_CASE(WPV, 8, true, 2, true)
+  UB_HALO_WP(8) UB_HALO_WP(16) UB_HALO_WP(32) UB_HALO_WP(64)
+#undef UB_HALO_WP
 #undef UB_HALO_CASE
   if (!kern) return UB_OK;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -519,7 +663,24 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rw != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo weight tensor map failed (%d)", (int)rw);
   }
-  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, tmw, p);
+  CUtensorMap tmx{};
+  if (at) {  // input [N][H][W][lead + cin] (channels past the slice read as zeros), one box per group
+    const int box_rows = p.ipt > 1 ? (S == 1 ? d->H + 2 : 2 * (Ho + 1)) : (S == 1 ? mt * p.R + 2 : 2 * (mt * p.R + 1));
+    p.a_box_bytes = static_cast<uint32_t>(kb) * Wp * (box_rows / S);
+    const cuuint64_t xs = static_cast<cuuint64_t>(d->x_cstride) * 2;
+    cuuint64_t xd[4] = {static_cast<cuuint64_t>(lead + d->cin), static_cast<cuuint64_t>(d->W),
+                        static_cast<cuuint64_t>(d->H), static_cast<cuuint64_t>(d->N)};
+    cuuint64_t xst[3] = {xs, xs * d->W, xs * d->W * d->H};
+    cuuint32_t xb[4] = {static_cast<cuuint32_t>(kb / 2), static_cast<cuuint32_t>(S * Wp),
+                        static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t xe[4] = {1, static_cast<cuuint32_t>(S), static_cast<cuuint32_t>(S), 1};
+    CUresult rx = encode_tiled_fn()(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(p.x), xd, xst,
+                                    xb, xe, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rx != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo input tensor map failed (%d)", (int)rx);
+  }
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, tmw, tmx, p);
   count_launch();
   *handled = true;
   if (e != cudaSuccess) {

@@ -69,6 +69,14 @@ CASES = [
     ("halo_c64_w7_stack_n3", 3, 7, 7, 64, 0, 64, 96, 3, 1, 1, 0, True, False, True, False),
     ("halo_c32_h3_w5_stack4_n5", 5, 3, 5, 32, 0, 32, 64, 3, 1, 1, 0, True, False, False, False),
     ("halo_c256_w7_stack_n5", 5, 7, 7, 264, 8, 256, 200, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c128_w15_h20_wrap", 2, 20, 15, 128, 0, 128, 64, 3, 1, 1, 0, True, False, True, False),
+    ("halo_c32_w31_tma_sw64", 2, 9, 31, 32, 0, 32, 48, 3, 1, 1, 0, True, False, False, False),
+    # stride-2 halo: 2x2 conv over the on-the-fly 2x2-folded input
+    ("halo_s2_c64_w56", 2, 56, 56, 64, 0, 64, 64, 3, 2, 1, 0, True, False, True, False),
+    ("halo_s2_c128_w28_cout100", 2, 28, 28, 128, 0, 128, 100, 3, 2, 1, 0, True, False, False, False),
+    ("halo_s2_c256_w14_stack_n3", 3, 14, 14, 256, 0, 256, 256, 3, 2, 1, 0, True, False, True, False),
+    ("halo_s2_c64_h15_w13_odd", 2, 15, 13, 64, 0, 64, 32, 3, 2, 1, 0, False, False, True, False),
+    ("halo_s2_c100_slice_w20", 2, 20, 20, 192, 64, 100, 48, 3, 2, 1, 0, True, False, True, False),
 ]
 
 

@@ -34,6 +34,9 @@ CASES = {
     "l1_conv2_3x3": (256, 56, 56, 64, 0, 32, 64, 3, 1, 1, 0, False, True),
     "l2_down_gather_s2": (256, 56, 56, 240, 0, 237, 512, 1, 2, 0, 128, False, False),
     "l3_conv2_3x3s2": (256, 28, 28, 128, 0, 128, 256, 3, 2, 1, 0, False, True),
+    "r50_l2_0_conv2_s2": (256, 56, 56, 64, 0, 64, 64, 3, 2, 1, 0, False, True),
+    "r50_l3_0_conv2_s2": (256, 28, 28, 128, 0, 128, 128, 3, 2, 1, 0, False, True),
+    "r50_l4_0_conv2_s2": (256, 14, 14, 256, 0, 256, 256, 3, 2, 1, 0, False, True),
     "stem_7x7": (256, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),
     "l4_conv3": (256, 7, 7, 256, 0, 256, 2048, 1, 1, 0, 0, True, True),
     "l4_down_r18": (4, 14, 14, 232, 66, 128, 390, 1, 2, 0, 0, False, False),
