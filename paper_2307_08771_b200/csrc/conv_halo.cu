@@ -677,7 +677,8 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
     CUresult rx = encode_tiled_fn()(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(p.x), xd, xst,
                                     xb, xe, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                     kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                    a_promo(d->x_coff - lead == 0 && cpad >= d->x_cstride),
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rx != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_fwd: encode halo input tensor map failed (%d)", (int)rx);
   }
   const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(HALO_THREADS), smem, stream, tm, tmw, tmx, p);

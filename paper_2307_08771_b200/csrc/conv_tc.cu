@@ -818,6 +818,18 @@ extern "C" int ub_conv_weight_layout2(int cin, int coff, int gather, int kh, int
 
 extern "C" int ub_conv_stem_kpad(int cin, int kh, int kw) { return (kh * kw * cin + 63) / 64 * 64; }
 
+// L2 sector promotion of the activation / residual maps.  A channel slice of a wider row (e.g.
+// 128 of 240 channels) is not 256-byte aligned, and 256-byte promotion fetches the neighbouring
+// slices too: 64 B there (measured 0.65 -> 0.86 of the HBM roofline for a 128-of-240 slice);
+// rows read whole keep 256 B (better for them).  UB_A_PROMO (0 none, 1 64 B, 2 128 B, 3 256 B)
+// overrides.
+CUtensorMapL2promotion ub::a_promo(bool whole_rows) {
+  static int v = -2;
+  if (v == -2) v = getenv("UB_A_PROMO") ? atoi(getenv("UB_A_PROMO")) : -1;
+  if (v >= 0) return static_cast<CUtensorMapL2promotion>(v);
+  return whole_rows ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+}
+
 extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   if (!d) return fail(UB_EINVAL, "ub_conv_fwd: null descriptor");
   if (!d->x || !d->w || !d->y) return fail(UB_EINVAL, "ub_conv_fwd: null x/w/y");
@@ -996,21 +1008,24 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   // 1x1/s1 (tiled) A and the residual by TMA as well
   CUtensorMap tmA{}, tmR{};
   if (p.a_tma) {
-    auto enc = [&](CUtensorMap* m, const void* base, int cstride, int cols, int box_c) -> CUresult {
+    auto enc = [&](CUtensorMap* m, const void* base, int cstride, int cols, int box_c, bool whole) -> CUresult {
       cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(p.M)};
       cuuint64_t strides[1] = {static_cast<cuuint64_t>(cstride) * 2};
       cuuint32_t box[2] = {static_cast<cuuint32_t>(box_c), BLOCK_M};
       cuuint32_t es[2] = {1, 1};
       CUresult r = encode_tiled_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(box_c * 2),
-                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                     a_promo(whole), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       apply_small_tensor_quirk(m, static_cast<size_t>(p.M) * cstride * 2);
       return r;
     };
     // A: channels [coff - lead, x_cstride) of every pixel row (beyond: zero fill)
-    if (enc(&tmA, p.x, d->x_cstride, d->x_cstride - (d->x_coff - lead), bk) != CUDA_SUCCESS)
+    const bool a_whole = d->x_coff - lead == 0 && cpad >= d->x_cstride;
+    if (enc(&tmA, p.x, d->x_cstride, d->x_cstride - (d->x_coff - lead), bk, a_whole) != CUDA_SUCCESS)
       return fail(UB_ECUDA, "ub_conv_fwd: encode activation tensor map failed");
-    if (p.has_res && enc(&tmR, p.res, d->res_cstride, d->res_cstride - d->res_coff, EPI_CHUNK) != CUDA_SUCCESS)
+    const bool r_whole = d->res_coff == 0 && d->cout + 8 > d->res_cstride;
+    if (p.has_res &&
+        enc(&tmR, p.res, d->res_cstride, d->res_cstride - d->res_coff, EPI_CHUNK, r_whole) != CUDA_SUCCESS)
       return fail(UB_ECUDA, "ub_conv_fwd: encode residual tensor map failed");
   }
   const int num_tiles = p.m_tiles * p.n_tiles;

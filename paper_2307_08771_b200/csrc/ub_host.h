@@ -72,4 +72,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// L2 promotion for activation tensor maps (conv_tc.cu): 256 B for rows read whole, else 64 B.
+CUtensorMapL2promotion a_promo(bool whole_rows);
+
 }  // namespace ub

@@ -445,9 +445,9 @@ class Engine:
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
         # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
         # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path;
-        # +8 no halo-tile kernel for a stride-1 3x3; +128 halo kernel with two epilogue groups)
+        # +8 no halo-tile kernel for a 3x3 (stride 1 or 2); +128 halo kernel with two epilogue groups)
         tiled = kk == 1 and st == 1
-        halo = kk == 3 and st == 1 and pd == 1
+        halo = kk == 3 and st in (1, 2) and pd == 1
         gen = [pw | nb | bt | at | e1 for pw in (1, 2) for nb in (0, 4) for bt in (0, 16)
                for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
         if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel

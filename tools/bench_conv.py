@@ -30,6 +30,12 @@ CASES = {
     "l1_conv1_gather": (256, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, False, True),
     "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_dense": (256, 56, 56, 128, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs248": (256, 56, 56, 248, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs256": (256, 56, 56, 256, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs256_off64": (256, 56, 56, 256, 64, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs288": (256, 56, 56, 288, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs320": (256, 56, 56, 320, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "l1_conv1_cs512": (256, 56, 56, 512, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_c32": (256, 56, 56, 240, 0, 128, 32, 1, 1, 0, 0, False, True),
     "l1_conv2_3x3": (256, 56, 56, 64, 0, 32, 64, 3, 1, 1, 0, False, True),
     "l2_down_gather_s2": (256, 56, 56, 240, 0, 237, 512, 1, 2, 0, 128, False, False),
