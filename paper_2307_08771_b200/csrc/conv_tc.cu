@@ -97,6 +97,8 @@ struct ConvKParams {
   int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
   int a_tma;         // tiled mode: A and residual k-blocks by TMA too (one producer thread)
   int epi2;          // (a_tma only) idle producer warps 12-15 form a second epilogue group
+  int epi_alt;       // (epi2, one 64-channel chunk per tile) the groups take alternate tiles
+                     // (group g drains accumulator g) instead of alternate chunks
 };
 #define UB_TRACE(slot)                                                                  \
   do {                                                                                  \
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], epi_warps);
+      mbar_init(&tempty[a], p.epi_alt ? 4 : epi_warps);
     }
     mbar_init(bres, p.a_tma ? 1 : PRODUCERS);
     fence_mbar_init();
@@ -620,12 +622,13 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     };
     // initial arming of both accumulators (tiles blockIdx.x and blockIdx.x + gridDim.x)
     for (int a = 0; a < 2; ++a) {
+      if (p.epi_alt && a != eg) continue;
       const int tt = blockIdx.x + a * gridDim.x;
       if (tt < num_tiles) {
         stage_bias(tt);
         const uint32_t ta = tmem_base + a * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
         for (int col = 0; col < static_cast<int>(p.acc_stride); col += 32)
-          if ((col / EPI_CHUNK) % ngrp == eg) arm32(ta + col, col);
+          if (p.epi_alt || (col / EPI_CHUNK) % ngrp == eg) arm32(ta + col, col);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -633,7 +636,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
     int it = 0;
+    const int c0 = p.epi_alt ? 0 : eg, cstep = p.epi_alt ? 1 : ngrp;  // this warp's chunks of a tile
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      if (p.epi_alt && (it & 1) != eg) continue;
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
       const int m0 = m_tile * BLOCK_M;
@@ -642,20 +647,24 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       const int nchunks = (ncols + EPI_CHUNK - 1) / EPI_CHUNK;
       const int t_next = t + 2 * gridDim.x;  // next user of this accumulator
       const bool rearm = t_next < num_tiles;
-      if (rearm) stage_bias(t_next);
+      if (rearm && p.n_tiles > 1) stage_bias(t_next);  // (one N tile: every tile's bias is the same)
       const int acc = it & 1;
       if (ew == 0) UB_TRACE(3);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       if (ew == 0) UB_TRACE(4);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = eg; c < nchunks; c += ngrp, ++ec) {
+      for (int c = c0; c < nchunks; c += cstep, ++ec) {
         uint8_t* oslot = oslots + (ec & 1) * EPI_SLOT;
         if (tma && lane == 0) bulk_wait_read<1>();  // this slot's store from 2 chunks ago has read it
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // two 32-column halves
           const int col = c * EPI_CHUNK + h * 32;
+          if (col >= ncols) {  // past cout: nothing to store (the TMA store clips these channels)
+            if (rearm) arm32(taddr + col, col);
+            continue;
+          }
           uint32_t r[32];
           tmem_ld32(taddr + col, r);
           tmem_ld_wait();
@@ -717,7 +726,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       // re-arm the columns past this tile's last chunk (the next user may be wider)
       if (rearm)
         for (int col = nchunks * EPI_CHUNK; col < static_cast<int>(p.acc_stride); col += 32)
-          if ((col / EPI_CHUNK) % ngrp == eg) arm32(taddr + col, col);
+          if (p.epi_alt || (col / EPI_CHUNK) % ngrp == eg) arm32(taddr + col, col);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -958,6 +967,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const bool tiled_1x1 = !stem && !packed && !gather && d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   p.a_tma = tiled_1x1 && !(d->variant & 32);
   p.epi2 = p.a_tma && !(d->variant & 64);
+  p.epi_alt = p.epi2 && p.block_n <= EPI_CHUNK && !(d->variant & 4096);
   const int epi_warps = p.epi2 ? 8 : 4;
   uint32_t fixed = 1024 + IDENT_BYTES + epi_warps * EPI_WARP_BYTES + epi_warps * MAX_BLOCK_N * 4 + BAR_BYTES +
                    ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);

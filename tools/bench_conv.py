@@ -30,6 +30,8 @@ CASES = {
     "l1_conv1_gather": (256, 56, 56, 240, 0, 237, 64, 1, 1, 0, 128, False, True),
     "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_dense": (256, 56, 56, 128, 0, 128, 64, 1, 1, 0, 0, False, True),
+    "r50_l1_0_conv1": (256, 56, 56, 56, 0, 32, 32, 1, 1, 0, 0, False, True),
+    "r50_l1_0_down": (256, 56, 56, 56, 17, 32, 237, 1, 1, 0, 0, False, False),
     "l1_conv1_cs248": (256, 56, 56, 248, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_cs256": (256, 56, 56, 256, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_cs256_off64": (256, 56, 56, 256, 64, 128, 64, 1, 1, 0, 0, False, True),
