@@ -87,6 +87,16 @@ int ub_permute_vector(const void* v, int dtype, const int32_t* idx, int n, void*
 int ub_channel_gather(const void* x, int x_cstride, int x_coff, const int32_t* idx, int n,
                       long long npix, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
+/*
+ * Channel gather fused with the pixel subsampling of a strided 1x1 conv that reads it:
+ * y[n][yo][xo][i] = x[n][yo*stride][xo*stride][x_coff + idx[i]] (idx[i] < 0: 0), for i < n_idx,
+ * and zeros for n_idx <= i < pad8(n_idx).  Output pixels are ceil(H/stride) x ceil(W/stride);
+ * y_cstride, y_coff multiples of 8.  Lets the conv that follows run as a dense 1x1 / stride-1
+ * GEMM over a compact operand (the engine's "copy" read plan).
+ */
+int ub_channel_gather_2d(const void* x, int x_cstride, int x_coff, const int32_t* idx, int n_idx, int N, int H,
+                         int W, int stride, void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
 /* K-chunk and padded per-tap K of the GEMM weight layout ub_conv_fwd expects for a
  * read of `cin` channels starting at channel offset `coff` (TMA needs 16-byte
  * aligned bases, so a misaligned SLICE start is rounded down and the first

@@ -62,6 +62,8 @@ SIGNATURES = {
                                    c_vp, c_int, c_int, c_int, c_vp, c_int, c_vp]),
     "ub_permute_vector": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp]),
     "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
+    "ub_channel_gather_2d": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int,
+                                     c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),

@@ -142,6 +142,41 @@ __global__ void channel_gather_kernel(const uint16_t* __restrict__ x, int x_cstr
   }
 }
 
+// Gather + pixel subsample: one warp per output pixel, 8 output channels (one 16-byte store)
+// per lane and step; the index list sits in shared memory and the source row's sectors are
+// shared through L1 by the lanes' 2-byte loads.
+__global__ void __launch_bounds__(256) channel_gather_2d_kernel(const uint16_t* __restrict__ x, int x_cstride,
+                                                                 int x_coff, const int32_t* __restrict__ idx,
+                                                                 int n_idx, int n8, int N, int H, int W, int stride,
+                                                                 int Ho, int Wo, uint16_t* __restrict__ y,
+                                                                 int y_cstride, int y_coff) {
+  extern __shared__ int32_t sidx[];
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) sidx[i] = i < n_idx ? __ldg(idx + i) : -1;
+  __syncthreads();
+  griddep_wait();
+  griddep_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const long long npix = static_cast<long long>(N) * Ho * Wo;
+  for (long long p = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5); p < npix;
+       p += static_cast<long long>(gridDim.x) * 8) {
+    const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
+    const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+    const int yo = r / Wo, xo = r - (r / Wo) * Wo;
+    const uint16_t* xr = x + ((static_cast<size_t>(n) * H + yo * stride) * W + xo * stride) * x_cstride + x_coff;
+    uint16_t* yr = y + static_cast<size_t>(p) * y_cstride + y_coff;
+    for (int i = lane * 8; i < n8; i += 256) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int a = sidx[i + 2 * j], b = sidx[i + 2 * j + 1];
+        const uint32_t lo = a >= 0 ? __ldg(xr + a) : 0u, hi = b >= 0 ? __ldg(xr + b) : 0u;
+        w[j] = lo | (hi << 16);
+      }
+      *reinterpret_cast<uint4*>(yr + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 // ------------------------------------------------------------- input staging
 // NCHW fp32 -> NHWC bf16 (channel-gathered), zero-filling the padded channels.
 __global__ void stage_input_kernel(const float* __restrict__ x, int N, int C, int HW, const int32_t* __restrict__ idx,
@@ -325,6 +360,26 @@ extern "C" int ub_channel_gather(const void* x, int x_cstride, int x_coff, const
                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "channel_gather_kernel");
+}
+
+extern "C" int ub_channel_gather_2d(const void* x, int x_cstride, int x_coff, const int32_t* idx, int n_idx, int N,
+                                    int H, int W, int stride, void* y, int y_cstride, int y_coff,
+                                    cudaStream_t stream) {
+  if (!x || !idx || !y || n_idx < 1 || N < 1 || H < 1 || W < 1 || stride < 1)
+    return fail(UB_EINVAL, "ub_channel_gather_2d: bad arguments");
+  const int n8 = (n_idx + 7) / 8 * 8;
+  if ((y_cstride & 7) || (y_coff & 7) || y_coff + n8 > y_cstride || !aligned16(y))
+    return fail(UB_EINVAL, "ub_channel_gather_2d: output rows must hold pad8(n) 16-byte aligned channels");
+  if (n8 > 8192) return fail(UB_EUNSUPPORTED, "ub_channel_gather_2d: %d channels", n_idx);
+  const int Ho = (H + stride - 1) / stride, Wo = (W + stride - 1) / stride;
+  const long long npix = static_cast<long long>(N) * Ho * Wo;
+  const long long want = (npix + 7) / 8;
+  const int grid = static_cast<int>(want < 148LL * 16 ? want : 148LL * 16);
+  const cudaError_t e = launch_pdl(channel_gather_2d_kernel, dim3(grid), dim3(256), n8 * sizeof(int32_t), stream,
+                                   static_cast<const uint16_t*>(x), x_cstride, x_coff, idx, n_idx, n8, N, H, W,
+                                   stride, Ho, Wo, static_cast<uint16_t*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(e, "channel_gather_2d_kernel");
 }
 
 extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n, void* y,

@@ -416,20 +416,33 @@ class Engine:
         #                   reference's
         #   ("cover", ...)  the gather's covering window read as a slice, with zero weight columns
         #                   for the channels the gather drops (same result; cp.async operand path)
+        #   ("copy", ...)   1x1 gathers: one kernel gathers the channels (and the strided pixels)
+        #                   into a compact buffer, then a dense 1x1 / stride-1 GEMM over it -- half
+        #                   the MMA work of "cover" when half the channels are kept
         plans = []
 
-        def add_plan(kind, xv, gidx, wcols, width):
+        def add_plan(kind, xv, gidx, wcols, width, pre=None, st_eff=None):
             lead, cpad = _lib.conv_weight_layout(width, xv.coff, gidx is not None, kk, kk)
             wg = K.permute_weights(W, rows, wcols, row_scale=scale, layout="gemm", lead=lead, cpad=cpad,
                                    out_dtype=torch.bfloat16)
             self._keep.append(wg)
-            plans.append((kind, xv, gidx, lead, cpad, wg))
+            plans.append((kind, xv, gidx, lead, cpad, wg, pre, st if st_eff is None else st_eff))
 
         if gather is None:
             add_plan("slice", x, None, cols, cin)
         else:
             k_order = sorted(range(cin), key=lambda k: (gather[k], k))
             add_plan("gather", x, self._i32([gather[k] for k in k_order]), [cols[k] for k in k_order], cin)
+            if kk == 1 and pd == 0 and self.gather_mode == "fused":
+                ho, wo = (x.H - 1) // st + 1, (x.W - 1) // st + 1
+                scratch = K.empty_act(self.batch, ho, wo, cin, self.device)
+                self._keep.append(scratch.buf)
+                gdev = self._i32(list(gather))
+
+                def pre(x=x, gdev=gdev, scratch=scratch):
+                    K.channel_gather_2d(x, gdev, st, scratch)
+
+                add_plan("copy", scratch, None, cols, cin, pre=pre, st_eff=1)
             lo, hi = min(gather), max(gather)
             width = hi - lo + 1
             if (self.gather_mode == "fused" and lo >= 0 and len(set(gather)) == cin
@@ -446,20 +459,26 @@ class Engine:
         # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
         # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path;
         # +8 no halo-tile kernel for a 3x3 (stride 1 or 2); +128 halo kernel with two epilogue groups)
-        tiled = kk == 1 and st == 1
         halo = kk == 3 and st in (1, 2) and pd == 1
-        gen = [pw | nb | bt | at | e1 for pw in (1, 2) for nb in (0, 4) for bt in (0, 16)
-               for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
-        if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
-            gen = [0, 128] + [v | 8 for v in gen]
-        op.info["variants"] = [(pi, v) for pi in range(len(plans)) for v in gen]
+
+        def gen_for(st_p):
+            tiled = kk == 1 and st_p == 1
+            gen = [pw | nb | bt | at | e1 for pw in (1, 2) for nb in (0, 4) for bt in (0, 16)
+                   for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
+            if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
+                gen = [0, 128] + [v | 8 for v in gen]
+            return gen
+
+        op.info["variants"] = [(pi, v) for pi, pl in enumerate(plans) for v in gen_for(pl[7])]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
 
         def launch():
             pi, pw = op.info["variant"]
-            _, xv, gidx, lead, cpad, wg = plans[pi]
-            K.conv(xv, wg, lead, cpad, cout, kk, kk, st, pd, y, gather_idx=gidx, bias=bias, residual=residual,
+            _, xv, gidx, lead, cpad, wg, pre, st_p = plans[pi]
+            if pre is not None:
+                pre()
+            K.conv(xv, wg, lead, cpad, cout, kk, kk, st_p, pd, y, gather_idx=gidx, bias=bias, residual=residual,
                    relu=relu, y_fp32=fp32_out, variant=pw)
 
         op.launch = launch

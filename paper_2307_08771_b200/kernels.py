@@ -119,6 +119,13 @@ def channel_gather(x: Act, idx_dev: torch.Tensor, y: Act) -> None:
               x.npix, _p(y.buf), y.cstride, y.coff, _stream())
 
 
+def channel_gather_2d(x: Act, idx_dev: torch.Tensor, stride: int, y: Act) -> None:
+    """Gather channels idx of every stride-th pixel of x into the compact y (the "copy" read
+    plan of a strided / gathered 1x1 conv)."""
+    _lib.call("ub_channel_gather_2d", _p(x.buf), x.cstride, x.coff, _p(idx_dev), idx_dev.numel(), x.N, x.H, x.W,
+              stride, _p(y.buf), y.cstride, y.coff, _stream())
+
+
 def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: int, stride: int, pad: int,
          y: Act, gather_idx: torch.Tensor | None = None, bias: torch.Tensor | None = None,
          residual: Act | None = None, relu: bool = False, y_fp32: bool = False, variant: int = 0) -> None:

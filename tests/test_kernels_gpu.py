@@ -254,6 +254,31 @@ def test_permute_weights_bit_exact():
     assert torch.equal(out.cpu(), ref)
 
 
+@pytest.mark.parametrize("N,H,W,cs,coff,idx,stride", [
+    (2, 9, 9, 40, 0, [5, 3, -1, 39, 0, 17, 18], 1),
+    (3, 14, 14, 64, 8, [1, 2, 3, 50, 7, 9, 11, 13, 40, 41], 2),
+    (2, 7, 5, 1024, 16, list(range(0, 1000, 3)), 2),
+])
+def test_channel_gather_2d(N, H, W, cs, coff, idx, stride):
+    """Gather + stride subsample into a compact buffer: bit-exact, zero-padded to pad8(n)."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(N + H + len(idx))
+    x = torch.randn(N, cs, H, W, generator=g)
+    xa = K.act_from_nchw(x.to(dev)).view(coff, cs - coff)
+    idx_t = torch.tensor(idx, dtype=torch.int32)
+    Ho, Wo = (H - 1) // stride + 1, (W - 1) // stride + 1
+    y = K.empty_act(N, Ho, Wo, len(idx), dev)
+    y.buf.fill_(float("nan"))
+    K.channel_gather_2d(xa, idx_t.to(dev), stride, y)
+    torch.cuda.synchronize()
+    ref = torch.zeros(N, K.pad8(len(idx)), Ho, Wo)
+    for i, j in enumerate(idx):
+        if j >= 0:
+            ref[:, i] = _bf(x[:, coff + j, ::stride, ::stride])
+    got = y.buf.float().reshape(N, Ho, Wo, -1).permute(0, 3, 1, 2).cpu()
+    assert torch.equal(got, ref)
+
+
 def test_channel_gather_and_pools():
     dev = "cuda"
     g = torch.Generator().manual_seed(1)
