@@ -49,7 +49,7 @@ extern "C" {
 const char* ub_last_error(void);
 
 /* ABI version (bumped on any signature change). */
-int ub_abi_version(void); /* 4 */
+int ub_abi_version(void); /* 5 */
 
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (used by bench.py's gpu_launches claim). */
@@ -143,7 +143,19 @@ typedef struct {
                                   bit 7: halo kernel with two epilogue groups (default: up to three);
                                   bit 4: weights by cp.async instead of one TMA box per K-block;
                                   bit 5: 1x1/s1 activations and residual by cp.async, not TMA;
-                                  bit 6: one epilogue warpgroup (not two) on the TMA-fed 1x1 path */
+                                  bit 6: one epilogue warpgroup (not two) on the TMA-fed 1x1 path;
+                                  bit 8: no stacked small images in the halo kernel;
+                                  bit 11: halo input by cp.async planes instead of TMA boxes;
+                                  bit 12: narrow tiles drained by alternate chunks, not tiles */
+  /* Optional second, compacted store of the output (the producer side of a GATHER read by
+   * a later 1x1 conv): y2[m][y2_map[c]] = y[m][y_coff + c] for every c with y2_map[c] >= 0.
+   * Layout contract: the kept channels of each 64-channel group [64g, 64g + 64) take
+   * consecutive columns starting at a multiple of 8; the columns up to the next multiple of 8
+   * are written as zeros.  The consumer runs as a dense GEMM over y2 (bf16, row pitch
+   * y2_cstride % 8 == 0, 16-byte aligned).  Needs the TMA epilogue (bf16 y, aligned). */
+  void* y2;
+  int y2_cstride;
+  const int32_t* y2_map;       /* [cout] or NULL */
 } ub_conv_desc;
 
 /* Dense-K padding (multiple of 64) of the fused-stem weight operand. */

@@ -49,6 +49,7 @@ class ConvDesc(ctypes.Structure):
         ("y_dtype", c_int),
         ("x_nchw_f32", c_int), ("x_channels", c_int),
         ("variant", c_int),
+        ("y2", c_vp), ("y2_cstride", c_int), ("y2_map", c_vp),
     ]
 
 

@@ -540,7 +540,7 @@ long long* g_halo_trace = nullptr;
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
   *handled = false;
   if (d->kh != 3 || d->kw != 3 || (d->stride != 1 && d->stride != 2) || d->pad != 1 || d->x_nchw_f32 ||
-      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8))
+      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8) || d->y2)
     return UB_OK;
   const int S = d->stride;
   if (cpad != 16 && cpad != 32 && cpad % 64 != 0) return UB_OK;

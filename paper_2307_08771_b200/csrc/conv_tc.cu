@@ -54,6 +54,8 @@ constexpr int BLOCK_M = 128;
 constexpr int EPI_CHUNK = 64;                 // output channels per epilogue chunk (128-byte rows)
 constexpr int EPI_SLOT = 32 * EPI_CHUNK * 2;  // one warp's 32 rows x 64 ch bf16 (4 KB)
 constexpr int EPI_WARP_BYTES = 2 * EPI_SLOT;  // two output slots per epilogue warp
+constexpr int Y2_PITCH = EPI_CHUNK + 8;        // compacted-store staging row (halves; 144 B: conflict-free)
+constexpr int Y2_STAGE = 32 * Y2_PITCH * 2;    // per epilogue warp
 constexpr int IDENT_BYTES = 64 * 128;         // 64x64 bf16 identity (SWIZZLE_128B, K-major)
 constexpr int MAX_BLOCK_N = 256;
 constexpr int BAR_BYTES = 512;   // mbarriers + TMEM slot region
@@ -97,6 +99,9 @@ struct ConvKParams {
   int b_tma;         // per-k-block weights by TMA (one box per stage) instead of cp.async
   int a_tma;         // tiled mode: A and residual k-blocks by TMA too (one producer thread)
   int epi2;          // (a_tma only) idle producer warps 12-15 form a second epilogue group
+  uint16_t* y2;           // compacted second store (ub_conv_desc.y2) or null
+  int y2_cstride;
+  const int32_t* y2_map;  // [cout] compact column of output channel c, -1 = not stored
   int epi_alt;       // (epi2, one 64-channel chunk per tile) the groups take alternate tiles
                      // (group g drains accumulator g) instead of alternate chunks
 };
@@ -152,7 +157,8 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   const int epi_warps = p.epi2 ? 8 : 4;
   uint8_t* sE = sI + IDENT_BYTES;                                          // epi_warps x 2 output slots
   float* sBias = reinterpret_cast<float*>(sE + epi_warps * EPI_WARP_BYTES);  // epi_warps x MAX_BLOCK_N
-  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + epi_warps * MAX_BLOCK_N);
+  uint16_t* sY2 = reinterpret_cast<uint16_t*>(sBias + epi_warps * MAX_BLOCK_N);  // y2 staging (when set)
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sY2) + (p.y2 ? epi_warps * Y2_STAGE : 0));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -721,6 +727,55 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
             tma_store_2d(&tmY, oslot, n0 + c * EPI_CHUNK, rows0);
             bulk_commit();
           }
+          if (p.y2) {
+            // compacted copy.  The kept channels of a 64-channel chunk occupy consecutive y2
+            // columns from an 8-aligned base (the caller's layout).  Phase 1 (lane = channel)
+            // packs each row's kept values into a staging row; phase 2 (lane = row) writes the
+            // row segment with 16-byte stores.
+            const int ch = n0 + c * EPI_CHUNK + lane;
+            const int pos0 = ch < p.cout ? __ldg(p.y2_map + ch) : -1;
+            const int pos1 = ch + 32 < p.cout ? __ldg(p.y2_map + ch + 32) : -1;
+            const uint32_t b0 = __ballot_sync(0xffffffffu, pos0 >= 0);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, pos1 >= 0);
+            const int k = __popc(b0) + __popc(b1);
+            if (k > 0) {
+              const int base = b0 ? __shfl_sync(0xffffffffu, pos0, __ffs(b0) - 1)
+                                  : __shfl_sync(0xffffffffu, pos1, __ffs(b1) - 1);
+              const uint32_t lt = (1u << lane) - 1u;
+              const int rank0 = __popc(b0 & lt), rank1 = __popc(b0) + __popc(b1 & lt);
+              uint16_t* stg = sY2 + ew * (Y2_STAGE / 2);
+              const uint32_t cb = (lane & 7) * 2;
+#pragma unroll 4
+              for (int r = 0; r < 32; ++r) {
+                if (pos0 >= 0)
+                  stg[r * Y2_PITCH + rank0] = *reinterpret_cast<const uint16_t*>(oslot + swz<64>(r, lane >> 3) + cb);
+                if (pos1 >= 0)
+                  stg[r * Y2_PITCH + rank1] =
+                      *reinterpret_cast<const uint16_t*>(oslot + swz<64>(r, 4 + (lane >> 3)) + cb);
+              }
+              __syncwarp();
+              const int m = rows0 + lane;
+              if (m < p.M) {
+                uint4* dst = reinterpret_cast<uint4*>(p.y2 + static_cast<size_t>(m) * p.y2_cstride + base);
+                const uint4* src = reinterpret_cast<const uint4*>(stg + lane * Y2_PITCH);
+                for (int g8 = 0; g8 * 8 < k; ++g8) {
+                  uint4 v = src[g8];
+                  const int valid = k - g8 * 8;  // zero the padding past the chunk's last kept channel
+                  if (valid < 8) {
+                    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                      if (2 * i >= valid) w[i] = 0u;
+                      else if (2 * i + 1 >= valid) w[i] &= 0xffffu;
+                    }
+                    v = make_uint4(w[0], w[1], w[2], w[3]);
+                  }
+                  dst[g8] = v;
+                }
+              }
+              __syncwarp();
+            }
+          }
         }
       }
       // re-arm the columns past this tile's last chunk (the next user may be wider)
@@ -961,6 +1016,14 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   if (p.has_res && (d->res_cstride % 8 || !aligned16(p.res)))
     return fail(UB_EINVAL, "ub_conv_fwd: residual rows must be 16-byte aligned (res_cstride, res_coff multiples of 8)");
   p.epi_tma = !p.y_f32 && d->y_cstride % 8 == 0 && aligned16(ybase);
+  if (d->y2) {
+    if (!p.epi_tma || !d->y2_map || d->y2_cstride % 8 || !aligned16(d->y2))
+      return fail(UB_EUNSUPPORTED, "ub_conv_fwd: the compacted second store needs the TMA epilogue (bf16, aligned)"
+                  " and a 16-byte aligned y2 with y2_cstride %% 8 == 0");
+    p.y2 = static_cast<uint16_t*>(d->y2);
+    p.y2_cstride = d->y2_cstride;
+    p.y2_map = d->y2_map;
+  }
 
   const uint32_t a_bytes = BLOCK_M * 128;  // sized for 64-wide residual k-blocks
   const uint32_t b_stride = (static_cast<uint32_t>(p.block_n) * bk * 2 + 1023u) & ~1023u;
@@ -970,6 +1033,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   p.epi_alt = p.epi2 && p.block_n <= EPI_CHUNK && !(d->variant & 4096);
   const int epi_warps = p.epi2 ? 8 : 4;
   uint32_t fixed = 1024 + IDENT_BYTES + epi_warps * EPI_WARP_BYTES + epi_warps * MAX_BLOCK_N * 4 + BAR_BYTES +
+                   (d->y2 ? epi_warps * Y2_STAGE : 0) +
                    ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
   // Weight-stationary B: when all k-blocks of one N tile fit next to >= 4 A stages, each CTA
   // keeps its N tile's weights in smem (grid a multiple of n_tiles, so a CTA's tiles share

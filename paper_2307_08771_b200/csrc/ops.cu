@@ -270,6 +270,50 @@ __global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, int HW, int 
   y[(long long)img * y_cstride + y_coff + c] = __float2bfloat16_rn(s / HW);
 }
 
+// 8 channels per thread (16-byte loads), the pixel loop unrolled so a thread has several
+// loads in flight; the fp32 sum is accumulated in pixel order (same result as the scalar
+// kernel).
+__global__ void avgpool8_kernel(const uint4* __restrict__ x, int HW, int C8, int x_cstride8, int x_coff8,
+                                uint4* __restrict__ y, int y_cstride8, int y_coff8) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int img = blockIdx.y;
+  const int c8 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c8 >= C8) return;
+  const uint4* xp = x + static_cast<long long>(img) * HW * x_cstride8 + x_coff8 + c8;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int p = 0;
+  for (; p + 7 <= HW; p += 7) {
+    uint4 v[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) v[u] = __ldg(xp + static_cast<long long>(p + u) * x_cstride8);
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = bf16x2_to_f32x2(w[j]);
+        s[2 * j] += f.x;
+        s[2 * j + 1] += f.y;
+      }
+    }
+  }
+  for (; p < HW; ++p) {
+    const uint4 v = __ldg(xp + static_cast<long long>(p) * x_cstride8);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = bf16x2_to_f32x2(w[j]);
+      s[2 * j] += f.x;
+      s[2 * j + 1] += f.y;
+    }
+  }
+  uint32_t o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o[j] = cvt_bf16x2(s[2 * j] / HW, s[2 * j + 1] / HW);
+  y[static_cast<long long>(img) * y_cstride8 + y_coff8 + c8] = make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // ------------------------------------------------------------- affine / add / relu
 __global__ void affine_add_relu_kernel(const __nv_bfloat16* __restrict__ a, int a_cstride, int a_coff,
                                        const float* __restrict__ scale, const float* __restrict__ shift,
@@ -533,6 +577,15 @@ extern "C" int ub_avgpool_global(const void* x, int N, int HW, int C, int x_cstr
                                  int y_cstride, int y_coff, cudaStream_t stream) {
   if (!x || !y || N < 1 || HW < 1 || C < 1) return fail(UB_EINVAL, "ub_avgpool_global: bad arguments");
   if (N > 65535) return fail(UB_EUNSUPPORTED, "ub_avgpool_global: N too large");
+  if (C % 8 == 0 && x_cstride % 8 == 0 && x_coff % 8 == 0 && y_cstride % 8 == 0 && y_coff % 8 == 0 && aligned16(x) &&
+      aligned16(y)) {
+    const int C8 = C / 8;
+    dim3 grid8((C8 + 127) / 128, N);
+    const cudaError_t e = launch_pdl(avgpool8_kernel, grid8, dim3(128), 0, stream, static_cast<const uint4*>(x), HW,
+                                     C8, x_cstride / 8, x_coff / 8, static_cast<uint4*>(y), y_cstride / 8, y_coff / 8);
+    count_launch();
+    return cuda_status(e, "avgpool8_kernel");
+  }
   dim3 grid((C + 127) / 128, N);
   const cudaError_t e = launch_pdl(avgpool_kernel, grid, dim3(128), 0, stream, static_cast<const __nv_bfloat16*>(x),
                                    HW, C, x_cstride, x_coff, static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);

@@ -61,12 +61,14 @@ class Engine:
 
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
-                 stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5):
+                 stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5,
+                 dual_store: bool = False):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
         self.stem_pool = stem_pool
         self.cover_ratio = cover_ratio
+        self.dual_store = dual_store
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -113,8 +115,8 @@ class Engine:
         s = self.graph.successors(lid)
         return s[0] if len(s) == 1 else None
 
-    def _alloc(self, vid: str, C: int, fp32: bool = False) -> K.Act:
-        _, h, w = self._shapes[vid]
+    def _alloc(self, vid: str, C: int, fp32: bool = False, shape_of: str | None = None) -> K.Act:
+        _, h, w = self._shapes[shape_of or vid]
         cs = K.pad8(C) if not fp32 else (C + 3) // 4 * 4
         buf = torch.zeros((self.batch * h * w, cs), dtype=torch.float32 if fp32 else torch.bfloat16,
                           device=self.device)
@@ -293,10 +295,37 @@ class Engine:
         self.input_buf = torch.zeros((self.batch, *self.input_chw), dtype=torch.float32, device=self.device)
         self.input_bufs = [self.input_buf]
         self._graphs: list = []
+        self._plan_dual_stores()
         for op in self.ops:
             getattr(self, f"_bind_{op.kind}")(op, weight_source, vector_source, output_feed)
         out_id = next(lid for lid in topo if kinds[lid] is LayerKind.OUTPUT)
         self.output_value = self._value(out_id)
+
+    def _plan_dual_stores(self) -> None:
+        """Producer side of GATHER reads: a conv whose output is gathered by later 1x1 convs
+        also stores the gathered channels compacted (ascending source order, the union when
+        several consumers gather different sets) in its epilogue (ub_conv_desc.y2); the
+        consumers are offered a dense "dual" read plan over that copy.  Off by default
+        (dual_store=False): the kept sets of the ResNet-50 export are fragmented (~0.8 runs
+        per channel), so the per-element compaction in the producer's epilogue costs more
+        (+60..160 us per producer) than the consumers save (-10..25 us each); DESIGN.md 5."""
+        self._dual: dict[str, list[int]] = {}
+        self._dual_bufs: dict[str, tuple] = {}
+        if self.gather_mode != "fused" or not self.dual_store:
+            return
+        need: dict[str, set] = {}
+        for op in self.ops:
+            if op.kind != "conv" or "stem_idx" in op.info or op.info["read"] is None:
+                continue
+            rl = self.graph.layer(op.info["read"])
+            spec = self.specs[op.info["conv"]]
+            kk = spec.kernel if spec.op == "conv" else 1
+            if rl.kind is LayerKind.GATHER and kk == 1:
+                need.setdefault(op.info["src"], set()).update(c for c in rl.params if c >= 0)
+        producers = {op.info["out"] for op in self.ops if op.kind == "conv" and "stem_idx" not in op.info}
+        for vid, chans in need.items():
+            if vid in producers and vid not in self._alias:
+                self._dual[vid] = sorted(chans)
 
     def _value(self, vid: str) -> K.Act:
         if vid in self.values:
@@ -450,9 +479,33 @@ class Engine:
                 pos = {c: k for k, c in enumerate(gather)}
                 wcols = [cols[pos[lo + j]] if (lo + j) in pos else -1 for j in range(width)]
                 add_plan("cover", x.view(lo, width), None, wcols, width)
+            if kk == 1 and info["src"] in self._dual_bufs:  # the producer's compacted copy
+                comp, col_of = self._dual_bufs[info["src"]]
+                pos = {c: k for k, c in enumerate(gather)}
+                wcols = [-1] * comp.C
+                for c, j in col_of.items():
+                    if c in pos:
+                        wcols[j] = cols[pos[c]]
+                add_plan("dual", comp, None, wcols, comp.C)
         residual = self._value(info["residual"]) if info.get("residual") else None
         fp32_out = info["out"] in output_feed
         y = self._alloc(info["out"], cout, fp32=fp32_out)
+        y2 = y2_map = None
+        if info["out"] in self._dual and not fp32_out:  # producer side of a later GATHER
+            # ub_conv_desc.y2 layout: each 64-channel group's kept channels consecutive from
+            # an 8-aligned column (zero columns pad the group to a multiple of 8)
+            col_of, width = {}, 0
+            for grp in range(0, cout, 64):
+                kept = [c for c in self._dual[info["out"]] if grp <= c < grp + 64]
+                for k, c in enumerate(kept):
+                    col_of[c] = width + k
+                width += K.pad8(len(kept))
+            y2 = self._alloc(info["out"] + "#compact", width, shape_of=info["out"])
+            m = [-1] * cout
+            for c, j in col_of.items():
+                m[c] = j
+            y2_map = self._i32(m)
+            self._dual_bufs[info["out"]] = (y2, col_of)
         relu = info["relu"] is not None
         # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
@@ -479,7 +532,7 @@ class Engine:
             if pre is not None:
                 pre()
             K.conv(xv, wg, lead, cpad, cout, kk, kk, st_p, pd, y, gather_idx=gidx, bias=bias, residual=residual,
-                   relu=relu, y_fp32=fp32_out, variant=pw)
+                   relu=relu, y_fp32=fp32_out, variant=pw, y2=y2, y2_map=y2_map)
 
         op.launch = launch
         op.info["desc"] = (f"{kk}x{kk}s{st} {cin}->{cout} {x.H}x{x.W}"

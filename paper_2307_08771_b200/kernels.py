@@ -128,7 +128,10 @@ def channel_gather_2d(x: Act, idx_dev: torch.Tensor, stride: int, y: Act) -> Non
 
 def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: int, stride: int, pad: int,
          y: Act, gather_idx: torch.Tensor | None = None, bias: torch.Tensor | None = None,
-         residual: Act | None = None, relu: bool = False, y_fp32: bool = False, variant: int = 0) -> None:
+         residual: Act | None = None, relu: bool = False, y_fp32: bool = False, variant: int = 0,
+         y2: Act | None = None, y2_map: torch.Tensor | None = None) -> None:
+    """One conv (ub_conv_fwd).  y2 / y2_map: compacted second store of the output channels c
+    with y2_map[c] >= 0 into column y2_map[c] of y2 (the producer side of a later GATHER)."""
     Ho = (x.H + 2 * pad - kh) // stride + 1
     Wo = (x.W + 2 * pad - kw) // stride + 1
     assert y.N == x.N and y.H == Ho and y.W == Wo, "output geometry mismatch"
@@ -147,6 +150,9 @@ def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: 
     d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
     d.y_dtype = _lib.UB_F32 if y_fp32 else _lib.UB_BF16
     d.variant = variant
+    if y2 is not None:
+        assert y2.coff == 0 and y2_map is not None and y2_map.numel() == cout
+        d.y2, d.y2_cstride, d.y2_map = y2.buf.data_ptr(), y2.cstride, y2_map.data_ptr()
     _lib.check(_lib.load().ub_conv_fwd(ctypes.byref(d), _stream()))
 
 

@@ -59,6 +59,26 @@ def test_resnet50_reorder_logits_match_oracle_graph_replay():
     assert top1_agreement(got, ref) == 1.0
 
 
+def test_resnet50_dual_store_plans_match_oracle():
+    """Producer-side compacted copies (ub_conv_desc.y2) + the consumers' dense "dual" read
+    plans: same logits as the oracle (the path is off by default)."""
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    N = 2
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(3))
+    eng = EN.from_plans(sm, eg, maps, batch=N, dual_store=True)
+    n_dual = 0
+    for op in eng.ops:
+        if "plans" in op.info and "dual" in op.info["plans"]:
+            op.info["variant"] = (op.info["plans"].index("dual"), 0)
+            n_dual += 1
+    assert n_dual >= 8
+    got = eng.forward(x.cuda()).cpu()
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
+    assert deviation(got, ref) <= TOL
+    assert top1_agreement(got, ref) == 1.0
+
+
 def test_export_model_weights_bit_exact_vs_oracle():
     """GPU permute (fp64, no BN fold) == numpy apply_plan restatement, bit for bit."""
     sm, plans, eg, maps = _setup("resnet50_s50", "reorder")

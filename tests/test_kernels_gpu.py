@@ -305,6 +305,74 @@ def test_channel_gather_and_pools():
     assert _rel(ya.to_nchw().cpu().reshape(2, 40), refa) < 1e-2
 
 
+@pytest.mark.parametrize("N,H,cin,cout,res,variant,kind", [
+    (2, 14, 64, 237, True, 0, "random"), (3, 7, 128, 1016, True, 65, "random"), (2, 9, 32, 40, False, 0, "random"),
+    (2, 14, 128, 1016, True, 0, "lo_halves"), (2, 56, 32, 237, True, 0, "hi_halves"),
+    (2, 14, 128, 1016, True, 2, "random"), (1, 5, 64, 130, False, 1, "all")])
+def test_conv_dual_store(N, H, cin, cout, res, variant, kind):
+    """Compacted second store (ub_conv_desc.y2): per 64-channel group the kept channels land in
+    consecutive columns from an 8-aligned base, the group's pad columns are zero; bit-exact
+    copies of y; columns past the layout untouched; y unchanged by the second store."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(cout + N)
+    x = K.act_from_nchw(torch.randn(N, cin, H, H, generator=g).to(dev))
+    Wt = torch.randn(cout, cin, 1, 1, generator=g) / cin ** 0.5
+    lead, cpad = _lib.conv_weight_layout(cin, 0, False, 1, 1)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)), layout="gemm", lead=lead,
+                           cpad=cpad, out_dtype=torch.bfloat16)
+    bias = torch.randn(cout, generator=g).to(dev)
+    r = K.act_from_nchw(torch.randn(N, cout, H, H, generator=g).to(dev)) if res else None
+    if kind == "random":
+        kept = sorted(torch.randperm(cout, generator=g)[:cout // 2 + 3].tolist())
+    elif kind == "lo_halves":  # every lane keeps exactly one of (j, j + 32): only the low halves
+        kept = [c for c in range(cout) if (c // 32) % 2 == 0 and c % 3]
+    elif kind == "hi_halves":
+        kept = [c for c in range(cout) if (c // 32) % 2 == 1]
+    else:
+        kept = list(range(cout))
+    m, cols, width = [-1] * cout, [], 0
+    for grp in range(0, cout, 64):
+        ks = [c for c in kept if grp <= c < grp + 64]
+        for k, c in enumerate(ks):
+            m[c] = width + k
+        cols += [width + k for k in range(len(ks))]
+        width += K.pad8(len(ks))
+    y = K.empty_act(N, H, H, cout, dev)
+    y2 = K.empty_act(N, H, H, width + 8, dev)
+    y2.buf.fill_(float("nan"))
+    K.conv(x, wg, lead, cpad, cout, 1, 1, 1, 0, y, bias=bias, residual=r, relu=True, variant=variant, y2=y2,
+           y2_map=torch.tensor(m, dtype=torch.int32, device=dev))
+    yref = K.empty_act(N, H, H, cout, dev)
+    K.conv(x, wg, lead, cpad, cout, 1, 1, 1, 0, yref, bias=bias, residual=r, relu=True, variant=variant)
+    torch.cuda.synchronize()
+    assert torch.equal(y.buf[:, :cout], yref.buf[:, :cout])
+    assert torch.equal(y2.buf[:, cols].view(torch.int16), y.buf[:, kept].view(torch.int16))
+    pad = sorted(set(range(width)) - set(cols))
+    if pad:
+        assert (y2.buf[:, pad].float() == 0).all()
+    assert torch.isnan(y2.buf[:, width:].float()).all()
+
+
+@pytest.mark.parametrize("HW,C", [(49, 1816), (81, 44), (5, 64)])
+def test_avgpool_global_sequential_sum(HW, C):
+    """Global average pool == fp32 sum in pixel order, / HW, rounded to bf16 (both the 8-channel
+    vector kernel (C % 8 == 0) and the scalar one)."""
+    import numpy as np
+    dev = "cuda"
+    g = torch.Generator().manual_seed(HW + C)
+    x = torch.randn(2, C, 1, HW, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    ya = K.empty_act(2, 1, 1, C, dev)
+    K.avgpool_global(xa, ya)
+    torch.cuda.synchronize()
+    xb = _bf(x).numpy().astype(np.float32)
+    s = np.zeros((2, C), dtype=np.float32)
+    for p in range(HW):
+        s = s + xb[:, :, 0, p]
+    ref = torch.from_numpy(s / np.float32(HW)).to(torch.bfloat16).float()
+    assert torch.equal(ya.to_nchw().cpu().reshape(2, C), ref)
+
+
 @pytest.mark.parametrize("H,C,coff,k,st,pd", [(112, 64, 0, 3, 2, 1), (57, 48, 16, 3, 2, 1), (20, 24, 8, 2, 2, 0),
                                              (30, 60, 0, 3, 2, 1)])
 def test_maxpool_rows_matches_torch(H, C, coff, k, st, pd):
