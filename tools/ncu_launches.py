@@ -12,7 +12,8 @@ from collections import OrderedDict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-CONV_KERNELS = ("conv_tc_kernel", "conv_halo3_kernel", "stem_s2d_kernel", "stem_s2d_pack_kernel")
+CONV_KERNELS = ("conv_tc_kernel", "conv_halo3_kernel", "stem_s2d_kernel", "stem_s2d_pack", "stem_pool_kernel",
+                "channel_gather_2d_kernel")
 
 
 def load(path):
