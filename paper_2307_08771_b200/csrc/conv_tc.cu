@@ -948,14 +948,16 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   // more tiles until the grid fills.  Multi-tile N rounds to the epilogue's 64-channel
   // chunk so a tile's last chunk never spills into the next tile's channels (the TMA
   // store only clips at cout).
-  p.n_tiles = (d->cout + MAX_BLOCK_N - 1) / MAX_BLOCK_N;
+  // variant bit 13: N tiles of at most 128 channels (their weights may then stay resident)
+  const int max_bn = (d->variant & 8192) ? 128 : MAX_BLOCK_N;
+  p.n_tiles = (d->cout + max_bn - 1) / max_bn;
   while (static_cast<long long>(p.m_tiles) * p.n_tiles < num_sms() &&
          (d->cout + p.n_tiles) / (p.n_tiles + 1) >= EPI_CHUNK)
     ++p.n_tiles;
   {
     const int n_gran = p.n_tiles > 1 ? EPI_CHUNK : 16;
     p.block_n = (((d->cout + p.n_tiles - 1) / p.n_tiles) + n_gran - 1) / n_gran * n_gran;
-    if (p.block_n > MAX_BLOCK_N) p.block_n = MAX_BLOCK_N;
+    if (p.block_n > max_bn) p.block_n = max_bn;
     p.n_tiles = (d->cout + p.block_n - 1) / p.block_n;
   }
   p.cchunks = (stem || packed) ? 1 : cpad / bk;

@@ -518,6 +518,8 @@ class Engine:
             tiled = kk == 1 and st_p == 1
             gen = [pw | nb | bt | at | e1 for pw in (1, 2) for nb in (0, 4) for bt in (0, 16)
                    for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
+            if kk == 1 and cout > 192:  # +8192: N tiles of <= 128 channels (weights may stay resident)
+                gen = gen + [v | 8192 for v in gen if not v & 4]
             if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
                 gen = [0, 128] + [v | 8 for v in gen]
             return gen
