@@ -59,6 +59,8 @@ struct PoolParams {
   int dbg;  // profiling ablations (UB_DEBUG_FLAGS): 4 no MMA, 16 no loads, 64 no pooled-row output
   int sleep_ns;  // epilogue accumulator wait: suspend-time hint (0: spin)
   int rw;  // ring words per channel (bf16 pairs of pooled pixels; rw / 4 odd: conflict-free rows)
+  uint16_t* y;  // direct-store output (pooled [n][yp][xp] rows at pitch y_cstride) or null: TMA store
+  int y_cstride;
 };
 
 // The CTA's tile sequence: bands u = blockIdx.x, +gridDim.x, ...; per band an optional halo
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
         mbar_wait(&hready[slot], (it / SP_RING) & 1);
         if (has_prev) mbar_wait(&hready[prev], ((it - 1) / SP_RING) & 1);
         const uint32_t* prv = reinterpret_cast<const uint32_t*>(sRing + prev * ring_sz) + c * p.rw;
-        if (leader) bulk_wait_read<0>();  // the group's previous pooled row has left `out`
+        if (leader && !p.y) bulk_wait_read<0>();  // the group's previous pooled row has left `out`
 #pragma unroll
         for (int i = 0; i < SP_COLS / 4; i += 4) {
           if (i >= nw) break;
@@ -280,6 +282,17 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
           h[i + 2] = bf16x2_max3(h[i + 2], o.z, pv.z);
           h[i + 3] = bf16x2_max3(h[i + 3], o.w, pv.w);
         }
+        if (p.y) {  // direct stores: per pixel the group's 64 lanes write 128 contiguous bytes
+          if (c < p.cout) {
+            uint16_t* dst = p.y + (static_cast<size_t>(ti.n) * p.Hp + yp) * p.Wp * p.y_cstride + c;
+#pragma unroll
+            for (int i = 0; i < SP_COLS / 4; ++i) {
+              if (i >= nw) break;
+              dst[static_cast<size_t>(2 * i) * p.y_cstride] = static_cast<uint16_t>(h[i] & 0xffffu);
+              if (2 * i + 1 < p.Wp) dst[static_cast<size_t>(2 * i + 1) * p.y_cstride] = static_cast<uint16_t>(h[i] >> 16);
+            }
+          }
+        } else {
         // [xp][64 ch] with SW128 chunk swizzle: this thread's channel, pixels 2i and 2i+1
         named_bar_sync(1 + grp, 64);
 #pragma unroll
@@ -297,6 +310,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
         if (leader) {
           tma_store_4d(&tmY, out, 0, 0, yp, ti.n);
           bulk_commit();
+        }
         }
       }
       __syncwarp();
@@ -365,6 +379,10 @@ extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, in
     static int sl = -1;
     if (sl < 0) sl = getenv("UB_SP_SLEEP") ? atoi(getenv("UB_SP_SLEEP")) : 0;
     p.sleep_ns = sl;
+  }
+  if (!getenv("UB_SP_TMA_STORE")) {  // direct stores (default); the TMA-store path stays for A/B
+    p.y = static_cast<uint16_t*>(y) + y_coff;
+    p.y_cstride = y_cstride;
   }
   p.cout = cout;
   p.rw = ((p.Wp + 1) / 2 + 3) / 4 * 4;
