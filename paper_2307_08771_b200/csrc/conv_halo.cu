@@ -307,19 +307,18 @@ __global__ void __maxnreg__(96)
     __syncwarp();
     tc_fence_after();
     fence_proxy_async_smem();
-    int s = 0, it = 0, bs = 0;
-    uint32_t ph = 0, bph = 0;
+    int s = 0, it = 0, bs = 0, acc = 0;
+    uint32_t ph = 0, bph = 0, aph = 0;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      const int acc = it % p.nacc;
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 0] = clock64();
-      mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
+      mbar_wait(&tempty[acc], aph ^ 1);
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 1] = clock64();
       for (int g = 0; g < groups; ++g) {
         mbar_wait(&afull[s], ph);
         if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64 && g == 0) p.trace[it * 16 + 2] = clock64();
         __syncwarp();
         tc_fence_after();
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+        if constexpr (!AT) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
         const uint64_t ad = adesc0 + s * stage_units;
         if constexpr (S == 2) {
           const int qd = g / (p.cpad >> 6);
@@ -381,6 +380,10 @@ __global__ void __maxnreg__(96)
       }
       umma_commit_warp(&tfull[acc]);
       if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 16 + 3] = clock64();
+      if (++acc == p.nacc) {
+        acc = 0;
+        aph ^= 1;
+      }
     }
   } else if (SB && warp == ALLOC_WARP) {
     // ================= streamed weights: one TMA box (64 K x np rows, SW128) per (group, tap)

@@ -256,7 +256,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           mbar_wait(&full[s], ph);
           __syncwarp();
           tc_fence_after();
-          fence_proxy_async_smem();  // generic-proxy (cp.async / st.shared) writes -> tensor-core reads
+          // generic-proxy (cp.async / st.shared) writes -> tensor-core reads; the TMA-fed path
+          // (A, B, residual all async-proxy writes) needs no proxy fence per k-block
+          if (!p.a_tma) fence_proxy_async_smem();
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           if (!(p.dbg & 4)) {
             if (kb < nk) {
