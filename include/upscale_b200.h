@@ -193,6 +193,15 @@ int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, int pad, cons
                         const float* bias, int relu, int pool_k, int pool_stride, int pool_pad,
                         void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
+/* The same stem + max pool reading the fp32 NCHW model input directly: the pair tiles' folded
+ * rows are built in shared memory by the kernel's producer warps from channels idx[0..cin) of
+ * x [N][C][H][W] (the INPUT node's GATHER, interp.py:75-77, and the fp32 -> bf16 cast), so the
+ * folded buffer S and the pack launch disappear.  Same result as ub_stem_s2d_pack +
+ * ub_conv_s2d_maxpool, bit for bit. */
+int ub_stem_maxpool(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, int k, int pad,
+                    const void* w, int cout, const float* bias, int relu, int pool_k, int pool_stride, int pool_pad,
+                    void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
 /* Model-input staging: NCHW fp32 -> NHWC bf16 [N*H*W][y_cstride], channels
  * idx[0..n) (a GATHER on the INPUT node, fused; idx == NULL: identity over C). */
 int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n,

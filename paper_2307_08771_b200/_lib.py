@@ -77,6 +77,8 @@ SIGNATURES = {
                             c_int, c_vp]),
     "ub_conv_s2d_maxpool": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int,
                                     c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_stem_maxpool": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int,
+                                c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_h2d_input_channels": (c_int, [c_vp, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_int32), c_int, c_vp,
                                       ctypes.POINTER(c_ll), c_vp]),
     "ub_plan_order_segment": (c_int, [c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

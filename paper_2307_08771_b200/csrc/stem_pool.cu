@@ -61,7 +61,14 @@ struct PoolParams {
   int rw;  // ring words per channel (bf16 pairs of pooled pixels; rw / 4 odd: conflict-free rows)
   uint16_t* y;  // direct-store output (pooled [n][yp][xp] rows at pitch y_cstride) or null: TMA store
   int y_cstride;
+  // fused pack (ub_stem_maxpool): the producer warps build the pair's folded rows straight from
+  // the fp32 NCHW model input (the INPUT GATHER's channels idx) instead of bulk-copying S
+  const float* x;  // null: S-based (ub_conv_s2d_maxpool)
+  const int32_t* idx;
+  int C, H, W, cin, pad;
 };
+
+constexpr int SP_PACK_THREADS = 64;  // warps 0 and 3 when packing
 
 // The CTA's tile sequence: bands u = blockIdx.x, +gridDim.x, ...; per band an optional halo
 // pair then the pairs of its pooled rows.
@@ -85,7 +92,7 @@ struct TileIter {
   }
 };
 
-template <int KQ>
+template <int KQ, bool PACK>  // PACK: the producer warps fold the fp32 input (p.x)
 __global__ void __launch_bounds__(SP_THREADS, 1)
     stem_pool_kernel(const __grid_constant__ CUtensorMap tmY, const PoolParams p) {
   constexpr int PAIRS = (KQ + 1) / 2, NMMA = (KQ + 1) * PAIRS;
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmY);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PACK ? SP_PACK_THREADS : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < SP_ACC; ++a) {
@@ -152,7 +159,58 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   ti.u = blockIdx.x;
   if (ti.valid(p)) ti.start_band(p);
 
-  if (warp == 0) {
+  if (PACK && (warp == 0 || warp == 3)) {
+    // ================= producer (fused pack): folded pixel e of the pair's S window =
+    // 8 bf16 = (py, px, c) of input rows 2Y+py-pad, cols 2X+px-pad (zero outside the image)
+    const int pt = (warp == 0 ? 0 : 32) + lane;
+    griddep_wait();  // the model input comes from the host copy / previous graph node
+    int s = 0;
+    uint32_t ph = 0;
+    const int nrows = static_cast<int>(p.load_bytes >> 4);
+    int ch[2] = {__ldg(p.idx), p.cin > 1 ? __ldg(p.idx + 1) : 0};
+    for (; ti.valid(p); ti.next(p)) {
+      const int Y0 = 2 * ti.yp();
+      const float* ximg = p.x + static_cast<size_t>(ti.n) * p.C * p.H * p.W;
+      if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(sS + s * p.stage_bytes);
+      constexpr int U = 4;  // folded pixels per thread in flight (32 loads)
+      for (int e0 = pt; e0 < nrows; e0 += SP_PACK_THREADS * U) {
+        float v[U][4][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * SP_PACK_THREADS;
+          const int dyr = e / p.Ws;
+          const int X = e - dyr * p.Ws;
+          const int Y = Y0 + dyr;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int hi = 2 * Y + (q >> 1) - p.pad, wi = 2 * X + (q & 1) - p.pad;
+            const bool ok = e < nrows && Y < p.Hs && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
+            const float* src = ximg + static_cast<size_t>(hi) * p.W + wi;
+            v[u][q][0] = ok ? __ldg(src + static_cast<size_t>(ch[0]) * p.H * p.W) : 0.f;
+            v[u][q][1] = (ok && p.cin > 1) ? __ldg(src + static_cast<size_t>(ch[1]) * p.H * p.W) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * SP_PACK_THREADS;
+          if (e >= nrows) break;
+          // slot (py, px, c) = q * cin + c, as ub_stem_s2d_pack
+          dst[e] = p.cin > 1 ? make_uint4(cvt_bf16x2(v[u][0][0], v[u][0][1]), cvt_bf16x2(v[u][1][0], v[u][1][1]),
+                                          cvt_bf16x2(v[u][2][0], v[u][2][1]), cvt_bf16x2(v[u][3][0], v[u][3][1]))
+                             : make_uint4(cvt_bf16x2(v[u][0][0], v[u][1][0]), cvt_bf16x2(v[u][2][0], v[u][3][0]), 0u,
+                                          0u);
+        }
+      }
+      fence_proxy_async_smem();  // st.shared (generic proxy) -> tensor-core reads
+      mbar_arrive(&full[s]);
+      if (++s == p.stages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {  // ================= producer: the pair's folded rows in one bulk copy
       griddep_wait();  // S comes from the pack kernel (PDL)
       int s = 0;
@@ -329,14 +387,14 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   }
 }
 
-template <int KQ>
+template <int KQ, bool PACK>
 void launch_pool(const CUtensorMap& tm, const PoolParams& p, int grid, size_t smem, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stem_pool_kernel<KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(stem_pool_kernel<KQ, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  (void)launch_pdl(stem_pool_kernel<KQ>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, p);
+  (void)launch_pdl(stem_pool_kernel<KQ, PACK>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, p);
 }
 
 }  // namespace
@@ -344,10 +402,13 @@ void launch_pool(const CUtensorMap& tm, const PoolParams& p, int grid, size_t sm
 
 using namespace ub;
 
-extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, int pad, const void* w, int cout,
-                                   const float* bias, int relu, int pool_k, int pool_stride, int pool_pad, void* y,
-                                   int y_cstride, int y_coff, cudaStream_t stream) {
-  if (!s || !w || !y || cout < 1 || N < 1) return fail(UB_EINVAL, "ub_conv_s2d_maxpool: bad arguments");
+namespace {
+// s: the folded input S (ub_stem_s2d_pack), or x: the fp32 NCHW model input packed on the fly
+int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx, int cin, int N, int H, int W, int k,
+                        int pad, const void* w, int cout, const float* bias, int relu, int pool_k, int pool_stride,
+                        int pool_pad, void* y, int y_cstride, int y_coff, cudaStream_t stream) {
+  if ((!s && !x) || !w || !y || cout < 1 || N < 1) return fail(UB_EINVAL, "ub_conv_s2d_maxpool: bad arguments");
+  if (x && (!idx || cin < 1 || 4 * cin > 8 || C < 1)) return fail(UB_EINVAL, "ub_stem_maxpool: bad input gather");
   if (pool_k != 3 || pool_stride != 2 || pool_pad != 1)
     return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: pool %d/%d/%d (3/2/1 only)", pool_k, pool_stride, pool_pad);
   if (cout > 64) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: cout %d > 64", cout);
@@ -364,6 +425,13 @@ extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, in
     return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: conv output %dx%d (even, width <= 128)", Ho, Wo);
   PoolParams p{};
   p.s = static_cast<const uint16_t*>(s);
+  p.x = x;
+  p.idx = idx;
+  p.C = C;
+  p.H = H;
+  p.W = W;
+  p.cin = cin;
+  p.pad = pad;
   p.n_img = N;
   p.Hs = Hs;
   p.Ws = Ws;
@@ -441,10 +509,27 @@ extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, in
   apply_small_tensor_quirk(&tm, static_cast<size_t>(N) * p.Hp * p.Wp * y_cstride * 2);
   const int grid = p.n_bands < sms ? p.n_bands : sms;
   switch (kq) {
-    case 2: launch_pool<2>(tm, p, grid, smem, stream); break;
-    case 3: launch_pool<3>(tm, p, grid, smem, stream); break;
-    default: launch_pool<4>(tm, p, grid, smem, stream); break;
+    case 2: x ? launch_pool<2, true>(tm, p, grid, smem, stream) : launch_pool<2, false>(tm, p, grid, smem, stream); break;
+    case 3: x ? launch_pool<3, true>(tm, p, grid, smem, stream) : launch_pool<3, false>(tm, p, grid, smem, stream); break;
+    default: x ? launch_pool<4, true>(tm, p, grid, smem, stream) : launch_pool<4, false>(tm, p, grid, smem, stream); break;
   }
   count_launch();
   return cuda_status(cudaGetLastError(), "stem_pool_kernel");
+}
+}  // namespace
+
+extern "C" int ub_conv_s2d_maxpool(const void* s, int N, int H, int W, int k, int pad, const void* w, int cout,
+                                   const float* bias, int relu, int pool_k, int pool_stride, int pool_pad, void* y,
+                                   int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!s) return fail(UB_EINVAL, "ub_conv_s2d_maxpool: bad arguments");
+  return stem_maxpool_launch(s, nullptr, 0, nullptr, 0, N, H, W, k, pad, w, cout, bias, relu, pool_k, pool_stride,
+                             pool_pad, y, y_cstride, y_coff, stream);
+}
+
+extern "C" int ub_stem_maxpool(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, int k, int pad,
+                               const void* w, int cout, const float* bias, int relu, int pool_k, int pool_stride,
+                               int pool_pad, void* y, int y_cstride, int y_coff, cudaStream_t stream) {
+  if (!x) return fail(UB_EINVAL, "ub_stem_maxpool: bad arguments");
+  return stem_maxpool_launch(nullptr, x, C, idx, cin, N, H, W, k, pad, w, cout, bias, relu, pool_k, pool_stride,
+                             pool_pad, y, y_cstride, y_coff, stream);
 }

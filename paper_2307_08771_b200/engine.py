@@ -62,13 +62,14 @@ class Engine:
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
                  stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5,
-                 dual_store: bool = False):
+                 dual_store: bool = False, stem_pack_fused: bool = False):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
         self.stem_pool = stem_pool
         self.cover_ratio = cover_ratio
         self.dual_store = dual_store
+        self.stem_pack_fused = stem_pack_fused
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -585,11 +586,16 @@ class Engine:
         if "pool" in info:
             assert s2d, "stem/max-pool fusion needs the space-to-depth stem"
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
-            sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
-            self._keep += [wg, sbuf]
-            op.launch = lambda: K.stem_s2d_maxpool(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias,
-                                                   relu=relu)
-            op.info["stem_kind"] = "s2d+maxpool"
+            self._keep.append(wg)
+            if self.stem_pack_fused:  # one launch: the kernel folds the fp32 input itself
+                op.launch = lambda: K.stem_maxpool(self.input_buf, idx_dev, wg, cout, kk, pd, y, bias=bias, relu=relu)
+                op.info["stem_kind"] = "s2d+maxpool+pack"
+            else:
+                sbuf = K.s2d_buffer(self.batch, hi, wi, kk, pd, self.device)
+                self._keep.append(sbuf)
+                op.launch = lambda: K.stem_s2d_maxpool(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias,
+                                                       relu=relu)
+                op.info["stem_kind"] = "s2d+maxpool"
             wbytes = 2.0 * wg.numel()
         elif s2d:
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
@@ -707,7 +713,7 @@ class Engine:
         one eager pass; before any pass, the op count (one launch per op, two for the
         space-to-depth stem)."""
         if getattr(self, "_launches", None) is None:
-            return sum(2 if op.info.get("stem_kind", "").startswith("s2d") else 1 for op in self.ops)
+            return sum(2 if op.info.get("stem_kind", "") in ("s2d", "s2d+maxpool") else 1 for op in self.ops)
         return self._launches
 
     def per_image_work(self) -> tuple[float, float]:

@@ -211,6 +211,14 @@ def stem_s2d_maxpool(x_nchw: torch.Tensor, idx_dev: torch.Tensor, s_buf: torch.T
                                        _p(y.buf), y.cstride, y.coff, _stream()))
 
 
+def stem_maxpool(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, cout: int, k: int, pad: int, y: Act,
+                 bias: torch.Tensor | None = None, relu: bool = False, pool=(3, 2, 1)) -> None:
+    """stem_s2d_maxpool with the pack fused into the kernel's producer (one launch, no S)."""
+    N, C, H, W = x_nchw.shape
+    _lib.check(_lib.load().ub_stem_maxpool(_p(x_nchw), N, C, H, W, _p(idx_dev), idx_dev.numel(), k, pad, _p(w), cout,
+                                           _p(bias), int(relu), *pool, _p(y.buf), y.cstride, y.coff, _stream()))
+
+
 def h2d_input_channels(host: torch.Tensor, dev: torch.Tensor, channels) -> int:
     """Pinned host NCHW fp32 -> device NCHW fp32, only `channels` (the INPUT GATHER's
     kept planes; the others are left untouched). Returns the bytes copied."""

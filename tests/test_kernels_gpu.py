@@ -228,8 +228,15 @@ def test_stem_s2d_maxpool_matches_torch(N, H, idx, cout):
     y.buf.fill_(float("nan"))
     y = y.view(8, cout)
     sbuf = K.s2d_buffer(N, H, H, k, pad, dev)
-    K.stem_s2d_maxpool(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), sbuf, wg, cout, k, pad, y,
-                       bias=bias.to(dev), relu=True)
+    xd, idxd = x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev)
+    K.stem_s2d_maxpool(xd, idxd, sbuf, wg, cout, k, pad, y, bias=bias.to(dev), relu=True)
+    # the fused-pack form (one launch, no S buffer) is bit-identical
+    y_f = K.empty_act(N, Hp, Hp, cout + 8, dev)
+    y_f.buf.fill_(float("nan"))
+    y_f = y_f.view(8, cout)
+    K.stem_maxpool(xd, idxd, wg, cout, k, pad, y_f, bias=bias.to(dev), relu=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y_f.buf.view(torch.int16), y.buf.view(torch.int16))
     torch.cuda.synchronize()
     conv = torch.nn.functional.conv2d(_bf(x[:, idx]), _bf(Wt), stride=2, padding=pad) + bias.view(1, -1, 1, 1)
     ref = torch.nn.functional.max_pool2d(_bf(conv.clamp_min(0)), 3, 2, 1)

@@ -73,6 +73,8 @@ def main():
         return
     tpool = timeit(pool)
     print(f"conv+maxpool {tpool:8.1f} us")
+    tf = timeit(lambda: K.stem_maxpool(x, idx, wg, cout, k, pad, yp, bias=bias, relu=True))
+    print(f"fused pack+conv+maxpool {tf:8.1f} us")
     tp, tc = timeit(pack), timeit(conv)
     out_b = N * 112 * 112 * cout * 2
     s_b = sbuf.numel() * 2

@@ -51,6 +51,9 @@ __global__ void __launch_bounds__(128, 1) probe_mma(int n, int mode, int iters, 
       if (commit_every == 1) {  // no-swizzle planes: A rows 16 B apart, K core matrices 4 KB apart
         ad[k] = sdesc(a0 + k * shift, 4096, 128, 0);
         bd[k] = sdesc(b0, n * 16, 128, 0);
+      } else if (commit_every == 2) {  // SW64 A (64-byte rows, row shifts of k), SW128 B
+        ad[k] = sdesc(a0 + (k & 1) * 32 + k * 64, 16, 512, 4);
+        bd[k] = sdesc(b0 + (k & 1) * 32, 16, 1024, 2);
       } else {
         ad[k] = sdesc(a0 + k * 32, 16, 1024, 2);
         bd[k] = sdesc(b0 + k * 32, 16, 1024, 2);
@@ -138,9 +141,9 @@ int main() {
   const int iters = 4096;
   const char* names[6] = {"sw128", "noswz", "noswz-lbo16", "sw128-pre", "sw128-pre-c", "warp-elect"};
   for (int mode = 5; mode < 6; ++mode) {
-    for (int n : {32, 64, 128, 256}) {
-      for (int sh : {-1, 0, 128, 256, 16, 48, 112}) {
-        const int ce = sh < 0 ? 0 : 1;
+    for (int n : {32, 64, 128}) {
+      for (int sh : {-1, -2, 0, 48}) {
+        const int ce = sh == -1 ? 0 : (sh == -2 ? 2 : 1);
         for (int grid : {148}) {
           probe_mma<<<grid, 128, 64 * 1024>>>(n, mode, iters, ce, dout, sh);
           cudaError_t e = cudaDeviceSynchronize();
