@@ -66,6 +66,12 @@ struct PoolParams {
   const float* x;  // null: S-based (ub_conv_s2d_maxpool)
   const int32_t* idx;
   int C, H, W, cin, pad;
+  uint32_t raw_off, raw_bytes, raw_plane;  // PACK: window offset in a stage, bytes, per-channel bytes
+  uint32_t raw_tx;                         // PACK: bytes the window's TMA boxes deliver
+  int raw_cols;                            // PACK: floats per window row
+  int raw_half;                            // PACK: floats per row of one of the two boxes
+  uint32_t raw_box;                        // PACK: smem bytes of one box (128-byte aligned)
+  int raw_xoff;                            // PACK: window column of input column 0 (multiple of 4, >= pad)
 };
 
 constexpr int SP_PACK_THREADS = 64;  // warps 0 and 3 when packing
@@ -94,7 +100,8 @@ struct TileIter {
 
 template <int KQ, bool PACK>  // PACK: the producer warps fold the fp32 input (p.x)
 __global__ void __launch_bounds__(SP_THREADS, 1)
-    stem_pool_kernel(const __grid_constant__ CUtensorMap tmY, const PoolParams p) {
+    stem_pool_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX,
+                     const PoolParams p) {
   constexpr int PAIRS = (KQ + 1) / 2, NMMA = (KQ + 1) * PAIRS;
   constexpr uint32_t A_BYTES = 128 * 32;  // one MMA's weights: 128 rows x K 16
   extern __shared__ uint8_t smem_raw[];
@@ -111,7 +118,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   uint64_t* tempty = tfull + SP_ACC;
   uint64_t* hready = tempty + SP_ACC;
   uint64_t* hfree = hready + SP_RING;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + SP_RING);
+  uint64_t* rfull = hfree + SP_RING;  // PACK: the raw fp32 window of stage s landed (TMA tx)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + SP_STAGES_MAX);
   float* sBias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = threadIdx.x >> 5;
@@ -131,6 +139,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
       mbar_init(&hready[r], 2);  // the two odd-row warps of the writing tile
       mbar_init(&hfree[r], 4);   // the even-row warps of the writing tile and of the next
     }
+    if (PACK)
+      for (int s = 0; s < p.stages; ++s) mbar_init(&rfull[s], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, SP_ACC * SP_COLS);
@@ -159,48 +169,68 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   ti.u = blockIdx.x;
   if (ti.valid(p)) ti.start_band(p);
 
-  if (PACK && (warp == 0 || warp == 3)) {
-    // ================= producer (fused pack): folded pixel e of the pair's S window =
-    // 8 bf16 = (py, px, c) of input rows 2Y+py-pad, cols 2X+px-pad (zero outside the image)
+  if (PACK && warp == 2) {
+    // ================= producer (fused pack, part 1): the pair's raw fp32 window -- input
+    // rows 2Y0 - pad .. 2(Y0 + KQ) + 1 - pad, columns -pad .. 2 Ws - 1 - pad of each kept
+    // channel -- by one TMA box per channel (zero-filled outside the image)
+    if (lane == 0) {
+      griddep_wait();  // the model input comes from the host copy / previous graph node
+      tma_prefetch_desc(&tmX);
+      int s = 0;
+      uint32_t ph = 0;
+      const int c0 = __ldg(p.idx), c1 = p.cin > 1 ? __ldg(p.idx + 1) : 0;
+      for (; ti.valid(p); ti.next(p)) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* raw = sS + s * p.stage_bytes + p.raw_off;
+        const int row0 = 4 * ti.yp() - p.pad;
+        if (p.dbg & 16) {  // ablation: no input loads
+          mbar_arrive(&rfull[s]);
+        } else {
+          mbar_arrive_expect_tx(&rfull[s], p.raw_tx);
+          // two half-width boxes per channel plane (a box may not be wider than the image)
+          for (int c = 0; c < p.cin; ++c) {
+            const int z = ti.n * p.C + (c ? c1 : c0);
+            uint8_t* dstp = raw + c * p.raw_plane;
+            // the innermost box coordinate must be 16-byte aligned: start at -xoff (xoff >= pad)
+            tma_load_3d(&tmX, &rfull[s], dstp, -p.raw_xoff, row0, z);
+            tma_load_3d(&tmX, &rfull[s], dstp + p.raw_box, -p.raw_xoff + p.raw_half, row0, z);
+          }
+        }
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    __syncwarp();  // reconverge: this warp deallocates TMEM (a .sync.aligned op) at the end
+  } else if (PACK && (warp == 0 || warp == 3)) {
+    // ================= producer (fused pack, part 2): fold the raw window in smem -- folded
+    // pixel e of the S window = 8 bf16 = (py, px, c) of window row 2 dyr + py, column 2X + px
     const int pt = (warp == 0 ? 0 : 32) + lane;
-    griddep_wait();  // the model input comes from the host copy / previous graph node
     int s = 0;
     uint32_t ph = 0;
     const int nrows = static_cast<int>(p.load_bytes >> 4);
-    int ch[2] = {__ldg(p.idx), p.cin > 1 ? __ldg(p.idx + 1) : 0};
+    const int hw = p.raw_half;  // floats per window row of one box (columns [0, hw) / [hw, 2 hw))
+    const int box_f = static_cast<int>(p.raw_box >> 2);
     for (; ti.valid(p); ti.next(p)) {
-      const int Y0 = 2 * ti.yp();
-      const float* ximg = p.x + static_cast<size_t>(ti.n) * p.C * p.H * p.W;
-      if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
-      __syncwarp();
+      mbar_wait(&rfull[s], ph);
       uint4* dst = reinterpret_cast<uint4*>(sS + s * p.stage_bytes);
-      constexpr int U = 4;  // folded pixels per thread in flight (32 loads)
-      for (int e0 = pt; e0 < nrows; e0 += SP_PACK_THREADS * U) {
-        float v[U][4][2];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * SP_PACK_THREADS;
-          const int dyr = e / p.Ws;
-          const int X = e - dyr * p.Ws;
-          const int Y = Y0 + dyr;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int hi = 2 * Y + (q >> 1) - p.pad, wi = 2 * X + (q & 1) - p.pad;
-            const bool ok = e < nrows && Y < p.Hs && hi >= 0 && hi < p.H && wi >= 0 && wi < p.W;
-            const float* src = ximg + static_cast<size_t>(hi) * p.W + wi;
-            v[u][q][0] = ok ? __ldg(src + static_cast<size_t>(ch[0]) * p.H * p.W) : 0.f;
-            v[u][q][1] = (ok && p.cin > 1) ? __ldg(src + static_cast<size_t>(ch[1]) * p.H * p.W) : 0.f;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * SP_PACK_THREADS;
-          if (e >= nrows) break;
-          // slot (py, px, c) = q * cin + c, as ub_stem_s2d_pack
-          dst[e] = p.cin > 1 ? make_uint4(cvt_bf16x2(v[u][0][0], v[u][0][1]), cvt_bf16x2(v[u][1][0], v[u][1][1]),
-                                          cvt_bf16x2(v[u][2][0], v[u][2][1]), cvt_bf16x2(v[u][3][0], v[u][3][1]))
-                             : make_uint4(cvt_bf16x2(v[u][0][0], v[u][1][0]), cvt_bf16x2(v[u][2][0], v[u][3][0]), 0u,
-                                          0u);
+      const float* raw = reinterpret_cast<const float*>(sS + s * p.stage_bytes + p.raw_off);
+      const int plane_f = static_cast<int>(p.raw_plane >> 2);
+      const int sh = p.raw_xoff - p.pad;  // window column of folded column 0, px = 0
+      for (int e = pt; e < nrows; e += SP_PACK_THREADS) {
+        const int dyr = e / p.Ws;
+        const int X = e - dyr * p.Ws;
+        const int ca = 2 * X + sh, cb = ca + 1;  // window columns of px = 0, 1 (may sit in different boxes)
+        const int oa = (ca < hw ? ca : box_f + ca - hw) + (2 * dyr) * hw;
+        const int ob = (cb < hw ? cb : box_f + cb - hw) + (2 * dyr) * hw;
+        const float* r = raw;
+        const float* q = raw + plane_f;
+        if (p.cin > 1) {  // slot (py, px, c) = q * cin + c, as ub_stem_s2d_pack
+          dst[e] = make_uint4(cvt_bf16x2(r[oa], q[oa]), cvt_bf16x2(r[ob], q[ob]), cvt_bf16x2(r[oa + hw], q[oa + hw]),
+                              cvt_bf16x2(r[ob + hw], q[ob + hw]));
+        } else {
+          dst[e] = make_uint4(cvt_bf16x2(r[oa], r[ob]), cvt_bf16x2(r[oa + hw], r[ob + hw]), 0u, 0u);
         }
       }
       fence_proxy_async_smem();  // st.shared (generic proxy) -> tensor-core reads
@@ -388,13 +418,14 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
 }
 
 template <int KQ, bool PACK>
-void launch_pool(const CUtensorMap& tm, const PoolParams& p, int grid, size_t smem, cudaStream_t stream) {
+void launch_pool(const CUtensorMap& tm, const CUtensorMap& tmx, const PoolParams& p, int grid, size_t smem,
+                 cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(stem_pool_kernel<KQ, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  (void)launch_pdl(stem_pool_kernel<KQ, PACK>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, p);
+  (void)launch_pdl(stem_pool_kernel<KQ, PACK>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, tmx, p);
 }
 
 }  // namespace
@@ -467,6 +498,19 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
   if (last_end * 16 > sbytes) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: staging buffer too small");
   p.load_bytes = load_rows * 16;
   p.stage_bytes = (p.load_bytes + 127) & ~127u;
+  if (x) {  // raw fp32 window after the folded rows: cin planes of 2 (kq + 1) rows x raw_cols
+    // two boxes of raw_half columns per channel plane: a box may not be wider than the image
+    p.raw_xoff = (pad + 3) & ~3;
+    p.raw_half = (Ws + (p.raw_xoff - pad + 1) / 2 + 3) / 4 * 4;  // 2 boxes cover window columns up to 2 Ws + sh
+    p.raw_cols = 2 * p.raw_half;
+    const uint32_t box_b = static_cast<uint32_t>(2 * (kq + 1) * p.raw_half * 4);
+    p.raw_box = (box_b + 127) & ~127u;  // TMA destinations 128-byte aligned
+    p.raw_plane = 2 * p.raw_box;
+    p.raw_bytes = p.raw_plane * static_cast<uint32_t>(cin);
+    p.raw_tx = 2 * box_b * static_cast<uint32_t>(cin);
+    p.raw_off = (p.stage_bytes + 1023) & ~1023u;
+    p.stage_bytes = (p.raw_off + p.raw_bytes + 1023) & ~1023u;
+  }
   // bands of `band` pooled rows balanced over the SMs (+1 halo pair for bands below the top)
   const int sms = num_sms();
   int best_band = p.Hp;
@@ -507,11 +551,24 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_conv_s2d_maxpool: encode output tensor map failed (%d)", (int)r);
   apply_small_tensor_quirk(&tm, static_cast<size_t>(N) * p.Hp * p.Wp * y_cstride * 2);
+  CUtensorMap tmx{};
+  if (x) {  // model input as [N*C planes][H][W] fp32; box: raw_cols x 2 (kq + 1) rows of one plane
+    cuuint64_t xd[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(N) * C};
+    cuuint64_t xs[2] = {static_cast<cuuint64_t>(W) * 4, static_cast<cuuint64_t>(W) * H * 4};
+    cuuint32_t xb[3] = {static_cast<cuuint32_t>(p.raw_half), static_cast<cuuint32_t>(2 * (kq + 1)), 1};
+    cuuint32_t xe[3] = {1, 1, 1};
+    if (p.raw_half > 256 || p.raw_half > W || (W * 4) % 16)
+      return fail(UB_EUNSUPPORTED, "ub_stem_maxpool: input width %d (window %d floats)", W, p.raw_cols);
+    CUresult rx = encode_tiled_fn()(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), xd, xs, xb, xe,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rx != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_stem_maxpool: encode input tensor map failed (%d)", (int)rx);
+  }
   const int grid = p.n_bands < sms ? p.n_bands : sms;
   switch (kq) {
-    case 2: x ? launch_pool<2, true>(tm, p, grid, smem, stream) : launch_pool<2, false>(tm, p, grid, smem, stream); break;
-    case 3: x ? launch_pool<3, true>(tm, p, grid, smem, stream) : launch_pool<3, false>(tm, p, grid, smem, stream); break;
-    default: x ? launch_pool<4, true>(tm, p, grid, smem, stream) : launch_pool<4, false>(tm, p, grid, smem, stream); break;
+    case 2: x ? launch_pool<2, true>(tm, tmx, p, grid, smem, stream) : launch_pool<2, false>(tm, tmx, p, grid, smem, stream); break;
+    case 3: x ? launch_pool<3, true>(tm, tmx, p, grid, smem, stream) : launch_pool<3, false>(tm, tmx, p, grid, smem, stream); break;
+    default: x ? launch_pool<4, true>(tm, tmx, p, grid, smem, stream) : launch_pool<4, false>(tm, tmx, p, grid, smem, stream); break;
   }
   count_launch();
   return cuda_status(cudaGetLastError(), "stem_pool_kernel");
