@@ -283,7 +283,7 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-                "kernel": "conv kernels (conv_tc, conv_halo3, stem_s2d) of one step",
+                "kernel": "conv kernels of one step (conv_tc, conv_halo3, stem_s2d_pack_rows + stem_pool, channel_gather_2d)",
                 "algorithmic_bytes_per_step": conv_bytes, "algorithmic_flops_per_step": conv_flops,
                 "conv_ms_per_step_eager": round(conv_ms, 4), "conv_share_of_step": round(conv_ms / eager_ms, 4),
                 "mixed_roofline_ms": round(troof * 1e3, 4),

@@ -3,7 +3,9 @@ dram__bytes_read.sum,dram__bytes_write.sum --csv`) of a bench.py run into one
 step's per-launch table (dev tool; writes profiles/<tag>_launches_step.json and
 profiles/conv_traffic.json).
 
-python tools/ncu_launches.py gpurun_out/launches.csv <launches_per_step> <tag>
+python tools/ncu_launches.py gpurun_out/launches.csv <launches_per_step> <tag> [first-kernel substring]
+(the step is the last complete window that starts at the forward's first kernel, by default the
+stem's pack kernel)
 """
 import csv
 import json
@@ -36,9 +38,9 @@ def load(path):
 
 def main():
     path, per_step, tag = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    first = sys.argv[4] if len(sys.argv) > 4 else "stem_s2d_pack"
     ls = load(path)
-    first = ls[0]["kernel"]
-    starts = [i for i, l in enumerate(ls) if l["kernel"] == first and i + per_step <= len(ls)]
+    starts = [i for i, l in enumerate(ls) if first in l["kernel"] and i + per_step <= len(ls)]
     i0 = starts[-1]
     step = ls[i0:i0 + per_step]
     out = []
