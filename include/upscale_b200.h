@@ -147,7 +147,8 @@ typedef struct {
                                   bit 8: no stacked small images in the halo kernel;
                                   bit 11: halo input by cp.async planes instead of TMA boxes;
                                   bit 12: narrow tiles drained by alternate chunks, not tiles;
-                                  bit 13: N tiles of at most 128 channels */
+                                  bit 13: N tiles of at most 128 channels;
+                                  bit 14: no narrower (16/32-channel) last A box on the TMA 1x1 path */
   /* Optional second, compacted store of the output (the producer side of a GATHER read by
    * a later 1x1 conv): y2[m][y2_map[c]] = y[m][y_coff + c] for every c with y2_map[c] >= 0.
    * Layout contract: the kept channels of each 64-channel group [64g, 64g + 64) take

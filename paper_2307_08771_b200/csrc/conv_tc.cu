@@ -102,6 +102,7 @@ struct ConvKParams {
   uint16_t* y2;           // compacted second store (ub_conv_desc.y2) or null
   int y2_cstride;
   const int32_t* y2_map;  // [cout] compact column of output channel c, -1 = not stored
+  int tail_w;        // (a_tma, BK 64) channels of the narrower last A box (16 / 32), 64 = none
   int epi_alt;       // (epi2, one 64-channel chunk per tile) the groups take alternate tiles
                      // (group g drains accumulator g) instead of alternate chunks
 };
@@ -134,7 +135,7 @@ template <int AMODE, int BK, int PRODUCERS>
 __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
-                   const ConvKParams p) {
+                   const __grid_constant__ CUtensorMap tmAt, const ConvKParams p) {
   constexpr int PWARPS = PRODUCERS / 32;
   constexpr int GROWS = BLOCK_M / PWARPS;       // gather mode: rows per producer warp
   constexpr int STEM_K = 64 * 128 / PRODUCERS;  // stem mode: k values per producer thread per k-block
@@ -263,10 +264,18 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           if (!(p.dbg & 4)) {
             if (kb < nk) {
               const uint32_t b_base = smem_u32(sB + (p.b_res ? kb : s) * b_stride);
+              if (BK == 64 && kb == nk - 1 && p.tail_w < 64) {
+                // narrower last A box: rows of tail_w channels (SWIZZLE_32B / 64B), the same B box
+                const uint32_t t_layout = p.tail_w == 16 ? 6u : 4u, t_sbo = 8u * p.tail_w * 2;
+                for (int k = 0; k < p.tail_w / 16; ++k)
+                  umma_bf16_warp(d, make_sdesc(a_base + k * 32, t_sbo, t_layout), make_sdesc(b_base + k * 32, SBO, LAYOUT),
+                                 idesc, 1u);
+              } else {
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
                 umma_bf16_warp(d, make_sdesc(a_base + k * 32, SBO, LAYOUT), make_sdesc(b_base + k * 32, SBO, LAYOUT),
                           idesc, 1u);
+              }
             } else {  // residual chunk rc: D[:, rc*64 : rc*64+64] += R_rc * I
               const uint32_t dc = d + (kb - nk) * EPI_CHUNK;
 #pragma unroll
@@ -348,9 +357,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
           for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&empty[s], ph ^ 1);
             const bool bload = p.b_tma && !(p.dbg & 8);
-            const uint32_t bytes = BLOCK_M * ROW_BYTES + (bload ? static_cast<uint32_t>(p.block_n) * ROW_BYTES : 0u);
+            const bool tail = kb == nk - 1 && p.tail_w < BK;  // only the channels the slice still needs
+            const uint32_t a_bytes = BLOCK_M * (tail ? static_cast<uint32_t>(p.tail_w) * 2 : ROW_BYTES);
+            const uint32_t bytes = a_bytes + (bload ? static_cast<uint32_t>(p.block_n) * ROW_BYTES : 0u);
             mbar_arrive_expect_tx(&full[s], bytes);
-            tma_load_2d(&tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
+            tma_load_2d(tail ? &tmAt : &tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
             if (bload) tma_load_2d(&tmB, &full[s], sB + s * b_stride, kb * BK, n0);
             if (++s == stages) {
               s = 0;
@@ -830,7 +841,7 @@ namespace {
 
 template <int AMODE, int BK, int PRODUCERS>
 int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
-                  const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
+                  const CUtensorMap& tmAt, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -839,7 +850,7 @@ int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensor
   });
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
   const cudaError_t e = launch_pdl(conv_tc_kernel<AMODE, BK, PRODUCERS>, dim3(grid), dim3(256 + PRODUCERS), smem,
-                                   stream, tmY, tmB, tmA, tmR, p);
+                                   stream, tmY, tmB, tmA, tmR, tmAt, p);
   if (e != cudaSuccess) return cuda_status(e, "conv_tc_kernel launch");
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
@@ -847,9 +858,9 @@ int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensor
 
 template <int AMODE, int BK>
 int launch_conv(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
-                const ConvKParams& p, int grid, size_t smem, cudaStream_t stream, int wide) {
-  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, tmB, tmA, tmR, p, grid, smem, stream)
-              : launch_conv_p<AMODE, BK, 256>(tmY, tmB, tmA, tmR, p, grid, smem, stream);
+                const CUtensorMap& tmAt, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream, int wide) {
+  return wide ? launch_conv_p<AMODE, BK, 512>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream)
+              : launch_conv_p<AMODE, BK, 256>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream);
 }
 
 int pick_bk(int cin_eff) { return cin_eff <= 16 ? 16 : (cin_eff <= 32 ? 32 : 64); }
@@ -1084,7 +1095,8 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     apply_small_tensor_quirk(&tmB, static_cast<size_t>(p.K_total) * d->cout * 2);
   }
   // 1x1/s1 (tiled) A and the residual by TMA as well
-  CUtensorMap tmA{}, tmR{};
+  CUtensorMap tmA{}, tmR{}, tmAt{};
+  p.tail_w = 64;
   if (p.a_tma) {
     auto enc = [&](CUtensorMap* m, const void* base, int cstride, int cols, int box_c, bool whole) -> CUresult {
       cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(p.M)};
@@ -1101,6 +1113,15 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     const bool a_whole = d->x_coff - lead == 0 && cpad >= d->x_cstride;
     if (enc(&tmA, p.x, d->x_cstride, d->x_cstride - (d->x_coff - lead), bk, a_whole) != CUDA_SUCCESS)
       return fail(UB_ECUDA, "ub_conv_fwd: encode activation tensor map failed");
+    // the last K block of a slice that ends just past a 64-channel boundary: a 16- / 32-channel
+    // box (SWIZZLE_32B / 64B) instead of 64 channels -- the slice's tail, not the next slice
+    const int tail = cin_eff - 64 * (p.num_kb - 1);
+    if (bk == 64 && p.num_kb > 1 && tail <= 32 && !(d->variant & 16384)) {
+      const int tw = tail <= 16 ? 16 : 32;
+      if (enc(&tmAt, p.x, d->x_cstride, d->x_cstride - (d->x_coff - lead), tw, a_whole) != CUDA_SUCCESS)
+        return fail(UB_ECUDA, "ub_conv_fwd: encode activation tail tensor map failed");
+      p.tail_w = tw;
+    }
     const bool r_whole = d->res_coff == 0 && d->cout + 8 > d->res_cstride;
     if (p.has_res &&
         enc(&tmR, p.res, d->res_cstride, d->res_cstride - d->res_coff, EPI_CHUNK, r_whole) != CUDA_SUCCESS)
@@ -1113,18 +1134,18 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int pw = d->variant & 3;
   int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
-  if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-  if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-  if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+  if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+  if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
   const bool pointwise = d->kh == 1 && d->kw == 1 && d->stride == 1 && d->pad == 0;
   if (pointwise) {
-    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-    return launch_conv<A_TILED, 16>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+    if (bk == 64) return launch_conv<A_TILED, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+    if (bk == 32) return launch_conv<A_TILED, 32>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+    return launch_conv<A_TILED, 16>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
   }
-  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
-  return launch_conv<A_IM2COL, 16>(tmY, tmB, tmA, tmR, p, grid, smem, stream, wide);
+  if (bk == 64) return launch_conv<A_IM2COL, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+  if (bk == 32) return launch_conv<A_IM2COL, 32>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
+  return launch_conv<A_IM2COL, 16>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
 }
 
 extern "C" long long* ub_debug_conv_trace() { return ub::g_conv_trace; }

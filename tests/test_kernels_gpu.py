@@ -47,6 +47,10 @@ CASES = [
     ("two_ntiles_unaligned_390", 4, 14, 14, 232, 66, 128, 390, 1, 2, 0, 0, True, True, True, False),
     ("three_ntiles_700_gather", 2, 7, 7, 512, 0, 512, 700, 1, 1, 0, 300, True, False, False, False),
     ("1x1_s2_misaligned", 2, 56, 56, 56, 17, 32, 256, 1, 2, 0, 0, True, False, False, False),
+    # narrower last A box (16 / 32 channels) for slices ending just past a 64-channel block
+    ("1x1_tail16_slice", 2, 14, 14, 240, 70, 128, 64, 1, 1, 0, 0, True, False, True, False),
+    ("1x1_tail32_res", 2, 14, 14, 96, 0, 84, 100, 1, 1, 0, 0, True, True, True, False),
+    ("1x1_tail16_lead1_two_ntiles", 2, 7, 7, 504, 137, 256, 300, 1, 1, 0, 0, True, False, True, False),
     # packed taps (cin + lead <= 32): several filter taps per 64-wide K-block
     ("packed_3x3_c16", 2, 28, 28, 16, 0, 16, 64, 3, 1, 1, 0, True, False, True, False),
     ("packed_3x3_c24_lead5", 2, 20, 20, 64, 5, 24, 40, 3, 1, 1, 0, True, True, True, False),

@@ -31,6 +31,9 @@ CASES = {
     "l1_conv1_slice": (256, 56, 56, 240, 0, 128, 64, 1, 1, 0, 0, False, True),
     "l1_conv1_dense": (256, 56, 56, 128, 0, 128, 64, 1, 1, 0, 0, False, True),
     "r50_l1_0_conv1": (256, 56, 56, 56, 0, 32, 32, 1, 1, 0, 0, False, True),
+    "r50_l2_0_conv1": (256, 56, 56, 240, 70, 128, 64, 1, 1, 0, 0, False, True),
+    "r50_l2_3_conv1": (256, 28, 28, 504, 137, 256, 64, 1, 1, 0, 0, False, True),
+    "r50_l4_2_conv1": (256, 7, 7, 1816, 530, 1024, 256, 1, 1, 0, 0, False, True),
     "r50_l4_conv3_res": (256, 7, 7, 256, 0, 256, 1816, 1, 1, 0, 0, True, True),
     "r50_l4_0_conv1_cover": (256, 14, 14, 1016, 0, 1016, 256, 1, 1, 0, 0, False, True),
     "r50_l4_0_conv1_dense": (256, 14, 14, 512, 0, 512, 256, 1, 1, 0, 0, False, True),
