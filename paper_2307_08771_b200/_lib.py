@@ -86,6 +86,8 @@ SIGNATURES = {
     "ub_maxpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                              c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_avgpool_global": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_avgpool_gather": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int,
+                                  c_vp]),
     "ub_affine_add_relu": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_ll,
                                    c_int, c_vp, c_int, c_int, c_vp]),
 }

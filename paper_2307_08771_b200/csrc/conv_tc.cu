@@ -969,7 +969,13 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
     ++p.n_tiles;
   {
     const int n_gran = p.n_tiles > 1 ? EPI_CHUNK : 16;
-    p.block_n = (((d->cout + p.n_tiles - 1) / p.n_tiles) + n_gran - 1) / n_gran * n_gran;
+    const int per_tile = (d->cout + p.n_tiles - 1) / p.n_tiles;
+    p.block_n = (per_tile + n_gran - 1) / n_gran * n_gran;
+    // rounding up can undo the split (fc 1000 / 15 tiles -> 67 -> 128 -> 8 tiles): while the
+    // grid is still short of the SMs, round down instead (1000 -> 16 tiles of 64)
+    if (p.n_tiles > 1 && per_tile >= n_gran &&
+        static_cast<long long>(p.m_tiles) * ((d->cout + p.block_n - 1) / p.block_n) < num_sms())
+      p.block_n = per_tile / n_gran * n_gran;
     if (p.block_n > max_bn) p.block_n = max_bn;
     p.n_tiles = (d->cout + p.block_n - 1) / p.block_n;
   }

@@ -62,7 +62,7 @@ class Engine:
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
                  stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5,
-                 dual_store: bool = False, stem_pack_fused: bool = False):
+                 dual_store: bool = False, stem_pack_fused: bool = False, pool_gather: bool = True):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
@@ -70,6 +70,7 @@ class Engine:
         self.cover_ratio = cover_ratio
         self.dual_store = dual_store
         self.stem_pack_fused = stem_pack_fused
+        self.pool_gather = pool_gather
         self.graph = graph
         self.specs = specs
         self.batch = batch
@@ -273,6 +274,26 @@ class Engine:
                     sop.output = mp.output
                     ops.remove(mp)
 
+        # --- global avg pool -> GATHER read fusion: when a pool's only reader is a conv that
+        # GATHERs its channels (ResNet: avgpool -> flatten -> fc.read -> fc), the pool writes
+        # the gathered channels compacted (ub_avgpool_gather) and the conv reads them densely
+        if self.pool_gather and self.gather_mode == "fused":
+            for pop in [o for o in ops if o.kind == "avgpool"]:
+                readers = [o for o in ops if any(base(i) == pop.output for i in o.inputs)]
+                if len(readers) != 1 or readers[0].kind != "conv":
+                    continue
+                cop = readers[0]
+                r = cop.info.get("read")
+                if (r is None or kinds[r] is not LayerKind.GATHER or "stem_idx" in cop.info
+                        or base(cop.info["src"]) != pop.output or cop.info.get("residual")
+                        or g.layer(pop.anchor).out_channels % 8):
+                    continue
+                pop.info["idx"] = g.layer(r).params
+                pop.output = r
+                cop.info["read"] = None
+                cop.info["src"] = r
+                cop.inputs[0] = r
+
         # --- schedule: Kahn over value dependencies, ties by topological position
         produced = {op.output: op for op in ops}
 
@@ -357,6 +378,12 @@ class Engine:
 
     def _bind_avgpool(self, op, ws, vs, output_feed):
         x = self._value(op.inputs[0])
+        idx = op.info.get("idx")
+        if idx is not None:  # fused GATHER read of the consumer: compacted kept channels
+            y = self._alloc(op.output, len(idx))
+            idx_dev = self._i32(idx)
+            op.launch = lambda: K.avgpool_gather(x, idx_dev, y)
+            return
         y = self._alloc(op.output, x.C)
         op.launch = lambda: K.avgpool_global(x, y)
 

@@ -247,6 +247,11 @@ def avgpool_global(x: Act, y: Act) -> None:
               _p(y.buf), y.cstride, y.coff, _stream())
 
 
+def avgpool_gather(x: Act, idx_dev: torch.Tensor, y: Act) -> None:
+    _lib.call("ub_avgpool_gather", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(idx_dev), idx_dev.numel(),
+              _p(y.buf), y.cstride, y.coff, _stream())
+
+
 def affine_add_relu(a: Act, y: Act, scale=None, shift=None, b: Act | None = None, relu=False) -> None:
     _lib.call("ub_affine_add_relu", _p(a.buf), a.cstride, a.coff, _p(scale), _p(shift),
               _p(b.buf) if b is not None else None, b.cstride if b else 0, b.coff if b else 0,

@@ -58,6 +58,14 @@ def test_resnet50_schedule(stub_kernels, r50, strategy, gather_mode, n_gather_op
             assert base(i) in produced or base(i) == "x", (op.output, i)
         produced.add(op.output)
     assert eng.output_value.C == 1000
+    # the fc's GATHER read is folded into the global pool (compacted kept channels) in fused mode
+    pool = next(op for op in eng.ops if op.kind == "avgpool")
+    fc = next(op for op in eng.ops if op.kind == "conv" and op.info["conv"] == "fc")
+    if gather_mode == "fused" and eg.layer("fc.read").kind.value == "gather":
+        assert pool.output == "fc.read" and fc.info["read"] is None and fc.inputs[0] == "fc.read"
+        assert tuple(pool.info["idx"]) == tuple(eg.layer("fc.read").params)
+    else:
+        assert "idx" not in pool.info
 
 
 def test_slices_are_views_not_copies(stub_kernels, r50):

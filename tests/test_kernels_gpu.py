@@ -413,3 +413,32 @@ def test_stage_input_gathers_channels():
     assert torch.equal(got[..., 0], _bf(x[:, 2]))
     assert torch.equal(got[..., 1], _bf(x[:, 0]))
     assert (got[..., 2:] == 0).all()
+
+
+@pytest.mark.parametrize("HW,C,coff,cs", [(49, 1816, 0, 1816), (49, 64, 8, 80), (3, 4096, 0, 4096), (81, 40, 0, 40)])
+def test_avgpool_gather_matches_pool_then_gather(HW, C, coff, cs):
+    """ub_avgpool_gather == global pool (fp32, / HW, bf16) followed by the GATHER (-1 -> 0),
+    compacted; checked against an fp64 host sum rounded to bf16 (the kernel's pixel-phase
+    partial sums may differ from a sequential fp32 sum by one bf16 ulp)."""
+    import numpy as np
+    dev = "cuda"
+    g = torch.Generator().manual_seed(HW * 7 + C)
+    N = 3
+    xw = torch.randn(N, cs, 1, HW, generator=g)
+    xa = K.act_from_nchw(xw.to(dev)).view(coff, C)
+    perm = torch.randperm(C, generator=g)[: max(4, C // 2)].sort().values.tolist()
+    idx = perm[:3] + [-1] + perm[3:]
+    idx_dev = torch.tensor(idx, dtype=torch.int32, device=dev)
+    ya = K.empty_act(N, 1, 1, len(idx), dev)
+    K.avgpool_gather(xa, idx_dev, ya)
+    torch.cuda.synchronize()
+    xb = _bf(xw).numpy().astype(np.float64)[:, coff:coff + C, 0, :]
+    pooled = (xb.sum(axis=2) / HW).astype(np.float32)
+    ref = np.zeros((N, len(idx)), dtype=np.float32)
+    for j, c in enumerate(idx):
+        if c >= 0:
+            ref[:, j] = pooled[:, c]
+    ref = torch.from_numpy(ref).to(torch.bfloat16).float()
+    got = ya.to_nchw().cpu().reshape(N, len(idx))
+    assert (got[:, 3] == 0).all()
+    assert torch.allclose(got, ref, rtol=8e-3, atol=1e-6)
