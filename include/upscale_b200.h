@@ -228,7 +228,7 @@ int ub_avgpool_global(const void* x, int N, int HW, int C, int x_cstride, int x_
 /* Global average pool fused with the GATHER that reads it (e.g. ResNet's avgpool -> fc.read):
  * y[n][y_coff + j] = bf16(mean over HW of x[n][.][x_coff + idx[j]]), 0 where idx[j] < 0
  * (interp.py:75-77 GATHER applied to the PASS_THROUGH pool output), written compacted so the
- * consumer reads a dense operand.  C, x_cstride, x_coff multiples of 8; C <= 12288. */
+ * consumer reads a dense operand.  C, x_cstride, x_coff multiples of 8; N <= 65535. */
 int ub_avgpool_gather(const void* x, int N, int HW, int C, int x_cstride, int x_coff,
                       const int32_t* idx, int n_idx, void* y, int y_cstride, int y_coff,
                       cudaStream_t stream);
