@@ -105,7 +105,23 @@ struct ConvKParams {
   int tail_w;        // (a_tma, BK 64) channels of the narrower last A box (16 / 32), 64 = none
   int epi_alt;       // (epi2, one 64-channel chunk per tile) the groups take alternate tiles
                      // (group g drains accumulator g) instead of alternate chunks
+  int mt2;           // (a_tma, streamed B, no residual) pairs of M-adjacent tiles share each B box:
+                     // 4 TMEM accumulators, the pair's second A box in the next ring stage
 };
+
+// Tile of a CTA's it-th step, -1 past its last.  Default: tiles blockIdx.x + it * gridDim.x.
+// Pair mode (p.mt2): units u = blockIdx.x + (it / 2) * gridDim.x of two M tiles (2 * (u / n_tiles)
+// and the next) with the same N tile; the half past m_tiles (odd m_tiles) ends the walk.
+__device__ __forceinline__ int tile_at(const ConvKParams& p, int it, int num_tiles) {
+  if (!p.mt2) {
+    const int t = blockIdx.x + it * gridDim.x;
+    return t < num_tiles ? t : -1;
+  }
+  const int u = blockIdx.x + (it >> 1) * gridDim.x;
+  const int mp = u / p.n_tiles;
+  const int m_tile = 2 * mp + (it & 1);
+  return m_tile < p.m_tiles ? m_tile * p.n_tiles + (u - mp * p.n_tiles) : -1;
+}
 #define UB_TRACE(slot)                                                                  \
   do {                                                                                  \
     if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && it < 64) p.trace[it * 8 + (slot)] = clock64(); \
@@ -161,10 +177,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   uint16_t* sY2 = reinterpret_cast<uint16_t*>(sBias + epi_warps * MAX_BLOCK_N);  // y2 staging (when set)
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sY2) + (p.y2 ? epi_warps * Y2_STAGE : 0));
   uint64_t* empty = full + stages;
-  uint64_t* tfull = empty + stages;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* bres = tempty + 3;  // resident B landed (PRODUCERS cp.async arrivals)
+  uint64_t* tfull = empty + stages;  // [4] (2 used unless pair mode)
+  uint64_t* tempty = tfull + 4;      // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  uint64_t* bres = tempty + 5;  // resident B landed (PRODUCERS cp.async arrivals)
+  const int nacc = p.mt2 ? 4 : 2;  // TMEM accumulators
+  const int acc_sh = p.mt2 ? 2 : 1;  // log2(nacc)
   int4* stem_tab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(full) + BAR_BYTES);  // A_STEM / A_PACKED
 
   const int warp = threadIdx.x >> 5;
@@ -183,7 +201,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       mbar_init(&full[s], p.a_tma ? 1 : PRODUCERS + (reg_mode(AMODE) ? PWARPS : 0) + (p.b_tma ? 1 : 0));
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < nacc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], p.epi_alt ? 4 : epi_warps);
     }
@@ -243,6 +261,58 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       int s = 0, it = 0;
       uint32_t ph = 0;
       if (p.b_res) mbar_wait(bres, 0);
+      if (p.mt2) {
+        // pair mode: per k-block, stage s holds A of the first tile + the shared B box, stage
+        // s + 1 the second tile's A; both MMAs read B from stage s
+        for (;; it += 2) {
+          const int t0 = tile_at(p, it, num_tiles);
+          if (t0 < 0) break;
+          const bool two = tile_at(p, it + 1, num_tiles) >= 0;
+          const int acc0 = it & 3, acc1 = (it + 1) & 3;
+          mbar_wait(&tempty[acc0], (it >> 2) & 1);
+          if (two) mbar_wait(&tempty[acc1], ((it + 1) >> 2) & 1);
+          __syncwarp();
+          tc_fence_after();
+          const uint32_t d0 = tmem_base + acc0 * p.acc_stride, d1 = tmem_base + acc1 * p.acc_stride;
+          for (int kb = 0; kb < nk; ++kb) {
+            const int s0 = s;
+            mbar_wait(&full[s0], ph);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+            }
+            int s1 = -1;
+            if (two) {
+              s1 = s;
+              mbar_wait(&full[s1], ph);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+            __syncwarp();
+            tc_fence_after();
+            const uint32_t b_base = smem_u32(sB + s0 * b_stride);
+            const bool tail = BK == 64 && kb == nk - 1 && p.tail_w < 64;
+            const uint32_t a_lay = tail ? (p.tail_w == 16 ? 6u : 4u) : LAYOUT;
+            const uint32_t a_sbo = tail ? 8u * p.tail_w * 2 : SBO;
+            const int ksteps = tail ? p.tail_w / 16 : BK / 16;
+            // the first tile's k-steps, then the second's (interleaving the two accumulators
+            // per k-step gave wrong columns 1.. on B200 -- measured, tools/pair_debug.py)
+            for (int k = 0; k < ksteps; ++k)
+              umma_bf16_warp(d0, make_sdesc(smem_u32(sA + s0 * A_BYTES) + k * 32, a_sbo, a_lay),
+                             make_sdesc(b_base + k * 32, SBO, LAYOUT), idesc, 1u);
+            if (two)
+              for (int k = 0; k < ksteps; ++k)
+                umma_bf16_warp(d1, make_sdesc(smem_u32(sA + s1 * A_BYTES) + k * 32, a_sbo, a_lay),
+                               make_sdesc(b_base + k * 32, SBO, LAYOUT), idesc, 1u);
+            umma_commit_warp(&empty[s0]);
+            if (two) umma_commit_warp(&empty[s1]);
+          }
+          umma_commit_warp(&tfull[acc0]);
+          if (two) umma_commit_warp(&tfull[acc1]);
+        }
+      } else
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         const int n0 = (t % p.n_tiles) * p.block_n;
@@ -348,7 +418,37 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     if (AMODE == A_TILED && p.a_tma) {
       // every operand of a 1x1/s1 tile is a TMA box: one thread issues A (BK ch x 128 px),
       // B (BK x block_n) and the residual chunks (64 ch x 128 px) per stage
-      if (pt == 0) {
+      if (pt == 0 && p.mt2) {
+        for (int it = 0;; it += 2) {
+          const int t0 = tile_at(p, it, num_tiles);
+          if (t0 < 0) break;
+          const bool two = tile_at(p, it + 1, num_tiles) >= 0;
+          const int m_tile = t0 / p.n_tiles;
+          const int n0 = (t0 - m_tile * p.n_tiles) * p.block_n;
+          const int m0 = m_tile * BLOCK_M;
+          for (int kb = 0; kb < nk; ++kb) {
+            const bool tail = kb == nk - 1 && p.tail_w < BK;
+            const uint32_t a_bytes = BLOCK_M * (tail ? static_cast<uint32_t>(p.tail_w) * 2 : ROW_BYTES);
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], a_bytes + static_cast<uint32_t>(p.block_n) * ROW_BYTES);
+            tma_load_2d(tail ? &tmAt : &tmA, &full[s], sA + s * A_BYTES, kb * BK, m0);
+            tma_load_2d(&tmB, &full[s], sB + s * b_stride, kb * BK, n0);
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1;
+            }
+            if (two) {
+              mbar_wait(&empty[s], ph ^ 1);
+              mbar_arrive_expect_tx(&full[s], a_bytes);
+              tma_load_2d(tail ? &tmAt : &tmA, &full[s], sA + s * A_BYTES, kb * BK, m0 + BLOCK_M);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+          }
+        }
+      } else if (pt == 0) {
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
           const int m_tile = t / p.n_tiles;
           const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
@@ -639,11 +739,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       }
       tmem_st32(taddr, bv);
     };
-    // initial arming of both accumulators (tiles blockIdx.x and blockIdx.x + gridDim.x)
-    for (int a = 0; a < 2; ++a) {
-      if (p.epi_alt && a != eg) continue;
-      const int tt = blockIdx.x + a * gridDim.x;
-      if (tt < num_tiles) {
+    // initial arming of the accumulators (the CTA's first nacc tiles)
+    for (int a = 0; a < nacc; ++a) {
+      if (p.epi_alt && (a & 1) != eg) continue;
+      const int tt = tile_at(p, a, num_tiles);
+      if (tt >= 0) {
         stage_bias(tt);
         const uint32_t ta = tmem_base + a * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
         for (int col = 0; col < static_cast<int>(p.acc_stride); col += 32)
@@ -656,7 +756,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     }
     int it = 0;
     const int c0 = p.epi_alt ? 0 : eg, cstep = p.epi_alt ? 1 : ngrp;  // this warp's chunks of a tile
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (;; ++it) {
+      const int t = tile_at(p, it, num_tiles);
+      if (t < 0) break;
       if (p.epi_alt && (it & 1) != eg) continue;
       const int m_tile = t / p.n_tiles;
       const int n0 = (t - m_tile * p.n_tiles) * p.block_n;
@@ -664,12 +766,12 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       const int rows0 = m0 + q * 32;
       const int ncols = min(p.block_n, p.cout - n0);
       const int nchunks = (ncols + EPI_CHUNK - 1) / EPI_CHUNK;
-      const int t_next = t + 2 * gridDim.x;  // next user of this accumulator
-      const bool rearm = t_next < num_tiles;
+      const int t_next = tile_at(p, it + nacc, num_tiles);  // next user of this accumulator
+      const bool rearm = t_next >= 0;
       if (rearm && p.n_tiles > 1) stage_bias(t_next);  // (one N tile: every tile's bias is the same)
-      const int acc = it & 1;
+      const int acc = it & (nacc - 1);
       if (ew == 0) UB_TRACE(3);
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      mbar_wait(&tfull[acc], (it >> acc_sh) & 1);
       if (ew == 0) UB_TRACE(4);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
@@ -993,12 +1095,18 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   p.Wo = d->Wo;
   p.stride = d->stride;
   p.pad = d->pad;
-  // two accumulators, each a whole number of 64-column epilogue chunks wide
+  // pair mode (variant bit 15): TMA-fed 1x1 without residual, N tiles <= 128 channels, streamed
+  // weights -- two M tiles per B box halve the weight bytes each SM pulls from L2
+  const bool tiled_1x1_mt = !stem && !packed && !gather && d->kh == 1 && d->kw == 1 && d->stride == 1 &&
+                            d->pad == 0 && !(d->variant & 32);
+  p.mt2 = (d->variant & 32768) && tiled_1x1_mt && !d->residual && !d->y2 && p.block_n <= 128 && p.m_tiles >= 2;
+  // two accumulators (four in pair mode), each a whole number of 64-column epilogue chunks wide
+  const uint32_t nacc = p.mt2 ? 4u : 2u;
   const uint32_t acc_cols = (static_cast<uint32_t>(p.block_n) + EPI_CHUNK - 1) / EPI_CHUNK * EPI_CHUNK;
   uint32_t tc = 32;
-  while (tc < 2u * acc_cols) tc <<= 1;
+  while (tc < nacc * acc_cols) tc <<= 1;
   p.tmem_cols = tc;
-  p.acc_stride = tc / 2;
+  p.acc_stride = tc / nacc;
   p.x = stem ? nullptr : reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
   p.x_cstride = d->x_cstride;
   p.w = reinterpret_cast<const uint16_t*>(d->w);
@@ -1060,7 +1168,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   // keeps its N tile's weights in smem (grid a multiple of n_tiles, so a CTA's tiles share
   // one N tile) instead of re-loading B for every tile.
   const uint32_t b_res_bytes = static_cast<uint32_t>(p.num_kb) * b_stride;
-  p.b_res = !(d->variant & 4) && p.n_tiles <= num_sms() && fixed + b_res_bytes + 4 * a_bytes <= 226u * 1024u;
+  p.b_res = !(d->variant & 4) && !p.mt2 && p.n_tiles <= num_sms() && fixed + b_res_bytes + 4 * a_bytes <= 226u * 1024u;
   if (p.b_res) fixed += b_res_bytes;
   const uint32_t stage_bytes = a_bytes + (p.b_res ? 0u : b_stride);
   const uint32_t budget = 226u * 1024u - fixed;
@@ -1133,7 +1241,7 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
         enc(&tmR, p.res, d->res_cstride, d->res_cstride - d->res_coff, EPI_CHUNK, r_whole) != CUDA_SUCCESS)
       return fail(UB_ECUDA, "ub_conv_fwd: encode residual tensor map failed");
   }
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int num_tiles = p.mt2 ? (p.m_tiles + 1) / 2 * p.n_tiles : p.m_tiles * p.n_tiles;  // work units
   int grid = num_tiles < num_sms() ? num_tiles : num_sms();
   if (p.b_res && grid % p.n_tiles) grid = grid / p.n_tiles * p.n_tiles;
   // producer width: explicit variant from the caller (engine autotune), else a heuristic

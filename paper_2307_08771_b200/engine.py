@@ -548,6 +548,8 @@ class Engine:
                    for at in ((0, 32) if tiled else (32,)) for e1 in ((0, 64) if tiled else (0,))]
             if kk == 1 and cout > 192:  # +8192: N tiles of <= 128 channels (weights may stay resident)
                 gen = gen + [v | 8192 for v in gen if not v & 4]
+            # (+32768 pair mode -- two M tiles per streamed weight box -- is not offered: it
+            # measured slower on every wide-K 1x1 of ResNet-50)
             if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
                 gen = [0, 128] + [v | 8 for v in gen]
             return gen

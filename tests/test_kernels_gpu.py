@@ -442,3 +442,42 @@ def test_avgpool_gather_matches_pool_then_gather(HW, C, coff, cs):
     got = ya.to_nchw().cpu().reshape(N, len(idx))
     assert (got[:, 3] == 0).all()
     assert torch.allclose(got, ref, rtol=8e-3, atol=1e-6)
+
+
+PAIR_CASES = [
+    # name, N, H, W, cstride, coff, cin, cout, variant extra
+    ("fc_1000_m2", 256, 1, 1, 1024, 0, 1024, 1000, 0),
+    ("cover_odd_mtiles", 3, 14, 14, 1016, 0, 1016, 128, 0),
+    ("slice_tail16_cout64", 4, 14, 14, 240, 70, 128, 64, 0),
+    ("slice_lead2_two_ntiles", 8, 7, 7, 1816, 530, 1024, 256, 8192),
+    ("single_pair_short", 1, 15, 15, 64, 0, 64, 96, 0),
+]
+
+
+@pytest.mark.parametrize("case", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
+def test_conv_pair_mode_bit_exact(case):
+    """Variant +32768 (two M tiles per streamed weight box, four TMEM accumulators) gives the
+    same bits as the default schedule (same k-block order per tile) and matches torch."""
+    name, N, H, W, cs, coff, cin, cout, extra = case
+    dev = "cuda"
+    g = torch.Generator(device="cpu").manual_seed(sum(map(ord, name)))
+    xfull = torch.randn(N, cs, H, W, generator=g)
+    x = K.act_from_nchw(xfull.to(dev))
+    xa = x.view(coff, cin)
+    Wt = torch.randn(cout, cin, 1, 1, generator=g) / cin ** 0.5
+    lead, cpad = _lib.conv_weight_layout(cin, coff, False, 1, 1)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)),
+                           layout="gemm", lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
+    bias = torch.randn(cout, generator=g).to(dev)
+    outs = []
+    for v in (1 | 4 | extra, 1 | 4 | 32768 | extra):
+        y = K.empty_act(N, H, W, cout, dev)
+        y.buf.fill_(float("nan"))
+        K.conv(xa, wg, lead, cpad, cout, 1, 1, 1, 0, y, bias=bias, relu=True, variant=v)
+        torch.cuda.synchronize()
+        outs.append(y.buf[:, :cout].clone())
+    ref = torch.nn.functional.conv2d(_bf(xfull[:, coff:coff + cin]).to(dev), _bf(Wt).to(dev))
+    ref = (ref + bias.view(1, -1, 1, 1)).clamp_min(0)
+    errs = [_rel(o.float().reshape(N, H, W, cout).permute(0, 3, 1, 2), ref) for o in outs]
+    assert max(errs) < 1e-2, (name, errs)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), name
