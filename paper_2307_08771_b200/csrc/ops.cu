@@ -377,6 +377,68 @@ __global__ void __launch_bounds__(128) avgpool_gather_kernel(const uint4* __rest
   }
 }
 
+// Small-batch form: CTA = (256-channel block, image), warp q reads pixels q, q + 8, ... (a warp
+// covers 512 contiguous bytes of a pixel row) with up to 7 predicated loads in flight per
+// thread -- one DRAM round trip per 56 pixels instead of 7 for the thread-walks-all-pixels
+// form.  The 8 phase sums meet in shared memory (added in phase order).  Faster when the
+// grid is small (N = 1: 12 vs 18 us, events, L2 flushed) but slower at N = 256 (25 vs 20 us),
+// so ub_avgpool_gather picks it only while the large form would leave SMs idle.
+constexpr int APG_PHASES = 8, APG_UNROLL = 7;
+__global__ void __launch_bounds__(256) avgpool_gather_phased_kernel(const uint4* __restrict__ x, int HW, int C8,
+                                                                    int x_cstride8, int x_coff8,
+                                                                    const int32_t* __restrict__ idx, int n_idx,
+                                                                    __nv_bfloat16* __restrict__ y, int y_cstride,
+                                                                    int y_coff) {
+  __shared__ float part[APG_PHASES][32 * 8];
+  __shared__ float pooled[32 * 8];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int img = blockIdx.y;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int c8 = blockIdx.x * 32 + lane;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c8 < C8) {
+    const uint4* xp = x + static_cast<long long>(img) * HW * x_cstride8 + x_coff8 + c8;
+    for (int p0 = q; p0 < HW; p0 += APG_PHASES * APG_UNROLL) {
+      uint4 v[APG_UNROLL];
+#pragma unroll
+      for (int u = 0; u < APG_UNROLL; ++u) {
+        const int p = p0 + u * APG_PHASES;
+        v[u] = p < HW ? __ldg(xp + static_cast<long long>(p) * x_cstride8) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < APG_UNROLL; ++u) {  // zero-filled slots add +0.0f
+        const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = bf16x2_to_f32x2(wv[j]);
+          s[2 * j] += f.x;
+          s[2 * j + 1] += f.y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[q][lane * 8 + j] = s[j];
+  __syncthreads();
+  {
+    float t = part[0][threadIdx.x];
+#pragma unroll
+    for (int r = 1; r < APG_PHASES; ++r) t += part[r][threadIdx.x];
+    pooled[threadIdx.x] = t / HW;
+  }
+  __syncthreads();
+  __nv_bfloat16* yi = y + static_cast<long long>(img) * y_cstride + y_coff;
+  const int c_lo = blockIdx.x * 256, c_hi = min(c_lo + 256, C8 * 8);
+  for (int j = threadIdx.x; j < n_idx; j += blockDim.x) {
+    const int c = __ldg(idx + j);
+    if (c >= c_lo && c < c_hi)
+      yi[j] = __float2bfloat16_rn(pooled[c - c_lo]);
+    else if (c < 0 && blockIdx.x == 0)
+      yi[j] = __float2bfloat16_rn(0.f);
+  }
+}
+
 // ------------------------------------------------------------- affine / add / relu
 __global__ void affine_add_relu_kernel(const __nv_bfloat16* __restrict__ a, int a_cstride, int a_coff,
                                        const float* __restrict__ scale, const float* __restrict__ shift,
@@ -665,6 +727,14 @@ extern "C" int ub_avgpool_gather(const void* x, int N, int HW, int C, int x_cstr
     return fail(UB_EUNSUPPORTED, "ub_avgpool_gather: C, x_cstride and x_coff must be multiples of 8");
   if (N > 65535) return fail(UB_EUNSUPPORTED, "ub_avgpool_gather: N too large");
   const int C8 = C / 8;
+  if (static_cast<long long>(N) * ((C8 + 127) / 128) < num_sms()) {  // small batch: phased form
+    const dim3 grid((C8 + 31) / 32, N);
+    const cudaError_t e = launch_pdl(avgpool_gather_phased_kernel, grid, dim3(256), 0, stream,
+                                     static_cast<const uint4*>(x), HW, C8, x_cstride / 8, x_coff / 8, idx, n_idx,
+                                     static_cast<__nv_bfloat16*>(y), y_cstride, y_coff);
+    count_launch();
+    return cuda_status(e, "avgpool_gather_phased_kernel");
+  }
   const dim3 grid((C8 + 127) / 128, N);
   const cudaError_t e = launch_pdl(avgpool_gather_kernel, grid, dim3(128), 0, stream, static_cast<const uint4*>(x), HW,
                                    C8, x_cstride / 8, x_coff / 8, idx, n_idx, static_cast<__nv_bfloat16*>(y),

@@ -153,3 +153,27 @@ def test_export_artifact_runs_like_the_live_export(tmp_path):
     res, model = artifact.load_export(tmp_path / "r18")
     back = EN.from_export(model, res, batch=2).forward(x.cuda()).cpu()
     assert torch.equal(live, back)
+
+
+def test_resnet50_full_batch_256_autotuned_matches_oracle_on_sampled_images():
+    """The bench configuration itself (N = 256, autotuned variants, CUDA-graph replay):
+    sampled images across the batch (first / last M tiles, both halves) match the oracle,
+    and match a small-batch engine on the same images (images are independent, so the batch
+    size -- i.e. the tiling and the variants autotune picks -- must not change the result
+    beyond the bf16 gate)."""
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    N = 256
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(7))
+    eng = EN.from_plans(sm, eg, maps, batch=N)
+    eng.capture()  # autotune + graph, as bench.py
+    got = eng.forward(x.cuda()).cpu()
+    assert torch.isfinite(got).all()
+    pick = [0, 1, 63, 127, 128, 200, 254, 255]
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x[pick], dtype=torch.float32)
+    assert deviation(got[pick], ref) <= TOL
+    assert top1_agreement(got[pick], ref) == 1.0
+    small = EN.from_plans(sm, eg, maps, batch=len(pick))
+    got_small = small.forward(x[pick].cuda()).cpu()
+    assert deviation(got[pick], got_small) <= TOL
+    assert top1_agreement(got[pick], got_small) == 1.0

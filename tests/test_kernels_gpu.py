@@ -415,15 +415,16 @@ def test_stage_input_gathers_channels():
     assert (got[..., 2:] == 0).all()
 
 
-@pytest.mark.parametrize("HW,C,coff,cs", [(49, 1816, 0, 1816), (49, 64, 8, 80), (3, 4096, 0, 4096), (81, 40, 0, 40)])
-def test_avgpool_gather_matches_pool_then_gather(HW, C, coff, cs):
+@pytest.mark.parametrize("HW,C,coff,cs,N", [(49, 1816, 0, 1816, 3), (49, 64, 8, 80, 3), (3, 4096, 0, 4096, 3),
+                                            (81, 40, 0, 40, 3), (49, 1816, 0, 1816, 80), (130, 64, 8, 80, 150)])
+def test_avgpool_gather_matches_pool_then_gather(HW, C, coff, cs, N):
     """ub_avgpool_gather == global pool (fp32, / HW, bf16) followed by the GATHER (-1 -> 0),
-    compacted; checked against an fp64 host sum rounded to bf16 (the kernel's pixel-phase
+    compacted, in both forms (N = 3: phased small-batch kernel; N = 80 / 150: the large one;
+    HW = 130 > 56 takes the phased loop twice); checked against an fp64 host sum rounded to bf16 (the kernel's pixel-phase
     partial sums may differ from a sequential fp32 sum by one bf16 ulp)."""
     import numpy as np
     dev = "cuda"
     g = torch.Generator().manual_seed(HW * 7 + C)
-    N = 3
     xw = torch.randn(N, cs, 1, HW, generator=g)
     xa = K.act_from_nchw(xw.to(dev)).view(coff, C)
     perm = torch.randperm(C, generator=g)[: max(4, C // 2)].sort().values.tolist()
