@@ -66,3 +66,19 @@ def test_sm100a_code_is_in_the_library(lib):
     assert "UTMASTG" in sass       # TMA bulk tensor store
     assert "LDGSTS" in sass        # cp.async producers
     assert "LDTM" in sass and "STTM" in sass  # tcgen05.ld / tcgen05.st
+
+
+def test_argument_errors_fail_loudly_without_touching_the_device(lib):
+    """Bad arguments come back as negative status + ub_last_error text (raised as UBError by
+    the binding) before any CUDA call, so this runs without a GPU."""
+    import ctypes
+
+    with pytest.raises(_lib.UBError, match="ub_avgpool_gather: bad arguments"):
+        _lib.call("ub_avgpool_gather", ctypes.c_void_p(16), 2, 49, 64, 64, 0, None, 8,
+                  ctypes.c_void_p(16), 8, 0, None)
+    with pytest.raises(_lib.UBError, match="multiples of 8"):
+        _lib.call("ub_avgpool_gather", ctypes.c_void_p(16), 2, 49, 60, 64, 0, ctypes.c_void_p(16), 8,
+                  ctypes.c_void_p(16), 8, 0, None)
+    with pytest.raises(_lib.UBError, match="ub_avgpool_global"):
+        _lib.call("ub_avgpool_global", None, 2, 49, 64, 64, 0, ctypes.c_void_p(16), 64, 0, None)
+    assert lib.ub_last_error()
