@@ -1065,12 +1065,16 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   // store only clips at cout).
   // variant bit 13: N tiles of at most 128 channels (their weights may then stay resident)
   const int max_bn = (d->variant & 8192) ? 128 : MAX_BLOCK_N;
+  // variant bit 16: 32-channel granularity for multi-tile N when the output is fp32 (direct
+  // stores bounded by the tile's own columns, no 64-channel TMA box that could spill into the
+  // next tile) and there is no residual -- the classifier: twice the CTAs share its weights
+  const int multi_gran = ((d->variant & 65536) && d->y_dtype == UB_F32 && !d->residual) ? 32 : EPI_CHUNK;
   p.n_tiles = (d->cout + max_bn - 1) / max_bn;
   while (static_cast<long long>(p.m_tiles) * p.n_tiles < num_sms() &&
-         (d->cout + p.n_tiles) / (p.n_tiles + 1) >= EPI_CHUNK)
+         (d->cout + p.n_tiles) / (p.n_tiles + 1) >= multi_gran)
     ++p.n_tiles;
   {
-    const int n_gran = p.n_tiles > 1 ? EPI_CHUNK : 16;
+    const int n_gran = p.n_tiles > 1 ? multi_gran : 16;
     const int per_tile = (d->cout + p.n_tiles - 1) / p.n_tiles;
     p.block_n = (per_tile + n_gran - 1) / n_gran * n_gran;
     // rounding up can undo the split (fc 1000 / 15 tiles -> 67 -> 128 -> 8 tiles): while the

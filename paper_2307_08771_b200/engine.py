@@ -538,7 +538,8 @@ class Engine:
         # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
         # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
-        # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path;
+        # +64 one epilogue warpgroup instead of two on the TMA-fed 1x1 path; +65536 32-channel
+        # N tiles for an fp32 output without residual (the classifier);
         # +8 no halo-tile kernel for a 3x3 (stride 1 or 2); +128 halo kernel with two epilogue groups)
         halo = kk == 3 and st in (1, 2) and pd == 1
 
@@ -550,6 +551,8 @@ class Engine:
                 gen = gen + [v | 8192 for v in gen if not v & 4]
             # (+32768 pair mode -- two M tiles per streamed weight box -- is not offered: it
             # measured slower on every wide-K 1x1 of ResNet-50)
+            if fp32_out and residual is None:  # +65536: 32-channel N tiles (fp32 classifier)
+                gen = gen + [v | 65536 for v in gen if not v & 8192]
             if halo:  # the halo kernel ignores the generic bits; offer it twice, then the generic kernel
                 gen = [0, 128] + [v | 8 for v in gen]
             return gen

@@ -482,3 +482,28 @@ def test_conv_pair_mode_bit_exact(case):
     errs = [_rel(o.float().reshape(N, H, W, cout).permute(0, 3, 1, 2), ref) for o in outs]
     assert max(errs) < 1e-2, (name, errs)
     assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), name
+
+
+@pytest.mark.parametrize("N,cout", [(4, 1000), (256, 1000), (2, 70)])
+def test_conv_fp32_classifier_32_channel_tiles_bit_exact(N, cout):
+    """Variant +65536 (32-channel N tiles for an fp32 output): same bits as the 64-channel
+    tiling (same k-block order per output), no write outside each tile's own columns."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(N + cout)
+    cin = 1024
+    x = K.act_from_nchw(torch.randn(N, cin, 1, 1, generator=g).to(dev))
+    Wt = torch.randn(cout, cin, 1, 1, generator=g) / cin ** 0.5
+    lead, cpad = _lib.conv_weight_layout(cin, 0, False, 1, 1)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)),
+                           layout="gemm", lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
+    bias = torch.randn(cout, generator=g).to(dev)
+    outs = []
+    for v in (0, 65536):
+        y = K.Act(torch.full((N, K.pad8(cout)), float("nan"), device=dev), N, 1, 1, cout)
+        K.conv(x, wg, lead, cpad, cout, 1, 1, 1, 0, y, bias=bias, y_fp32=True, variant=v)
+        torch.cuda.synchronize()
+        outs.append(y.buf.clone())
+    assert torch.equal(outs[0][:, :cout], outs[1][:, :cout])
+    assert torch.isnan(outs[1][:, cout:]).all()
+    ref = x.to_nchw().reshape(N, cin).to(dev) @ _bf(Wt).reshape(cout, cin).to(dev).T + bias
+    assert _rel(outs[1][:, :cout], ref) < 1e-2
