@@ -23,6 +23,8 @@ CASES = {
     "l3_conv3_1016": (256, 14, 14, 128, 0, 128, 1016, 1, 1, 0, 0, True, True),
     "l4_conv1_1024": (256, 7, 7, 1816, 0, 1024, 256, 1, 1, 0, 0, False, True),
     "fc_dense": (256, 1, 1, 1024, 0, 1024, 1000, 1, 1, 0, 0, False, False),
+    "b1_l4_conv2_3x3": (1, 7, 7, 256, 0, 256, 256, 3, 1, 1, 0, False, True),
+    "b1_l3_conv2_3x3": (1, 14, 14, 128, 0, 128, 128, 3, 1, 1, 0, False, True),
     "l3_conv1_cover": (256, 14, 14, 1016, 0, 1016, 128, 1, 1, 0, 0, False, True),
     "l4_conv2_3x3": (256, 7, 7, 256, 0, 256, 256, 3, 1, 1, 0, False, True),
     "l3_conv2_3x3": (256, 14, 14, 128, 0, 128, 128, 3, 1, 1, 0, False, True),
