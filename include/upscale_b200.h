@@ -73,6 +73,14 @@ int ub_permute_weights(const void* W, int dtype_in, int O, int I, int kh, int kw
                        void* out, int dtype_out, cudaStream_t stream);
 
 /*
+ * Number of plan indices ub_permute_weights found outside [0, O) x [0, I) since the
+ * last call (those elements are written as 0 and nothing is read for them); resets
+ * the counter.  Synchronous (device-wide); export time only.  Guards against a bad
+ * or mismatched plan file turning into an out-of-bounds device read.
+ */
+int ub_index_faults(unsigned long long* count);
+
+/*
  * Per-channel vector permutation.  Replaces planner.py:731-733
  * (new_weights[u] = new_weights[u][perm]).  out[i] = v[idx[i]] (idx[i] == -1 -> 0).
  */

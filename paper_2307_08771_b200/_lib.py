@@ -62,6 +62,7 @@ SIGNATURES = {
     "ub_permute_weights": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_int,
                                    c_vp, c_int, c_int, c_int, c_vp, c_int, c_vp]),
     "ub_permute_vector": (c_int, [c_vp, c_int, c_vp, c_int, c_vp, c_vp]),
+    "ub_index_faults": (c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
     "ub_channel_gather_2d": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int,
                                      c_vp]),
@@ -125,6 +126,14 @@ def check(rc: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args))
+
+
+def index_faults() -> int:
+    """Plan indices the permute kernel found outside the source tensor since the last
+    call (synchronising; export time only)."""
+    n = ctypes.c_ulonglong()
+    check(load().ub_index_faults(ctypes.byref(n)))
+    return int(n.value)
 
 
 def launch_count() -> int:

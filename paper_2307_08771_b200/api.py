@@ -131,7 +131,9 @@ class Runner:
     def run_many(self, batches):
         """Pipelined run over an iterable of equally-sized pinned host batches; yields
         the logits of each batch (host numpy) in order.  Batch i+1's H2D overlaps batch
-        i's forward; every batch still crosses PCIe and every result comes back."""
+        i's forward; every batch still crosses PCIe and every result comes back.  A host
+        batch is no longer read once the next one is pulled from `batches` (its copy has
+        landed), so a loader may refill one pinned buffer in place."""
         compute = torch.cuda.current_stream()
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(device=self.device)
@@ -159,6 +161,9 @@ class Runner:
             host.copy_(eng.output_tensor(), non_blocking=True)
             d2h = torch.cuda.Event()
             d2h.record(compute)
+            # the caller may refill the host tensor it just handed over once we pull the
+            # next batch: its H2D must have landed first
+            landed.synchronize()
             if pending is not None:
                 pending[0].synchronize()
                 yield pending[1].numpy().copy()

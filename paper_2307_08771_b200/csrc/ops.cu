@@ -17,11 +17,15 @@ namespace {
 template <typename T>
 __device__ __forceinline__ float to_f(T v) { return static_cast<float>(v); }
 
+// Plan indices that point outside the source tensor (a bad or mismatched plan file):
+// the kernels read nothing for them and count them here; ub_index_faults() reports.
+__device__ unsigned long long g_index_faults = 0;
+
 // ------------------------------------------------------------- permute weights
 // planner.py:661-673 (rows) + 755-767 (columns), both sides of a layer fused.
 // Iterates over OUTPUT elements so the writes are coalesced; reads gather.
 template <typename TI, typename TO, int LAYOUT>
-__global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps, const int32_t* __restrict__ rows,
+__global__ void permute_weights_kernel(const TI* __restrict__ W, int O, int I, int taps, const int32_t* __restrict__ rows,
                                        int n_rows, const int32_t* __restrict__ cols, int n_cols,
                                        const float* __restrict__ scale, int lead, int cpad, TO* __restrict__ out,
                                        long long total) {
@@ -63,7 +67,9 @@ __global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps
     if (inside) {
       const int src_r = rows[r];
       const int src_c = cols[c];
-      if (src_r >= 0 && src_c >= 0) {
+      if (src_r >= O || src_c >= I) {
+        atomicAdd(&g_index_faults, 1ull);
+      } else if (src_r >= 0 && src_c >= 0) {
         const TI w = W[((long long)src_r * I + src_c) * taps + t];
         if (scale) {
           v = static_cast<TO>(static_cast<float>(w) * scale[r]);
@@ -77,7 +83,7 @@ __global__ void permute_weights_kernel(const TI* __restrict__ W, int I, int taps
 }
 
 template <typename TI, typename TO>
-int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows, int n_rows, const int32_t* cols,
+int permute_dispatch_layout(const void* W, int O, int I, int taps, const int32_t* rows, int n_rows, const int32_t* cols,
                             int n_cols, const float* scale, int layout, int lead, int cpad, void* out,
                             cudaStream_t s) {
   const long long total = layout == UB_LAYOUT_OIHW    ? (long long)n_rows * n_cols * taps
@@ -87,16 +93,16 @@ int permute_dispatch_layout(const void* W, int I, int taps, const int32_t* rows,
   const int grid = grid_for(total, block, 4);
   if (layout == UB_LAYOUT_OIHW)
     permute_weights_kernel<TI, TO, UB_LAYOUT_OIHW><<<grid, block, 0, s>>>(
-        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+        static_cast<const TI*>(W), O, I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   else if (layout == UB_LAYOUT_GEMM)
     permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM><<<grid, block, 0, s>>>(
-        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+        static_cast<const TI*>(W), O, I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   else if (layout == UB_LAYOUT_S2D)
     permute_weights_kernel<TI, TO, UB_LAYOUT_S2D><<<grid, block, 0, s>>>(
-        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+        static_cast<const TI*>(W), O, I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   else
     permute_weights_kernel<TI, TO, UB_LAYOUT_GEMM_DENSE><<<grid, block, 0, s>>>(
-        static_cast<const TI*>(W), I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
+        static_cast<const TI*>(W), O, I, taps, rows, n_rows, cols, n_cols, scale, lead, cpad, static_cast<TO*>(out), total);
   count_launch();
   return cuda_status(cudaGetLastError(), "permute_weights_kernel");
 }
@@ -486,20 +492,28 @@ extern "C" int ub_permute_weights(const void* W, int dtype_in, int O, int I, int
   const int taps = kh * kw;
   if (dtype_in == UB_F32) {
     if (dtype_out == UB_F32)
-      return permute_dispatch_layout<float, float>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+      return permute_dispatch_layout<float, float>(W, O, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
                                                    cpad, out, stream);
     if (dtype_out == UB_BF16)
-      return permute_dispatch_layout<float, __nv_bfloat16>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout,
+      return permute_dispatch_layout<float, __nv_bfloat16>(W, O, I, taps, rows, n_rows, cols, n_cols, row_scale, layout,
                                                            lead, cpad, out, stream);
   } else if (dtype_in == UB_F64) {
     if (dtype_out == UB_F64)
-      return permute_dispatch_layout<double, double>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+      return permute_dispatch_layout<double, double>(W, O, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
                                                      cpad, out, stream);
     if (dtype_out == UB_F32)
-      return permute_dispatch_layout<double, float>(W, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
+      return permute_dispatch_layout<double, float>(W, O, I, taps, rows, n_rows, cols, n_cols, row_scale, layout, lead,
                                                     cpad, out, stream);
   }
   return fail(UB_EUNSUPPORTED, "ub_permute_weights: dtype pair (%d -> %d)", dtype_in, dtype_out);
+}
+
+extern "C" int ub_index_faults(unsigned long long* count) {
+  if (!count) return fail(UB_EINVAL, "ub_index_faults: null pointer");
+  const unsigned long long zero = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(count, g_index_faults, sizeof(zero));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_index_faults, &zero, sizeof(zero));
+  return cuda_status(e, "ub_index_faults");
 }
 
 extern "C" int ub_permute_vector(const void* v, int dtype, const int32_t* idx, int n, void* out,

@@ -84,6 +84,9 @@ class Engine:
         self._graph_exec = None
         self._shapes = self._infer_shapes()
         self._compile(weight_source, vector_source)
+        bad = _lib.index_faults() if self.device.type == "cuda" else 0
+        if bad:
+            raise ValueError(f"engine: {bad} plan indices outside their source tensors")
 
     # ------------------------------------------------------------------ shapes
     def _infer_shapes(self) -> dict[str, tuple[int, int, int]]:

@@ -76,22 +76,60 @@ def test_compose_maps_matches_sequential_plans():
         assert len(set(perm)) == len(perm) == eg.layer(uid).out_channels
 
 
-def test_output_mode_is_refused():
+def test_output_mode_export_graph_is_the_references():
+    """Output mode (planner.py:479-607 + apply_plan steps 2-3): the exported graph is
+    the reference's own apply_plan output, and the composed maps cover every
+    rewritten layer (rows = kept filters, cols = full-slice permutations)."""
+    from paper_2307_08771_b200.ref import reslice
+    L = ir.LayerKind
+    # two producers joined by an add, read by two consumers: no per-channel interior
+    g = ir.ModelGraph(
+        [ir.Layer("x", L.INPUT, 4, 4), ir.Layer("a", L.CHANNEL_MIX, 4, 6), ir.Layer("b", L.CHANNEL_MIX, 4, 6),
+         ir.Layer("s", L.ADD, 6, 6), ir.Layer("r", L.PASS_THROUGH, 6, 6), ir.Layer("c", L.CHANNEL_MIX, 6, 3),
+         ir.Layer("d", L.CHANNEL_MIX, 6, 2), ir.Layer("cat", L.CONCAT, 5, 5), ir.Layer("out", L.OUTPUT, 5, 5)],
+        [("x", "a"), ("x", "b"), ("a", "s"), ("b", "s"), ("s", "r"), ("r", "c"), ("r", "d"),
+         ("c", "cat"), ("d", "cat"), ("cat", "out")])
+    masks = {"a": (0, 1, 4), "b": (1, 2, 4, 5)}
+    for strategy in ("reorder", "baseline"):
+        plans, _ = reslice.pipeline.plan_model(g, masks, "output", strategy, "baseline")
+        st = E._shape_store(g)
+        ref_g = g
+        for pl in plans:
+            ref_g, st = reslice.planner.apply_plan(pl, ref_g, st)
+        eg = E.export_graph(g, plans)
+        assert ir.graph_to_dict(eg) == ir.graph_to_dict(ref_g)
+        maps = E.compose_maps(g, plans)
+        assert eg.layer("a").out_channels == len(maps.rows["a"]) == 3
+        assert eg.layer("b").out_channels == len(maps.rows["b"]) == 4
+        kinds = {lay.kind for lay in eg.layers}
+        if strategy == "baseline":
+            assert L.GATHER in kinds  # zero-fill infill after each pruned producer
+        else:
+            assert "s" not in eg  # the join was rewritten into runs of slices + adds + a concat
+
+
+def test_compose_maps_rejects_out_of_range_indices():
     g = ir.load_graph(R50 / "graph.json")
-    with pytest.raises(NotImplementedError):
-        E.export_model(g, {}, {}, {}, mode="output", plans=[])
+    plans = P.load_plans(R50 / "plans_reorder.json")
+    bad = plans[0]
+    p0 = bad.producers[-1]
+    width = g.layer(p0).out_channels
+    orders = dict(bad.producer_orders)
+    orders[p0] = tuple(orders.get(p0, range(width)))[:-1] + (width,)
+    import dataclasses
+    with pytest.raises(ir.ValidationError):
+        E.compose_maps(g, [dataclasses.replace(bad, producer_orders=orders)])
 
 
-def test_plan_model_without_reference_needs_plans(monkeypatch):
-    import builtins
+def test_reference_is_imported_unmodified():
+    """ir/plans/export consume the reference package itself (no re-typed copy)."""
+    import hashlib
+    from pathlib import Path
 
-    real = builtins.__import__
-
-    def no_reslice(name, *a, **k):
-        if name.startswith("reslice"):
-            raise ImportError("reslice hidden")
-        return real(name, *a, **k)
-
-    monkeypatch.setattr(builtins, "__import__", no_reslice)
-    with pytest.raises(E.PlannerUnavailableError):
-        E.plan_model(ir.load_graph(R50 / "graph.json"), {})
+    from paper_2307_08771_b200.ref import REF_SOURCE, reslice
+    assert ir.ModelGraph is reslice.graph.ModelGraph and P.SegmentPlan is reslice.planner.SegmentPlan
+    src = REF_SOURCE / "src" / "reslice"
+    if src.exists():
+        for f in ("graph.py", "planner.py", "pipeline.py", "interp.py"):
+            here = Path(reslice.__file__).parent / f
+            assert hashlib.sha256(here.read_bytes()).digest() == hashlib.sha256((src / f).read_bytes()).digest()
