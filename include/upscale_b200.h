@@ -96,6 +96,18 @@ int ub_channel_gather(const void* x, int x_cstride, int x_coff, const int32_t* i
                       long long npix, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
 /*
+ * Row-staged channel gather (the baseline export's copy and the engine's "copy" read
+ * plan).  Same result as ub_channel_gather_2d:
+ *   y[p][y_coff + i] = idx[i] >= 0 ? x[src(p)][x_coff + idx[i]] : 0,  i < n_idx,
+ * with src(p) the stride-subsampled source pixel, zero-filled to pad8(n_idx) channels.
+ * [lo, hi] must cover every non-negative idx[i] (the host knows the plan's indices); the
+ * covering window of each source row is staged in shared memory with 16-byte cp.async,
+ * so HBM sees one coalesced read of the window and one 16-byte-vector write per row.
+ */
+int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx, int n_idx, int N,
+                   int H, int W, int stride, void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
+/*
  * Channel gather fused with the pixel subsampling of a strided 1x1 conv that reads it:
  * y[n][yo][xo][i] = x[n][yo*stride][xo*stride][x_coff + idx[i]] (idx[i] < 0: 0), for i < n_idx,
  * and zeros for n_idx <= i < pad8(n_idx).  Output pixels are ceil(H/stride) x ceil(W/stride);

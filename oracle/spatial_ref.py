@@ -31,6 +31,8 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
     masks = masks or {}
     vals: dict[str, torch.Tensor] = {}
     out_id = None
+    # values are dropped after their last reader (bounded memory at large batches)
+    readers = {lid: len(graph.successors(lid)) for lid in graph.topological_order()}
     for lid in graph.topological_order():
         lay = graph.layer(lid)
         k = _kind(lay)
@@ -92,6 +94,11 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
         if out.shape[1] != lay.out_channels:
             raise ValueError(f"{lid}: produced {out.shape[1]} channels, expected {lay.out_channels}")
         vals[lid] = out
+        if values is None:
+            for p in graph.predecessors(lid):
+                readers[p] -= 1
+                if readers[p] == 0 and p in vals and _kind(graph.layer(p)) != "output":
+                    del vals[p]
     if values is not None:
         values.update(vals)
     res = vals[out_id]

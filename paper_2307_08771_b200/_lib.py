@@ -66,6 +66,8 @@ SIGNATURES = {
     "ub_channel_gather": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_ll, c_vp, c_int, c_int, c_vp]),
     "ub_channel_gather_2d": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int,
                                      c_vp]),
+    "ub_gather_rows": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp,
+                               c_int, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),

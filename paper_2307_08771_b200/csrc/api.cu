@@ -1,6 +1,8 @@
 // C-ABI plumbing: error reporting, launch counter, driver entry points.
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "ub_host.h"
 
@@ -50,6 +52,42 @@ bool pdl_enabled() {
     on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
+}
+
+// Per-device state: one process may drive several GPUs (the C ABI does not assume one
+// device per process), so SM counts and kernel attributes are kept per device ordinal.
+namespace {
+std::mutex g_dev_mu;
+std::vector<int> g_sms;                                   // device -> SM count (0 = unknown)
+std::vector<std::pair<int, const void*>> g_smem_done;     // (device, kernel) with max dyn smem set
+}  // namespace
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+int num_sms() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (static_cast<int>(g_sms.size()) <= dev) g_sms.resize(dev + 1, 0);
+  if (g_sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n > 0 ? n : 148;
+  }
+  return g_sms[dev];
+}
+
+cudaError_t ensure_max_smem(const void* kernel, int bytes) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  for (const auto& e : g_smem_done)
+    if (e.first == dev && e.second == kernel) return cudaSuccess;
+  const cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err == cudaSuccess) g_smem_done.emplace_back(dev, kernel);
+  return err;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn() {

@@ -654,7 +654,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
 #undef UB_HALO_WP
 #undef UB_HALO_CASE
   if (!kern) return UB_OK;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (const cudaError_t ae = ensure_max_smem(kern)) return cuda_status(ae, "cudaFuncSetAttribute(halo)");
   CUtensorMap tmw{};
   if (p.groups > 1) {  // weights [cout][9 * cpad]: box 64 K x np rows
     cuuint64_t wd[2] = {static_cast<cuuint64_t>(9 * cpad), static_cast<cuuint64_t>(d->cout)};

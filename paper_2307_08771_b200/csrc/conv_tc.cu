@@ -916,7 +916,6 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
 
 int g_driver_version = -1;
 long long* g_conv_trace = nullptr;
-int g_num_sms = -1;
 
 void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes) {
   // Same workaround CUTLASS applies for drivers <= 13.1 (copy_traits_sm90_tma.hpp).
@@ -929,27 +928,13 @@ void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes) {
     reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
 }
 
-int num_sms() {
-  if (g_num_sms < 0) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_num_sms = n > 0 ? n : 148;
-  }
-  return g_num_sms;
-}
 
 namespace {
 
 template <int AMODE, int BK, int PRODUCERS>
 int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
                   const CUtensorMap& tmAt, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(conv_tc_kernel<AMODE, BK, PRODUCERS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
+  const cudaError_t attr_err = ensure_max_smem(conv_tc_kernel<AMODE, BK, PRODUCERS>);
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
   const cudaError_t e = launch_pdl(conv_tc_kernel<AMODE, BK, PRODUCERS>, dim3(grid), dim3(256 + PRODUCERS), smem,
                                    stream, tmY, tmB, tmA, tmR, tmAt, p);

@@ -185,6 +185,70 @@ __global__ void __launch_bounds__(256) channel_gather_2d_kernel(const uint16_t* 
   }
 }
 
+// ------------------------------------------------------------- row-staged gather
+// The baseline export's copy and the engine's "copy" read plan: a reference GATHER
+// (interp.py:75-77) with an optional pixel subsample.  One warp per output pixel; the
+// source row's covering window [ws, ws + 16*win16) is staged in shared memory with
+// 16-byte cp.async (the next pixel's window is in flight while the current one is
+// gathered), then each lane gathers 8 channels from shared memory and writes one 16-byte
+// vector.  Global traffic: the window read once (coalesced), the gathered row written once.
+__global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
+                                                          int win16, const int32_t* __restrict__ idx, int n_idx,
+                                                          int rel, int n8, int N, int H, int W, int stride, int Ho,
+                                                          int Wo, uint16_t* __restrict__ y, int y_cstride,
+                                                          int y_coff) {
+  extern __shared__ __align__(16) uint8_t g_smem[];
+  int32_t* sidx = reinterpret_cast<int32_t*>(g_smem);
+  const int idx_bytes = (n8 * 4 + 15) & ~15;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  uint8_t* buf0 = g_smem + idx_bytes + static_cast<size_t>(warp) * 2 * win16 * 16;
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) {
+    const int j = i < n_idx ? __ldg(idx + i) : -1;
+    sidx[i] = j >= 0 ? j + rel : -1;  // element offset inside the staged window
+  }
+  __syncthreads();
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long npix = static_cast<long long>(N) * Ho * Wo;
+  const long long step = static_cast<long long>(gridDim.x) * warps;
+  auto src_row = [&](long long p) {
+    const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
+    const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+    const int yo = r / Wo, xo = r - (r / Wo) * Wo;
+    return x + ((static_cast<size_t>(n) * H + static_cast<size_t>(yo) * stride) * W +
+                static_cast<size_t>(xo) * stride) * x_cstride + ws;
+  };
+  auto issue = [&](long long p, uint8_t* dst) {
+    const uint16_t* src = src_row(p);
+    for (int j = lane; j < win16; j += 32) cp_async16(dst + j * 16, src + j * 8, 16);
+  };
+  long long p = static_cast<long long>(blockIdx.x) * warps + warp;
+  int k = 0;
+  if (p < npix) issue(p, buf0);
+  cp_async_commit();
+  for (; p < npix; p += step, k ^= 1) {
+    if (p + step < npix) issue(p + step, buf0 + (k ^ 1) * win16 * 16);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * win16 * 16);
+    uint16_t* yr = y + static_cast<size_t>(p) * y_cstride + y_coff;
+    for (int i = lane * 8; i < n8; i += 256) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int a = sidx[i + 2 * j], b = sidx[i + 2 * j + 1];
+        const uint32_t lo = a >= 0 ? row[a] : 0u, hi = b >= 0 ? row[b] : 0u;
+        w[j] = lo | (hi << 16);
+      }
+      *reinterpret_cast<uint4*>(yr + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------- input staging
 // NCHW fp32 -> NHWC bf16 (channel-gathered), zero-filling the padded channels.
 __global__ void stage_input_kernel(const float* __restrict__ x, int N, int C, int HW, const int32_t* __restrict__ idx,
@@ -563,6 +627,41 @@ extern "C" int ub_channel_gather_2d(const void* x, int x_cstride, int x_coff, co
                                    stride, Ho, Wo, static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "channel_gather_2d_kernel");
+}
+
+extern "C" int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx,
+                              int n_idx, int N, int H, int W, int stride, void* y, int y_cstride, int y_coff,
+                              cudaStream_t stream) {
+  if (!x || !idx || !y || n_idx < 1 || N < 1 || H < 1 || W < 1 || stride < 1 || lo < 0 || hi < lo)
+    return fail(UB_EINVAL, "ub_gather_rows: bad arguments");
+  const int n8 = (n_idx + 7) / 8 * 8;
+  if ((y_cstride & 7) || (y_coff & 7) || y_coff + n8 > y_cstride || !aligned16(y))
+    return fail(UB_EINVAL, "ub_gather_rows: output rows must hold pad8(n) 16-byte aligned channels");
+  if ((x_cstride & 7) || !aligned16(x) || x_coff < 0 || x_coff + hi >= x_cstride)
+    return fail(UB_EINVAL, "ub_gather_rows: source window outside 16-byte aligned rows");
+  const int ws = (x_coff + lo) & ~7;
+  const int we = (x_coff + hi + 8) & ~7;
+  const int win16 = (we - ws) / 8;
+  const int idx_bytes = (n8 * 4 + 15) & ~15;
+  int warps = 8;
+  while (warps > 1 && idx_bytes + static_cast<size_t>(warps) * 2 * win16 * 16 > 200 * 1024) warps >>= 1;
+  const size_t smem = idx_bytes + static_cast<size_t>(warps) * 2 * win16 * 16;
+  if (smem > 227 * 1024) return fail(UB_EUNSUPPORTED, "ub_gather_rows: window of %d channels", we - ws);
+  if (const cudaError_t ae = ensure_max_smem(gather_rows_kernel)) return cuda_status(ae, "gather_rows attr");
+  const int Ho = (H + stride - 1) / stride, Wo = (W + stride - 1) / stride;
+  const long long npix = static_cast<long long>(N) * Ho * Wo;
+  int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
+  if (per_sm > 2048 / (32 * warps)) per_sm = 2048 / (32 * warps);
+  if (per_sm < 1) per_sm = 1;
+  const long long want = (npix + warps - 1) / warps;
+  const long long cap = static_cast<long long>(num_sms()) * per_sm;
+  const int grid = static_cast<int>(want < cap ? want : cap);
+  const cudaError_t e = launch_pdl(gather_rows_kernel, dim3(grid), dim3(32 * warps), smem, stream,
+                                   static_cast<const uint16_t*>(x), x_cstride, ws, win16, idx, n_idx,
+                                   x_coff - ws, n8, N, H, W, stride, Ho, Wo, static_cast<uint16_t*>(y), y_cstride,
+                                   y_coff);
+  count_launch();
+  return cuda_status(e, "gather_rows_kernel");
 }
 
 extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n, void* y,

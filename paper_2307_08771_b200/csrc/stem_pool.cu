@@ -420,11 +420,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
 template <int KQ, bool PACK>
 void launch_pool(const CUtensorMap& tm, const CUtensorMap& tmx, const PoolParams& p, int grid, size_t smem,
                  cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stem_pool_kernel<KQ, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  (void)ensure_max_smem(stem_pool_kernel<KQ, PACK>);
   (void)launch_pdl(stem_pool_kernel<KQ, PACK>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, tmx, p);
 }
 

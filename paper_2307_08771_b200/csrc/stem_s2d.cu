@@ -380,11 +380,7 @@ __global__ void __launch_bounds__(PACK_THREADS) stem_s2d_pack_rows_kernel(
 
 template <int KQ>
 void launch_s2d(const CUtensorMap& tm, const S2DParams& p, int grid, size_t smem, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stem_s2d_kernel<KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  (void)ensure_max_smem(stem_s2d_kernel<KQ>);
   stem_s2d_kernel<KQ><<<grid, S2D_THREADS, smem, stream>>>(tm, p);
 }
 

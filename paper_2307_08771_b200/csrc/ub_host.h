@@ -24,7 +24,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_fn();
 PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn();
 // Clear the descriptor bit CUTLASS clears for small tensors on drivers <= 13.1.
 void apply_small_tensor_quirk(CUtensorMap* map, size_t footprint_bytes);
-int num_sms();  // multiprocessors of the current device
+int num_sms();  // multiprocessors of the current device (cached per device)
+int current_device();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel).
+cudaError_t ensure_max_smem(const void* kernel, int bytes);
+template <typename... A>
+cudaError_t ensure_max_smem(void (*kernel)(A...), int bytes = 227 * 1024) {
+  return ensure_max_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
 // Stride-1 3x3 halo-tile kernel (conv_halo.cu); *handled = false when the layer is outside
 // its scope and the generic kernel should run instead.
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled);
@@ -39,12 +46,10 @@ inline CUtensorMapSwizzle swizzle_of(int bytes) {
   }
 }
 
-constexpr int kSMs = 148;
-
 // Grid for a grid-stride loop over `work` items: at most 16 CTAs per SM.
 inline int grid_for(long long work, int block, int per_thread = 1) {
   long long g = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
-  const long long cap = (long long)kSMs * 16;
+  const long long cap = (long long)num_sms() * 16;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<int>(g);

@@ -395,7 +395,8 @@ class Engine:
         idx = op.info["idx"]
         y = self._alloc(op.output, len(idx))
         idx_dev = self._i32(idx)
-        op.launch = lambda: K.channel_gather(x, idx_dev, y)
+        win = K.gather_window(idx)
+        op.launch = lambda: K.gather_rows(x, idx_dev, win, 1, y)
         n_img_pix = x.H * x.W
         self.conv_stats.append(ConvStats(f"{op.output}(copy)", 0.0, 0.0, 2 * 2 * len(idx) * n_img_pix))
 
@@ -499,8 +500,10 @@ class Engine:
                 self._keep.append(scratch.buf)
                 gdev = self._i32(list(gather))
 
-                def pre(x=x, gdev=gdev, scratch=scratch):
-                    K.channel_gather_2d(x, gdev, st, scratch)
+                win = K.gather_window(gather)
+
+                def pre(x=x, gdev=gdev, scratch=scratch, win=win):
+                    K.gather_rows(x, gdev, win, st, scratch)
 
                 add_plan("copy", scratch, None, cols, cin, pre=pre, st_eff=1)
             lo, hi = min(gather), max(gather)
@@ -560,6 +563,7 @@ class Engine:
                 gen = [0, 128] + [v | 8 for v in gen]
             return gen
 
+        op.info["halo"] = halo
         op.info["variants"] = [(pi, v) for pi, pl in enumerate(plans) for v in gen_for(pl[7])]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]
@@ -750,6 +754,19 @@ class Engine:
         if getattr(self, "_launches", None) is None:
             return sum(2 if op.info.get("stem_kind", "") in ("s2d", "s2d+maxpool") else 1 for op in self.ops)
         return self._launches
+
+    def kernel_label(self, op) -> str:
+        """Which library kernel(s) one op launches with its current variant."""
+        if op.kind == "conv":
+            if "stem_idx" in op.info:
+                return "stem_" + op.info.get("stem_kind", "")
+            pi, pw = op.info["variant"]
+            if op.info.get("halo") and not pw & 8:
+                return "conv_halo3_kernel"
+            return "conv_tc_kernel+gather_rows" if op.info["plans"][pi] == "copy" else "conv_tc_kernel"
+        return {"gather": "gather_rows_kernel", "stage": "stage_input_kernel", "maxpool": "maxpool_kernel",
+                "avgpool": "avgpool_gather_kernel" if "idx" in op.info else "avgpool_kernel",
+                "eltwise": "affine_add_relu_kernel"}.get(op.kind, op.kind)
 
     def per_image_work(self) -> tuple[float, float]:
         f = sum(c.flops for c in self.conv_stats)

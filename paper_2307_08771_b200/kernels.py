@@ -126,6 +126,19 @@ def channel_gather_2d(x: Act, idx_dev: torch.Tensor, stride: int, y: Act) -> Non
               stride, _p(y.buf), y.cstride, y.coff, _stream())
 
 
+def gather_rows(x: Act, idx_dev: torch.Tensor, window: tuple[int, int], stride: int, y: Act) -> None:
+    """ub_gather_rows: the channels idx (all within window = (lo, hi)) of every stride-th
+    pixel of x into the compact y; the source rows are staged through shared memory."""
+    lo, hi = window
+    _lib.call("ub_gather_rows", _p(x.buf), x.cstride, x.coff, lo, hi, _p(idx_dev), idx_dev.numel(), x.N, x.H, x.W,
+              stride, _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def gather_window(idx) -> tuple[int, int]:
+    kept = [int(i) for i in idx if i >= 0]
+    return (min(kept), max(kept)) if kept else (0, 0)
+
+
 def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: int, stride: int, pad: int,
          y: Act, gather_idx: torch.Tensor | None = None, bias: torch.Tensor | None = None,
          residual: Act | None = None, relu: bool = False, y_fp32: bool = False, variant: int = 0,

@@ -139,6 +139,13 @@ def lower(model: nn.Module, input_chw=(3, 224, 224)) -> SpatialModel:
                 p = p if isinstance(p, int) else p[0]
                 add_layer(node.name, LayerKind.PASS_THROUGH, cin, cin, OpSpec("maxpool", k, st, p), [s])
                 alias[node.name] = node.name
+            elif isinstance(m, nn.AvgPool2d):
+                k, st, p = (m.kernel_size, m.stride, m.padding)
+                k = k if isinstance(k, int) else k[0]
+                st = st if isinstance(st, int) else st[0]
+                p = p if isinstance(p, int) else p[0]
+                add_layer(node.name, LayerKind.PASS_THROUGH, cin, cin, OpSpec("avgpool_k", k, st, p), [s])
+                alias[node.name] = node.name
             elif isinstance(m, nn.AdaptiveAvgPool2d):
                 osz = m.output_size
                 assert osz in (1, (1, 1)), "only global average pooling is supported"
@@ -157,6 +164,12 @@ def lower(model: nn.Module, input_chw=(3, 224, 224)) -> SpatialModel:
             elif node.target in (torch.flatten,) or (node.op == "call_method" and node.target in ("flatten", "view")):
                 s = src(node.args[0])
                 add_layer(node.name, LayerKind.PASS_THROUGH, width[s], width[s], OpSpec("flatten"), [s])
+                alias[node.name] = node.name
+            elif node.target in (torch.nn.functional.adaptive_avg_pool2d,):
+                s = src(node.args[0])
+                osz = node.args[1] if len(node.args) > 1 else node.kwargs.get("output_size")
+                assert osz in (1, (1, 1)), "only global average pooling is supported"
+                add_layer(node.name, LayerKind.PASS_THROUGH, width[s], width[s], OpSpec("avgpool"), [s])
                 alias[node.name] = node.name
             elif node.target in (torch.relu, torch.nn.functional.relu):
                 s = src(node.args[0])

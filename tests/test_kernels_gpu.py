@@ -265,12 +265,16 @@ def test_permute_weights_bit_exact():
     assert torch.equal(out.cpu(), ref)
 
 
+@pytest.mark.parametrize("rows", [False, True])
 @pytest.mark.parametrize("N,H,W,cs,coff,idx,stride", [
     (2, 9, 9, 40, 0, [5, 3, -1, 39, 0, 17, 18], 1),
     (3, 14, 14, 64, 8, [1, 2, 3, 50, 7, 9, 11, 13, 40, 41], 2),
     (2, 7, 5, 1024, 16, list(range(0, 1000, 3)), 2),
+    (2, 6, 6, 136, 3, [130, 2, -1, 77, 4, 5, 6, 100, 99], 1),   # window crosses 8-channel blocks, odd offset
+    (1, 3, 3, 2048, 0, list(range(2047, -1, -1)), 1),           # full reversed row
+    (2, 5, 5, 64, 57, [-1, -1, 6], 1),                           # one kept channel at the row's end
 ])
-def test_channel_gather_2d(N, H, W, cs, coff, idx, stride):
+def test_channel_gather_2d(N, H, W, cs, coff, idx, stride, rows):
     """Gather + stride subsample into a compact buffer: bit-exact, zero-padded to pad8(n)."""
     dev = "cuda"
     g = torch.Generator().manual_seed(N + H + len(idx))
@@ -280,7 +284,10 @@ def test_channel_gather_2d(N, H, W, cs, coff, idx, stride):
     Ho, Wo = (H - 1) // stride + 1, (W - 1) // stride + 1
     y = K.empty_act(N, Ho, Wo, len(idx), dev)
     y.buf.fill_(float("nan"))
-    K.channel_gather_2d(xa, idx_t.to(dev), stride, y)
+    if rows:
+        K.gather_rows(xa, idx_t.to(dev), K.gather_window(idx), stride, y)
+    else:
+        K.channel_gather_2d(xa, idx_t.to(dev), stride, y)
     torch.cuda.synchronize()
     ref = torch.zeros(N, K.pad8(len(idx)), Ho, Wo)
     for i, j in enumerate(idx):
@@ -507,3 +514,48 @@ def test_conv_fp32_classifier_32_channel_tiles_bit_exact(N, cout):
     assert torch.isnan(outs[1][:, cout:]).all()
     ref = x.to_nchw().reshape(N, cin).to(dev) @ _bf(Wt).reshape(cout, cin).to(dev).T + bias
     assert _rel(outs[1][:, :cout], ref) < 1e-2
+
+
+@pytest.mark.parametrize("layout,kk,cin,lead", [("gemm", 1, 100, 5), ("gemm", 3, 64, 0), ("gemm", 3, 24, 3),
+                                                 ("s2d", 7, 2, 0), ("dense", 7, 3, 0)])
+def test_production_bf16_layouts_bit_exact_vs_fp32_oihw(layout, kk, cin, lead):
+    """The production weight operands (bf16, BN scale folded into the rows, K-major GEMM /
+    space-to-depth / dense im2col layouts) are bit-identical to the fp32 OIHW result of the
+    same plan maps, scaled in fp32 and rounded once to bf16."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(kk * 100 + cin)
+    O, I = 48, cin + 7
+    W = torch.randn(O, I, kk, kk, generator=g)
+    rows = [5, 0, 47, -1, 12, 3, 30, 31]
+    cols = list(range(I - 1, I - 1 - cin, -1))
+    cols[1] = -1
+    scale = (0.5 + torch.rand(len(rows), generator=g)).to(dev)
+    Wd = W.to(dev).contiguous()
+    oihw = K.permute_weights(Wd, rows, cols, out_dtype=torch.float32)
+    ref = (oihw * scale.view(-1, 1, 1, 1)).to(torch.bfloat16)  # one fp32 product, one RN to bf16
+    if layout == "gemm":
+        lead_, cpad = _lib.conv_weight_layout(cin, lead, False, kk, kk)
+        got = K.permute_weights(Wd, rows, cols, row_scale=scale, layout="gemm", lead=lead_, cpad=cpad,
+                                out_dtype=torch.bfloat16)
+        assert got.shape == (len(rows), kk * kk, cpad)
+        want = torch.zeros(len(rows), kk * kk, cpad, dtype=torch.bfloat16, device=dev)
+        want[:, :, lead_:lead_ + cin] = ref.permute(0, 2, 3, 1).reshape(len(rows), kk * kk, cin)
+    elif layout == "s2d":
+        got = K.permute_weights(Wd, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
+        kq = (kk + 1) // 2
+        want = torch.zeros(len(rows), kq, kq, 2, 2, 2, dtype=torch.bfloat16, device=dev)  # [o][dy][dx][py][px][c]
+        for dy in range(kq):
+            for dx in range(kq):
+                for py in range(2):
+                    for px in range(2):
+                        r, s = 2 * dy + py, 2 * dx + px
+                        if r < kk and s < kk:
+                            want[:, dy, dx, py, px, :cin] = ref[:, :, r, s]
+        want = want.reshape(len(rows), kq * kq * 8)
+    else:
+        kpad = _lib.conv_stem_kpad(cin, kk, kk)
+        got = K.permute_weights(Wd, rows, cols, row_scale=scale, layout="dense", cpad=kpad, out_dtype=torch.bfloat16)
+        want = torch.zeros(len(rows), kpad, dtype=torch.bfloat16, device=dev)
+        want[:, :kk * kk * cin] = ref.permute(0, 2, 3, 1).reshape(len(rows), -1)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), want.view(torch.int16))
