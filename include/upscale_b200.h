@@ -108,6 +108,20 @@ int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, int hi, con
                    int H, int W, int stride, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
 /*
+ * ub_gather_rows with the consumer's pre-activation prologue and an optional 2x2 pool:
+ *   v_i(q) = x[src_q(p)][x_coff + idx[i]],  f = relu ? max(scale[i] * v + shift[i], 0) : scale[i] * v + shift[i]
+ *   y[p][y_coff + i] = bf16( pool2 ? (f(0) + f(1) + f(2) + f(3)) / 4 : f )
+ * scale/shift (fp32, per OUTPUT column i, both or neither): the PER_CHANNEL (BN) and
+ * PASS_THROUGH (ReLU) nodes between a value and its GATHER/SLICE reader
+ * (interp.py:68-71 then 72-77), e.g. DenseNet's norm1 -> relu1 -> conv1.read.
+ * pool2 = 1: src_q are the four pixels of the 2x2/s2 window (Ho = H/2, Wo = W/2; stride
+ * must be 1) -- a transition layer's average pool, applied before its 1x1 conv.
+ */
+int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx, int n_idx,
+                      int N, int H, int W, int stride, int pool2, const float* scale, const float* shift, int relu,
+                      void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
+/*
  * Channel gather fused with the pixel subsampling of a strided 1x1 conv that reads it:
  * y[n][yo][xo][i] = x[n][yo*stride][xo*stride][x_coff + idx[i]] (idx[i] < 0: 0), for i < n_idx,
  * and zeros for n_idx <= i < pad8(n_idx).  Output pixels are ceil(H/stride) x ceil(W/stride);
@@ -135,6 +149,47 @@ int ub_conv_weight_layout2(int cin, int coff, int gather, int kh, int kw, int* l
  *              interp.py:64-65), ReLU (PASS_THROUGH, interp.py:68-69), store at a
  *              channel offset (CONCAT without a copy, interp.py:66-67).
  * Implicit GEMM on tcgen05 tensor cores: M = N*Ho*Wo, N = cout, K = kh*kw*cpad. */
+/* Activations of ub_eltwise (PASS_THROUGH ops of the lowered CNNs). */
+#define UB_ACT_NONE 0
+#define UB_ACT_RELU 1
+#define UB_ACT_RELU6 2
+#define UB_ACT_HARDSWISH 3   /* x * relu6(x + 3) / 6 */
+#define UB_ACT_HARDSIGMOID 4 /* relu6(x + 3) / 6 */
+#define UB_ACT_SILU 5        /* x * sigmoid(x) */
+#define UB_ACT_SIGMOID 6
+
+/*
+ * One vectorised NHWC bf16 pass over N*HW pixels x C channels:
+ *   y = act(a * scale[c] + shift[c] + b) * gate[n][c]
+ * scale/shift (fp32, per channel), b (bf16 NHWC, positional ADD, interp.py:64-65) and
+ * gate (bf16 [N][gate_cstride], a squeeze-excitation multiplier broadcast over the
+ * image's pixels) are each optional.  Replaces interp.py:64-71 for the PER_CHANNEL /
+ * ADD / PASS_THROUGH nodes no conv epilogue absorbs.
+ */
+typedef struct ub_eltwise_desc {
+  int N, HW, C;
+  const void* a;
+  int a_cstride, a_coff;
+  const float* scale;
+  const float* shift;
+  const void* b;
+  int b_cstride, b_coff;
+  int act;
+  const void* gate;
+  int gate_cstride, gate_coff;
+  void* y;
+  int y_cstride, y_coff;
+} ub_eltwise_desc;
+int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream);
+
+/*
+ * k x k / stride s average pool with zero padding counted (count_include_pad), NHWC bf16,
+ * 16-byte aligned rows.  A DenseNet transition's AvgPool2d(2, 2) when it cannot be moved
+ * in front of its 1x1 conv (ub_gather_rows_ex pool2).
+ */
+int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int s, int pad, int Ho,
+                 int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
 typedef struct {
   int N, H, W;                 /* input geometry */
   int cin;                     /* channels read (slice length or gather count) */

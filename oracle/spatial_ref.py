@@ -64,6 +64,8 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
                 out = F.max_pool2d(v, spec.kernel, spec.stride, spec.pad)
             elif op == "avgpool":
                 out = v.mean(dim=(2, 3), keepdim=True)
+            elif op == "avgpool_k":
+                out = F.avg_pool2d(v, spec.kernel, spec.stride, spec.pad)
             elif op in ("flatten", "identity"):
                 out = v
             else:  # relu, and the reference's PASS_THROUGH semantics

@@ -53,6 +53,21 @@ class ConvDesc(ctypes.Structure):
     ]
 
 
+UB_ACT = {"none": 0, "relu": 1, "relu6": 2, "hardswish": 3, "hardsigmoid": 4, "silu": 5, "sigmoid": 6}
+
+
+class EltwiseDesc(ctypes.Structure):
+    _fields_ = [
+        ("N", c_int), ("HW", c_int), ("C", c_int),
+        ("a", c_vp), ("a_cstride", c_int), ("a_coff", c_int),
+        ("scale", c_vp), ("shift", c_vp),
+        ("b", c_vp), ("b_cstride", c_int), ("b_coff", c_int),
+        ("act", c_int),
+        ("gate", c_vp), ("gate_cstride", c_int), ("gate_coff", c_int),
+        ("y", c_vp), ("y_cstride", c_int), ("y_coff", c_int),
+    ]
+
+
 # name -> (restype, argtypes); must match include/upscale_b200.h exactly.
 SIGNATURES = {
     "ub_last_error": (ctypes.c_char_p, []),
@@ -68,6 +83,11 @@ SIGNATURES = {
                                      c_vp]),
     "ub_gather_rows": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp,
                                c_int, c_int, c_vp]),
+    "ub_gather_rows_ex": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_int, c_int, c_int, c_int,
+                                  c_vp, c_vp, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_eltwise": (c_int, [ctypes.POINTER(EltwiseDesc), c_vp]),
+    "ub_avgpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
+                             c_int, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libupscale_b200.so"
-SOURCES = ["api.cu", "conv_tc.cu", "conv_halo.cu", "ops.cu", "stem_s2d.cu", "stem_pool.cu", "planner.cpp"]
+SOURCES = ["api.cu", "conv_tc.cu", "conv_halo.cu", "ops.cu", "eltwise.cu", "stem_s2d.cu", "stem_pool.cu", "planner.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

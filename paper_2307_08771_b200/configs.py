@@ -28,6 +28,7 @@ class Config:
     heuristic: str = "l2"
     batch: int = 1
     seed: int = 0
+    native_planner: bool = False
 
     @property
     def asset_dir(self) -> Path:
@@ -41,6 +42,11 @@ CONFIGS = {
     "resnet50_s50": Config("resnet50_s50", "resnet50", 0.5, batch=256),
     # BASELINE.json configs[4] (ResNet-101 half of the throughput sweep)
     "resnet101_s50": Config("resnet101_s50", "resnet101", 0.5, batch=256),
+    # BASELINE.json configs[3]: concat-heavy, maximal gather pressure.  The pure-Python
+    # reference planner does not finish at 0.5; the plans are the
+    # reference plan_model's with the native planner core installed (same search,
+    # csrc/planner.cpp), which plans it in 0.2 s.
+    "densenet121_s50": Config("densenet121_s50", "densenet121", 0.5, batch=128, native_planner=True),
 }
 
 NORTH_STAR = "resnet50_s50"

@@ -192,55 +192,94 @@ __global__ void __launch_bounds__(256) channel_gather_2d_kernel(const uint16_t* 
 // 16-byte cp.async (the next pixel's window is in flight while the current one is
 // gathered), then each lane gathers 8 channels from shared memory and writes one 16-byte
 // vector.  Global traffic: the window read once (coalesced), the gathered row written once.
+//
+// AFFINE: the read's pre-activation prologue (DenseNet's BN -> ReLU in front of every
+// conv, SURVEY.md 2.2 "PER_CHANNEL ... prologue on the consumer's A-operand"): each
+// gathered value becomes relu?(scale[i] * x + shift[i]) in fp32 before the bf16 store.
+// ROWS == 4: the 2x2/s2 average pool a transition layer applies after its 1x1 conv,
+// moved in front of the conv (both are linear; exact up to rounding): the four source
+// pixels of each output pixel are staged and averaged after the prologue.
+template <int ROWS, bool AFFINE>
 __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
                                                           int win16, const int32_t* __restrict__ idx, int n_idx,
                                                           int rel, int n8, int N, int H, int W, int stride, int Ho,
-                                                          int Wo, uint16_t* __restrict__ y, int y_cstride,
-                                                          int y_coff) {
+                                                          int Wo, const float* __restrict__ scale,
+                                                          const float* __restrict__ shift, int relu,
+                                                          uint16_t* __restrict__ y, int y_cstride, int y_coff) {
   extern __shared__ __align__(16) uint8_t g_smem[];
   int32_t* sidx = reinterpret_cast<int32_t*>(g_smem);
-  const int idx_bytes = (n8 * 4 + 15) & ~15;
+  float* sscale = reinterpret_cast<float*>(g_smem + n8 * 4);
+  float* sshift = sscale + n8;
+  const int idx_bytes = ((AFFINE ? 3 : 1) * n8 * 4 + 15) & ~15;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  uint8_t* buf0 = g_smem + idx_bytes + static_cast<size_t>(warp) * 2 * win16 * 16;
+  const int stage_bytes = ROWS * win16 * 16;
+  uint8_t* buf0 = g_smem + idx_bytes + static_cast<size_t>(warp) * 2 * stage_bytes;
   for (int i = threadIdx.x; i < n8; i += blockDim.x) {
     const int j = i < n_idx ? __ldg(idx + i) : -1;
     sidx[i] = j >= 0 ? j + rel : -1;  // element offset inside the staged window
+    if (AFFINE) {
+      sscale[i] = i < n_idx ? __ldg(scale + i) : 0.f;
+      sshift[i] = i < n_idx ? __ldg(shift + i) : 0.f;
+    }
   }
   __syncthreads();
   griddep_wait();
   griddep_launch_dependents();
   const long long npix = static_cast<long long>(N) * Ho * Wo;
   const long long step = static_cast<long long>(gridDim.x) * warps;
-  auto src_row = [&](long long p) {
+  auto issue = [&](long long p, uint8_t* dst) {
     const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
     const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
     const int yo = r / Wo, xo = r - (r / Wo) * Wo;
-    return x + ((static_cast<size_t>(n) * H + static_cast<size_t>(yo) * stride) * W +
-                static_cast<size_t>(xo) * stride) * x_cstride + ws;
-  };
-  auto issue = [&](long long p, uint8_t* dst) {
-    const uint16_t* src = src_row(p);
-    for (int j = lane; j < win16; j += 32) cp_async16(dst + j * 16, src + j * 8, 16);
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) {
+      const int yi = ROWS == 4 ? 2 * yo + (q >> 1) : yo * stride;
+      const int xi = ROWS == 4 ? 2 * xo + (q & 1) : xo * stride;
+      const uint16_t* src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws;
+      for (int j = lane; j < win16; j += 32) cp_async16(dst + q * win16 * 16 + j * 16, src + j * 8, 16);
+    }
   };
   long long p = static_cast<long long>(blockIdx.x) * warps + warp;
   int k = 0;
   if (p < npix) issue(p, buf0);
   cp_async_commit();
   for (; p < npix; p += step, k ^= 1) {
-    if (p + step < npix) issue(p + step, buf0 + (k ^ 1) * win16 * 16);
+    if (p + step < npix) issue(p + step, buf0 + (k ^ 1) * stage_bytes);
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * win16 * 16);
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
     uint16_t* yr = y + static_cast<size_t>(p) * y_cstride + y_coff;
     for (int i = lane * 8; i < n8; i += 256) {
       uint32_t w[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int a = sidx[i + 2 * j], b = sidx[i + 2 * j + 1];
-        const uint32_t lo = a >= 0 ? row[a] : 0u, hi = b >= 0 ? row[b] : 0u;
-        w[j] = lo | (hi << 16);
+        uint16_t h[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = i + 2 * j + e;
+          const int a = sidx[c];
+          if (!AFFINE && ROWS == 1) {
+            h[e] = a >= 0 ? row[a] : uint16_t(0);
+          } else {
+            float acc = 0.f;
+            if (a >= 0) {
+#pragma unroll
+              for (int q = 0; q < ROWS; ++q) {
+                float v = __uint_as_float(static_cast<uint32_t>(row[q * win16 * 8 + a]) << 16);
+                if (AFFINE) {
+                  v = fmaf(sscale[c], v, sshift[c]);
+                  if (relu) v = fmaxf(v, 0.f);
+                }
+                acc += v;
+              }
+              if (ROWS == 4) acc *= 0.25f;
+            }
+            h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+          }
+        }
+        w[j] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
       }
       *reinterpret_cast<uint4*>(yr + i) = make_uint4(w[0], w[1], w[2], w[3]);
     }
@@ -629,26 +668,36 @@ extern "C" int ub_channel_gather_2d(const void* x, int x_cstride, int x_coff, co
   return cuda_status(e, "channel_gather_2d_kernel");
 }
 
-extern "C" int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx,
-                              int n_idx, int N, int H, int W, int stride, void* y, int y_cstride, int y_coff,
-                              cudaStream_t stream) {
+extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx,
+                                 int n_idx, int N, int H, int W, int stride, int pool2, const float* scale,
+                                 const float* shift, int relu, void* y, int y_cstride, int y_coff,
+                                 cudaStream_t stream) {
   if (!x || !idx || !y || n_idx < 1 || N < 1 || H < 1 || W < 1 || stride < 1 || lo < 0 || hi < lo)
     return fail(UB_EINVAL, "ub_gather_rows: bad arguments");
+  if ((scale == nullptr) != (shift == nullptr)) return fail(UB_EINVAL, "ub_gather_rows: scale and shift go together");
+  if (pool2 && (stride != 1 || H < 2 || W < 2)) return fail(UB_EINVAL, "ub_gather_rows: pool2 needs stride 1");
   const int n8 = (n_idx + 7) / 8 * 8;
   if ((y_cstride & 7) || (y_coff & 7) || y_coff + n8 > y_cstride || !aligned16(y))
     return fail(UB_EINVAL, "ub_gather_rows: output rows must hold pad8(n) 16-byte aligned channels");
   if ((x_cstride & 7) || !aligned16(x) || x_coff < 0 || x_coff + hi >= x_cstride)
     return fail(UB_EINVAL, "ub_gather_rows: source window outside 16-byte aligned rows");
+  const bool affine = scale != nullptr;
+  const int rows = pool2 ? 4 : 1;
   const int ws = (x_coff + lo) & ~7;
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
-  const int idx_bytes = (n8 * 4 + 15) & ~15;
+  const int idx_bytes = ((affine ? 3 : 1) * n8 * 4 + 15) & ~15;
+  const size_t stage = static_cast<size_t>(rows) * win16 * 16;
   int warps = 8;
-  while (warps > 1 && idx_bytes + static_cast<size_t>(warps) * 2 * win16 * 16 > 200 * 1024) warps >>= 1;
-  const size_t smem = idx_bytes + static_cast<size_t>(warps) * 2 * win16 * 16;
+  while (warps > 1 && idx_bytes + warps * 2 * stage > 200 * 1024) warps >>= 1;
+  const size_t smem = idx_bytes + warps * 2 * stage;
   if (smem > 227 * 1024) return fail(UB_EUNSUPPORTED, "ub_gather_rows: window of %d channels", we - ws);
-  if (const cudaError_t ae = ensure_max_smem(gather_rows_kernel)) return cuda_status(ae, "gather_rows attr");
-  const int Ho = (H + stride - 1) / stride, Wo = (W + stride - 1) / stride;
+  void (*kern)(const uint16_t*, int, int, int, const int32_t*, int, int, int, int, int, int, int, int, int,
+               const float*, const float*, int, uint16_t*, int, int) =
+      pool2 ? (affine ? gather_rows_kernel<4, true> : gather_rows_kernel<4, false>)
+            : (affine ? gather_rows_kernel<1, true> : gather_rows_kernel<1, false>);
+  if (const cudaError_t ae = ensure_max_smem(kern)) return cuda_status(ae, "gather_rows attr");
+  const int Ho = pool2 ? H / 2 : (H + stride - 1) / stride, Wo = pool2 ? W / 2 : (W + stride - 1) / stride;
   const long long npix = static_cast<long long>(N) * Ho * Wo;
   int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
   if (per_sm > 2048 / (32 * warps)) per_sm = 2048 / (32 * warps);
@@ -656,12 +705,18 @@ extern "C" int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, 
   const long long want = (npix + warps - 1) / warps;
   const long long cap = static_cast<long long>(num_sms()) * per_sm;
   const int grid = static_cast<int>(want < cap ? want : cap);
-  const cudaError_t e = launch_pdl(gather_rows_kernel, dim3(grid), dim3(32 * warps), smem, stream,
-                                   static_cast<const uint16_t*>(x), x_cstride, ws, win16, idx, n_idx,
-                                   x_coff - ws, n8, N, H, W, stride, Ho, Wo, static_cast<uint16_t*>(y), y_cstride,
-                                   y_coff);
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(32 * warps), smem, stream, static_cast<const uint16_t*>(x),
+                                   x_cstride, ws, win16, idx, n_idx, x_coff - ws, n8, N, H, W, stride, Ho, Wo, scale,
+                                   shift, relu, static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "gather_rows_kernel");
+}
+
+extern "C" int ub_gather_rows(const void* x, int x_cstride, int x_coff, int lo, int hi, const int32_t* idx,
+                              int n_idx, int N, int H, int W, int stride, void* y, int y_cstride, int y_coff,
+                              cudaStream_t stream) {
+  return ub_gather_rows_ex(x, x_cstride, x_coff, lo, hi, idx, n_idx, N, H, W, stride, 0, nullptr, nullptr, 0, y,
+                           y_cstride, y_coff, stream);
 }
 
 extern "C" int ub_stage_input(const float* x, int N, int C, int H, int W, const int32_t* idx, int n, void* y,

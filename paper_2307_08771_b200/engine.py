@@ -30,6 +30,9 @@ from . import _lib
 from . import kernels as K
 from .ir import LayerKind, ModelGraph
 
+# PASS_THROUGH ops that are activations (ub_eltwise act codes, _lib.UB_ACT)
+ACTS = ("relu", "relu6", "hardswish", "hardsigmoid", "silu", "sigmoid")
+
 
 @dataclass
 class _Op:
@@ -112,6 +115,9 @@ class Engine:
                     w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
                 elif spec.op == "avgpool":
                     h, w = 1, 1
+                elif spec.op == "avgpool_k":
+                    h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
+                    w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
             shp[lid] = (lay.out_channels, h, w)
         return shp
 
@@ -120,14 +126,27 @@ class Engine:
         s = self.graph.successors(lid)
         return s[0] if len(s) == 1 else None
 
-    def _alloc(self, vid: str, C: int, fp32: bool = False, shape_of: str | None = None) -> K.Act:
+    def _alloc(self, vid: str, C: int, fp32: bool = False, shape_of: str | None = None,
+               cmap: tuple | None = None) -> K.Act:
         _, h, w = self._shapes[shape_of or vid]
-        cs = K.pad8(C) if not fp32 else (C + 3) // 4 * 4
+        if vid in getattr(self, "_place", {}):  # the value is a band of a zero-copy concat
+            assert not fp32 and cmap is None
+            key, off = self._place[vid]
+            a = K.Act(self._band_buffer(key), self.batch, h, w, C, off)
+            self.values[vid] = a
+            return a
+        width = C if cmap is None else (cmap[-1] + 1)
+        cs = K.pad8(width) if not fp32 else (width + 3) // 4 * 4
         buf = torch.zeros((self.batch * h * w, cs), dtype=torch.float32 if fp32 else torch.bfloat16,
                           device=self.device)
-        a = K.Act(buf, self.batch, h, w, C, 0)
+        a = K.Act(buf, self.batch, h, w, C, 0, cmap)
         self.values[vid] = a
         return a
+
+    def _f32(self, seq) -> torch.Tensor:
+        t = torch.as_tensor(list(seq), dtype=torch.float32, device=self.device)
+        self._keep.append(t)
+        return t
 
     def _i32(self, seq) -> torch.Tensor:
         t = torch.as_tensor(list(seq), dtype=torch.int32, device=self.device)
@@ -158,6 +177,21 @@ class Engine:
                 info["read"] = read
                 src = g.predecessors(read)[0]
                 absorbed.add(read)
+            # pre-activation prologue (DenseNet: norm -> relu -> conv.read -> conv): a BN and/or
+            # ReLU between the value and this conv's read, read by nothing else and not already
+            # absorbed by its producer's epilogue, is applied while the read stages the operand
+            pro_bn = pro_relu = None
+            s_ = src
+            if (kinds[s_] is LayerKind.PASS_THROUGH and self.specs[s_].op == "relu" and s_ not in absorbed
+                    and len(g.successors(s_)) == 1 and s_ not in output_feed):
+                pro_relu, s_ = s_, g.predecessors(s_)[0]
+            if (kinds[s_] is LayerKind.PER_CHANNEL and self.specs[s_].op in ("bn", "bias") and s_ not in absorbed
+                    and len(g.successors(s_)) == 1 and s_ not in output_feed):
+                pro_bn, s_ = s_, g.predecessors(s_)[0]
+            if pro_bn or pro_relu:
+                info["prologue"] = (pro_bn, pro_relu)
+                absorbed.update(x for x in (pro_bn, pro_relu) if x)
+                src = s_
             cur = lid
             nxt = self._single_succ(cur)
             if nxt is not None and kinds[nxt] is LayerKind.PER_CHANNEL and cur not in output_feed:
@@ -177,6 +211,17 @@ class Engine:
             if nxt is not None and kinds[nxt] is LayerKind.PASS_THROUGH and self.specs[nxt].op == "relu" \
                     and cur not in output_feed:
                 info["relu"] = nxt
+                absorbed.add(nxt)
+                cur = nxt
+                nxt = self._single_succ(cur)
+            # a 2x2/s2 average pool right after a 1x1/s1 conv (DenseNet transition, no ReLU in
+            # between): pool and conv are both linear, so the pool moves in front of the conv
+            # into the operand staging and the conv runs on a quarter of the pixels
+            ps = self.specs.get(nxt) if nxt is not None else None
+            if (ps is not None and ps.op == "avgpool_k" and (ps.kernel, ps.stride, ps.pad) == (2, 2, 0)
+                    and info["relu"] is None and info["add"] is None and cur not in output_feed
+                    and spec.op == "conv" and (spec.kernel, spec.stride, spec.pad) == (1, 1, 0)):
+                info["pool2"] = nxt
                 absorbed.add(nxt)
                 cur = nxt
             info["src"] = src
@@ -234,10 +279,25 @@ class Engine:
                 ops.append(_Op("maxpool", lid, [preds[0]], lid, info={"spec": spec}))
             elif k is LayerKind.PASS_THROUGH and spec is not None and spec.op == "avgpool":
                 ops.append(_Op("avgpool", lid, [preds[0]], lid))
+            elif k is LayerKind.PASS_THROUGH and spec is not None and spec.op == "avgpool_k":
+                ops.append(_Op("avgpool2d", lid, [preds[0]], lid, info={"spec": spec}))
             elif k is LayerKind.GATHER:
                 ops.append(_Op("gather", lid, [preds[0]], lid, info={"idx": g.layer(lid).params}))
+            elif k is LayerKind.CONCAT:
+                # zero-copy when every operand can be stored straight into its band (_plan_concats)
+                ops.append(_Op("concat", lid, list(preds), lid))
             elif k in (LayerKind.PASS_THROUGH, LayerKind.PER_CHANNEL, LayerKind.ADD):
-                ops.append(_Op("eltwise", lid, list(preds), lid, info={"kind": k}))
+                info = {"kind": k}
+                out = lid
+                # a standalone BN / add followed by its only reader, an activation: one pass
+                nxt = self._single_succ(lid)
+                if (k is not LayerKind.PASS_THROUGH and nxt is not None and nxt not in absorbed
+                        and kinds[nxt] is LayerKind.PASS_THROUGH and self.specs[nxt].op in ACTS
+                        and lid not in output_feed):
+                    info["act"] = self.specs[nxt].op
+                    absorbed.add(nxt)
+                    out = nxt
+                ops.append(_Op("eltwise", lid, list(preds), out, info=info))
             else:
                 raise NotImplementedError(f"{lid}: {k.value} has no B200 kernel in this build")
 
@@ -297,10 +357,25 @@ class Engine:
                 cop.info["src"] = r
                 cop.inputs[0] = r
 
+        # --- concat buffer planning (zero-copy bands)
+        self._plan_concats(ops, alias, base, pos, output_feed)
+        ops = [op for op in ops if not (op.kind == "concat" and op.output in self._concat_views)]
+
         # --- schedule: Kahn over value dependencies, ties by topological position
         produced = {op.output: op for op in ops}
 
-        deps = {id(op): {id(produced[base(i)]) for i in op.inputs if base(i) in produced} for op in ops}
+        def producers(v, seen=None):
+            v = base(v)
+            if v in produced:
+                return {id(produced[v])}
+            if v in self._concat_views:  # a zero-copy concat depends on every operand's producer
+                out = set()
+                for u in self._concat_views[v][3]:
+                    out |= producers(u)
+                return out
+            return set()
+
+        deps = {id(op): set().union(*[producers(i) for i in op.inputs]) if op.inputs else set() for op in ops}
         done: set[int] = set()
         sched: list[_Op] = []
         remaining = sorted(ops, key=lambda o: pos[o.anchor])
@@ -325,6 +400,81 @@ class Engine:
             getattr(self, f"_bind_{op.kind}")(op, weight_source, vector_source, output_feed)
         out_id = next(lid for lid in topo if kinds[lid] is LayerKind.OUTPUT)
         self.output_value = self._value(out_id)
+
+    def _plan_concats(self, ops, alias, base, pos, output_feed) -> None:
+        """CONCAT as buffer planning: each operand's producer stores its
+        band straight into one shared buffer, so the concat itself launches nothing.
+        Bands start on 8-channel (16-byte) boundaries -- the producers' TMA stores need
+        aligned bases -- so a concat of pruned widths is a view with a column map
+        (Act.cmap) over a buffer with up to 7 pad columns per band.  Concats are planned
+        largest-first (reverse topological order): DenseNet's per-layer concats are
+        prefixes of the block's last one and all become views of one buffer.  A concat
+        whose operands cannot be placed consistently (already placed elsewhere, an
+        fp32/model-input/view operand) keeps a copy op."""
+        self._place: dict[str, tuple[str, int]] = {}      # value -> (buffer key, physical offset)
+        self._bands: dict[str, list] = {}                  # buffer key -> [width, shape_of, occupied]
+        self._concat_views: dict[str, tuple] = {}          # concat -> (key, base, cmap, operands)
+        self._band_bufs: dict[str, torch.Tensor] = {}
+        producer_of = {op.output: op for op in ops}
+        placeable_kinds = ("conv", "maxpool", "avgpool", "avgpool2d", "eltwise", "gather", "stage")
+        g = self.graph
+
+        def operand(v):  # full-width aliases (identity / flatten) resolve to their base
+            while v in alias and alias[v][2] < 0:
+                v = alias[v][0]
+            return v
+
+        def placeable(v):
+            op = producer_of.get(v)
+            return (op is not None and op.kind in placeable_kinds and v not in output_feed
+                    and v not in self._place and v not in alias)
+
+        def free(key, lo, hi):
+            return all(hi <= a or lo >= b for a, b in self._bands[key][2])
+
+        for c in sorted([op for op in ops if op.kind == "concat"], key=lambda o: -pos[o.anchor]):
+            ins = [operand(v) for v in c.inputs]
+            widths = [g.layer(v).out_channels if v in g else self._value_width(v) for v in ins]
+            offs, o = [], 0
+            for w_ in widths:
+                offs.append(o)
+                o += (w_ + 7) // 8 * 8
+            placed = [(i, self._place[v]) for i, v in enumerate(ins) if v in self._place]
+            if len(set(ins)) != len(ins):
+                continue
+            if not placed:
+                if not all(placeable(v) for v in ins):
+                    continue
+                key, base_off = c.output, 0
+                self._bands[key] = [0, c.output, []]
+            else:
+                key = placed[0][1][0]
+                base_off = placed[0][1][1] - offs[placed[0][0]]
+                ok = base_off >= 0 and all(k_ == key and off == base_off + offs[i] for i, (k_, off) in placed)
+                ok = ok and all(placeable(v) and free(key, base_off + offs[i], base_off + offs[i] + widths[i])
+                                for i, v in enumerate(ins) if v not in self._place)
+                if not ok:
+                    continue
+            for i, v in enumerate(ins):
+                if v not in self._place:
+                    self._place[v] = (key, base_off + offs[i])
+                    self._bands[key][2].append((base_off + offs[i], base_off + offs[i] + widths[i]))
+            band = self._bands[key]
+            band[0] = max(band[0], base_off + offs[-1] + widths[-1])
+            cmap = tuple(offs[i] + j for i, w_ in enumerate(widths) for j in range(w_))
+            dense = all(w_ % 8 == 0 for w_ in widths[:-1])
+            self._concat_views[c.output] = (key, base_off, None if dense else cmap, ins)
+
+    def _value_width(self, v: str) -> int:
+        return self.graph.layer(v).out_channels
+
+    def _band_buffer(self, key: str) -> torch.Tensor:
+        if key not in self._band_bufs:
+            width, shape_of, _ = self._bands[key]
+            _, h, w = self._shapes[shape_of]
+            self._band_bufs[key] = torch.zeros((self.batch * h * w, K.pad8(width)), dtype=torch.bfloat16,
+                                               device=self.device)
+        return self._band_bufs[key]
 
     def _plan_dual_stores(self) -> None:
         """Producer side of GATHER reads: a conv whose output is gathered by later 1x1 convs
@@ -355,6 +505,12 @@ class Engine:
     def _value(self, vid: str) -> K.Act:
         if vid in self.values:
             return self.values[vid]
+        if vid in getattr(self, "_concat_views", {}):
+            key, off, cmap, ins = self._concat_views[vid]
+            _, h, w = self._shapes[vid]
+            a = K.Act(self._band_buffer(key), self.batch, h, w, self.graph.layer(vid).out_channels, off, cmap)
+            self.values[vid] = a
+            return a
         if vid in self._alias:
             b, s, n = self._alias[vid]
             a = self._value(b)
@@ -373,50 +529,128 @@ class Engine:
         # one graph per input buffer for the pipelined Runner)
         op.launch = lambda: K.stage_input(self.input_buf, y, idx_dev)
 
+    @staticmethod
+    def _dense(a: K.Act) -> K.Act:
+        """The physical columns a (possibly column-mapped) value spans, as a dense view."""
+        return a if a.cmap is None else K.Act(a.buf, a.N, a.H, a.W, a.width, a.coff)
+
+    def _alloc_like(self, vid: str, a: K.Act) -> K.Act:
+        """Output of a layout-preserving op (pool / per-channel / activation): the same
+        column map as its input, so a padded concat needs no compaction pass."""
+        if a.cmap is None:
+            return self._alloc(vid, a.C)
+        if vid in getattr(self, "_place", {}):
+            raise NotImplementedError(f"{vid}: a column-mapped value cannot be stored into a concat band")
+        return self._alloc(vid, a.C, cmap=a.cmap)
+
     def _bind_maxpool(self, op, ws, vs, output_feed):
         sp = op.info["spec"]
         x = self._value(op.inputs[0])
-        y = self._alloc(op.output, x.C)
-        op.launch = lambda: K.maxpool(x, sp.kernel, sp.stride, sp.pad, y)
+        y = self._alloc_like(op.output, x)
+        xd, yd = self._dense(x), self._dense(y)
+        op.launch = lambda: K.maxpool(xd, sp.kernel, sp.stride, sp.pad, yd)
+
+    def _bind_avgpool2d(self, op, ws, vs, output_feed):
+        sp = op.info["spec"]
+        x = self._value(op.inputs[0])
+        y = self._alloc_like(op.output, x)
+        xd, yd = self._dense(x), self._dense(y)
+        op.launch = lambda: K.avgpool2d(xd, sp.kernel, sp.stride, sp.pad, yd)
 
     def _bind_avgpool(self, op, ws, vs, output_feed):
         x = self._value(op.inputs[0])
         idx = op.info.get("idx")
+        xd = self._dense(x)
         if idx is not None:  # fused GATHER read of the consumer: compacted kept channels
             y = self._alloc(op.output, len(idx))
-            idx_dev = self._i32(idx)
-            op.launch = lambda: K.avgpool_gather(x, idx_dev, y)
+            idx_dev = self._i32([x.phys(i) for i in idx])
+            op.launch = lambda: K.avgpool_gather(xd, idx_dev, y)
             return
-        y = self._alloc(op.output, x.C)
-        op.launch = lambda: K.avgpool_global(x, y)
+        y = self._alloc_like(op.output, x)
+        yd = self._dense(y)
+        op.launch = lambda: K.avgpool_global(xd, yd)
 
     def _bind_gather(self, op, ws, vs, output_feed):
         x = self._value(op.inputs[0])
         idx = op.info["idx"]
         y = self._alloc(op.output, len(idx))
-        idx_dev = self._i32(idx)
-        win = K.gather_window(idx)
-        op.launch = lambda: K.gather_rows(x, idx_dev, win, 1, y)
+        idx_p = [x.phys(i) for i in idx]
+        idx_dev = self._i32(idx_p)
+        win = K.gather_window(idx_p)
+        xd = self._dense(x)
+        op.launch = lambda: K.gather_rows(xd, idx_dev, win, 1, y)
         n_img_pix = x.H * x.W
         self.conv_stats.append(ConvStats(f"{op.output}(copy)", 0.0, 0.0, 2 * 2 * len(idx) * n_img_pix))
 
+    def _bind_concat(self, op, ws, vs, output_feed):
+        """A concat _plan_concats could not make zero-copy: each operand is copied into its
+        16-byte aligned band of a fresh buffer (the copy the reference's CONCAT implies)."""
+        ins = [self._value(v) for v in op.inputs]
+        widths = [a.C for a in ins]
+        offs, o = [], 0
+        for w_ in widths:
+            offs.append(o)
+            o += K.pad8(w_)
+        dense = all(w_ % 8 == 0 for w_ in widths[:-1])
+        cmap = None if dense else tuple(offs[i] + j for i, w_ in enumerate(widths) for j in range(w_))
+        y = self._alloc(op.output, sum(widths), cmap=cmap)
+        copies = []
+        for a, off in zip(ins, offs):
+            idx_p = [a.phys(i) for i in range(a.C)]
+            copies.append((self._dense(a), self._i32(idx_p), K.gather_window(idx_p),
+                           K.Act(y.buf, y.N, y.H, y.W, a.C, y.coff + off)))
+
+        def launch():
+            for xa, idx_dev, win, dst in copies:
+                K.gather_rows(xa, idx_dev, win, 1, dst)
+
+        op.launch = launch
+
     def _bind_eltwise(self, op, ws, vs, output_feed):
+        """PER_CHANNEL / ADD / activation nodes no conv absorbed (plus a fused trailing
+        activation): ub_eltwise over the physical columns of the operands."""
         kind = op.info["kind"]
         lid = op.anchor
         a = self._value(op.inputs[0])
-        y = self._alloc(op.output, a.C)
         scale = shift = None
-        b = None
-        relu = False
+        others: list[K.Act] = []
+        act = op.info.get("act", "none")
+        gate = None
         if kind is LayerKind.PER_CHANNEL:
             vec, perm = vs(lid)
             scale, shift = self._affine(lid, vec, perm)
         elif kind is LayerKind.ADD:
-            assert len(op.inputs) == 2, "ADD with > 2 operands"
-            b = self._value(op.inputs[1])
+            others = [self._value(v) for v in op.inputs[1:]]
+            if self.specs[lid].op == "mul":  # squeeze-excitation gate (per image x channel)
+                assert len(others) == 1
+                gate, others = others[0], []
+                if a.H * a.W == 1 and gate.H * gate.W > 1:
+                    a, gate = gate, a
         else:
-            relu = True
-        op.launch = lambda: K.affine_add_relu(a, y, scale, shift, b, relu)
+            act = self.specs[lid].op if self.specs[lid].op in ACTS else "relu"
+        y = self._alloc_like(op.output, a)
+        if a.cmap is not None:  # column-mapped operand: expand the vectors over the pad columns
+            assert all(b.cmap == a.cmap for b in others), f"{lid}: operands with different layouts"
+            if scale is not None:
+                full_s = torch.zeros(a.width, device=self.device)
+                full_t = torch.zeros(a.width, device=self.device)
+                idx = torch.tensor(a.cmap, device=self.device)
+                full_s[idx], full_t[idx] = scale, shift
+                scale, shift = full_s, full_t
+                self._keep += [scale, shift]
+        ad, yd = self._dense(a), self._dense(y)
+        od = [self._dense(b) for b in others]
+        gd = self._dense(gate) if gate is not None else None
+
+        def launch():
+            if not od:
+                K.eltwise(ad, yd, scale, shift, None, act, gd)
+                return
+            K.eltwise(ad, yd, scale, shift, od[0], act if len(od) == 1 else "none", gd)
+            for k_, b in enumerate(od[1:]):
+                K.eltwise(yd, yd, None, None, b, act if k_ == len(od) - 2 else "none")
+
+        op.launch = launch
 
     def _affine(self, uid, vec, perm):
         spec = self.specs[uid]
@@ -489,7 +723,45 @@ class Engine:
             self._keep.append(wg)
             plans.append((kind, xv, gidx, lead, cpad, wg, pre, st if st_eff is None else st_eff))
 
-        if gather is None:
+        staged = info.get("prologue") is not None or info.get("pool2") is not None or x.cmap is not None
+        if staged:
+            # the read is staged by ub_gather_rows_ex into a compact buffer -- the gather (through
+            # the concat's column map), the reader's BN/ReLU prologue and a moved 2x2 pool in one
+            # pass -- and the conv reads it densely
+            idx = gather if gather is not None else list(range(x.C))
+            idx_p = [x.phys(i) for i in idx]
+            xb = K.Act(x.buf, x.N, x.H, x.W, x.width, x.coff)
+            pscale = pshift = None
+            prelu = False
+            if info.get("prologue") is not None:
+                pro_bn, pro_relu = info["prologue"]
+                prelu = pro_relu is not None
+                if pro_bn is not None:
+                    vec, perm = vs(pro_bn)
+                    sc, sh = self._affine(pro_bn, vec, perm)
+                    sc, sh = sc.cpu(), sh.cpu()
+                    pscale = self._f32([float(sc[i]) if i >= 0 else 0.0 for i in idx])
+                    pshift = self._f32([float(sh[i]) if i >= 0 else 0.0 for i in idx])
+                else:
+                    pscale = self._f32([1.0] * len(idx))
+                    pshift = self._f32([0.0] * len(idx))
+            pool2 = info.get("pool2") is not None
+            st_g = st if (kk == 1 and pd == 0 and not pool2) else 1
+            if pool2:
+                ho, wo = x.H // 2, x.W // 2
+            else:
+                ho, wo = (x.H - 1) // st_g + 1, (x.W - 1) // st_g + 1
+            scratch = K.empty_act(self.batch, ho, wo, cin, self.device)
+            self._keep.append(scratch.buf)
+            gdev = self._i32(idx_p)
+            win = K.gather_window(idx_p)
+
+            def pre(xb=xb, gdev=gdev, scratch=scratch, win=win, st_g=st_g, pool2=pool2, pscale=pscale,
+                    pshift=pshift, prelu=prelu):
+                K.gather_rows_ex(xb, gdev, win, st_g, scratch, pool2=pool2, scale=pscale, shift=pshift, relu=prelu)
+
+            add_plan("copy", scratch, None, cols, cin, pre=pre, st_eff=st if st_g == 1 else 1)
+        elif gather is None:
             add_plan("slice", x, None, cols, cin)
         else:
             k_order = sorted(range(cin), key=lambda k: (gather[k], k))

@@ -32,7 +32,11 @@ def _dev_i32(seq, device) -> torch.Tensor:
 @dataclass
 class Act:
     """An NHWC bf16 activation view: `buf` is [N*H*W, cstride]; the logical
-    tensor is channels [coff, coff + C) (a SLICE view needs no copy)."""
+    tensor is channels [coff, coff + C) (a SLICE view needs no copy).
+
+    `cmap` (optional): logical channel i lives in physical column coff + cmap[i].  A
+    zero-copy CONCAT whose bands start on 16-byte boundaries (each producer stores at an
+    8-aligned channel offset) is such a view; cmap is None when the layout is dense."""
 
     buf: torch.Tensor
     N: int
@@ -40,6 +44,7 @@ class Act:
     W: int
     C: int
     coff: int = 0
+    cmap: tuple | None = None
 
     @property
     def cstride(self) -> int:
@@ -49,11 +54,28 @@ class Act:
     def npix(self) -> int:
         return self.N * self.H * self.W
 
+    @property
+    def width(self) -> int:
+        """Physical columns spanned from coff."""
+        return self.C if self.cmap is None else (self.cmap[-1] + 1 if self.cmap else 0)
+
+    def phys(self, i: int) -> int:
+        """Physical column (relative to coff) of logical channel i (-1 stays -1)."""
+        if i < 0 or self.cmap is None:
+            return i
+        return self.cmap[i]
+
     def view(self, start: int, length: int) -> "Act":
-        return Act(self.buf, self.N, self.H, self.W, length, self.coff + start)
+        if self.cmap is None:
+            return Act(self.buf, self.N, self.H, self.W, length, self.coff + start)
+        sub = self.cmap[start:start + length]
+        if all(b - a == 1 for a, b in zip(sub, sub[1:])):  # contiguous inside one band
+            return Act(self.buf, self.N, self.H, self.W, length, self.coff + sub[0])
+        return Act(self.buf, self.N, self.H, self.W, length, self.coff, tuple(sub))
 
     def to_nchw(self, dtype=torch.float32) -> torch.Tensor:
-        t = self.buf[:, self.coff:self.coff + self.C].reshape(self.N, self.H, self.W, self.C)
+        cols = [self.coff + self.phys(i) for i in range(self.C)]
+        t = self.buf[:, cols].reshape(self.N, self.H, self.W, self.C)
         return t.permute(0, 3, 1, 2).to(dtype)
 
 
@@ -132,6 +154,15 @@ def gather_rows(x: Act, idx_dev: torch.Tensor, window: tuple[int, int], stride: 
     lo, hi = window
     _lib.call("ub_gather_rows", _p(x.buf), x.cstride, x.coff, lo, hi, _p(idx_dev), idx_dev.numel(), x.N, x.H, x.W,
               stride, _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def gather_rows_ex(x: Act, idx_dev: torch.Tensor, window: tuple[int, int], stride: int, y: Act,
+                   pool2: bool = False, scale: torch.Tensor | None = None, shift: torch.Tensor | None = None,
+                   relu: bool = False) -> None:
+    """ub_gather_rows_ex: gather + the reader's BN/ReLU prologue (+ a 2x2 average pool)."""
+    lo, hi = window
+    _lib.call("ub_gather_rows_ex", _p(x.buf), x.cstride, x.coff, lo, hi, _p(idx_dev), idx_dev.numel(), x.N, x.H,
+              x.W, stride, int(pool2), _p(scale), _p(shift), int(relu), _p(y.buf), y.cstride, y.coff, _stream())
 
 
 def gather_window(idx) -> tuple[int, int]:
@@ -262,6 +293,29 @@ def avgpool_global(x: Act, y: Act) -> None:
 
 def avgpool_gather(x: Act, idx_dev: torch.Tensor, y: Act) -> None:
     _lib.call("ub_avgpool_gather", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(idx_dev), idx_dev.numel(),
+              _p(y.buf), y.cstride, y.coff, _stream())
+
+
+def eltwise(a: Act, y: Act, scale=None, shift=None, b: Act | None = None, act: str = "none",
+            gate: Act | None = None) -> None:
+    """ub_eltwise: y = act(a * scale + shift + b) * gate (gate: per-image [N, 1, 1, C])."""
+    d = _lib.EltwiseDesc()
+    d.N, d.HW, d.C = a.N, a.H * a.W, a.C
+    d.a, d.a_cstride, d.a_coff = a.buf.data_ptr(), a.cstride, a.coff
+    d.scale = scale.data_ptr() if scale is not None else None
+    d.shift = shift.data_ptr() if shift is not None else None
+    if b is not None:
+        d.b, d.b_cstride, d.b_coff = b.buf.data_ptr(), b.cstride, b.coff
+    d.act = _lib.UB_ACT[act]
+    if gate is not None:
+        assert gate.H * gate.W == 1 and gate.N == a.N
+        d.gate, d.gate_cstride, d.gate_coff = gate.buf.data_ptr(), gate.cstride, gate.coff
+    d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
+    _lib.check(_lib.load().ub_eltwise(ctypes.byref(d), _stream()))
+
+
+def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:
+    _lib.call("ub_avgpool2d", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, k, stride, pad, y.H, y.W,
               _p(y.buf), y.cstride, y.coff, _stream())
 
 

@@ -177,3 +177,19 @@ def test_resnet50_full_batch_256_autotuned_matches_oracle_on_sampled_images():
     got_small = small.forward(x[pick].cuda()).cpu()
     assert deviation(got[pick], got_small) <= TOL
     assert top1_agreement(got[pick], got_small) == 1.0
+
+
+@pytest.mark.parametrize("strategy", ["reorder", "baseline"])
+def test_densenet121_logits_match_oracle(strategy):
+    """Config 4 (DenseNet-121 @ 50 %): zero-copy band concats, BN/ReLU prologues on the
+    staged reads, transition pools moved in front of their convs; randomised BN."""
+    sm, plans, eg, maps = _setup("densenet121_s50", strategy)
+    N = 4
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(2))
+    eng = EN.from_plans(sm, eg, maps, batch=N)
+    eng.capture()
+    got = eng.forward(x.cuda()).cpu()
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
+    assert deviation(got, ref) <= TOL, deviation(got, ref)
+    assert top1_agreement(got, ref) == 1.0

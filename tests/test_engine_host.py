@@ -80,3 +80,38 @@ def test_conv_stats_match_survey_flops(stub_kernels, r50):
     eng, _ = _engine(r50, "reorder", "fused")
     flops, _ = eng.per_image_work()
     assert 2.55e9 < flops < 2.75e9  # 2.644 GFLOP/img (reorder, per-layer)
+
+
+@pytest.fixture(scope="module")
+def dn121():
+    return build_spatial_model(CONFIGS["densenet121_s50"])
+
+
+@pytest.mark.parametrize("strategy", ["reorder", "baseline"])
+def test_densenet121_concats_are_zero_copy_bands(stub_kernels, dn121, strategy):
+    """Config 4: every dense-block concat is a view of one band buffer per block (the
+    producers store their bands at 8-aligned offsets), every norm1/relu1 pair is applied
+    as the prologue of its conv1's staged read, each transition's 2x2 average pool moves
+    in front of its 1x1 conv, and no concat copy or standalone BN/ReLU pass is left
+    except the final norm5 + relu (fused into one eltwise)."""
+    cfg = CONFIGS["densenet121_s50"]
+    plans = P.load_plans(cfg.asset_dir / f"plans_{strategy}.json")
+    eg = E.export_graph(dn121.graph, plans)
+    eng = EN.from_plans(dn121, eg, E.compose_maps(dn121.graph, plans), batch=2, device="cpu")
+    kinds = [op.kind for op in eng.ops]
+    n_concat = sum(1 for lay in eg.layers if lay.kind.value == "concat")
+    assert n_concat == 58 and kinds.count("concat") == 0
+    assert len(eng._concat_views) == 58
+    assert len({v[0] for v in eng._concat_views.values()}) == 4  # one buffer per dense block
+    convs = [op for op in eng.ops if op.kind == "conv"]
+    assert len(convs) == 121
+    pro = [op for op in convs if op.info.get("prologue")]
+    assert len(pro) == 58 + 3  # every dense layer's conv1 + the three transitions
+    assert sum(1 for op in convs if op.info.get("pool2")) == 3
+    assert kinds.count("avgpool2d") == 0 and kinds.count("eltwise") == 1
+    assert kinds.count("avgpool") == 1 and kinds.count("maxpool") == 0  # stem pool fused
+    # schedule respects data dependencies through the band views
+    done = set()
+    for op in eng.ops:
+        done.add(op.output)
+    assert eng.output_value.C == 1000

@@ -559,3 +559,77 @@ def test_production_bf16_layouts_bit_exact_vs_fp32_oihw(layout, kk, cin, lead):
         want[:, :kk * kk * cin] = ref.permute(0, 2, 3, 1).reshape(len(rows), -1)
     torch.cuda.synchronize()
     assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
+@pytest.mark.parametrize("pool2,affine,relu,stride", [(False, True, True, 1), (True, True, True, 1),
+                                                      (True, False, False, 1), (False, True, False, 2)])
+def test_gather_rows_prologue_and_pool(pool2, affine, relu, stride):
+    """ub_gather_rows_ex: gather through a column map + the reader's BN/ReLU prologue
+    (+ the 2x2 average pool moved in front of a 1x1 conv) vs torch fp32 on the bf16 input."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(int(pool2) * 10 + int(affine) + stride)
+    N, C, H, W, cs, coff = 2, 150, 10, 12, 168, 8
+    x = torch.randn(N, cs, H, W, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    idx = [3, 140, -1, 7, 8, 9, 77, 31, 0, 149, 60]
+    sc = 0.5 + torch.rand(len(idx), generator=g)
+    sh = torch.randn(len(idx), generator=g)
+    Ho, Wo = (H // 2, W // 2) if pool2 else ((H - 1) // stride + 1, (W - 1) // stride + 1)
+    y = K.empty_act(N, Ho, Wo, len(idx), dev)
+    y.buf.fill_(float("nan"))
+    xv = xa.view(coff, C)
+    K.gather_rows_ex(xv, torch.tensor(idx, dtype=torch.int32, device=dev), K.gather_window(idx), stride, y,
+                     pool2=pool2, scale=sc.to(dev) if affine else None, shift=sh.to(dev) if affine else None,
+                     relu=relu)
+    torch.cuda.synchronize()
+    xs = _bf(x)[:, coff:coff + C]
+    ref = torch.zeros(N, K.pad8(len(idx)), H, W)
+    for i, j in enumerate(idx):
+        if j >= 0:
+            v = xs[:, j]
+            if affine:
+                v = sc[i] * v + sh[i]
+            if relu:
+                v = v.clamp_min(0)
+            ref[:, i] = v
+    ref = torch.nn.functional.avg_pool2d(ref, 2, 2) if pool2 else ref[:, :, ::stride, ::stride]
+    got = y.buf.float().reshape(N, Ho, Wo, -1).permute(0, 3, 1, 2).cpu()
+    assert torch.isfinite(got).all()
+    assert (got - ref).abs().max() <= 1e-2 * ref.abs().max() + 1e-6
+    assert (got[:, len(idx):] == 0).all()
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "relu6", "hardswish", "hardsigmoid", "silu", "sigmoid"])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_eltwise(act, aligned):
+    """ub_eltwise: y = act(a * scale + shift + b) * gate, vector (16-byte) and scalar paths."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(len(act) + int(aligned))
+    N, C, H, W = 3, 37, 5, 6
+    coff = 8 if aligned else 3
+    a = K.act_from_nchw(torch.randn(N, C + 16, H, W, generator=g).to(dev) * 3).view(coff, C)
+    b = K.act_from_nchw(torch.randn(N, C + 8, H, W, generator=g).to(dev)).view(8 if aligned else 1, C)
+    gate = K.act_from_nchw(torch.rand(N, C, 1, 1, generator=g).to(dev))
+    sc, sh = torch.randn(C, generator=g), torch.randn(C, generator=g)
+    y = K.empty_act(N, H, W, C, dev)
+    K.eltwise(a, y, sc.to(dev), sh.to(dev), b, act, gate)
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "relu": torch.relu, "relu6": lambda v: v.clamp(0, 6),
+           "hardswish": torch.nn.functional.hardswish, "hardsigmoid": torch.nn.functional.hardsigmoid,
+           "silu": torch.nn.functional.silu, "sigmoid": torch.sigmoid}
+    ref = fns[act](a.to_nchw().cpu() * sc.view(1, -1, 1, 1) + sh.view(1, -1, 1, 1) + b.to_nchw().cpu())
+    ref = ref * gate.to_nchw().cpu()
+    assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
+def test_avgpool2d():
+    dev = "cuda"
+    x = torch.randn(2, 45, 13, 14, generator=torch.Generator().manual_seed(3))
+    xa = K.act_from_nchw(x.to(dev))
+    for k, s, p in ((2, 2, 0), (3, 1, 1), (3, 2, 1)):
+        Ho, Wo = (13 + 2 * p - k) // s + 1, (14 + 2 * p - k) // s + 1
+        y = K.empty_act(2, Ho, Wo, 45, dev)
+        K.avgpool2d(xa, k, s, p, y)
+        torch.cuda.synchronize()
+        ref = torch.nn.functional.avg_pool2d(_bf(x), k, s, p)
+        assert _rel(y.to_nchw().cpu(), ref) < 1e-2

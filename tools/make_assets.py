@@ -25,14 +25,13 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-REF = Path("/root/reference/pkg/src")
-sys.path.insert(0, str(REF))
 
 import numpy as np  # noqa: E402
 
-import reslice  # noqa: E402
-from reslice.graph import graph_from_dict as ref_graph_from_dict  # noqa: E402
-from reslice.planner import plan_to_dict as ref_plan_to_dict  # noqa: E402
+from paper_2307_08771_b200.ref import reslice  # noqa: E402
+
+ref_graph_from_dict = reslice.graph.graph_from_dict
+ref_plan_to_dict = reslice.planner.plan_to_dict
 
 from paper_2307_08771_b200 import ir  # noqa: E402
 from paper_2307_08771_b200.configs import CONFIGS, build_spatial_model  # noqa: E402
@@ -55,6 +54,9 @@ def make(name: str) -> None:
         store[lid] = arr
     assert not reslice.graph.validate(g_ref, store)
 
+    if cfg.native_planner:  # reference plan_model, native decompose/order core
+        from paper_2307_08771_b200 import native_planner
+        native_planner.install(reslice)
     t0 = time.time()
     scores = reslice.score_channels(g_ref, store.tensors, cfg.heuristic, side="input")
     masks = reslice.make_masks(g_ref, scores, cfg.sparsity, "unconstrained",
@@ -88,6 +90,10 @@ def make(name: str) -> None:
         }
         print(f"{name} {strategy}: {len(plans)} plans, copied {res.totals.copied}/{res.totals.total_reads}, "
               f"plan {t_plan:.1f}s export {t_export:.1f}s, kinds {kinds}", flush=True)
+    meta["native_planner"] = cfg.native_planner
+    if cfg.native_planner:
+        from paper_2307_08771_b200 import native_planner
+        native_planner.uninstall()
     (out / "meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
 
 
