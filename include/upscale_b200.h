@@ -187,6 +187,16 @@ int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream);
  * 16-byte aligned rows.  A DenseNet transition's AvgPool2d(2, 2) when it cannot be moved
  * in front of its 1x1 conv (ub_gather_rows_ex pool2).
  */
+/*
+ * Depthwise k x k conv (groups == channels) with the following BN folded in and the
+ * activation fused, NHWC bf16, 16-byte aligned rows:
+ *   y[n][yo][xo][c] = act(bias[c] + sum_{dy,dx} w[(dy*k + dx)*pad8(C) + c] * x[n][yo*s-pad+dy][xo*s-pad+dx][c])
+ * w: fp32 [k*k][pad8(C)] (16-byte aligned); bias nullable.  The depthwise convs of
+ * MobileNetV3 / EfficientNetV2, lowered to PER_CHANNEL-like nodes.
+ */
+int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w, const float* bias,
+              int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
+
 int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int s, int pad, int Ho,
                  int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
@@ -204,7 +214,7 @@ typedef struct {
   const float* bias;           /* [cout] fp32 or NULL */
   const void* residual;        /* bf16 NHWC [N*Ho*Wo][res_cstride] or NULL */
   int res_cstride, res_coff;
-  int relu;                    /* apply max(0, .) after bias + residual */
+  int relu;                    /* activation after bias + residual: UB_ACT_* code (1 = ReLU, 0 = none) */
   void* y;                     /* output, NHWC [N*Ho*Wo][y_cstride] */
   int y_cstride, y_coff;
   int y_dtype;                 /* UB_BF16 or UB_F32 */

@@ -18,16 +18,23 @@ import torch
 import torch.nn.functional as F
 
 
+_ACTS = {"relu": torch.relu, "relu6": lambda v: v.clamp(0.0, 6.0), "hardswish": F.hardswish,
+         "hardsigmoid": F.hardsigmoid, "silu": F.silu, "sigmoid": torch.sigmoid}
+
+
 def _kind(lay) -> str:
     return lay.kind.value if hasattr(lay.kind, "value") else str(lay.kind)
 
 
 def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
                 vectors: Mapping[str, Mapping[str, torch.Tensor]], x: torch.Tensor,
-                masks: Mapping[str, tuple] | None = None, dtype=torch.float64, values: dict | None = None
-                ) -> torch.Tensor:
+                masks: Mapping[str, tuple] | None = None, dtype=torch.float64, values: dict | None = None,
+                store_dtype=None) -> torch.Tensor:
     """Returns the OUTPUT node's value ([N, C] if spatially collapsed).  If
-    `values` is a dict it receives every node's output (debugging aid)."""
+    `values` is a dict it receives every node's output (debugging aid).
+    `store_dtype` (e.g. torch.bfloat16): every node's output is rounded to it and back
+    -- the reference evaluated at a GPU's storage precision (a precision control for
+    the parity tests, not a model of any particular kernel fusion)."""
     masks = masks or {}
     vals: dict[str, torch.Tensor] = {}
     out_id = None
@@ -52,6 +59,8 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
                 out = F.conv2d(v, w, stride=spec.stride, padding=spec.pad)
             else:  # linear / 1x1 channel mix over a collapsed tensor
                 out = F.conv2d(v, w)
+        elif k == "add" and op == "mul":  # squeeze-excitation gate (lowered to a positional ADD)
+            out = ins[0] * ins[1]
         elif k == "add":
             out = ins[0]
             for t in ins[1:]:
@@ -68,11 +77,18 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
                 out = F.avg_pool2d(v, spec.kernel, spec.stride, spec.pad)
             elif op in ("flatten", "identity"):
                 out = v
+            elif op in _ACTS:
+                out = _ACTS[op](v)
             else:  # relu, and the reference's PASS_THROUGH semantics
                 out = torch.clamp_min(v, 0.0)
         elif k == "per_channel":
             vec = vectors[lid]
-            if op == "bn":
+            if op == "dwconv":  # depthwise conv lowered to a channel-wise node
+                C = ins[0].shape[1]
+                w = vec["dw"].to(dtype).view(C, 1, spec.kernel, spec.kernel)
+                b = vec["bias"].to(dtype) if "bias" in vec else None
+                out = F.conv2d(ins[0], w, b, stride=spec.stride, padding=spec.pad, groups=C)
+            elif op == "bn":
                 scale = vec["weight"].to(dtype) / torch.sqrt(vec["var"].to(dtype) + spec.eps)
                 out = (ins[0] - vec["mean"].to(dtype).view(1, -1, 1, 1)) * scale.view(1, -1, 1, 1) \
                     + vec["bias"].to(dtype).view(1, -1, 1, 1)
@@ -93,6 +109,8 @@ def run_spatial(graph, specs: Mapping, weights: Mapping[str, torch.Tensor],
             out_id = lid
         else:
             raise ValueError(f"{lid}: unknown kind {k}")
+        if store_dtype is not None and k != "output":
+            out = out.to(store_dtype).to(dtype)
         if out.shape[1] != lay.out_channels:
             raise ValueError(f"{lid}: produced {out.shape[1]} channels, expected {lay.out_channels}")
         vals[lid] = out

@@ -88,6 +88,8 @@ SIGNATURES = {
     "ub_eltwise": (c_int, [ctypes.POINTER(EltwiseDesc), c_vp]),
     "ub_avgpool2d": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
                              c_int, c_int, c_vp]),
+    "ub_dwconv": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_int,
+                          c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),

@@ -48,6 +48,19 @@ CONFIGS = {
     # csrc/planner.cpp), which plans it in 0.2 s.
     "densenet121_s50": Config("densenet121_s50", "densenet121", 0.5, batch=128, native_planner=True),
 }
+# BASELINE.json configs[1]: the MobileNetV3-Small batch-1 latency sweep, UPSCALE vs baseline
+# export (depthwise convs + squeeze-excitation lowered per SURVEY.md A.5)
+MOBILENET_SWEEP = (0.1, 0.3, 0.5, 0.7, 0.9, 0.95)
+for _s in MOBILENET_SWEEP:
+    _n = f"mobilenet_v3_small_s{round(_s * 100):02d}"
+    CONFIGS[_n] = Config(_n, "mobilenet_v3_small", _s, batch=1, native_planner=True)
+# BASELINE.json configs[4]: EfficientNetV2-S / ResNet-101 at 30/50/70 %, batch 256
+for _s in (0.3, 0.5, 0.7):
+    _n = f"efficientnet_v2_s_s{round(_s * 100):02d}"
+    CONFIGS[_n] = Config(_n, "efficientnet_v2_s", _s, batch=256, native_planner=True)
+for _s in (0.3, 0.7):
+    _n = f"resnet101_s{round(_s * 100):02d}"
+    CONFIGS[_n] = Config(_n, "resnet101", _s, batch=256, native_planner=True)
 
 NORTH_STAR = "resnet50_s50"
 

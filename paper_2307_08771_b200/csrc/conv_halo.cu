@@ -502,9 +502,13 @@ __global__ void __maxnreg__(96)
             const float2 s3 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])),
                                         make_float2(b1.z, b1.w));
             uint4 o;
-            if (p.relu) {
+            if (p.relu == 1) {
               o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y), cvt_relu_bf16x2(s2.x, s2.y),
                              cvt_relu_bf16x2(s3.x, s3.y));
+            } else if (p.relu > 1) {  // other UB_ACT_* activations
+              const int a = p.relu;
+              o = make_uint4(cvt_bf16x2(act_f(s0.x, a), act_f(s0.y, a)), cvt_bf16x2(act_f(s1.x, a), act_f(s1.y, a)),
+                             cvt_bf16x2(act_f(s2.x, a), act_f(s2.y, a)), cvt_bf16x2(act_f(s3.x, a), act_f(s3.y, a)));
             } else {
               o = make_uint4(cvt_bf16x2(s0.x, s0.y), cvt_bf16x2(s1.x, s1.y), cvt_bf16x2(s2.x, s2.y),
                              cvt_bf16x2(s3.x, s3.y));

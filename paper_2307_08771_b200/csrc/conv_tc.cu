@@ -796,11 +796,16 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
               for (int jj = 0; jj < 4; ++jj) {
                 uint4 o;
                 const float* f = reinterpret_cast<const float*>(r) + jj * 8;
-                if (p.relu) {
+                if (p.relu == 1) {
                   o.x = cvt_relu_bf16x2(f[0], f[1]);
                   o.y = cvt_relu_bf16x2(f[2], f[3]);
                   o.z = cvt_relu_bf16x2(f[4], f[5]);
                   o.w = cvt_relu_bf16x2(f[6], f[7]);
+                } else if (p.relu > 1) {  // other UB_ACT_* activations (hardswish, SiLU, ...)
+                  o.x = cvt_bf16x2(act_f(f[0], p.relu), act_f(f[1], p.relu));
+                  o.y = cvt_bf16x2(act_f(f[2], p.relu), act_f(f[3], p.relu));
+                  o.z = cvt_bf16x2(act_f(f[4], p.relu), act_f(f[5], p.relu));
+                  o.w = cvt_bf16x2(act_f(f[6], p.relu), act_f(f[7], p.relu));
                 } else {
                   o.x = cvt_bf16x2(f[0], f[1]);
                   o.y = cvt_bf16x2(f[2], f[3]);
@@ -819,7 +824,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
             if (m < p.M && nv > 0) {
               float v[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = p.relu ? fmaxf(__uint_as_float(r[i]), 0.f) : __uint_as_float(r[i]);
+              for (int i = 0; i < 32; ++i) v[i] = act_f(__uint_as_float(r[i]), p.relu);
               const size_t yo = static_cast<size_t>(m) * p.y_cstride + p.y_coff + nb;
               if (p.y_f32) {
                 float* yp = reinterpret_cast<float*>(p.y) + yo;

@@ -16,18 +16,6 @@
 namespace ub {
 namespace {
 
-UB_DEVI float act_f(float v, int act) {
-  switch (act) {
-    case UB_ACT_RELU: return fmaxf(v, 0.f);
-    case UB_ACT_RELU6: return fminf(fmaxf(v, 0.f), 6.f);
-    case UB_ACT_HARDSWISH: return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
-    case UB_ACT_HARDSIGMOID: return fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
-    case UB_ACT_SILU: return v / (1.f + __expf(-v));
-    case UB_ACT_SIGMOID: return 1.f / (1.f + __expf(-v));
-    default: return v;
-  }
-}
-
 UB_DEVI float bf(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 UB_DEVI uint16_t tobf(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
 
@@ -123,6 +111,73 @@ __global__ void __launch_bounds__(256) avgpool2d_kernel(const uint16_t* __restri
   }
 }
 
+
+// Depthwise k x k conv (groups == channels, multiplier 1) with the following BN folded
+// into w/bias and the activation fused: y[n][yo][xo][c] = act(bias[c] +
+// sum_{dy,dx} w[dy*k+dx][c] * x[n][yo*s-pad+dy][xo*s-pad+dx][c]).  MobileNetV3 /
+// EfficientNetV2 lower it to a PER_CHANNEL-like interior node, so the
+// planner permutes its filters with the channel order.  One thread per (output pixel,
+// 8 channels): 16-byte input loads per tap (neighbouring pixels' taps hit L1), fp32
+// accumulation, weights [k*k][C] fp32 read as float4 pairs.
+__global__ void __launch_bounds__(256) dwconv_kernel(const uint16_t* __restrict__ x, int N, int H, int W, int C,
+                                                     int x_cstride, int x_coff, const float* __restrict__ w,
+                                                     const float* __restrict__ bias, int k, int s, int pad, int act,
+                                                     int Ho, int Wo, uint16_t* __restrict__ y, int y_cstride,
+                                                     int y_coff) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int groups = (C + 7) / 8;
+  const long long total = static_cast<long long>(N) * Ho * Wo * groups;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(e % groups);
+    const long long p = e / groups;
+    const int c0 = g * 8;
+    const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
+    const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+    const int yo = r / Wo, xo = r - yo * Wo;
+    float acc[8];
+    if (bias) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = c0 + j < C ? bias[c0 + j] : 0.f;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    }
+    for (int dy = 0; dy < k; ++dy) {
+      const int yi = yo * s - pad + dy;
+      if (yi < 0 || yi >= H) continue;
+      for (int dx = 0; dx < k; ++dx) {
+        const int xi = xo * s - pad + dx;
+        if (xi < 0 || xi >= W) continue;
+        uint16_t v[8];
+        *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(
+            x + ((static_cast<long long>(n) * H + yi) * W + xi) * x_cstride + x_coff + c0));
+        const float* wt = w + static_cast<long long>(dy * k + dx) * ((C + 7) / 8 * 8) + c0;
+        const float4 w0 = __ldg(reinterpret_cast<const float4*>(wt));
+        const float4 w1 = __ldg(reinterpret_cast<const float4*>(wt + 4));
+        acc[0] = fmaf(w0.x, bf(v[0]), acc[0]);
+        acc[1] = fmaf(w0.y, bf(v[1]), acc[1]);
+        acc[2] = fmaf(w0.z, bf(v[2]), acc[2]);
+        acc[3] = fmaf(w0.w, bf(v[3]), acc[3]);
+        acc[4] = fmaf(w1.x, bf(v[4]), acc[4]);
+        acc[5] = fmaf(w1.y, bf(v[5]), acc[5]);
+        acc[6] = fmaf(w1.z, bf(v[6]), acc[6]);
+        acc[7] = fmaf(w1.w, bf(v[7]), acc[7]);
+      }
+    }
+    uint16_t o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[j], act));
+    uint16_t* yp = y + p * y_cstride + y_coff + c0;
+    if (c0 + 8 <= C) {
+      *reinterpret_cast<uint4*>(yp) = *reinterpret_cast<const uint4*>(o);
+    } else {
+      for (int j = 0; c0 + j < C; ++j) yp[j] = o[j];
+    }
+  }
+}
+
 bool a16(const void* base, int cstride, int coff) {
   return base == nullptr || (aligned16(base) && (cstride & 7) == 0 && (coff & 7) == 0);
 }
@@ -160,4 +215,21 @@ extern "C" int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cst
                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "avgpool2d_kernel");
+}
+
+extern "C" int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w,
+                         const float* bias, int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride,
+                         int y_coff, cudaStream_t stream) {
+  if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || s < 1 || pad < 0 || Ho < 1 || Wo < 1 ||
+      act < UB_ACT_NONE || act > UB_ACT_SIGMOID)
+    return fail(UB_EINVAL, "ub_dwconv: bad arguments");
+  if (!a16(x, x_cstride, x_coff) || !a16(y, y_cstride, y_coff) || x_coff + C > x_cstride || y_coff + C > y_cstride ||
+      (reinterpret_cast<uintptr_t>(w) & 15))
+    return fail(UB_EINVAL, "ub_dwconv: rows must be 16-byte aligned");
+  const long long work = static_cast<long long>(N) * Ho * Wo * ((C + 7) / 8);
+  const cudaError_t e = launch_pdl(dwconv_kernel, dim3(grid_for(work, 256, 1)), dim3(256), 0, stream,
+                                   static_cast<const uint16_t*>(x), N, H, W, C, x_cstride, x_coff, w, bias, k, s, pad,
+                                   act, Ho, Wo, static_cast<uint16_t*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(e, "dwconv_kernel");
 }

@@ -340,6 +340,19 @@ UB_DEVI uint32_t cvt_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
 }
+// Activation codes of include/upscale_b200.h (UB_ACT_*); conv epilogues take the code in
+// their `relu` field (1 = ReLU keeps its packed cvt.relu fast path).
+UB_DEVI float act_f(float v, int act) {
+  switch (act) {
+    case 1: return fmaxf(v, 0.f);
+    case 2: return fminf(fmaxf(v, 0.f), 6.f);
+    case 3: return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
+    case 4: return fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
+    case 5: return v / (1.f + __expf(-v));
+    case 6: return 1.f / (1.f + __expf(-v));
+    default: return v;
+  }
+}
 UB_DEVI uint32_t cvt_relu_bf16x2(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));

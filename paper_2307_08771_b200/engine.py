@@ -109,6 +109,9 @@ class Engine:
                 w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
             elif lay.kind is LayerKind.CHANNEL_MIX:
                 assert (h, w) == (1, 1), f"{lid}: linear layer on a spatial tensor"
+            elif lay.kind is LayerKind.PER_CHANNEL and spec is not None and spec.op == "dwconv":
+                h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
+                w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
             elif lay.kind is LayerKind.PASS_THROUGH and spec is not None:
                 if spec.op == "maxpool":
                     h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
@@ -142,6 +145,11 @@ class Engine:
         a = K.Act(buf, self.batch, h, w, C, 0, cmap)
         self.values[vid] = a
         return a
+
+    def _act_code(self, node: str | None) -> int:
+        if node is None:
+            return 0
+        return _lib.UB_ACT[self.specs[node].op]
 
     def _f32(self, seq) -> torch.Tensor:
         t = torch.as_tensor(list(seq), dtype=torch.float32, device=self.device)
@@ -188,7 +196,13 @@ class Engine:
             if (kinds[s_] is LayerKind.PER_CHANNEL and self.specs[s_].op in ("bn", "bias") and s_ not in absorbed
                     and len(g.successors(s_)) == 1 and s_ not in output_feed):
                 pro_bn, s_ = s_, g.predecessors(s_)[0]
-            if pro_bn or pro_relu:
+            # ... unless the value comes straight from a conv / depthwise conv, whose epilogue
+            # takes the BN and activation instead (MobileNet: dw -> bn -> act -> conv)
+            src_k = kinds[s_]
+            fusable_src = ((src_k is LayerKind.CHANNEL_MIX or (src_k is LayerKind.PER_CHANNEL
+                                                                and self.specs[s_].op == "dwconv"))
+                           and len(g.successors(s_)) == 1)
+            if (pro_bn or pro_relu) and not fusable_src:
                 info["prologue"] = (pro_bn, pro_relu)
                 absorbed.update(x for x in (pro_bn, pro_relu) if x)
                 src = s_
@@ -208,9 +222,9 @@ class Engine:
                     absorbed.add(nxt)
                     cur = nxt
                     nxt = self._single_succ(cur)
-            if nxt is not None and kinds[nxt] is LayerKind.PASS_THROUGH and self.specs[nxt].op == "relu" \
+            if nxt is not None and kinds[nxt] is LayerKind.PASS_THROUGH and self.specs[nxt].op in ACTS \
                     and cur not in output_feed:
-                info["relu"] = nxt
+                info["relu"] = nxt  # the epilogue activation (UB_ACT_* code; ReLU for ResNet/DenseNet)
                 absorbed.add(nxt)
                 cur = nxt
                 nxt = self._single_succ(cur)
@@ -283,6 +297,23 @@ class Engine:
                 ops.append(_Op("avgpool2d", lid, [preds[0]], lid, info={"spec": spec}))
             elif k is LayerKind.GATHER:
                 ops.append(_Op("gather", lid, [preds[0]], lid, info={"idx": g.layer(lid).params}))
+            elif k is LayerKind.PER_CHANNEL and spec is not None and spec.op == "dwconv":
+                # depthwise conv + its BN + activation in one launch (ub_dwconv)
+                info = {"bn": None, "act": None}
+                cur = lid
+                nxt = self._single_succ(cur)
+                if (nxt is not None and nxt not in absorbed and kinds[nxt] is LayerKind.PER_CHANNEL
+                        and self.specs[nxt].op == "bn" and cur not in output_feed):
+                    info["bn"] = nxt
+                    absorbed.add(nxt)
+                    cur = nxt
+                    nxt = self._single_succ(cur)
+                if (nxt is not None and nxt not in absorbed and kinds[nxt] is LayerKind.PASS_THROUGH
+                        and self.specs[nxt].op in ACTS and cur not in output_feed):
+                    info["act"] = nxt
+                    absorbed.add(nxt)
+                    cur = nxt
+                ops.append(_Op("dwconv", lid, [preds[0]], cur, info=info))
             elif k is LayerKind.CONCAT:
                 # zero-copy when every operand can be stored straight into its band (_plan_concats)
                 ops.append(_Op("concat", lid, list(preds), lid))
@@ -330,6 +361,7 @@ class Engine:
                 _, ho, wo = self._shapes[sop.output]
                 cout = g.layer(sop.info["conv"]).out_channels
                 if ((sp.kernel, sp.stride, sp.pad) == (3, 2, 1) and base(mp.inputs[0]) == sop.output
+                        and self._act_code(sop.info["relu"]) in (0, _lib.UB_ACT["relu"])
                         and self._s2d_ok(len(sop.info["stem_idx"]), cs, cout) and cout <= 64
                         and ho % 2 == 0 and wo % 2 == 0 and wo <= 128):
                     sop.info["pool"] = sp
@@ -416,7 +448,7 @@ class Engine:
         self._concat_views: dict[str, tuple] = {}          # concat -> (key, base, cmap, operands)
         self._band_bufs: dict[str, torch.Tensor] = {}
         producer_of = {op.output: op for op in ops}
-        placeable_kinds = ("conv", "maxpool", "avgpool", "avgpool2d", "eltwise", "gather", "stage")
+        placeable_kinds = ("conv", "maxpool", "avgpool", "avgpool2d", "eltwise", "gather", "stage", "dwconv")
         g = self.graph
 
         def operand(v):  # full-width aliases (identity / flatten) resolve to their base
@@ -605,6 +637,39 @@ class Engine:
                 K.gather_rows(xa, idx_dev, win, 1, dst)
 
         op.launch = launch
+
+    def _bind_dwconv(self, op, ws, vs, output_feed):
+        """Depthwise conv (PER_CHANNEL-like node; its filters follow the planner's per-channel
+        permutation like any vector) with the following BN folded: W' = s*W, b' = s*b + t."""
+        lid = op.anchor
+        sp = self.specs[lid]
+        x = self._value(op.inputs[0])
+        assert x.cmap is None, f"{lid}: depthwise conv over a column-mapped value"
+        vec, perm = vs(lid)
+        C = self.graph.layer(lid).out_channels
+
+        def p(v):
+            v = v.detach().float().cpu()
+            return v[list(perm)] if perm is not None else v
+
+        wdw = p(vec["dw"])  # [C, k*k]
+        b = p(vec["bias"]) if "bias" in vec else torch.zeros(C)
+        if op.info["bn"] is not None:
+            bvec, bperm = vs(op.info["bn"])
+            sc, sh = self._affine(op.info["bn"], bvec, bperm)
+            sc, sh = sc.cpu(), sh.cpu()
+            wdw = wdw * sc.view(-1, 1)
+            b = b * sc + sh
+        k = sp.kernel
+        wt = torch.zeros(k * k, K.pad8(C))
+        wt[:, :C] = wdw.t()
+        wt, b = wt.to(self.device).contiguous(), b.to(self.device).contiguous()
+        self._keep += [wt, b]
+        act = self.specs[op.info["act"]].op if op.info["act"] else "none"
+        y = self._alloc(op.output, C)
+        op.launch = lambda: K.dwconv(x, wt, b, k, sp.stride, sp.pad, act, y)
+        # roofline bookkeeping: 2*k*k flops per output, input + output bytes
+        self.conv_stats.append(ConvStats(lid, 2.0 * k * k * C * y.H * y.W, 2.0 * C * (x.H * x.W + y.H * y.W), 0.0))
 
     def _bind_eltwise(self, op, ws, vs, output_feed):
         """PER_CHANNEL / ADD / activation nodes no conv absorbed (plus a fused trailing
@@ -812,7 +877,7 @@ class Engine:
                 m[c] = j
             y2_map = self._i32(m)
             self._dual_bufs[info["out"]] = (y2, col_of)
-        relu = info["relu"] is not None
+        relu = self._act_code(info["relu"])
         # variant = (plan index, ub_conv_desc.variant bits: producer width 1 = 256 / 2 = 512
         # threads; +4 re-load the weights per tile instead of keeping them resident; +16 weights
         # by cp.async instead of TMA; +32 1x1 activations by cp.async instead of TMA;
@@ -888,12 +953,15 @@ class Engine:
         cols = cols if cols is not None else range(I)
         assert info.get("residual") is None and info["out"] not in output_feed
         y = self._alloc(info["out"], lay.out_channels)
-        relu = info["relu"] is not None
+        relu = self._act_code(info["relu"])
         cout, kk, st, pd = lay.out_channels, spec.kernel, spec.stride, spec.pad
         ci, hi, wi = self.input_chw
         # space-to-depth stem when the folded 2x2 pixel fits 16 bytes (ub_conv_s2d); else the
-        # single-launch im2col stem.  info["pool"]: the following max pool is fused.
-        s2d = self._s2d_ok(cin, spec, cout) and y.cstride % 8 == 0 and y.coff % 8 == 0
+        # single-launch im2col stem.  info["pool"]: the following max pool is fused.  The s2d
+        # kernels' epilogues know ReLU only; other activations (MobileNetV3's hardswish stem)
+        # take the im2col stem on the generic conv kernel.
+        s2d = (self._s2d_ok(cin, spec, cout) and y.cstride % 8 == 0 and y.coff % 8 == 0
+               and relu in (0, _lib.UB_ACT["relu"]))
         if "pool" in info:
             assert s2d, "stem/max-pool fusion needs the space-to-depth stem"
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="s2d", out_dtype=torch.bfloat16)
@@ -1038,7 +1106,8 @@ class Engine:
             return "conv_tc_kernel+gather_rows" if op.info["plans"][pi] == "copy" else "conv_tc_kernel"
         return {"gather": "gather_rows_kernel", "stage": "stage_input_kernel", "maxpool": "maxpool_kernel",
                 "avgpool": "avgpool_gather_kernel" if "idx" in op.info else "avgpool_kernel",
-                "eltwise": "affine_add_relu_kernel"}.get(op.kind, op.kind)
+                "eltwise": "eltwise_kernel", "dwconv": "dwconv_kernel", "avgpool2d": "avgpool2d_kernel",
+                "concat": "gather_rows_kernel"}.get(op.kind, op.kind)
 
     def per_image_work(self) -> tuple[float, float]:
         f = sum(c.flops for c in self.conv_stats)

@@ -190,7 +190,7 @@ def conv(x: Act, w: torch.Tensor, lead: int, cpad: int, cout: int, kh: int, kw: 
     d.bias = bias.data_ptr() if bias is not None else None
     if residual is not None:
         d.residual, d.res_cstride, d.res_coff = residual.buf.data_ptr(), residual.cstride, residual.coff
-    d.relu = int(relu)
+    d.relu = int(relu)  # UB_ACT_* code (True / 1 = ReLU)
     d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
     d.y_dtype = _lib.UB_F32 if y_fp32 else _lib.UB_BF16
     d.variant = variant
@@ -312,6 +312,13 @@ def eltwise(a: Act, y: Act, scale=None, shift=None, b: Act | None = None, act: s
         d.gate, d.gate_cstride, d.gate_coff = gate.buf.data_ptr(), gate.cstride, gate.coff
     d.y, d.y_cstride, d.y_coff = y.buf.data_ptr(), y.cstride, y.coff
     _lib.check(_lib.load().ub_eltwise(ctypes.byref(d), _stream()))
+
+
+def dwconv(x: Act, w: torch.Tensor, bias: torch.Tensor | None, k: int, stride: int, pad: int, act: str,
+           y: Act) -> None:
+    """ub_dwconv: depthwise k x k conv, w fp32 [k*k, pad8(C)] (BN folded), fused activation."""
+    _lib.call("ub_dwconv", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, _p(w), _p(bias), k, stride, pad,
+              _lib.UB_ACT[act], y.H, y.W, _p(y.buf), y.cstride, y.coff, _stream())
 
 
 def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:

@@ -31,7 +31,8 @@ from .ir import Layer, LayerKind, ModelGraph
 
 @dataclass(frozen=True)
 class OpSpec:
-    op: str  # input|conv|linear|bn|bias|relu|maxpool|avgpool|flatten|identity|add|concat|output
+    op: str  # input|conv|linear|bn|bias|dwconv|relu|relu6|hardswish|hardsigmoid|silu|sigmoid|maxpool|avgpool|
+    #          avgpool_k|flatten|identity|add|mul|concat|output
     kernel: int = 1
     stride: int = 1
     pad: int = 0
@@ -58,8 +59,16 @@ class SpatialModel:
             else:
                 out[lid] = torch.sqrt((w64 * w64).sum(dim=(2, 3))).numpy()
         for lid, vec in self.vectors.items():
-            out[lid] = vec["bias"].detach().to(torch.float64).cpu().numpy()
+            if "dw" in vec:  # depthwise filter bank: one L2 norm per channel (a (C,) vector)
+                w64 = vec["dw"].detach().to(torch.float64).cpu()
+                out[lid] = torch.sqrt((w64 * w64).sum(dim=1)).numpy()
+            else:
+                out[lid] = vec["bias"].detach().to(torch.float64).cpu().numpy()
         return out
+
+
+ACT_MODULES = {nn.ReLU: "relu", nn.ReLU6: "relu6", nn.Hardswish: "hardswish", nn.Hardsigmoid: "hardsigmoid",
+               nn.SiLU: "silu", nn.Sigmoid: "sigmoid"}
 
 
 def _is_add(node: torch.fx.Node) -> bool:
@@ -100,9 +109,22 @@ def lower(model: nn.Module, input_chw=(3, 224, 224)) -> SpatialModel:
             m = mods[node.target]
             s = src(node.args[0])
             cin = width[s]
-            if isinstance(m, nn.Conv2d):
-                if m.groups != 1:
-                    raise NotImplementedError(f"{node.name}: grouped/depthwise conv not in the reference IR")
+            if isinstance(m, nn.Conv2d) and m.groups != 1:
+                # depthwise (groups == channels, multiplier 1): channel-wise, so a PER_CHANNEL-like
+                # interior node whose "vector" is the filter bank; the planner
+                # permutes it with the channel order like a BN vector
+                if not (m.groups == m.in_channels == m.out_channels == cin):
+                    raise NotImplementedError(f"{node.name}: grouped conv other than depthwise")
+                assert m.kernel_size[0] == m.kernel_size[1] and m.stride[0] == m.stride[1]
+                assert m.padding[0] == m.padding[1] and m.dilation == (1, 1)
+                add_layer(node.name, LayerKind.PER_CHANNEL, cin, cin,
+                          OpSpec("dwconv", m.kernel_size[0], m.stride[0], m.padding[0]), [s])
+                vec = {"dw": m.weight.detach().float().reshape(cin, -1).contiguous()}
+                if m.bias is not None:
+                    vec["bias"] = m.bias.detach().float()
+                vectors[node.name] = vec
+                alias[node.name] = node.name
+            elif isinstance(m, nn.Conv2d):
                 assert m.kernel_size[0] == m.kernel_size[1] and m.stride[0] == m.stride[1]
                 assert m.padding[0] == m.padding[1] and m.dilation == (1, 1) and cin == m.in_channels
                 add_layer(node.name, LayerKind.CHANNEL_MIX, cin, m.out_channels,
@@ -129,8 +151,9 @@ def lower(model: nn.Module, input_chw=(3, 224, 224)) -> SpatialModel:
                 vectors[node.name] = {"weight": m.weight.detach().float(), "bias": m.bias.detach().float(),
                                       "mean": m.running_mean.detach().float(), "var": m.running_var.detach().float()}
                 alias[node.name] = node.name
-            elif isinstance(m, nn.ReLU):
-                add_layer(node.name, LayerKind.PASS_THROUGH, cin, cin, OpSpec("relu"), [s])
+            elif isinstance(m, tuple(ACT_MODULES)):
+                op = next(v for t, v in ACT_MODULES.items() if isinstance(m, t))
+                add_layer(node.name, LayerKind.PASS_THROUGH, cin, cin, OpSpec(op), [s])
                 alias[node.name] = node.name
             elif isinstance(m, nn.MaxPool2d):
                 k, st, p = (m.kernel_size, m.stride, m.padding)
@@ -161,6 +184,16 @@ def lower(model: nn.Module, input_chw=(3, 224, 224)) -> SpatialModel:
                 w = width[ins[0]]
                 add_layer(node.name, LayerKind.ADD, w, w, OpSpec("add"), ins)
                 alias[node.name] = node.name
+            elif node.target in (operator.mul, torch.mul):
+                # squeeze-excitation `scale * x`: a positional join of two C-wide values, i.e. an
+                # ADD in the reference IR -- both operands must share one order
+                ins = [src(a) for a in node.args[:2]]
+                w = width[ins[0]]
+                assert width[ins[1]] == w, f"{node.name}: mul of different widths"
+                add_layer(node.name, LayerKind.ADD, w, w, OpSpec("mul"), ins)
+                alias[node.name] = node.name
+            elif getattr(node.target, "__name__", "") == "stochastic_depth":
+                alias[node.name] = src(node.args[0])  # identity in eval mode
             elif node.target in (torch.flatten,) or (node.op == "call_method" and node.target in ("flatten", "view")):
                 s = src(node.args[0])
                 add_layer(node.name, LayerKind.PASS_THROUGH, width[s], width[s], OpSpec("flatten"), [s])

@@ -193,3 +193,23 @@ def test_densenet121_logits_match_oracle(strategy):
     ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
     assert deviation(got, ref) <= TOL, deviation(got, ref)
     assert top1_agreement(got, ref) == 1.0
+
+
+@pytest.mark.parametrize("cfg_name", ["mobilenet_v3_small_s10", "mobilenet_v3_small_s50", "mobilenet_v3_small_s90",
+                                      "efficientnet_v2_s_s50"])
+@pytest.mark.parametrize("strategy", ["reorder", "baseline"])
+def test_depthwise_se_models_match_oracle(cfg_name, strategy):
+    """Configs 2 and 5: MobileNetV3-Small / EfficientNetV2-S with the depthwise convs and
+    squeeze-excitation gates lowered per SURVEY.md A.5 (depthwise -> PER_CHANNEL-like node,
+    SE mul -> positional ADD); randomised BN."""
+    sm, plans, eg, maps = _setup(cfg_name, strategy)
+    N = 4
+    x = torch.randn(N, 3, 224, 224, generator=torch.Generator().manual_seed(6))
+    eng = EN.from_plans(sm, eg, maps, batch=N)
+    eng.capture()
+    got = eng.forward(x.cuda()).cpu()
+    w, v = apply_plans_spatial(plans, sm.graph, sm.weights, sm.vectors)
+    ref = run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32)
+    assert torch.isfinite(got).all()
+    assert deviation(got, ref) <= TOL, deviation(got, ref)
+    assert top1_agreement(got, ref) == 1.0

