@@ -75,7 +75,15 @@ class Engine:
         self.stem_pack_fused = stem_pack_fused
         self.pool_gather = pool_gather
         self.graph = graph
-        self.specs = specs
+        # nodes the reference's apply_plan adds (join-rewrite ADD / CONCAT runs, SLICE / GATHER
+        # reads) carry no spatial spec: they get the plain op of their kind
+        from .lowering import OpSpec
+        defaults = {LayerKind.ADD: "add", LayerKind.CONCAT: "concat", LayerKind.SLICE: "slice",
+                    LayerKind.GATHER: "gather"}
+        self.specs = dict(specs)
+        for lay in graph.layers:
+            if lay.id not in self.specs and lay.kind in defaults:
+                self.specs[lay.id] = OpSpec(defaults[lay.kind])
         self.batch = batch
         self.device = torch.device(device)
         self.gather_mode = gather_mode
@@ -104,6 +112,8 @@ class Engine:
                 shp[lid] = (lay.out_channels, h, w)
                 continue
             _, h, w = shp[preds[0]]
+            if lay.kind is LayerKind.ADD:  # an SE `mul` broadcasts its [N, C, 1, 1] gate
+                h, w = max(shp[q][1] for q in preds), max(shp[q][2] for q in preds)
             if lay.kind is LayerKind.CHANNEL_MIX and spec is not None and spec.op == "conv":
                 h = (h + 2 * spec.pad - spec.kernel) // spec.stride + 1
                 w = (w + 2 * spec.pad - spec.kernel) // spec.stride + 1
