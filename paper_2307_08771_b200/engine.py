@@ -1008,9 +1008,17 @@ class Engine:
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
     # ------------------------------------------------------------------ execution
-    def launch_all(self) -> None:
+    def launch_all(self, nvtx: bool = False) -> None:
+        """Enqueue the forward.  nvtx=True wraps every op in an NVTX range named after its
+        exported node (for nsys / ncu --nvtx filtering; eager runs only)."""
+        if not nvtx:
+            for op in self.ops:
+                op.launch()
+            return
         for op in self.ops:
+            torch.cuda.nvtx.range_push(f"{op.kind}:{op.anchor}")
             op.launch()
+            torch.cuda.nvtx.range_pop()
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x: [N, C, H, W] fp32 (device or host).  Returns logits (device)."""
