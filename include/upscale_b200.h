@@ -197,6 +197,26 @@ int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream);
 int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w, const float* bias,
               int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
+/*
+ * Global average pool for small grids (N x ceil(C/8) too small to fill the GPU, many
+ * pixels): pixels split over a CTA's threads, partial sums added in a fixed order.
+ * y[n][y_coff + c] = bf16(mean_p x[n][p][x_coff + c]).  16-byte aligned source rows.
+ */
+int ub_avgpool_split(const void* x, int N, int HW, int C, int x_cstride, int x_coff, void* y, int y_cstride,
+                     int y_coff, cudaStream_t stream);
+
+/*
+ * Small-M CHANNEL_MIX (interp.py:57-63) for M = images x pixels <= 16 (squeeze-excitation
+ * FCs, classifiers at small batch) on CUDA cores:
+ *   y[m][y_coff + o] = act(sum_k x[m * x_cstride + xcol[k]] * w[o * w_stride + k] + bias[o])
+ * xcol (device, K entries): the element offset of input column k in a row -- a SLICE
+ * view, a GATHER or a concat column map alike.  w: bf16 rows of pad8(K) columns (16-byte
+ * aligned, zero-padded).  y: bf16 or fp32 (y_dtype).
+ */
+int ub_linear_small(const void* x, int M, int x_cstride, const int32_t* xcol, int K, const void* w, int w_stride,
+                    int O, const float* bias, int act, void* y, int y_dtype, int y_cstride, int y_coff,
+                    cudaStream_t stream);
+
 int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int s, int pad, int Ho,
                  int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 

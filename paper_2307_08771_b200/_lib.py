@@ -90,6 +90,9 @@ SIGNATURES = {
                              c_int, c_int, c_vp]),
     "ub_dwconv": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_int,
                           c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_avgpool_split": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_linear_small": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int,
+                                c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),
@@ -158,6 +161,18 @@ def index_faults() -> int:
     n = ctypes.c_ulonglong()
     check(load().ub_index_faults(ctypes.byref(n)))
     return int(n.value)
+
+
+def num_sms_hint() -> int:
+    """SM count of the current device (148 on B200) for host-side launch heuristics."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    except Exception:
+        pass
+    return 148
 
 
 def launch_count() -> int:

@@ -178,6 +178,189 @@ __global__ void __launch_bounds__(256) dwconv_kernel(const uint16_t* __restrict_
   }
 }
 
+
+// Global average pool for small grids (few images x few channel groups, many pixels --
+// MobileNet / EfficientNet squeeze-excitation pools at batch 1): a CTA takes one image and
+// up to 32 groups of 8 channels; its 256 threads split the pixels into phases, each phase
+// sums its pixels in order, and the phases are added in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) avgpool_split_kernel(const uint16_t* __restrict__ x, int HW, int C,
+                                                            int x_cstride, int x_coff, uint16_t* __restrict__ y,
+                                                            int y_cstride, int y_coff) {
+  __shared__ float red[256 * 8];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int G = (C + 7) / 8;
+  const int g0 = blockIdx.x * 32;
+  const int gb = min(32, G - g0);
+  const int phases = 256 / gb;
+  const int n = blockIdx.y;
+  const int t = threadIdx.x;
+  const int g = t % gb, ph = t / gb;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ph < phases) {
+    const uint16_t* base = x + static_cast<long long>(n) * HW * x_cstride + x_coff + (g0 + g) * 8;
+    for (int p = ph; p < HW; p += phases) {
+      uint16_t v[8];
+      *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(p) * x_cstride));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[t * 8 + j] = acc[j];
+  __syncthreads();
+  if (t < gb * 8) {
+    const int gg = t >> 3, j = t & 7;
+    float sum = 0.f;
+    for (int q = 0; q < phases; ++q) sum += red[(q * gb + gg) * 8 + j];
+    const int c = (g0 + gg) * 8 + j;
+    if (c < C) y[static_cast<long long>(n) * y_cstride + y_coff + c] = tobf(sum / static_cast<float>(HW));
+  }
+}
+
+// Small-M linear / 1x1 conv (M = images x pixels <= 16: squeeze-excitation FCs and
+// classifiers at small batch): y[m][o] = act(sum_k x[m][xcol[k]] * w[o][k] + bias[o]).
+// The M activation rows are gathered once into shared memory (fp32); one warp per output
+// channel streams its weight row with 16-byte loads (every weight byte read once, spread
+// over all SMs) and reduces the M dot products with shuffles.  CUDA cores: at M <= 16 a
+// 128-row tensor-core tile would be >= 87 % padding and the launch is latency-bound.
+__global__ void __launch_bounds__(256) linear_small_kernel(const uint16_t* __restrict__ x, int M, int x_cstride,
+                                                           const int32_t* __restrict__ xcol, int K,
+                                                           const uint16_t* __restrict__ w, int w_stride, int O,
+                                                           const float* __restrict__ bias, int act, void* y,
+                                                           int y_f32, int y_cstride, int y_coff) {
+  extern __shared__ float xs[];  // [M][K8]
+  const int K8 = (K + 7) / 8 * 8;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int e = threadIdx.x; e < M * K8; e += blockDim.x) {
+    const int m = e / K8, k = e - m * K8;
+    const int col = k < K ? __ldg(xcol + k) : -1;  // -1: a zero-filled GATHER entry
+    xs[e] = col >= 0 ? bf(x[static_cast<long long>(m) * x_cstride + col]) : 0.f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int o = blockIdx.x * 8 + warp; o < O; o += gridDim.x * 8) {
+    float acc[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) acc[m] = 0.f;
+    const uint16_t* wr = w + static_cast<long long>(o) * w_stride;
+    for (int k = lane * 8; k < K8; k += 256) {
+      uint16_t wv[8];
+      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+      float wf[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wf[j] = bf(wv[j]);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        if (m < M) {
+          const float4 a = *reinterpret_cast<const float4*>(xs + m * K8 + k);
+          const float4 b = *reinterpret_cast<const float4*>(xs + m * K8 + k + 4);
+          acc[m] += a.x * wf[0] + a.y * wf[1] + a.z * wf[2] + a.w * wf[3] + b.x * wf[4] + b.y * wf[5] + b.z * wf[6] +
+                    b.w * wf[7];
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      if (m < M) {
+        float v = acc[m];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        acc[m] = v;
+      }
+    }
+    if (lane < M) {
+      float v = 0.f;
+#pragma unroll
+      for (int m = 0; m < 16; ++m)
+        if (m == lane) v = acc[m];
+      if (bias) v += bias[o];
+      v = act_f(v, act);
+      const long long off = static_cast<long long>(lane) * y_cstride + y_coff + o;
+      if (y_f32) static_cast<float*>(y)[off] = v;
+      else static_cast<uint16_t*>(y)[off] = tobf(v);
+    }
+  }
+}
+
+
+// Depthwise conv, smem-tiled: a CTA computes an 8 x 8 output tile of one image for a block
+// of up to 64 channels.  The input window ((8-1)*S + K)^2 x 64 ch is staged ONCE by 16-byte
+// cp.async (zero-filled outside the image), the folded weights / bias of the block are
+// staged too, then every (pixel, 8-channel group) output reads its K*K taps from shared
+// memory.  HBM sees the input once (+ the tile halo) and the output once.
+__host__ __device__ constexpr int dw_tile(int k, int s) { return (k == 5 && s == 2) ? 6 : 8; }
+
+template <int K, int S>
+__global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __restrict__ x, int N, int H, int W, int C,
+                                                          int x_cstride, int x_coff, const float* __restrict__ w,
+                                                          const float* __restrict__ bias, int pad, int act, int Ho,
+                                                          int Wo, int tiles_h, int tiles_w,
+                                                          uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+  constexpr int TH = dw_tile(K, S), TW = TH;  // the staged window fits the 48 KB static smem
+  constexpr int IH = (TH - 1) * S + K, IW = (TW - 1) * S + K;
+  __shared__ uint4 tile[IH * IW * 8];
+  __shared__ float sw[K * K * 64];
+  __shared__ float sb[64];
+  const int C8 = (C + 7) / 8 * 8;
+  const int cb = blockIdx.y * 64;
+  const int G = min(8, (C - cb + 7) / 8);
+  const int t = blockIdx.x;
+  const int n = t / (tiles_h * tiles_w);
+  const int r = t - n * tiles_h * tiles_w;
+  const int y0 = (r / tiles_w) * TH, x0 = (r % tiles_w) * TW;
+  const int iy0 = y0 * S - pad, ix0 = x0 * S - pad;
+  for (int e = threadIdx.x; e < K * K * 64; e += 256) {
+    const int tap = e >> 6, c = e & 63;
+    sw[e] = cb + c < C8 ? w[tap * C8 + cb + c] : 0.f;
+  }
+  if (threadIdx.x < 64) sb[threadIdx.x] = (bias && cb + threadIdx.x < C) ? bias[cb + threadIdx.x] : 0.f;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int e = threadIdx.x; e < IH * IW * G; e += 256) {
+    const int pix = e / G, g = e - (e / G) * G;
+    const int iy = iy0 + pix / IW, ix = ix0 + pix % IW;
+    uint4* dst = &tile[pix * 8 + g];
+    if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+      cp_async16(dst, x + ((static_cast<long long>(n) * H + iy) * W + ix) * x_cstride + x_coff + cb + g * 8, 16);
+    else
+      *dst = make_uint4(0, 0, 0, 0);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int e = threadIdx.x; e < TH * TW * G; e += 256) {
+    const int op = e / G, g = e - (e / G) * G;
+    const int oy = op / TW, ox = op - (op / TW) * TW;
+    if (y0 + oy >= Ho || x0 + ox >= Wo) continue;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = sb[g * 8 + j];
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy) {
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx) {
+        uint16_t v[8];
+        *reinterpret_cast<uint4*>(v) = tile[((oy * S + dy) * IW + ox * S + dx) * 8 + g];
+        const float* wt = sw + (dy * K + dx) * 64 + g * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(wt[j], bf(v[j]), acc[j]);
+      }
+    }
+    uint16_t o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[j], act));
+    const int c0 = cb + g * 8;
+    uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy) * Wo + x0 + ox) * y_cstride + y_coff + c0;
+    if (c0 + 8 <= C) {
+      *reinterpret_cast<uint4*>(yp) = *reinterpret_cast<const uint4*>(o);
+    } else {
+      for (int j = 0; c0 + j < C; ++j) yp[j] = o[j];
+    }
+  }
+}
+
 bool a16(const void* base, int cstride, int coff) {
   return base == nullptr || (aligned16(base) && (cstride & 7) == 0 && (coff & 7) == 0);
 }
@@ -226,10 +409,60 @@ extern "C" int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstrid
   if (!a16(x, x_cstride, x_coff) || !a16(y, y_cstride, y_coff) || x_coff + C > x_cstride || y_coff + C > y_cstride ||
       (reinterpret_cast<uintptr_t>(w) & 15))
     return fail(UB_EINVAL, "ub_dwconv: rows must be 16-byte aligned");
+  if ((k == 3 || k == 5) && (s == 1 || s == 2)) {  // smem-tiled form
+    const int tsz = dw_tile(k, s);
+    const int th = (Ho + tsz - 1) / tsz, tw = (Wo + tsz - 1) / tsz;
+    const long long tiles = static_cast<long long>(N) * th * tw;
+    if (tiles < (1ll << 31)) {
+      const dim3 grid(static_cast<unsigned>(tiles), (C + 63) / 64);
+      void (*kern)(const uint16_t*, int, int, int, int, int, int, const float*, const float*, int, int, int, int, int,
+                   int, uint16_t*, int, int) =
+          k == 3 ? (s == 1 ? dwconv_tile_kernel<3, 1> : dwconv_tile_kernel<3, 2>)
+                 : (s == 1 ? dwconv_tile_kernel<5, 1> : dwconv_tile_kernel<5, 2>);
+      const cudaError_t e = launch_pdl(kern, grid, dim3(256), 0, stream, static_cast<const uint16_t*>(x), N, H, W, C,
+                                       x_cstride, x_coff, w, bias, pad, act, Ho, Wo, th, tw,
+                                       static_cast<uint16_t*>(y), y_cstride, y_coff);
+      count_launch();
+      return cuda_status(e, "dwconv_tile_kernel");
+    }
+  }
   const long long work = static_cast<long long>(N) * Ho * Wo * ((C + 7) / 8);
   const cudaError_t e = launch_pdl(dwconv_kernel, dim3(grid_for(work, 256, 1)), dim3(256), 0, stream,
                                    static_cast<const uint16_t*>(x), N, H, W, C, x_cstride, x_coff, w, bias, k, s, pad,
                                    act, Ho, Wo, static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "dwconv_kernel");
+}
+
+extern "C" int ub_avgpool_split(const void* x, int N, int HW, int C, int x_cstride, int x_coff, void* y, int y_cstride,
+                                int y_coff, cudaStream_t stream) {
+  if (!x || !y || N < 1 || HW < 1 || C < 1 || N > 65535) return fail(UB_EINVAL, "ub_avgpool_split: bad arguments");
+  if (!a16(x, x_cstride, x_coff) || x_coff + (C + 7) / 8 * 8 > x_cstride || y_coff + C > y_cstride)
+    return fail(UB_EINVAL, "ub_avgpool_split: rows must be 16-byte aligned");
+  const dim3 grid(((C + 7) / 8 + 31) / 32, N);
+  const cudaError_t e = launch_pdl(avgpool_split_kernel, grid, dim3(256), 0, stream, static_cast<const uint16_t*>(x),
+                                   HW, C, x_cstride, x_coff, static_cast<uint16_t*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(e, "avgpool_split_kernel");
+}
+
+extern "C" int ub_linear_small(const void* x, int M, int x_cstride, const int32_t* xcol, int K, const void* w,
+                               int w_stride, int O, const float* bias, int act, void* y, int y_dtype, int y_cstride,
+                               int y_coff, cudaStream_t stream) {
+  if (!x || !xcol || !w || !y || M < 1 || M > 16 || K < 1 || O < 1 || act < UB_ACT_NONE || act > UB_ACT_SIGMOID)
+    return fail(UB_EINVAL, "ub_linear_small: bad arguments (M must be 1..16)");
+  if ((w_stride & 7) || w_stride < (K + 7) / 8 * 8 || (reinterpret_cast<uintptr_t>(w) & 15) ||
+      y_coff + O > y_cstride || (y_dtype != UB_BF16 && y_dtype != UB_F32))
+    return fail(UB_EINVAL, "ub_linear_small: weight rows must be 16-byte aligned and hold pad8(K) columns");
+  const size_t smem = static_cast<size_t>(M) * ((K + 7) / 8 * 8) * sizeof(float);
+  if (smem > 200 * 1024) return fail(UB_EUNSUPPORTED, "ub_linear_small: M x K too large");
+  if (const cudaError_t ae = ensure_max_smem(linear_small_kernel)) return cuda_status(ae, "linear_small attr");
+  int grid = (O + 7) / 8;
+  if (grid > 4 * num_sms()) grid = 4 * num_sms();
+  const cudaError_t e = launch_pdl(linear_small_kernel, dim3(grid), dim3(256), smem, stream,
+                                   static_cast<const uint16_t*>(x), M, x_cstride, xcol, K,
+                                   static_cast<const uint16_t*>(w), w_stride, O, bias, act, y,
+                                   y_dtype == UB_F32 ? 1 : 0, y_cstride, y_coff);
+  count_launch();
+  return cuda_status(e, "linear_small_kernel");
 }

@@ -201,11 +201,14 @@ __global__ void __launch_bounds__(256) channel_gather_2d_kernel(const uint16_t* 
 // pixels of each output pixel are staged and averaged after the prologue.
 template <int ROWS, bool AFFINE>
 __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
-                                                          int win16, const int32_t* __restrict__ idx, int n_idx,
-                                                          int rel, int n8, int N, int H, int W, int stride, int Ho,
-                                                          int Wo, const float* __restrict__ scale,
+                                                          int win16, int pb, const int32_t* __restrict__ idx,
+                                                          int n_idx, int rel, int n8, int N, int H, int W, int stride,
+                                                          int Ho, int Wo, const float* __restrict__ scale,
                                                           const float* __restrict__ shift, int relu,
                                                           uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+  // A warp moves a batch of `pb` output pixels per step (narrow rows: several pixels' windows
+  // per cp.async wave), with GR_STAGES batches in flight.
+  constexpr int GR_STAGES = 3;
   extern __shared__ __align__(16) uint8_t g_smem[];
   int32_t* sidx = reinterpret_cast<int32_t*>(g_smem);
   float* sscale = reinterpret_cast<float*>(g_smem + n8 * 4);
@@ -213,8 +216,9 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
   const int idx_bytes = ((AFFINE ? 3 : 1) * n8 * 4 + 15) & ~15;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  const int stage_bytes = ROWS * win16 * 16;
-  uint8_t* buf0 = g_smem + idx_bytes + static_cast<size_t>(warp) * 2 * stage_bytes;
+  const int pix_chunks = ROWS * win16;                 // 16-byte chunks staged per output pixel
+  const int stage_bytes = pb * pix_chunks * 16;
+  uint8_t* buf0 = g_smem + idx_bytes + static_cast<size_t>(warp) * GR_STAGES * stage_bytes;
   for (int i = threadIdx.x; i < n8; i += blockDim.x) {
     const int j = i < n_idx ? __ldg(idx + i) : -1;
     sidx[i] = j >= 0 ? j + rel : -1;  // element offset inside the staged window
@@ -227,38 +231,57 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
   griddep_wait();
   griddep_launch_dependents();
   const long long npix = static_cast<long long>(N) * Ho * Wo;
+  const long long nbatch = (npix + pb - 1) / pb;
   const long long step = static_cast<long long>(gridDim.x) * warps;
-  auto issue = [&](long long p, uint8_t* dst) {
-    const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
-    const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
-    const int yo = r / Wo, xo = r - (r / Wo) * Wo;
-#pragma unroll
-    for (int q = 0; q < ROWS; ++q) {
+  const int groups = n8 >> 3;
+  auto issue = [&](long long b, uint8_t* dst) {
+    const long long p0 = b * pb;
+    const int total = pb * pix_chunks;
+    for (int t = lane; t < total; t += 32) {
+      const int k = t / pix_chunks;
+      const long long p = p0 + k;
+      if (p >= npix) break;
+      const int rem = t - k * pix_chunks;
+      const int q = rem / win16, ch = rem - q * win16;
+      const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
+      const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+      const int yo = r / Wo, xo = r - (r / Wo) * Wo;
       const int yi = ROWS == 4 ? 2 * yo + (q >> 1) : yo * stride;
       const int xi = ROWS == 4 ? 2 * xo + (q & 1) : xo * stride;
-      const uint16_t* src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws;
-      for (int j = lane; j < win16; j += 32) cp_async16(dst + q * win16 * 16 + j * 16, src + j * 8, 16);
+      const uint16_t* src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws + ch * 8;
+      cp_async16(dst + t * 16, src, 16);
     }
   };
-  long long p = static_cast<long long>(blockIdx.x) * warps + warp;
-  int k = 0;
-  if (p < npix) issue(p, buf0);
-  cp_async_commit();
-  for (; p < npix; p += step, k ^= 1) {
-    if (p + step < npix) issue(p + step, buf0 + (k ^ 1) * stage_bytes);
+  long long b = static_cast<long long>(blockIdx.x) * warps + warp;
+#pragma unroll
+  for (int st = 0; st < GR_STAGES - 1; ++st) {
+    if (b + st * step < nbatch) issue(b + st * step, buf0 + st * stage_bytes);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  int k = 0;
+  for (; b < nbatch; b += step, k = (k + 1 == GR_STAGES ? 0 : k + 1)) {
+    const long long bn = b + (GR_STAGES - 1) * step;
+    const int kn = (k + GR_STAGES - 1) % GR_STAGES;
+    if (bn < nbatch) issue(bn, buf0 + kn * stage_bytes);
+    cp_async_commit();
+    cp_async_wait<GR_STAGES - 1>();
     __syncwarp();
-    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
-    uint16_t* yr = y + static_cast<size_t>(p) * y_cstride + y_coff;
-    for (int i = lane * 8; i < n8; i += 256) {
+    const uint8_t* stage = buf0 + k * stage_bytes;
+    const long long p0 = b * pb;
+    const int work = pb * groups;
+    for (int t = lane; t < work; t += 32) {
+      const int kp = t / groups;
+      const long long p = p0 + kp;
+      if (p >= npix) break;
+      const int i = (t - kp * groups) * 8;
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(stage + kp * pix_chunks * 16);
       uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j2 = 0; j2 < 4; ++j2) {
         uint16_t h[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = i + 2 * j + e;
+          const int c = i + 2 * j2 + e;
           const int a = sidx[c];
           if (!AFFINE && ROWS == 1) {
             h[e] = a >= 0 ? row[a] : uint16_t(0);
@@ -279,9 +302,9 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
             h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
           }
         }
-        w[j] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
+        w[j2] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
       }
-      *reinterpret_cast<uint4*>(yr + i) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(y + static_cast<size_t>(p) * y_cstride + y_coff + i) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     __syncwarp();
   }
@@ -687,12 +710,15 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
   const int idx_bytes = ((affine ? 3 : 1) * n8 * 4 + 15) & ~15;
-  const size_t stage = static_cast<size_t>(rows) * win16 * 16;
+  // pixels per warp step: ~96 16-byte chunks per cp.async wave (3 per lane), at most 16 pixels
+  int pb = 96 / (rows * win16);
+  pb = pb < 1 ? 1 : (pb > 16 ? 16 : pb);
+  const size_t stage = static_cast<size_t>(pb) * rows * win16 * 16;
   int warps = 8;
-  while (warps > 1 && idx_bytes + warps * 2 * stage > 200 * 1024) warps >>= 1;
-  const size_t smem = idx_bytes + warps * 2 * stage;
+  while (warps > 1 && idx_bytes + warps * 3 * stage > 200 * 1024) warps >>= 1;
+  const size_t smem = idx_bytes + warps * 3 * stage;
   if (smem > 227 * 1024) return fail(UB_EUNSUPPORTED, "ub_gather_rows: window of %d channels", we - ws);
-  void (*kern)(const uint16_t*, int, int, int, const int32_t*, int, int, int, int, int, int, int, int, int,
+  void (*kern)(const uint16_t*, int, int, int, int, const int32_t*, int, int, int, int, int, int, int, int, int,
                const float*, const float*, int, uint16_t*, int, int) =
       pool2 ? (affine ? gather_rows_kernel<4, true> : gather_rows_kernel<4, false>)
             : (affine ? gather_rows_kernel<1, true> : gather_rows_kernel<1, false>);
@@ -702,12 +728,13 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
   if (per_sm > 2048 / (32 * warps)) per_sm = 2048 / (32 * warps);
   if (per_sm < 1) per_sm = 1;
-  const long long want = (npix + warps - 1) / warps;
+  const long long nbatch = (npix + pb - 1) / pb;
+  const long long want = (nbatch + warps - 1) / warps;
   const long long cap = static_cast<long long>(num_sms()) * per_sm;
   const int grid = static_cast<int>(want < cap ? want : cap);
   const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(32 * warps), smem, stream, static_cast<const uint16_t*>(x),
-                                   x_cstride, ws, win16, idx, n_idx, x_coff - ws, n8, N, H, W, stride, Ho, Wo, scale,
-                                   shift, relu, static_cast<uint16_t*>(y), y_cstride, y_coff);
+                                   x_cstride, ws, win16, pb, idx, n_idx, x_coff - ws, n8, N, H, W, stride, Ho, Wo,
+                                   scale, shift, relu, static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "gather_rows_kernel");
 }

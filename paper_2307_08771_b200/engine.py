@@ -610,7 +610,13 @@ class Engine:
             return
         y = self._alloc_like(op.output, x)
         yd = self._dense(y)
-        op.launch = lambda: K.avgpool_global(xd, yd)
+        groups = (xd.C + 7) // 8
+        if (self.batch * ((groups + 127) // 128) < _lib.num_sms_hint() and xd.coff % 8 == 0
+                and xd.cstride % 8 == 0 and x.H * x.W >= 16):
+            op.launch = lambda: K.avgpool_split(xd, yd)  # few images: split the pixels over threads
+            op.info["split"] = True
+        else:
+            op.launch = lambda: K.avgpool_global(xd, yd)
 
     def _bind_gather(self, op, ws, vs, output_feed):
         x = self._value(op.inputs[0])
@@ -798,6 +804,10 @@ class Engine:
             self._keep.append(wg)
             plans.append((kind, xv, gidx, lead, cpad, wg, pre, st if st_eff is None else st_eff))
 
+        residual_id = info.get("residual")
+        if (kk == 1 and st == 1 and pd == 0 and self.batch * x.H * x.W <= 16 and residual_id is None
+                and info.get("prologue") is None and info.get("pool2") is None and info["out"] not in self._dual):
+            return self._bind_small_linear(op, x, gather, W, rows, cols, scale, bias, cin, cout, output_feed)
         staged = info.get("prologue") is not None or info.get("pool2") is not None or x.cmap is not None
         if staged:
             # the read is staged by ub_gather_rows_ex into a compact buffer -- the gather (through
@@ -937,6 +947,26 @@ class Engine:
             byts += 2.0 * cout * ho * wo
         self.conv_stats.append(ConvStats(lid, flops, byts, 0.0))
 
+    def _bind_small_linear(self, op, x, gather, W, rows, cols, scale, bias, cin, cout, output_feed):
+        """CHANNEL_MIX over at most 16 rows (images x pixels): ub_linear_small on CUDA cores,
+        the read (SLICE / GATHER / column map) folded into its column offsets."""
+        info = op.info
+        idx = gather if gather is not None else list(range(x.C))
+        xcol = self._i32([x.coff + x.phys(i) if i >= 0 else -1 for i in idx])
+        wd = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=K.pad8(cin),
+                               out_dtype=torch.bfloat16)
+        self._keep.append(wd)
+        fp32_out = info["out"] in output_feed
+        y = self._alloc(info["out"], cout, fp32=fp32_out)
+        act = self._act_code(info["relu"])
+        xb = K.Act(x.buf, x.N, x.H, x.W, x.width, 0)
+        op.launch = lambda: K.linear_small(xb, xcol, wd, cout, y, bias=bias, act=act, y_fp32=fp32_out)
+        op.info.update(variants=[], variant=(0, 0), plans=["small"], halo=False,
+                       desc=f"linear_small {cin}->{cout} M={self.batch * x.H * x.W}")
+        self.conv_stats.append(ConvStats(info["conv"], 2.0 * cout * cin * x.H * x.W,
+                                         2.0 * (cin * x.H * x.W + cout * x.H * x.W) + 2.0 * cout * cin / self.batch,
+                                         0.0))
+
     def _s2d_ok(self, cin: int, spec, cout: int) -> bool:
         """Stem shapes the space-to-depth kernel takes (the folded 2x2 pixel fits 16 bytes)."""
         kk = spec.kernel
@@ -1057,7 +1087,7 @@ class Engine:
         engine's own buffers (CUDA events, after a warm-up)."""
         picks = {}
         for op in self.ops:
-            if op.kind != "conv" or "stem_idx" in op.info:
+            if op.kind != "conv" or "stem_idx" in op.info or not op.info.get("variants"):
                 continue
             best = None
             for v in op.info["variants"]:
@@ -1121,9 +1151,13 @@ class Engine:
             pi, pw = op.info["variant"]
             if op.info.get("halo") and not pw & 8:
                 return "conv_halo3_kernel"
-            return "conv_tc_kernel+gather_rows" if op.info["plans"][pi] == "copy" else "conv_tc_kernel"
+            plan = op.info["plans"][pi]
+            if plan == "small":
+                return "linear_small_kernel"
+            return "conv_tc_kernel+gather_rows" if plan == "copy" else "conv_tc_kernel"
         return {"gather": "gather_rows_kernel", "stage": "stage_input_kernel", "maxpool": "maxpool_kernel",
-                "avgpool": "avgpool_gather_kernel" if "idx" in op.info else "avgpool_kernel",
+                "avgpool": "avgpool_gather_kernel" if "idx" in op.info else (
+                    "avgpool_split_kernel" if op.info.get("split") else "avgpool_kernel"),
                 "eltwise": "eltwise_kernel", "dwconv": "dwconv_kernel", "avgpool2d": "avgpool2d_kernel",
                 "concat": "gather_rows_kernel"}.get(op.kind, op.kind)
 

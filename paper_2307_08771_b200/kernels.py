@@ -321,6 +321,20 @@ def dwconv(x: Act, w: torch.Tensor, bias: torch.Tensor | None, k: int, stride: i
               _lib.UB_ACT[act], y.H, y.W, _p(y.buf), y.cstride, y.coff, _stream())
 
 
+def avgpool_split(x: Act, y: Act) -> None:
+    _lib.call("ub_avgpool_split", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(y.buf), y.cstride, y.coff,
+              _stream())
+
+
+def linear_small(x: Act, xcol_dev: torch.Tensor, w: torch.Tensor, O: int, y: Act, bias=None, act: int = 0,
+                 y_fp32: bool = False) -> None:
+    """ub_linear_small: CHANNEL_MIX over M = N*H*W <= 16 rows; xcol_dev = element offsets of
+    the K input columns inside a row (SLICE / GATHER / column map); w bf16 [O][pad8(K)]."""
+    assert w.dim() == 2 and w.shape[0] >= O
+    _lib.call("ub_linear_small", _p(x.buf), x.npix, x.cstride, _p(xcol_dev), xcol_dev.numel(), _p(w), w.shape[1], O,
+              _p(bias), act, _p(y.buf), _lib.UB_F32 if y_fp32 else _lib.UB_BF16, y.cstride, y.coff, _stream())
+
+
 def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:
     _lib.call("ub_avgpool2d", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, k, stride, pad, y.H, y.W,
               _p(y.buf), y.cstride, y.coff, _stream())

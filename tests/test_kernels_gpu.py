@@ -679,3 +679,43 @@ def test_conv_epilogue_activations(act):
         torch.cuda.synchronize()
         ref = fns[act](torch.nn.functional.conv2d(_bf(x), _bf(Wt), bias, padding=k // 2))
         assert _rel(y.to_nchw().cpu(), ref) < 1e-2, (k, act)
+
+
+@pytest.mark.parametrize("M,KK,O,fp32,act", [(1, 72, 425, False, "hardsigmoid"), (4, 2048, 1000, True, "none"),
+                                             (16, 37, 9, False, "relu"), (3, 512, 1000, True, "none")])
+def test_linear_small(M, KK, O, fp32, act):
+    """ub_linear_small (CHANNEL_MIX over <= 16 rows on CUDA cores) through a gather with a
+    zero-filled entry, vs torch fp32 on the bf16 operands."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(M * 1000 + KK)
+    src_w = KK + 20
+    x = torch.randn(M, src_w, 1, 1, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    perm = torch.randperm(src_w, generator=g)[:KK].tolist()
+    perm[min(3, KK - 1)] = -1
+    W = torch.randn(O, KK, generator=g) / KK ** 0.5
+    b = torch.randn(O, generator=g)
+    wd = torch.zeros(O, (KK + 7) // 8 * 8)
+    wd[:, :KK] = W
+    y = K.empty_act(M, 1, 1, O, dev) if not fp32 else None
+    if fp32:
+        y = K.Act(torch.zeros(M, (O + 3) // 4 * 4, device=dev), M, 1, 1, O, 0)
+    xcol = torch.tensor([xa.coff + p if p >= 0 else -1 for p in perm], dtype=torch.int32, device=dev)
+    K.linear_small(xa, xcol, wd.to(torch.bfloat16).to(dev), O, y, bias=b.to(dev), act=_lib.UB_ACT[act], y_fp32=fp32)
+    torch.cuda.synchronize()
+    xin = torch.stack([_bf(x[:, p, 0, 0]) if p >= 0 else torch.zeros(M) for p in perm], dim=1)
+    fns = {"none": lambda v: v, "relu": torch.relu, "hardsigmoid": torch.nn.functional.hardsigmoid}
+    ref = fns[act](xin @ _bf(W).t() + b)
+    got = y.buf[:, :O].float().cpu()
+    assert _rel(got, ref) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,C", [(1, 56, 12), (2, 28, 433), (1, 7, 1024)])
+def test_avgpool_split(N, H, C):
+    dev = "cuda"
+    x = torch.randn(N, C, H, H, generator=torch.Generator().manual_seed(C))
+    xa = K.act_from_nchw(x.to(dev))
+    y = K.empty_act(N, 1, 1, C, dev)
+    K.avgpool_split(xa, y)
+    torch.cuda.synchronize()
+    assert _rel(y.to_nchw().cpu(), _bf(x).mean(dim=(2, 3), keepdim=True)) < 1e-2

@@ -127,8 +127,8 @@ def test_every_autotune_variant_is_bit_identical_within_its_kernel():
     torch.cuda.synchronize()
     n_checked = 0
     for op in eng.ops:
-        if op.kind != "conv" or "stem_idx" in op.info:
-            continue
+        if op.kind != "conv" or "stem_idx" in op.info or not op.info["variants"]:
+            continue  # the stem, and small-M linears (one schedule)
         y = eng._value(op.output)
         default = op.info["variant"]
         fams = {}
