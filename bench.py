@@ -535,6 +535,8 @@ def extras(args, make, dev, G, b, world, driver, ms) -> dict:
         out["b1_launches"] = up["launches"]
         if args.strategy == "reorder":
             out["b1_baseline_export_ms"] = b1_latency(make, dev, args.steps, "copy", strategy="baseline")["ms"]
+    if rank == 0 and args.strategy == "reorder" and args.config == "resnet50_s50" and world == 1:
+        out["configs"] = config_legs(args.steps)
     if args.strategy == "reorder":
         res = {}
         for label, gather in (("copy", "copy"), ("fused", "fused")):
@@ -550,6 +552,36 @@ def extras(args, make, dev, G, b, world, driver, ms) -> dict:
                     "pruned reader) run copy-then-conv: every GATHER materialised by the vectorised channel-gather "
                     "kernel, then the same conv kernels",
             "fused_reads": res["fused"]}
+    return out
+
+
+def config_legs(steps: int) -> dict:
+    """BASELINE.json configs 2 and 4 beside the headline: the MobileNetV3-Small batch-1
+    latency sweep and DenseNet-121 @ 50 % at batch 128, each as UPSCALE (reorder) vs the
+    baseline export run copy-then-conv (tools/sweep.py has the full sweep incl. config 5)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("sweep", ROOT / "tools" / "sweep.py")
+    sw = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sw)
+    from paper_2307_08771_b200.configs import CONFIGS, MOBILENET_SWEEP, build_spatial_model
+
+    out = {"mobilenet_v3_small_b1": [], "densenet121_s50_b128": None}
+    for s_ in MOBILENET_SWEEP:
+        name = f"mobilenet_v3_small_s{round(s_ * 100):02d}"
+        cfg = CONFIGS[name]
+        sm = build_spatial_model(cfg)
+        up = sw.time_engine(sm, cfg, "reorder", "fused", 1, max(steps, 50))
+        base = sw.time_engine(sm, cfg, "baseline", "copy", 1, max(steps, 50))
+        out["mobilenet_v3_small_b1"].append({"sparsity": s_, "upscale_ms": up["ms"], "baseline_copy_ms": base["ms"],
+                                             "upscale_speedup": round(base["ms"] / up["ms"], 4),
+                                             "launches": [up["launches"], base["launches"]]})
+    cfg = CONFIGS["densenet121_s50"]
+    sm = build_spatial_model(cfg)
+    up = sw.time_engine(sm, cfg, "reorder", "fused", cfg.batch, steps)
+    base = sw.time_engine(sm, cfg, "baseline", "copy", cfg.batch, steps)
+    out["densenet121_s50_b128"] = {"upscale": up, "baseline_copy": base,
+                                   "upscale_speedup": round(base["ms"] / up["ms"], 4)}
     return out
 
 

@@ -361,6 +361,83 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
   }
 }
 
+
+// Direct stem conv on CUDA cores for few input channels (MobileNetV3 / EfficientNetV2:
+// 3x3/s2 on the 3 image planes).  Reads the fp32 NCHW model input through the INPUT
+// node's GATHER (idx), BN folded into w/bias, activation fused, NHWC bf16 out.  A CTA
+// computes an 8 x 16 output tile: the cin input windows and all weights are staged in
+// shared memory once; a thread owns one pixel x 32 output channels (the warp's 32 pixels
+// share the channel block, so every weight read is a broadcast).  At cin <= 4 the
+// tensor-core im2col stem spends its time building a 9x-expanded operand; here the input
+// is read once and the output written once.
+constexpr int DS_TH = 8, DS_TW = 16;
+__global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restrict__ x, int N, int C, int H, int W,
+                                                          const int32_t* __restrict__ idx, int cin, const float* __restrict__ w,
+                                                          const float* __restrict__ bias, int cout, int k, int s,
+                                                          int pad, int act, int Ho, int Wo, int tiles_h, int tiles_w,
+                                                          uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+  extern __shared__ float ds_smem[];
+  const int IH = (DS_TH - 1) * s + k, IW = (DS_TW - 1) * s + k;
+  const int cout32 = (cout + 31) / 32 * 32;
+  float* sx = ds_smem;                      // [cin][IH][IW]
+  float* sw = sx + cin * IH * IW;           // [k*k*cin][cout32]
+  float* sb = sw + k * k * cin * cout32;    // [cout32]
+  const int t = blockIdx.x;
+  const int n = t / (tiles_h * tiles_w);
+  const int r = t - n * tiles_h * tiles_w;
+  const int y0 = (r / tiles_w) * DS_TH, x0 = (r % tiles_w) * DS_TW;
+  const int iy0 = y0 * s - pad, ix0 = x0 * s - pad;
+  for (int e = threadIdx.x; e < k * k * cin * cout32; e += blockDim.x) sw[e] = w[e];
+  for (int e = threadIdx.x; e < cout32; e += blockDim.x) sb[e] = (bias && e < cout) ? bias[e] : 0.f;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int e = threadIdx.x; e < cin * IH * IW; e += blockDim.x) {
+    const int c = e / (IH * IW);
+    const int rr = e - c * IH * IW;
+    const int iy = iy0 + rr / IW, ix = ix0 + rr % IW;
+    float v = 0.f;
+    if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+      v = __ldg(x + ((static_cast<long long>(n) * C + __ldg(idx + c)) * H + iy) * W + ix);
+    sx[e] = v;
+  }
+  __syncthreads();
+  const int pix = threadIdx.x & 127;
+  const int oy = pix / DS_TW, ox = pix % DS_TW;
+  const bool live = y0 + oy < Ho && x0 + ox < Wo;
+  for (int cb = (threadIdx.x >> 7) * 32; cb < cout32; cb += 64) {
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = sb[cb + j];
+    for (int c = 0; c < cin; ++c) {
+      for (int dy = 0; dy < k; ++dy) {
+        const float* row = sx + (c * IH + oy * s + dy) * IW + ox * s;
+        for (int dx = 0; dx < k; ++dx) {
+          const float v = row[dx];
+          const float* wt = sw + ((dy * k + dx) * cin + c) * cout32 + cb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = fmaf(wt[j], v, acc[j]);
+        }
+      }
+    }
+    if (live) {
+      uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy) * Wo + x0 + ox) * y_cstride + y_coff + cb;
+      if (cb + 32 <= cout) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint16_t o[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[q * 8 + j], act));
+          *reinterpret_cast<uint4*>(yp + q * 8) = *reinterpret_cast<const uint4*>(o);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (cb + j < cout) yp[j] = tobf(act_f(acc[j], act));
+      }
+    }
+  }
+}
+
 bool a16(const void* base, int cstride, int coff) {
   return base == nullptr || (aligned16(base) && (cstride & 7) == 0 && (coff & 7) == 0);
 }
@@ -465,4 +542,29 @@ extern "C" int ub_linear_small(const void* x, int M, int x_cstride, const int32_
                                    y_dtype == UB_F32 ? 1 : 0, y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "linear_small_kernel");
+}
+
+extern "C" int ub_conv_direct(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, const float* w,
+                              const float* bias, int cout, int k, int s, int pad, int act, void* y, int y_cstride,
+                              int y_coff, cudaStream_t stream) {
+  if (!x || !idx || !w || !y || N < 1 || C < 1 || H < 1 || W < 1 || cin < 1 || cout < 1 || k < 1 || s < 1 ||
+      pad < 0 || act < UB_ACT_NONE || act > UB_ACT_SIGMOID)
+    return fail(UB_EINVAL, "ub_conv_direct: bad arguments");
+  if (cin > 8 || k > 7 || cout > 256) return fail(UB_EUNSUPPORTED, "ub_conv_direct: cin %d k %d cout %d", cin, k, cout);
+  if (!a16(y, y_cstride, y_coff) || y_coff + cout > y_cstride)
+    return fail(UB_EINVAL, "ub_conv_direct: output rows must be 16-byte aligned");
+  const int Ho = (H + 2 * pad - k) / s + 1, Wo = (W + 2 * pad - k) / s + 1;
+  const int IH = (DS_TH - 1) * s + k, IW = (DS_TW - 1) * s + k;
+  const int cout32 = (cout + 31) / 32 * 32;
+  const size_t smem = (static_cast<size_t>(cin) * IH * IW + static_cast<size_t>(k) * k * cin * cout32 + cout32) * 4;
+  if (smem > 200 * 1024) return fail(UB_EUNSUPPORTED, "ub_conv_direct: shared memory");
+  if (const cudaError_t ae = ensure_max_smem(conv_direct_kernel)) return cuda_status(ae, "conv_direct attr");
+  const int th = (Ho + DS_TH - 1) / DS_TH, tw = (Wo + DS_TW - 1) / DS_TW;
+  const long long tiles = static_cast<long long>(N) * th * tw;
+  if (tiles >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_conv_direct: too many tiles");
+  const cudaError_t e = launch_pdl(conv_direct_kernel, dim3(static_cast<unsigned>(tiles)), dim3(256), smem, stream, x,
+                                   N, C, H, W, idx, cin, w, bias, cout, k, s, pad, act, Ho, Wo, th, tw,
+                                   static_cast<uint16_t*>(y), y_cstride, y_coff);
+  count_launch();
+  return cuda_status(e, "conv_direct_kernel");
 }

@@ -234,22 +234,34 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
   const long long nbatch = (npix + pb - 1) / pb;
   const long long step = static_cast<long long>(gridDim.x) * warps;
   const int groups = n8 >> 3;
+  // chunk t = lane + 32 i of a batch -> (pixel k, row q, chunk ch): the same for every batch,
+  // walked with increments (no divisions in the loop)
+  const bool direct = ROWS == 1 && stride == 1;  // source pixel == output pixel
   auto issue = [&](long long b, uint8_t* dst) {
     const long long p0 = b * pb;
     const int total = pb * pix_chunks;
+    int k = lane / pix_chunks, rem = lane - (lane / pix_chunks) * pix_chunks;
     for (int t = lane; t < total; t += 32) {
-      const int k = t / pix_chunks;
       const long long p = p0 + k;
       if (p >= npix) break;
-      const int rem = t - k * pix_chunks;
-      const int q = rem / win16, ch = rem - q * win16;
-      const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
-      const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
-      const int yo = r / Wo, xo = r - (r / Wo) * Wo;
-      const int yi = ROWS == 4 ? 2 * yo + (q >> 1) : yo * stride;
-      const int xi = ROWS == 4 ? 2 * xo + (q & 1) : xo * stride;
-      const uint16_t* src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws + ch * 8;
+      const uint16_t* src;
+      if (direct) {
+        src = x + static_cast<size_t>(p) * x_cstride + ws + rem * 8;
+      } else {
+        const int q = ROWS == 1 ? 0 : rem / win16, ch = rem - q * win16;
+        const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
+        const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+        const int yo = r / Wo, xo = r - (r / Wo) * Wo;
+        const int yi = ROWS == 4 ? 2 * yo + (q >> 1) : yo * stride;
+        const int xi = ROWS == 4 ? 2 * xo + (q & 1) : xo * stride;
+        src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws + ch * 8;
+      }
       cp_async16(dst + t * 16, src, 16);
+      rem += 32;
+      while (rem >= pix_chunks) {
+        rem -= pix_chunks;
+        ++k;
+      }
     }
   };
   long long b = static_cast<long long>(blockIdx.x) * warps + warp;
@@ -269,12 +281,18 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
     const uint8_t* stage = buf0 + k * stage_bytes;
     const long long p0 = b * pb;
     const int work = pb * groups;
+    int kp = lane / groups, gi = lane - (lane / groups) * groups;
     for (int t = lane; t < work; t += 32) {
-      const int kp = t / groups;
       const long long p = p0 + kp;
       if (p >= npix) break;
-      const int i = (t - kp * groups) * 8;
-      const uint16_t* row = reinterpret_cast<const uint16_t*>(stage + kp * pix_chunks * 16);
+      const int i = gi * 8;
+      gi += 32;
+      const int kp_here = kp;
+      while (gi >= groups) {
+        gi -= groups;
+        ++kp;
+      }
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(stage + kp_here * pix_chunks * 16);
       uint32_t w[4];
 #pragma unroll
       for (int j2 = 0; j2 < 4; ++j2) {
@@ -300,6 +318,108 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
               if (ROWS == 4) acc *= 0.25f;
             }
             h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+          }
+        }
+        w[j2] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
+      }
+      *reinterpret_cast<uint4*>(y + static_cast<size_t>(p) * y_cstride + y_coff + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
+// Fast form of gather_rows_kernel for the common case -- stride 1, no pool, at most 256
+// output channels: a warp step moves pb = 32 / groups pixels so that every lane owns ONE
+// (pixel, 8-channel group) of the batch, and the lane's source columns, BN scale/shift and
+// its cp.async chunk offsets are the same for every batch: they are hoisted into registers
+// once.  A batch then costs a handful of cp.async and one 16-byte gather/store per lane
+// (the general kernel is instruction-bound on these narrow DenseNet rows).
+constexpr int GRF_MAXI = 8;  // cp.async chunks per lane per batch
+template <bool AFFINE>
+__global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
+                                                               int win16, int pb, const int32_t* __restrict__ idx,
+                                                               int n_idx, int rel, int n8, long long npix,
+                                                               const float* __restrict__ scale,
+                                                               const float* __restrict__ shift, int relu,
+                                                               uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+  constexpr int STAGES = 4;
+  extern __shared__ __align__(16) uint8_t g_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int stage_bytes = pb * win16 * 16;
+  uint8_t* buf0 = g_smem + static_cast<size_t>(warp) * STAGES * stage_bytes;
+  const int groups = n8 >> 3;
+  // this lane's output: pixel kp of the batch, channels i .. i+7
+  const bool out_lane = lane < pb * groups;
+  const int kp = out_lane ? lane / groups : 0;
+  const int i = out_lane ? (lane - kp * groups) * 8 : 0;
+  int col[8];
+  float sc[8], sh[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = i + j;
+    const int a = (out_lane && c < n_idx) ? __ldg(idx + c) : -1;
+    col[j] = a >= 0 ? kp * win16 * 8 + a + rel : -1;
+    if (AFFINE) {
+      sc[j] = (out_lane && c < n_idx) ? __ldg(scale + c) : 0.f;
+      sh[j] = (out_lane && c < n_idx) ? __ldg(shift + c) : 0.f;
+    }
+  }
+  // this lane's cp.async chunks: t = lane + 32 m -> pixel t / win16, chunk t % win16
+  const int total = pb * win16;
+  int ck[GRF_MAXI], coffs[GRF_MAXI];
+  int nchunk = 0;
+#pragma unroll
+  for (int m = 0; m < GRF_MAXI; ++m) {
+    const int t = lane + 32 * m;
+    ck[m] = t < total ? t / win16 : 1 << 30;
+    coffs[m] = t < total ? ck[m] * x_cstride + (t - ck[m] * win16) * 8 : 0;
+    if (t < total) nchunk = m + 1;
+  }
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long nbatch = (npix + pb - 1) / pb;
+  const long long step = static_cast<long long>(gridDim.x) * warps;
+  auto issue = [&](long long b, uint8_t* dst) {
+    const long long p0 = b * pb;
+    const uint16_t* src = x + static_cast<size_t>(p0) * x_cstride + ws;
+#pragma unroll
+    for (int m = 0; m < GRF_MAXI; ++m)
+      if (m < nchunk && p0 + ck[m] < npix) cp_async16(dst + (lane + 32 * m) * 16, src + coffs[m], 16);
+  };
+  long long b = static_cast<long long>(blockIdx.x) * warps + warp;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (b + st * step < nbatch) issue(b + st * step, buf0 + st * stage_bytes);
+    cp_async_commit();
+  }
+  int k = 0;
+  for (; b < nbatch; b += step, k = (k + 1 == STAGES ? 0 : k + 1)) {
+    const long long bn = b + (STAGES - 1) * step;
+    if (bn < nbatch) issue(bn, buf0 + ((k + STAGES - 1) % STAGES) * stage_bytes);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncwarp();
+    const long long p = b * pb + kp;
+    if (out_lane && p < npix) {
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
+      uint32_t w[4];
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2) {
+        uint16_t h[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * j2 + e;
+          if (!AFFINE) {
+            h[e] = col[j] >= 0 ? row[col[j]] : uint16_t(0);
+          } else {
+            float v = 0.f;
+            if (col[j] >= 0) {
+              v = fmaf(sc[j], __uint_as_float(static_cast<uint32_t>(row[col[j]]) << 16), sh[j]);
+              if (relu) v = fmaxf(v, 0.f);
+            }
+            h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
           }
         }
         w[j2] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
@@ -709,6 +829,33 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   const int ws = (x_coff + lo) & ~7;
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
+  if (!pool2 && stride == 1 && n8 <= 256) {  // fast form: one (pixel, 8-channel group) per lane
+    const int groups = n8 / 8;
+    const int pbf = 32 / groups;
+    if (pbf * win16 <= 32 * GRF_MAXI) {
+      const size_t stage_f = static_cast<size_t>(pbf) * win16 * 16;
+      int wf = 8;
+      while (wf > 1 && wf * 4 * stage_f > 200 * 1024) wf >>= 1;
+      const size_t smem_f = wf * 4 * stage_f;
+      void (*kf)(const uint16_t*, int, int, int, int, const int32_t*, int, int, int, long long, const float*,
+                 const float*, int, uint16_t*, int, int) =
+          affine ? gather_rows_fast_kernel<true> : gather_rows_fast_kernel<false>;
+      if (const cudaError_t ae = ensure_max_smem(kf)) return cuda_status(ae, "gather_rows_fast attr");
+      const long long npix_f = static_cast<long long>(N) * H * W;
+      const long long nb = (npix_f + pbf - 1) / pbf;
+      int per_sm = static_cast<int>((227 * 1024) / (smem_f + 1024));
+      if (per_sm > 2048 / (32 * wf)) per_sm = 2048 / (32 * wf);
+      if (per_sm < 1) per_sm = 1;
+      const long long want = (nb + wf - 1) / wf;
+      const long long cap = static_cast<long long>(num_sms()) * per_sm;
+      const int grid = static_cast<int>(want < cap ? want : cap);
+      const cudaError_t e = launch_pdl(kf, dim3(grid), dim3(32 * wf), smem_f, stream, static_cast<const uint16_t*>(x),
+                                       x_cstride, ws, win16, pbf, idx, n_idx, x_coff - ws, n8, npix_f, scale, shift,
+                                       relu, static_cast<uint16_t*>(y), y_cstride, y_coff);
+      count_launch();
+      return cuda_status(e, "gather_rows_fast_kernel");
+    }
+  }
   const int idx_bytes = ((affine ? 3 : 1) * n8 * 4 + 15) & ~15;
   // pixels per warp step: ~96 16-byte chunks per cp.async wave (3 per lane), at most 16 pixels
   int pb = 96 / (rows * win16);

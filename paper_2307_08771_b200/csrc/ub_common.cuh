@@ -348,8 +348,8 @@ UB_DEVI float act_f(float v, int act) {
     case 2: return fminf(fmaxf(v, 0.f), 6.f);
     case 3: return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
     case 4: return fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
-    case 5: return v / (1.f + __expf(-v));
-    case 6: return 1.f / (1.f + __expf(-v));
+    case 5: return __fdividef(v, 1.f + __expf(-v));  // fast reciprocal: a bf16 store follows
+    case 6: return __fdividef(1.f, 1.f + __expf(-v));
     default: return v;
   }
 }

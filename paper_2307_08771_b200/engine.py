@@ -1023,6 +1023,23 @@ class Engine:
             op.launch = lambda: K.stem_s2d(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias, relu=relu)
             op.info["stem_kind"] = "s2d"
             wbytes = 2.0 * wg.numel()
+        elif cin <= 8 and kk <= 7 and cout <= 256 and y.coff % 8 == 0 and y.cstride % 8 == 0:
+            # few input channels (MobileNetV3 / EfficientNetV2 3x3/s2 stems): direct conv on CUDA
+            # cores, the input read once (the im2col operand would be k*k times the input)
+            Wf = W.detach().float().cpu()
+            rr = torch.tensor([r_ for r_ in rows], dtype=torch.long)
+            cc = torch.tensor([c_ for c_ in cols], dtype=torch.long)
+            Wsel = Wf[rr.clamp_min(0)][:, cc.clamp_min(0)] * (rr >= 0).view(-1, 1, 1, 1) * (cc >= 0).view(1, -1, 1, 1)
+            if scale is not None:
+                Wsel = Wsel * scale.detach().float().cpu().view(-1, 1, 1, 1)
+            c32 = (cout + 31) // 32 * 32
+            wd = torch.zeros(kk * kk, cin, c32)
+            wd[:, :, :cout] = Wsel.permute(2, 3, 1, 0).reshape(kk * kk, cin, cout)
+            wd = wd.to(self.device).contiguous()
+            self._keep.append(wd)
+            op.launch = lambda: K.conv_direct(self.input_buf, idx_dev, wd, bias, cout, kk, st, pd, relu, y)
+            op.info["stem_kind"] = "direct"
+            wbytes = 4.0 * wd.numel()
         else:
             kpad = _lib.conv_stem_kpad(cin, kk, kk)
             wg = K.permute_weights(W, rows, cols, row_scale=scale, layout="dense", cpad=kpad,

@@ -335,6 +335,14 @@ def linear_small(x: Act, xcol_dev: torch.Tensor, w: torch.Tensor, O: int, y: Act
               _p(bias), act, _p(y.buf), _lib.UB_F32 if y_fp32 else _lib.UB_BF16, y.cstride, y.coff, _stream())
 
 
+def conv_direct(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, bias, cout: int, k: int, stride: int,
+                pad: int, act: int, y: Act) -> None:
+    """ub_conv_direct: few-channel stem on CUDA cores; w fp32 [k*k, cin, pad32(cout)]."""
+    N, C, H, W = x_nchw.shape
+    _lib.call("ub_conv_direct", _p(x_nchw), N, C, H, W, _p(idx_dev), idx_dev.numel(), _p(w), _p(bias), cout, k, stride,
+              pad, act, _p(y.buf), y.cstride, y.coff, _stream())
+
+
 def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:
     _lib.call("ub_avgpool2d", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, k, stride, pad, y.H, y.W,
               _p(y.buf), y.cstride, y.coff, _stream())

@@ -719,3 +719,29 @@ def test_avgpool_split(N, H, C):
     K.avgpool_split(xa, y)
     torch.cuda.synchronize()
     assert _rel(y.to_nchw().cpu(), _bf(x).mean(dim=(2, 3), keepdim=True)) < 1e-2
+
+
+@pytest.mark.parametrize("cin,k,s,cout,act", [(3, 3, 2, 24, "silu"), (2, 3, 2, 16, "hardswish"), (3, 7, 2, 70, "relu"),
+                                               (1, 5, 1, 40, "none")])
+def test_conv_direct(cin, k, s, cout, act):
+    """ub_conv_direct (few-channel stem on CUDA cores, INPUT GATHER applied) vs torch fp32."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(cin * 100 + k * 10 + cout)
+    N, C, H, W = 2, 3, 37, 45
+    x = torch.randn(N, C, H, W, generator=g)
+    idx = [2, 0, 1][:cin]
+    Wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
+    b = torch.randn(cout, generator=g)
+    pad = k // 2
+    Ho, Wo = (H + 2 * pad - k) // s + 1, (W + 2 * pad - k) // s + 1
+    c32 = (cout + 31) // 32 * 32
+    wd = torch.zeros(k * k, cin, c32)
+    wd[:, :, :cout] = Wt.permute(2, 3, 1, 0).reshape(k * k, cin, cout)
+    y = K.empty_act(N, Ho, Wo, cout, dev)
+    K.conv_direct(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), wd.to(dev), b.to(dev), cout, k, s, pad,
+                  _lib.UB_ACT[act], y)
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "relu": torch.relu, "hardswish": torch.nn.functional.hardswish,
+           "silu": torch.nn.functional.silu}
+    ref = fns[act](torch.nn.functional.conv2d(x[:, idx], Wt, b, stride=s, padding=pad))
+    assert _rel(y.to_nchw().cpu(), ref) < 1e-2
