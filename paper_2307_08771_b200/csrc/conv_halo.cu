@@ -502,13 +502,9 @@ __global__ void __maxnreg__(96)
             const float2 s3 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])),
                                         make_float2(b1.z, b1.w));
             uint4 o;
-            if (p.relu == 1) {
+            if (p.relu) {
               o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y), cvt_relu_bf16x2(s2.x, s2.y),
                              cvt_relu_bf16x2(s3.x, s3.y));
-            } else if (p.relu > 1) {  // other UB_ACT_* activations
-              const int a = p.relu;
-              o = make_uint4(cvt_bf16x2(act_f(s0.x, a), act_f(s0.y, a)), cvt_bf16x2(act_f(s1.x, a), act_f(s1.y, a)),
-                             cvt_bf16x2(act_f(s2.x, a), act_f(s2.y, a)), cvt_bf16x2(act_f(s3.x, a), act_f(s3.y, a)));
             } else {
               o = make_uint4(cvt_bf16x2(s0.x, s0.y), cvt_bf16x2(s1.x, s1.y), cvt_bf16x2(s2.x, s2.y),
                              cvt_bf16x2(s3.x, s3.y));
@@ -547,8 +543,8 @@ long long* g_halo_trace = nullptr;
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
   *handled = false;
   if (d->kh != 3 || d->kw != 3 || (d->stride != 1 && d->stride != 2) || d->pad != 1 || d->x_nchw_f32 ||
-      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8) || d->y2)
-    return UB_OK;
+      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8) || d->y2 || d->relu > 1)
+    return UB_OK;  // (activations other than ReLU: the generic kernel's XACT epilogue)
   const int S = d->stride;
   if (cpad != 16 && cpad != 32 && cpad % 64 != 0) return UB_OK;
   if (S == 2 && (cpad % 64 != 0 || lead != 0)) return UB_OK;  // a folded plane = 8 channels of one pixel

@@ -147,7 +147,10 @@ __device__ __forceinline__ int tile_res_chunks(const ConvKParams& p, int n0) {
   return p.has_res ? (min(p.block_n, p.cout - n0) + EPI_CHUNK - 1) / EPI_CHUNK : 0;
 }
 
-template <int AMODE, int BK, int PRODUCERS>
+// XACT: the epilogue applies a UB_ACT_* activation other than ReLU (hardswish, SiLU, ...).
+// A separate instantiation, so the ReLU / identity epilogue of the ResNet path keeps its
+// compact code (folding the generic activation into one kernel cost ~8 % on ResNet-50).
+template <int AMODE, int BK, int PRODUCERS, bool XACT>
 __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
@@ -796,16 +799,16 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
               for (int jj = 0; jj < 4; ++jj) {
                 uint4 o;
                 const float* f = reinterpret_cast<const float*>(r) + jj * 8;
-                if (p.relu == 1) {
-                  o.x = cvt_relu_bf16x2(f[0], f[1]);
-                  o.y = cvt_relu_bf16x2(f[2], f[3]);
-                  o.z = cvt_relu_bf16x2(f[4], f[5]);
-                  o.w = cvt_relu_bf16x2(f[6], f[7]);
-                } else if (p.relu > 1) {  // other UB_ACT_* activations (hardswish, SiLU, ...)
+                if (XACT) {  // other UB_ACT_* activations (hardswish, SiLU, ...)
                   o.x = cvt_bf16x2(act_f(f[0], p.relu), act_f(f[1], p.relu));
                   o.y = cvt_bf16x2(act_f(f[2], p.relu), act_f(f[3], p.relu));
                   o.z = cvt_bf16x2(act_f(f[4], p.relu), act_f(f[5], p.relu));
                   o.w = cvt_bf16x2(act_f(f[6], p.relu), act_f(f[7], p.relu));
+                } else if (p.relu) {
+                  o.x = cvt_relu_bf16x2(f[0], f[1]);
+                  o.y = cvt_relu_bf16x2(f[2], f[3]);
+                  o.z = cvt_relu_bf16x2(f[4], f[5]);
+                  o.w = cvt_relu_bf16x2(f[6], f[7]);
                 } else {
                   o.x = cvt_bf16x2(f[0], f[1]);
                   o.y = cvt_bf16x2(f[2], f[3]);
@@ -824,7 +827,9 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
             if (m < p.M && nv > 0) {
               float v[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = act_f(__uint_as_float(r[i]), p.relu);
+              for (int i = 0; i < 32; ++i)
+                v[i] = XACT ? act_f(__uint_as_float(r[i]), p.relu)
+                            : (p.relu ? fmaxf(__uint_as_float(r[i]), 0.f) : __uint_as_float(r[i]));
               const size_t yo = static_cast<size_t>(m) * p.y_cstride + p.y_coff + nb;
               if (p.y_f32) {
                 float* yp = reinterpret_cast<float*>(p.y) + yo;
@@ -939,10 +944,10 @@ namespace {
 template <int AMODE, int BK, int PRODUCERS>
 int launch_conv_p(const CUtensorMap& tmY, const CUtensorMap& tmB, const CUtensorMap& tmA, const CUtensorMap& tmR,
                   const CUtensorMap& tmAt, const ConvKParams& p, int grid, size_t smem, cudaStream_t stream) {
-  const cudaError_t attr_err = ensure_max_smem(conv_tc_kernel<AMODE, BK, PRODUCERS>);
+  auto kern = p.relu > 1 ? conv_tc_kernel<AMODE, BK, PRODUCERS, true> : conv_tc_kernel<AMODE, BK, PRODUCERS, false>;
+  const cudaError_t attr_err = ensure_max_smem(kern);
   if (attr_err != cudaSuccess) return cuda_status(attr_err, "cudaFuncSetAttribute(conv)");
-  const cudaError_t e = launch_pdl(conv_tc_kernel<AMODE, BK, PRODUCERS>, dim3(grid), dim3(256 + PRODUCERS), smem,
-                                   stream, tmY, tmB, tmA, tmR, tmAt, p);
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(256 + PRODUCERS), smem, stream, tmY, tmB, tmA, tmR, tmAt, p);
   if (e != cudaSuccess) return cuda_status(e, "conv_tc_kernel launch");
   count_launch();
   return cuda_status(cudaGetLastError(), "conv_tc_kernel launch");
