@@ -329,14 +329,16 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
   cp_async_wait<0>();
 }
 
-// Fast form of gather_rows_kernel for the common case -- stride 1, no pool, at most 256
-// output channels: a warp step moves pb = 32 / groups pixels so that every lane owns ONE
-// (pixel, 8-channel group) of the batch, and the lane's source columns, BN scale/shift and
-// its cp.async chunk offsets are the same for every batch: they are hoisted into registers
-// once.  A batch then costs a handful of cp.async and one 16-byte gather/store per lane
-// (the general kernel is instruction-bound on these narrow DenseNet rows).
-constexpr int GRF_MAXI = 8;  // cp.async chunks per lane per batch
-template <bool AFFINE>
+// Fast form of gather_rows_kernel for the common case -- stride 1, no pool.  Narrow outputs
+// (groups = pad8(n)/8 <= 32): a warp step moves pb = 32 / groups pixels so that every lane
+// owns ONE (pixel, 8-channel group) of the batch.  Wide outputs (groups > 32): pb = 1 and
+// lane l owns groups l, l+32, ... (GJ of them).  Either way the lane's source columns and
+// cp.async chunk offsets are the same for every batch and live in registers (the BN
+// scale/shift of wide outputs in shared memory, read conflict-free), so a batch costs a
+// few cp.async and one 16-byte gather/store per owned group; with the engine's ascending
+// source order the 2-byte shared-memory reads of a warp hit distinct banks.
+constexpr int GRF_MAXI = 4;  // cp.async chunks per lane per batch
+template <bool AFFINE, int GJ>
 __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
                                                                int win16, int pb, const int32_t* __restrict__ idx,
                                                                int n_idx, int rel, int n8, long long npix,
@@ -348,34 +350,44 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   const int stage_bytes = pb * win16 * 16;
-  uint8_t* buf0 = g_smem + static_cast<size_t>(warp) * STAGES * stage_bytes;
+  float* s_sc = reinterpret_cast<float*>(g_smem);  // wide outputs: [n8] scale then [n8] shift
+  float* s_sh = s_sc + n8;
+  const int par_bytes = (GJ > 1 && AFFINE) ? ((2 * n8 * 4 + 15) & ~15) : 0;
+  uint8_t* buf0 = g_smem + par_bytes + static_cast<size_t>(warp) * STAGES * stage_bytes;
   const int groups = n8 >> 3;
-  // this lane's output: pixel kp of the batch, channels i .. i+7
-  const bool out_lane = lane < pb * groups;
-  const int kp = out_lane ? lane / groups : 0;
-  const int i = out_lane ? (lane - kp * groups) * 8 : 0;
-  int col[8];
-  float sc[8], sh[8];
+  if (GJ > 1 && AFFINE) {
+    for (int c = threadIdx.x; c < n8; c += blockDim.x) {
+      s_sc[c] = c < n_idx ? __ldg(scale + c) : 0.f;
+      s_sh[c] = c < n_idx ? __ldg(shift + c) : 0.f;
+    }
+    __syncthreads();
+  }
+  // owned outputs: GJ == 1 -> pixel kp, group lane % groups; GJ > 1 -> pixel 0, groups lane + 32 j
+  const int kp = GJ == 1 ? lane / groups : 0;
+  int col[GJ][8];
+  float sc[GJ == 1 ? 8 : 1], sh[GJ == 1 ? 8 : 1];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int c = i + j;
-    const int a = (out_lane && c < n_idx) ? __ldg(idx + c) : -1;
-    col[j] = a >= 0 ? kp * win16 * 8 + a + rel : -1;
-    if (AFFINE) {
-      sc[j] = (out_lane && c < n_idx) ? __ldg(scale + c) : 0.f;
-      sh[j] = (out_lane && c < n_idx) ? __ldg(shift + c) : 0.f;
+  for (int jj = 0; jj < GJ; ++jj) {
+    const int g = GJ == 1 ? lane - kp * groups : lane + 32 * jj;
+    const bool own = GJ == 1 ? lane < pb * groups : g < groups;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = g * 8 + j;
+      const int a = (own && c < n_idx) ? __ldg(idx + c) : -1;
+      col[jj][j] = a >= 0 ? kp * win16 * 8 + a + rel : -1;
+      if (GJ == 1 && AFFINE) {
+        sc[j] = (own && c < n_idx) ? __ldg(scale + c) : 0.f;
+        sh[j] = (own && c < n_idx) ? __ldg(shift + c) : 0.f;
+      }
     }
   }
-  // this lane's cp.async chunks: t = lane + 32 m -> pixel t / win16, chunk t % win16
   const int total = pb * win16;
   int ck[GRF_MAXI], coffs[GRF_MAXI];
-  int nchunk = 0;
 #pragma unroll
   for (int m = 0; m < GRF_MAXI; ++m) {
     const int t = lane + 32 * m;
     ck[m] = t < total ? t / win16 : 1 << 30;
     coffs[m] = t < total ? ck[m] * x_cstride + (t - ck[m] * win16) * 8 : 0;
-    if (t < total) nchunk = m + 1;
   }
   griddep_wait();
   griddep_launch_dependents();
@@ -385,8 +397,10 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
     const long long p0 = b * pb;
     const uint16_t* src = x + static_cast<size_t>(p0) * x_cstride + ws;
 #pragma unroll
-    for (int m = 0; m < GRF_MAXI; ++m)
-      if (m < nchunk && p0 + ck[m] < npix) cp_async16(dst + (lane + 32 * m) * 16, src + coffs[m], 16);
+    for (int m = 0; m < GRF_MAXI; ++m) {
+      if (lane + 32 * m >= total) break;
+      if (p0 + ck[m] < npix) cp_async16(dst + (lane + 32 * m) * 16, src + coffs[m], 16);
+    }
   };
   long long b = static_cast<long long>(blockIdx.x) * warps + warp;
 #pragma unroll
@@ -402,8 +416,12 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
     cp_async_wait<STAGES - 1>();
     __syncwarp();
     const long long p = b * pb + kp;
-    if (out_lane && p < npix) {
-      const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
+#pragma unroll
+    for (int jj = 0; jj < GJ; ++jj) {
+      const int g = GJ == 1 ? lane - kp * groups : lane + 32 * jj;
+      const bool own = GJ == 1 ? lane < pb * groups : g < groups;
+      if (!own || p >= npix) continue;
       uint32_t w[4];
 #pragma unroll
       for (int j2 = 0; j2 < 4; ++j2) {
@@ -411,12 +429,15 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = 2 * j2 + e;
+          const int cj = col[jj][j];
           if (!AFFINE) {
-            h[e] = col[j] >= 0 ? row[col[j]] : uint16_t(0);
+            h[e] = cj >= 0 ? row[cj] : uint16_t(0);
           } else {
             float v = 0.f;
-            if (col[j] >= 0) {
-              v = fmaf(sc[j], __uint_as_float(static_cast<uint32_t>(row[col[j]]) << 16), sh[j]);
+            if (cj >= 0) {
+              const float a = GJ == 1 ? sc[j] : s_sc[g * 8 + j];
+              const float t = GJ == 1 ? sh[j] : s_sh[g * 8 + j];
+              v = fmaf(a, __uint_as_float(static_cast<uint32_t>(row[cj]) << 16), t);
               if (relu) v = fmaxf(v, 0.f);
             }
             h[e] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
@@ -424,7 +445,8 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
         }
         w[j2] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
       }
-      *reinterpret_cast<uint4*>(y + static_cast<size_t>(p) * y_cstride + y_coff + i) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(y + static_cast<size_t>(p) * y_cstride + y_coff + g * 8) =
+          make_uint4(w[0], w[1], w[2], w[3]);
     }
     __syncwarp();
   }
@@ -829,17 +851,24 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   const int ws = (x_coff + lo) & ~7;
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
-  if (!pool2 && stride == 1 && n8 <= 256) {  // fast form: one (pixel, 8-channel group) per lane
+  if (!pool2 && stride == 1 && n8 <= 1024) {  // fast form: fixed per-lane ownership of output groups
     const int groups = n8 / 8;
-    const int pbf = 32 / groups;
+    const int gj = groups <= 32 ? 1 : (groups + 31) / 32;
+    const int pbf = gj == 1 ? 32 / groups : 1;
     if (pbf * win16 <= 32 * GRF_MAXI) {
       const size_t stage_f = static_cast<size_t>(pbf) * win16 * 16;
+      const size_t par = (gj > 1 && affine) ? ((2 * n8 * 4 + 15) & ~15) : 0;
       int wf = 8;
-      while (wf > 1 && wf * 4 * stage_f > 200 * 1024) wf >>= 1;
-      const size_t smem_f = wf * 4 * stage_f;
+      while (wf > 1 && par + wf * 4 * stage_f > 200 * 1024) wf >>= 1;
+      const size_t smem_f = par + wf * 4 * stage_f;
       void (*kf)(const uint16_t*, int, int, int, int, const int32_t*, int, int, int, long long, const float*,
-                 const float*, int, uint16_t*, int, int) =
-          affine ? gather_rows_fast_kernel<true> : gather_rows_fast_kernel<false>;
+                 const float*, int, uint16_t*, int, int) = nullptr;
+      switch (gj) {
+        case 1: kf = affine ? gather_rows_fast_kernel<true, 1> : gather_rows_fast_kernel<false, 1>; break;
+        case 2: kf = affine ? gather_rows_fast_kernel<true, 2> : gather_rows_fast_kernel<false, 2>; break;
+        case 3: kf = affine ? gather_rows_fast_kernel<true, 3> : gather_rows_fast_kernel<false, 3>; break;
+        default: kf = affine ? gather_rows_fast_kernel<true, 4> : gather_rows_fast_kernel<false, 4>; break;
+      }
       if (const cudaError_t ae = ensure_max_smem(kf)) return cuda_status(ae, "gather_rows_fast attr");
       const long long npix_f = static_cast<long long>(N) * H * W;
       const long long nb = (npix_f + pbf - 1) / pbf;

@@ -814,6 +814,12 @@ class Engine:
             # the concat's column map), the reader's BN/ReLU prologue and a moved 2x2 pool in one
             # pass -- and the conv reads it densely
             idx = gather if gather is not None else list(range(x.C))
+            # internal K order = ascending source column (a GEMM is invariant to a consistent
+            # permutation of K; the exported (perm, indices) stay the reference's): the staged
+            # read's shared-memory gathers then touch distinct banks
+            k_order = sorted(range(len(idx)), key=lambda k: (idx[k] < 0, x.phys(idx[k]), k))
+            idx = [idx[k] for k in k_order]
+            cols = [cols[k] for k in k_order]
             idx_p = [x.phys(i) for i in idx]
             xb = K.Act(x.buf, x.N, x.H, x.W, x.width, x.coff)
             pscale = pshift = None
@@ -921,6 +927,7 @@ class Engine:
             return gen
 
         op.info["halo"] = halo
+        op.info["read_pre"] = [pl[6] for pl in plans]  # staged-read launches (tools time them apart)
         op.info["variants"] = [(pi, v) for pi, pl in enumerate(plans) for v in gen_for(pl[7])]
         op.info["variant"] = (len(plans) - 1, 0)  # cover when offered, else the only plan
         op.info["plans"] = [pl[0] for pl in plans]

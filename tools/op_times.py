@@ -35,6 +35,25 @@ for r in rows:
 print(json.dumps({"config": name, "batch": batch, "strategy": strategy, "eager_sum_us": round(total * 1e3, 1),
                   "by_kernel": {k: {"launches": v[0], "us": round(v[1], 1), "roofline_us": round(v[2], 1)}
                                 for k, v in sorted(by_kernel.items(), key=lambda kv: -kv[1][1])}}))
-for r in sorted(rows, key=lambda r: -r["us"])[:25]:
+
+def t_us(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e3
+
+
+for r in sorted(rows, key=lambda r: -r["us"])[:int(sys.argv[5]) if len(sys.argv) > 5 else 25]:
     op = next(o for o in eng.ops if o.info.get("conv", o.output) == r["op"])
-    print(json.dumps({**r, "desc": op.info.get("desc", "")}))
+    extra = {}
+    pre = op.info.get("read_pre")
+    if pre and op.info.get("variant"):
+        fn = pre[op.info["variant"][0]]
+        if fn is not None:
+            extra["read_us"] = round(t_us(fn), 1)
+    print(json.dumps({**r, "desc": op.info.get("desc", ""), "variant": op.info.get("variant"), **extra}))
