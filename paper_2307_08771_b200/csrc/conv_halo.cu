@@ -554,7 +554,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   // stride 1: one zero column (the right pad of a row is the left pad of the next); stride 2:
   // folded columns 0 .. Wo (origin -1)
   while (Wp < d->Wo + 1) Wp <<= 1;
-  if (Wp > 64) return UB_OK;
+  if (Wp > 128) return UB_OK;  // WP = 128: one output row per MMA tile (EfficientNetV2's 112-wide stages)
   HaloParams p{};
   p.x = reinterpret_cast<const uint16_t*>(d->x) + (d->x_coff - lead);
   p.x_cstride = d->x_cstride;
@@ -650,7 +650,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   UB_HALO_CASE(WPV, 4, false, 1, true) UB_HALO_CASE(WPV, 8, false, 1, false)                               \
   UB_HALO_CASE(WPV, 8, false, 1, true) UB_HALO_CASE(WPV, 8, true, 1, false) UB_HALO_CASE(WPV, 8, true, 1, true) \
   UB_HALO_CASE(WPV, 8, true, 2, true)
-  UB_HALO_WP(8) UB_HALO_WP(16) UB_HALO_WP(32) UB_HALO_WP(64)
+  UB_HALO_WP(8) UB_HALO_WP(16) UB_HALO_WP(32) UB_HALO_WP(64) UB_HALO_WP(128)
 #undef UB_HALO_WP
 #undef UB_HALO_CASE
   if (!kern) return UB_OK;

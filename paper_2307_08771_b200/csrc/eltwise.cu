@@ -29,11 +29,13 @@ __global__ void __launch_bounds__(256) eltwise_kernel(ub_eltwise_desc d) {
   const uint16_t* b = static_cast<const uint16_t*>(d.b);
   const uint16_t* g = static_cast<const uint16_t*>(d.gate);
   uint16_t* y = static_cast<uint16_t*>(d.y);
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long p = e / groups;
-    const int c0 = static_cast<int>(e - p * groups) * (VEC ? 8 : 1);
-    const int n = static_cast<int>(p / d.HW);
+  // 32-bit index math (a 64-bit division costs ~100 instructions; totals stay < 2^31 here)
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<unsigned>(total);
+       e += gridDim.x * blockDim.x) {
+    const unsigned pu = e / static_cast<unsigned>(groups);
+    const long long p = pu;
+    const int c0 = static_cast<int>(e - pu * groups) * (VEC ? 8 : 1);
+    const int n = static_cast<int>(pu / static_cast<unsigned>(d.HW));
     if (VEC) {
       uint16_t va[8], vb[8], vg[8], vy[8];
       *reinterpret_cast<uint4*>(va) = *reinterpret_cast<const uint4*>(a + p * d.a_cstride + d.a_coff + c0);
@@ -78,12 +80,13 @@ __global__ void __launch_bounds__(256) avgpool2d_kernel(const uint16_t* __restri
   const int groups = (C + 7) / 8;
   const long long total = static_cast<long long>(N) * Ho * Wo * groups;
   const float inv = 1.f / static_cast<float>(k * k);
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long p = e / groups;
-    const int c0 = static_cast<int>(e - p * groups) * 8;
-    const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
-    const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<unsigned>(total);
+       e += gridDim.x * blockDim.x) {
+    const unsigned pu = e / static_cast<unsigned>(groups);
+    const long long p = pu;
+    const int c0 = static_cast<int>(e - pu * groups) * 8;
+    const int n = static_cast<int>(pu / static_cast<unsigned>(Ho * Wo));
+    const int r = static_cast<int>(pu - static_cast<unsigned>(n) * Ho * Wo);
     const int yo = r / Wo, xo = r - yo * Wo;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int dy = 0; dy < k; ++dy) {
@@ -456,6 +459,7 @@ extern "C" int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream) {
   const bool vec = a16(d->a, d->a_cstride, d->a_coff) && a16(d->y, d->y_cstride, d->y_coff) &&
                    a16(d->b, d->b_cstride, d->b_coff) && a16(d->gate, d->gate_cstride, d->gate_coff);
   const long long work = static_cast<long long>(d->N) * d->HW * (vec ? (d->C + 7) / 8 : d->C);
+  if (work >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_eltwise: tensor too large");
   const int grid = grid_for(work, 256, 2);
   const cudaError_t e = vec ? launch_pdl(eltwise_kernel<true>, dim3(grid), dim3(256), 0, stream, *d)
                             : launch_pdl(eltwise_kernel<false>, dim3(grid), dim3(256), 0, stream, *d);
@@ -470,6 +474,7 @@ extern "C" int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cst
   if (!a16(x, x_cstride, x_coff) || !a16(y, y_cstride, y_coff) || x_coff + C > x_cstride || y_coff + C > y_cstride)
     return fail(UB_EINVAL, "ub_avgpool2d: rows must be 16-byte aligned");
   const long long work = static_cast<long long>(N) * Ho * Wo * ((C + 7) / 8);
+  if (work >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_avgpool2d: tensor too large");
   const cudaError_t e = launch_pdl(avgpool2d_kernel, dim3(grid_for(work, 256, 2)), dim3(256), 0, stream,
                                    static_cast<const uint16_t*>(x), N, H, W, C, x_cstride, x_coff, k, s, pad, Ho, Wo,
                                    static_cast<uint16_t*>(y), y_cstride, y_coff);

@@ -1105,7 +1105,7 @@ class Engine:
             t = t.reshape(o.N, o.H, o.W, o.C).permute(0, 3, 1, 2)
         return t.float()
 
-    def autotune(self, reps: int = 3) -> dict[str, tuple]:
+    def autotune(self, reps: int = 5) -> dict[str, tuple]:
         """Pick, per conv layer, the read plan (fused gather vs covering slice) and the
         producer width (256 vs 512 cp.async threads) by timing every combination on this
         engine's own buffers (CUDA events, after a warm-up)."""

@@ -75,6 +75,11 @@ CASES = [
     ("halo_c256_w7_stack_n5", 5, 7, 7, 264, 8, 256, 200, 3, 1, 1, 0, True, False, True, False),
     ("halo_c128_w15_h20_wrap", 2, 20, 15, 128, 0, 128, 64, 3, 1, 1, 0, True, False, True, False),
     ("halo_c32_w31_tma_sw64", 2, 9, 31, 32, 0, 32, 48, 3, 1, 1, 0, True, False, False, False),
+    # padded width 128 (one output row per MMA tile): EfficientNetV2's 112-wide 3x3 stages
+    ("halo_wp128_c16_w112", 2, 6, 112, 24, 0, 12, 22, 3, 1, 1, 0, True, False, True, False),
+    ("halo_wp128_c32_w100_cout96", 2, 5, 100, 32, 0, 24, 96, 3, 1, 1, 0, True, False, False, False),
+    ("halo_wp128_c64_w112_slice", 1, 4, 112, 72, 8, 64, 64, 3, 1, 1, 0, True, False, True, False),
+    ("halo_wp128_c128_w70", 2, 3, 70, 128, 0, 128, 48, 3, 1, 1, 0, True, False, True, False),
     # stride-2 halo: 2x2 conv over the on-the-fly 2x2-folded input
     ("halo_s2_c64_w56", 2, 56, 56, 64, 0, 64, 64, 3, 2, 1, 0, True, False, True, False),
     ("halo_s2_c128_w28_cout100", 2, 28, 28, 128, 0, 128, 100, 3, 2, 1, 0, True, False, False, False),

@@ -26,6 +26,23 @@ if a[0] == "conv":
     y = K.empty_act(N, Ho, Wo, cout, dev)
     for _ in range(3):
         K.conv(x, wg, lead, cpad, cout, k, k, st, pad, y, relu=True, variant=var)
+elif a[0] == "dw":
+    N, H, C, k, st = map(int, a[1:6])
+    x = K.Act(torch.randn(N * H * H, K.pad8(C), generator=g).to(torch.bfloat16).to(dev), N, H, H, C, 0)
+    Ho = (H + 2 * (k // 2) - k) // st + 1
+    y = K.empty_act(N, Ho, Ho, C, dev)
+    wt = torch.randn(k * k, K.pad8(C), device=dev)
+    b = torch.randn(C, device=dev)
+    for _ in range(3):
+        K.dwconv(x, wt, b, k, st, k // 2, "silu", y)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(20):
+        K.dwconv(x, wt, b, k, st, k // 2, "silu", y)
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(f"dwconv N{N} {H}x{H} C{C} k{k} s{st}: {ev[0].elapsed_time(ev[1]) / 20 * 1e3:.1f} us")
 else:
     N, H, cs, width, n = map(int, a[1:6])
     x = K.Act(torch.randn(N * H * H, cs, generator=g).to(torch.bfloat16).to(dev), N, H, H, width, 0)
