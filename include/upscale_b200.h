@@ -228,6 +228,18 @@ int ub_conv_direct(const float* x, int N, int C, int H, int W, const int32_t* id
                    const float* bias, int cout, int k, int s, int pad, int act, void* y, int y_cstride, int y_coff,
                    cudaStream_t stream);
 
+/*
+ * A squeeze-excitation gate in one launch (one CTA per image): the global pool of x,
+ * fc1 = act1(W1 pooled + b1), gate = act2(W2 fc1 + b2) -- the PASS_THROUGH pool and the two
+ * CHANNEL_MIX layers (interp.py:57-63, 68-71) in front of an SE `mul`.  W1: bf16
+ * [C1][ldw1] over the pooled channels, W2: bf16 [C2][ldw2] over fc1's outputs (the layers'
+ * SLICE / GATHER reads folded in as zero columns; ldw multiples of 8, rows 16-byte
+ * aligned); b1/b2 fp32 nullable.  gate[n][g_coff + c] bf16.
+ */
+int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1, int C1,
+               const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2, int act2, void* gate,
+               int g_cstride, int g_coff, cudaStream_t stream);
+
 int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int s, int pad, int Ho,
                  int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 

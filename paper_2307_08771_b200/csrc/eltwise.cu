@@ -441,6 +441,94 @@ __global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restric
   }
 }
 
+
+// Squeeze-excitation gate in one launch (MobileNetV3 / EfficientNetV2): per image,
+//   pooled = mean_p x[n][p][:C]                       (PASS_THROUGH global pool)
+//   h      = act1(W1 pooled + b1)   W1: [C1][ldw1]     (CHANNEL_MIX fc1 + bias + ReLU/SiLU)
+//   gate   = act2(W2 h + b2)        W2: [C2][ldw2]     (CHANNEL_MIX fc2 + bias + hardsigmoid/sigmoid)
+// replacing three launches (pool, fc1, fc2) by one CTA per image.  The fc reads (SLICE /
+// GATHER of the pooled vector, of fc1's output) are folded into W1 / W2 as zero columns
+// on the host.  Pooled and hidden vectors live in shared memory (fp32); a warp per output
+// row streams its weight row with 16-byte loads.
+__global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict__ x, int HW, int C, int x_cstride,
+                                                      int x_coff, const uint16_t* __restrict__ w1, int ldw1, int C1,
+                                                      const float* __restrict__ b1, int act1,
+                                                      const uint16_t* __restrict__ w2, int ldw2, int C2,
+                                                      const float* __restrict__ b2, int act2,
+                                                      uint16_t* __restrict__ gate, int g_cstride, int g_coff) {
+  extern __shared__ float se_smem[];
+  const int C8 = (C + 7) / 8 * 8, C18 = (C1 + 7) / 8 * 8;
+  float* pooled = se_smem;            // [max(C8, ldw1)]
+  float* hidden = pooled + (ldw1 > C8 ? ldw1 : C8);  // [max(C18, ldw2)]
+  float* red = hidden + (ldw2 > C18 ? ldw2 : C18);   // [512 * 8] partial sums
+  const int n = blockIdx.x;
+  const int t = threadIdx.x;
+  griddep_wait();
+  griddep_launch_dependents();
+  // ---- pool: groups of 8 channels x pixel phases
+  const int G = C8 / 8;
+  const uint16_t* base = x + static_cast<long long>(n) * HW * x_cstride + x_coff;
+  for (int g0 = 0; g0 < G; g0 += 64) {
+    const int gb = min(64, G - g0);
+    const int phases = blockDim.x / gb;
+    const int g = t % gb, ph = t / gb;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (ph < phases) {
+      for (int p = ph; p < HW; p += phases) {
+        uint16_t v[8];
+        *reinterpret_cast<uint4*>(v) =
+            __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(p) * x_cstride + (g0 + g) * 8));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[t * 8 + j] = acc[j];
+    __syncthreads();
+    if (t < gb * 8) {
+      const int gg = t >> 3, j = t & 7;
+      float sum = 0.f;
+      for (int q = 0; q < phases; ++q) sum += red[(q * gb + gg) * 8 + j];
+      const int c = (g0 + gg) * 8 + j;
+      pooled[c] = c < C ? sum / static_cast<float>(HW) : 0.f;
+    }
+    __syncthreads();
+  }
+  for (int c = C8 + t; c < ldw1; c += blockDim.x) pooled[c] = 0.f;
+  __syncthreads();
+  const int warp = t >> 5, lane = t & 31, warps = blockDim.x >> 5;
+  // ---- fc1 (+ bias, act1): warp per hidden unit
+  for (int j = warp; j < C1; j += warps) {
+    const uint16_t* wr = w1 + static_cast<long long>(j) * ldw1;
+    float acc = 0.f;
+    for (int k = lane * 8; k < ldw1; k += 256) {
+      uint16_t wv[8];
+      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(bf(wv[e]), pooled[k + e], acc);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) hidden[j] = act_f(acc + (b1 ? b1[j] : 0.f), act1);
+  }
+  for (int j = C1 + t; j < (ldw2 > C18 ? ldw2 : C18); j += blockDim.x) hidden[j] = 0.f;
+  __syncthreads();
+  // ---- fc2 (+ bias, act2): warp per gate channel
+  for (int c = warp; c < C2; c += warps) {
+    const uint16_t* wr = w2 + static_cast<long long>(c) * ldw2;
+    float acc = 0.f;
+    for (int k = lane * 8; k < ldw2; k += 256) {
+      uint16_t wv[8];
+      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(bf(wv[e]), hidden[k + e], acc);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) gate[static_cast<long long>(n) * g_cstride + g_coff + c] = tobf(act_f(acc + (b2 ? b2[c] : 0.f), act2));
+  }
+}
+
 bool a16(const void* base, int cstride, int coff) {
   return base == nullptr || (aligned16(base) && (cstride & 7) == 0 && (coff & 7) == 0);
 }
@@ -572,4 +660,26 @@ extern "C" int ub_conv_direct(const float* x, int N, int C, int H, int W, const 
                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "conv_direct_kernel");
+}
+
+extern "C" int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1,
+                          int C1, const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2,
+                          int act2, void* gate, int g_cstride, int g_coff, cudaStream_t stream) {
+  if (!x || !w1 || !w2 || !gate || N < 1 || HW < 1 || C < 1 || C1 < 1 || C2 < 1 || act1 < UB_ACT_NONE ||
+      act1 > UB_ACT_SIGMOID || act2 < UB_ACT_NONE || act2 > UB_ACT_SIGMOID)
+    return fail(UB_EINVAL, "ub_se_gate: bad arguments");
+  if (!a16(x, x_cstride, x_coff) || x_coff + (C + 7) / 8 * 8 > x_cstride || (ldw1 & 7) || ldw1 < (C + 7) / 8 * 8 ||
+      (ldw2 & 7) || ldw2 < (C1 + 7) / 8 * 8 || (reinterpret_cast<uintptr_t>(w1) & 15) ||
+      (reinterpret_cast<uintptr_t>(w2) & 15) || g_coff + C2 > g_cstride)
+    return fail(UB_EINVAL, "ub_se_gate: rows must be 16-byte aligned / weight rows too short");
+  const int C8 = (C + 7) / 8 * 8, C18 = (C1 + 7) / 8 * 8;
+  const size_t smem = (static_cast<size_t>(ldw1 > C8 ? ldw1 : C8) + (ldw2 > C18 ? ldw2 : C18) + 512 * 8) * 4;
+  if (smem > 200 * 1024) return fail(UB_EUNSUPPORTED, "ub_se_gate: vectors too wide");
+  if (const cudaError_t ae = ensure_max_smem(se_gate_kernel)) return cuda_status(ae, "se_gate attr");
+  const cudaError_t e = launch_pdl(se_gate_kernel, dim3(N), dim3(512), smem, stream, static_cast<const uint16_t*>(x),
+                                   HW, C, x_cstride, x_coff, static_cast<const uint16_t*>(w1), ldw1, C1, b1, act1,
+                                   static_cast<const uint16_t*>(w2), ldw2, C2, b2, act2, static_cast<uint16_t*>(gate),
+                                   g_cstride, g_coff);
+  count_launch();
+  return cuda_status(e, "se_gate_kernel");
 }

@@ -65,7 +65,8 @@ class Engine:
     def __init__(self, graph: ModelGraph, specs: Mapping, weight_source, vector_source, batch: int,
                  input_chw=(3, 224, 224), device="cuda", gather_mode: str = "fused", fuse_stem: bool = True,
                  stem_s2d: bool = True, stem_pool: bool = True, cover_ratio: float = 2.5,
-                 dual_store: bool = False, stem_pack_fused: bool = False, pool_gather: bool = True):
+                 dual_store: bool = False, stem_pack_fused: bool = False, pool_gather: bool = True,
+                 se_fuse: bool = True):
         assert gather_mode in ("fused", "copy")
         self.fuse_stem = fuse_stem
         self.stem_s2d = stem_s2d
@@ -74,6 +75,7 @@ class Engine:
         self.dual_store = dual_store
         self.stem_pack_fused = stem_pack_fused
         self.pool_gather = pool_gather
+        self.se_fuse = se_fuse
         self.graph = graph
         # nodes the reference's apply_plan adds (join-rewrite ADD / CONCAT runs, SLICE / GATHER
         # reads) carry no spatial spec: they get the plain op of their kind
@@ -379,6 +381,11 @@ class Engine:
                     sop.output = mp.output
                     ops.remove(mp)
 
+        # --- squeeze-excitation gate: global pool -> fc1 (+bias, act) -> fc2 (+bias, act) whose
+        # only reader is an SE `mul` becomes ONE launch (ub_se_gate, one CTA per image)
+        if self.se_fuse:
+            self._fuse_se(ops, base, kinds)
+
         # --- global avg pool -> GATHER read fusion: when a pool's only reader is a conv that
         # GATHERs its channels (ResNet: avgpool -> flatten -> fc.read -> fc), the pool writes
         # the gathered channels compacted (ub_avgpool_gather) and the conv reads them densely
@@ -442,6 +449,90 @@ class Engine:
             getattr(self, f"_bind_{op.kind}")(op, weight_source, vector_source, output_feed)
         out_id = next(lid for lid in topo if kinds[lid] is LayerKind.OUTPUT)
         self.output_value = self._value(out_id)
+
+    def _fuse_se(self, ops, base, kinds) -> None:
+        def readers(v):
+            return [o for o in ops if any(base(i) == v for i in o.inputs)]
+
+        for pop in [o for o in ops if o.kind == "avgpool" and "idx" not in o.info]:
+            r1 = readers(pop.output)
+            if len(r1) != 1 or r1[0].kind != "conv":
+                continue
+            a = r1[0]
+            r2 = readers(a.output)
+            if len(r2) != 1 or r2[0].kind != "conv":
+                continue
+            b = r2[0]
+            r3 = readers(b.output)
+            if not r3 or any(o.kind != "eltwise" or self.specs.get(o.anchor) is None or
+                             self.specs[o.anchor].op != "mul" for o in r3):
+                continue
+            ok = all(c.info.get(k) is None for c in (a, b) for k in ("residual", "prologue", "pool2"))
+            ok = ok and all(self.specs[c.info["conv"]].op in ("conv", "linear") and
+                            (self.specs[c.info["conv"]].op == "linear" or
+                             (self.specs[c.info["conv"]].kernel, self.specs[c.info["conv"]].stride) == (1, 1))
+                            for c in (a, b))
+            ok = ok and base(a.info["src"]) == pop.output and base(b.info["src"]) == a.output
+            if not ok:
+                continue
+            se = _Op("se", pop.anchor, list(pop.inputs), b.output, info={"pool": pop, "fc1": a, "fc2": b})
+            idx = ops.index(pop)
+            for o in (pop, a, b):
+                ops.remove(o)
+            ops.insert(idx, se)
+
+    def _linear_dense(self, op, ws, vs, src_width: int):
+        """A 1x1 CHANNEL_MIX over an [N, C, 1, 1] value as a dense fp32 matrix over ALL of its
+        source's channels (its SLICE / GATHER read folded in as zero columns), with the BN
+        scale folded into the rows; returns (W [O, src_width], bias [O] or None, act code)."""
+        info = op.info
+        lid = info["conv"]
+        W, rows, cols = ws(lid)
+        Wf = W.detach().float().cpu()[:, :, 0, 0]
+        O, I = Wf.shape
+        rows = list(rows if rows is not None else range(O))
+        cols = list(cols if cols is not None else range(I))
+        read = info["read"]
+        if read is None:
+            src = list(range(len(cols)))
+        else:
+            rl = self.graph.layer(read)
+            src = list(range(rl.params[0], rl.params[0] + rl.params[1])) if rl.kind is LayerKind.SLICE \
+                else list(rl.params)
+        Wd = torch.zeros(len(rows), src_width)
+        for k, (c, s_) in enumerate(zip(cols, src)):
+            if c >= 0 and s_ >= 0:
+                Wd[:, s_] += torch.where(torch.tensor(rows) >= 0, Wf[torch.tensor(rows).clamp_min(0), c], 0.0)
+        scale = bias = None
+        if info["bn"] is not None:
+            vec, perm = vs(info["bn"])
+            scale, bias = self._affine(info["bn"], vec, perm)
+            if self.specs[info["bn"]].op == "bn":
+                Wd = Wd * scale.cpu().view(-1, 1)
+        return Wd, bias, self._act_code(info["relu"])
+
+    def _bind_se(self, op, ws, vs, output_feed):
+        x = self._value(op.inputs[0])
+        assert x.cmap is None, "SE pool over a column-mapped value"
+        a, b = op.info["fc1"], op.info["fc2"]
+        C = x.C
+        W1, b1, act1 = self._linear_dense(a, ws, vs, C)
+        C1 = W1.shape[0]
+        W2, b2, act2 = self._linear_dense(b, ws, vs, C1)
+        C2 = W2.shape[0]
+
+        def pack(Wd):
+            t = torch.zeros(Wd.shape[0], K.pad8(Wd.shape[1]), dtype=torch.bfloat16)
+            t[:, :Wd.shape[1]] = Wd.to(torch.bfloat16)
+            t = t.to(self.device).contiguous()
+            self._keep.append(t)
+            return t
+
+        w1, w2 = pack(W1), pack(W2)
+        gate = self._alloc(b.info["out"], C2)
+        xd = self._dense(x)
+        op.launch = lambda: K.se_gate(xd, w1, C1, b1, act1, w2, C2, b2, act2, gate)
+        self.conv_stats.append(ConvStats(f"{op.anchor}(se)", 0.0, 2.0 * C * x.H * x.W, 0.0))
 
     def _plan_concats(self, ops, alias, base, pos, output_feed) -> None:
         """CONCAT as buffer planning: each operand's producer stores its
@@ -1183,7 +1274,7 @@ class Engine:
                 "avgpool": "avgpool_gather_kernel" if "idx" in op.info else (
                     "avgpool_split_kernel" if op.info.get("split") else "avgpool_kernel"),
                 "eltwise": "eltwise_kernel", "dwconv": "dwconv_kernel", "avgpool2d": "avgpool2d_kernel",
-                "concat": "gather_rows_kernel"}.get(op.kind, op.kind)
+                "concat": "gather_rows_kernel", "se": "se_gate_kernel"}.get(op.kind, op.kind)
 
     def per_image_work(self) -> tuple[float, float]:
         f = sum(c.flops for c in self.conv_stats)

@@ -343,6 +343,13 @@ def conv_direct(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, bi
               pad, act, _p(y.buf), y.cstride, y.coff, _stream())
 
 
+def se_gate(x: Act, w1: torch.Tensor, C1: int, b1, act1: int, w2: torch.Tensor, C2: int, b2, act2: int,
+            gate: Act) -> None:
+    """ub_se_gate: pool + fc1 + fc2 of a squeeze-excitation block; w1 [C1, ldw1], w2 [C2, ldw2] bf16."""
+    _lib.call("ub_se_gate", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(w1), w1.shape[1], C1, _p(b1), act1,
+              _p(w2), w2.shape[1], C2, _p(b2), act2, _p(gate.buf), gate.cstride, gate.coff, _stream())
+
+
 def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:
     _lib.call("ub_avgpool2d", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, k, stride, pad, y.H, y.W,
               _p(y.buf), y.cstride, y.coff, _stream())

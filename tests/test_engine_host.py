@@ -115,3 +115,17 @@ def test_densenet121_concats_are_zero_copy_bands(stub_kernels, dn121, strategy):
     for op in eng.ops:
         done.add(op.output)
     assert eng.output_value.C == 1000
+
+
+def test_mobilenet_se_blocks_fuse_into_one_launch(stub_kernels):
+    """Config 2: each squeeze-excitation block (global pool -> fc1 -> fc2 -> mul) runs its
+    gate as ONE ub_se_gate launch; depthwise convs absorb their BN + activation."""
+    sm = build_spatial_model(CONFIGS["mobilenet_v3_small_s50"])
+    plans = P.load_plans(CONFIGS["mobilenet_v3_small_s50"].asset_dir / "plans_reorder.json")
+    eg = E.export_graph(sm.graph, plans)
+    eng = EN.from_plans(sm, eg, E.compose_maps(sm.graph, plans), batch=1, device="cpu")
+    kinds = [op.kind for op in eng.ops]
+    assert kinds.count("se") == 9 and kinds.count("dwconv") == 11
+    assert kinds.count("avgpool") == 1  # the classifier's pool only
+    assert all(op.info.get("bn") is not None for op in eng.ops if op.kind == "dwconv")
+    assert len(eng.ops) == 55

@@ -750,3 +750,33 @@ def test_conv_direct(cin, k, s, cout, act):
            "silu": torch.nn.functional.silu}
     ref = fns[act](torch.nn.functional.conv2d(x[:, idx], Wt, b, stride=s, padding=pad))
     assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("N,H,C,C1,C2,acts", [(1, 56, 16, 8, 16, ("relu", "hardsigmoid")),
+                                              (3, 14, 730, 48, 730, ("silu", "sigmoid")),
+                                              (2, 7, 576, 144, 570, ("relu", "hardsigmoid"))])
+def test_se_gate(N, H, C, C1, C2, acts):
+    """ub_se_gate (pool + fc1 + fc2 in one launch) vs torch fp32 on the bf16 operands."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(C + C1)
+    x = torch.randn(N, C, H, H, generator=g)
+    W1 = torch.randn(C1, C, generator=g) / C ** 0.5
+    W2 = torch.randn(C2, C1, generator=g) / C1 ** 0.5
+    b1, b2 = torch.randn(C1, generator=g), torch.randn(C2, generator=g)
+
+    def pack(W):
+        t = torch.zeros(W.shape[0], (W.shape[1] + 7) // 8 * 8, dtype=torch.bfloat16)
+        t[:, :W.shape[1]] = W.to(torch.bfloat16)
+        return t.to(dev)
+
+    xa = K.act_from_nchw(x.to(dev))
+    gate = K.empty_act(N, 1, 1, C2, dev)
+    K.se_gate(xa, pack(W1), C1, b1.to(dev), _lib.UB_ACT[acts[0]], pack(W2), C2, b2.to(dev), _lib.UB_ACT[acts[1]],
+              gate)
+    torch.cuda.synchronize()
+    fns = {"relu": torch.relu, "silu": torch.nn.functional.silu, "sigmoid": torch.sigmoid,
+           "hardsigmoid": torch.nn.functional.hardsigmoid}
+    pooled = _bf(x).mean(dim=(2, 3))
+    h = fns[acts[0]](pooled @ _bf(W1).t() + b1)
+    ref = fns[acts[1]](h @ _bf(W2).t() + b2)
+    assert _rel(gate.to_nchw().cpu().reshape(N, C2), ref) < 1e-2
