@@ -450,22 +450,58 @@ __global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restric
 // GATHER of the pooled vector, of fc1's output) are folded into W1 / W2 as zero columns
 // on the host.  Pooled and hidden vectors live in shared memory (fp32); a warp per output
 // row streams its weight row with 16-byte loads.
+// Dot products of RPW weight rows (bf16, 16-byte aligned, ld multiple of 8) with the fp32
+// vector v (shared memory) by one warp: all rows' loads are issued before the FMAs.
+template <int RPW>
+__device__ __forceinline__ void warp_rows_dot(const uint16_t* __restrict__ w, int ld, int row0, int nrows,
+                                              const float* v, int lane, float* out) {
+  float acc[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) acc[r] = 0.f;
+  for (int k = lane * 8; k < ld; k += 256) {
+    uint16_t wv[RPW][8];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      if (row0 + r < nrows)
+        *reinterpret_cast<uint4*>(wv[r]) =
+            __ldg(reinterpret_cast<const uint4*>(w + static_cast<long long>(row0 + r) * ld + k));
+      else
+        *reinterpret_cast<uint4*>(wv[r]) = make_uint4(0, 0, 0, 0);
+    }
+    float xv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xv[e] = v[k + e];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r] = fmaf(bf(wv[r][e]), xv[e], acc[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], d);
+    out[r] = acc[r];
+  }
+}
+
 __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict__ x, int HW, int C, int x_cstride,
                                                       int x_coff, const uint16_t* __restrict__ w1, int ldw1, int C1,
                                                       const float* __restrict__ b1, int act1,
                                                       const uint16_t* __restrict__ w2, int ldw2, int C2,
                                                       const float* __restrict__ b2, int act2,
                                                       uint16_t* __restrict__ gate, int g_cstride, int g_coff) {
+  constexpr int RPW = 8;  // weight rows per warp step (loads in flight)
   extern __shared__ float se_smem[];
   const int C8 = (C + 7) / 8 * 8, C18 = (C1 + 7) / 8 * 8;
   float* pooled = se_smem;            // [max(C8, ldw1)]
   float* hidden = pooled + (ldw1 > C8 ? ldw1 : C8);  // [max(C18, ldw2)]
   float* red = hidden + (ldw2 > C18 ? ldw2 : C18);   // [512 * 8] partial sums
   const int n = blockIdx.x;
+  const int split = blockIdx.y, nsplit = gridDim.y;  // gate channels are split over nsplit CTAs
   const int t = threadIdx.x;
   griddep_wait();
   griddep_launch_dependents();
-  // ---- pool: groups of 8 channels x pixel phases
+  // ---- pool: groups of 8 channels x pixel phases (4 independent loads in flight per thread)
   const int G = C8 / 8;
   const uint16_t* base = x + static_cast<long long>(n) * HW * x_cstride + x_coff;
   for (int g0 = 0; g0 < G; g0 += 64) {
@@ -474,10 +510,23 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
     const int g = t % gb, ph = t / gb;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (ph < phases) {
-      for (int p = ph; p < HW; p += phases) {
+      const uint16_t* col = base + (g0 + g) * 8;
+      int p = ph;
+      for (; p + 3 * phases < HW; p += 4 * phases) {
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          q[u] = __ldg(reinterpret_cast<const uint4*>(col + static_cast<long long>(p + u * phases) * x_cstride));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint16_t* v = reinterpret_cast<const uint16_t*>(&q[u]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+        }
+      }
+      for (; p < HW; p += phases) {
         uint16_t v[8];
-        *reinterpret_cast<uint4*>(v) =
-            __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(p) * x_cstride + (g0 + g) * 8));
+        *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(col + static_cast<long long>(p) * x_cstride));
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
       }
@@ -497,35 +546,34 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
   for (int c = C8 + t; c < ldw1; c += blockDim.x) pooled[c] = 0.f;
   __syncthreads();
   const int warp = t >> 5, lane = t & 31, warps = blockDim.x >> 5;
-  // ---- fc1 (+ bias, act1): warp per hidden unit
-  for (int j = warp; j < C1; j += warps) {
-    const uint16_t* wr = w1 + static_cast<long long>(j) * ldw1;
-    float acc = 0.f;
-    for (int k = lane * 8; k < ldw1; k += 256) {
-      uint16_t wv[8];
-      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+  // ---- fc1 (+ bias, act1): RPW hidden units per warp step
+  for (int j0 = warp * RPW; j0 < C1; j0 += warps * RPW) {
+    float o[RPW];
+    warp_rows_dot<RPW>(w1, ldw1, j0, C1, pooled, lane, o);
+    if (lane < RPW && j0 + lane < C1) {
+      float v = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(bf(wv[e]), pooled[k + e], acc);
+      for (int r = 0; r < RPW; ++r)
+        if (r == lane) v = o[r];
+      hidden[j0 + lane] = act_f(v + (b1 ? b1[j0 + lane] : 0.f), act1);
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if (lane == 0) hidden[j] = act_f(acc + (b1 ? b1[j] : 0.f), act1);
   }
   for (int j = C1 + t; j < (ldw2 > C18 ? ldw2 : C18); j += blockDim.x) hidden[j] = 0.f;
   __syncthreads();
-  // ---- fc2 (+ bias, act2): warp per gate channel
-  for (int c = warp; c < C2; c += warps) {
-    const uint16_t* wr = w2 + static_cast<long long>(c) * ldw2;
-    float acc = 0.f;
-    for (int k = lane * 8; k < ldw2; k += 256) {
-      uint16_t wv[8];
-      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+  // ---- fc2 (+ bias, act2): this CTA's share of the gate channels, RPW per warp step
+  const int per = (C2 + nsplit - 1) / nsplit;
+  const int c_lo = split * per, c_hi = min(C2, c_lo + per);
+  for (int c0 = c_lo + warp * RPW; c0 < c_hi; c0 += warps * RPW) {
+    float o[RPW];
+    warp_rows_dot<RPW>(w2, ldw2, c0, c_hi, hidden, lane, o);
+    if (lane < RPW && c0 + lane < c_hi) {
+      float v = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(bf(wv[e]), hidden[k + e], acc);
+      for (int r = 0; r < RPW; ++r)
+        if (r == lane) v = o[r];
+      gate[static_cast<long long>(n) * g_cstride + g_coff + c0 + lane] =
+          tobf(act_f(v + (b2 ? b2[c0 + lane] : 0.f), act2));
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if (lane == 0) gate[static_cast<long long>(n) * g_cstride + g_coff + c] = tobf(act_f(acc + (b2 ? b2[c] : 0.f), act2));
   }
 }
 
@@ -676,7 +724,12 @@ extern "C" int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, in
   const size_t smem = (static_cast<size_t>(ldw1 > C8 ? ldw1 : C8) + (ldw2 > C18 ? ldw2 : C18) + 512 * 8) * 4;
   if (smem > 200 * 1024) return fail(UB_EUNSUPPORTED, "ub_se_gate: vectors too wide");
   if (const cudaError_t ae = ensure_max_smem(se_gate_kernel)) return cuda_status(ae, "se_gate attr");
-  const cudaError_t e = launch_pdl(se_gate_kernel, dim3(N), dim3(512), smem, stream, static_cast<const uint16_t*>(x),
+  // few images: split the gate channels over several CTAs per image (each recomputes the
+  // cheap pool + fc1) so the fc2 weight stream is spread over more SMs
+  int nsplit = num_sms() / N;
+  nsplit = nsplit < 1 ? 1 : (nsplit > 16 ? 16 : nsplit);
+  if (nsplit > (C2 + 63) / 64) nsplit = (C2 + 63) / 64;
+  const cudaError_t e = launch_pdl(se_gate_kernel, dim3(N, nsplit), dim3(512), smem, stream, static_cast<const uint16_t*>(x),
                                    HW, C, x_cstride, x_coff, static_cast<const uint16_t*>(w1), ldw1, C1, b1, act1,
                                    static_cast<const uint16_t*>(w2), ldw2, C2, b2, act2, static_cast<uint16_t*>(gate),
                                    g_cstride, g_coff);
