@@ -453,6 +453,112 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
   cp_async_wait<0>();
 }
 
+// Wide outputs (more than 256 gathered channels, DenseNet blocks 3-4): one pixel per warp
+// step; lane l owns outputs l, l+32, ... so the per-output tables (source column, BN scale
+// and shift) are read from shared memory conflict-free and consecutive lanes gather from
+// nearby (ascending) source columns -- distinct banks; 2-byte stores of consecutive lanes
+// coalesce.  (Owning 8 consecutive outputs per lane put lanes 32 bytes apart: 4-way bank
+// conflicts, ncu L1 88 %.)
+template <bool AFFINE, int MPL>  // MPL > 0: the lane's <= MPL (column, scale, shift) triples live in registers
+__global__ void __launch_bounds__(256) gather_rows_wide_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
+                                                               int win16, const int32_t* __restrict__ idx, int n_idx,
+                                                               int rel, int n8, long long npix,
+                                                               const float* __restrict__ scale,
+                                                               const float* __restrict__ shift, int relu,
+                                                               uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+  constexpr int STAGES = 3;
+  extern __shared__ __align__(16) uint8_t g_smem[];
+  int32_t* s_col = reinterpret_cast<int32_t*>(g_smem);
+  float* s_sc = reinterpret_cast<float*>(g_smem + n8 * 4);
+  float* s_sh = s_sc + n8;
+  const int par_bytes = MPL > 0 ? 0 : (((AFFINE ? 3 : 1) * n8 * 4 + 15) & ~15);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const int stage_bytes = win16 * 16;
+  uint8_t* buf0 = g_smem + par_bytes + static_cast<size_t>(warp) * STAGES * stage_bytes;
+  constexpr int R = MPL > 0 ? MPL : 1;
+  int rcol[R];
+  float rsc[R], rsh[R];
+  if (MPL > 0) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int c = lane + 32 * m;
+      const int a = c < n_idx ? __ldg(idx + c) : -1;
+      rcol[m] = a >= 0 ? a + rel : -1;
+      rsc[m] = (AFFINE && c < n_idx) ? __ldg(scale + c) : 0.f;
+      rsh[m] = (AFFINE && c < n_idx) ? __ldg(shift + c) : 0.f;
+    }
+  } else {
+    for (int c = threadIdx.x; c < n8; c += blockDim.x) {
+      const int a = c < n_idx ? __ldg(idx + c) : -1;
+      s_col[c] = a >= 0 ? a + rel : -1;
+      if (AFFINE) {
+        s_sc[c] = c < n_idx ? __ldg(scale + c) : 0.f;
+        s_sh[c] = c < n_idx ? __ldg(shift + c) : 0.f;
+      }
+    }
+    __syncthreads();
+  }
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long step = static_cast<long long>(gridDim.x) * warps;
+  auto issue = [&](long long p, uint8_t* dst) {
+    const uint16_t* src = x + static_cast<size_t>(p) * x_cstride + ws;
+    for (int j = lane; j < win16; j += 32) cp_async16(dst + j * 16, src + j * 8, 16);
+  };
+  long long p = static_cast<long long>(blockIdx.x) * warps + warp;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (p + st * step < npix) issue(p + st * step, buf0 + st * stage_bytes);
+    cp_async_commit();
+  }
+  int k = 0;
+  for (; p < npix; p += step, k = (k + 1 == STAGES ? 0 : k + 1)) {
+    const long long pn = p + (STAGES - 1) * step;
+    if (pn < npix) issue(pn, buf0 + ((k + STAGES - 1) % STAGES) * stage_bytes);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncwarp();
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(buf0 + k * stage_bytes);
+    uint16_t* yr = y + static_cast<size_t>(p) * y_cstride + y_coff;
+    if (MPL > 0) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int c = lane + 32 * m;
+        if (c >= n8) break;
+        const int cj = rcol[m];
+        const uint16_t raw = cj >= 0 ? row[cj] : uint16_t(0);
+        uint16_t h = raw;
+        if (AFFINE) {
+          float v = 0.f;
+          if (cj >= 0) {
+            v = fmaf(rsc[m], __uint_as_float(static_cast<uint32_t>(raw) << 16), rsh[m]);
+            if (relu) v = fmaxf(v, 0.f);
+          }
+          h = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        }
+        yr[c] = h;
+      }
+    } else {
+      for (int c = lane; c < n8; c += 32) {
+        const int cj = s_col[c];
+        uint16_t h = cj >= 0 ? row[cj] : uint16_t(0);
+        if (AFFINE) {
+          float v = 0.f;
+          if (cj >= 0) {
+            v = fmaf(s_sc[c], __uint_as_float(static_cast<uint32_t>(h) << 16), s_sh[c]);
+            if (relu) v = fmaxf(v, 0.f);
+          }
+          h = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        }
+        yr[c] = h;
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------- input staging
 // NCHW fp32 -> NHWC bf16 (channel-gathered), zero-filling the padded channels.
 __global__ void stage_input_kernel(const float* __restrict__ x, int N, int C, int HW, const int32_t* __restrict__ idx,
@@ -851,6 +957,31 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   const int ws = (x_coff + lo) & ~7;
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
+  if (!pool2 && stride == 1 && n8 > 256 && win16 <= 256) {  // wide outputs: lane-interleaved ownership
+    const bool regs = n8 <= 32 * 24;  // the lane's tables in registers
+    const size_t par = regs ? 0 : ((affine ? 3 : 1) * static_cast<size_t>(n8) * 4 + 15) & ~static_cast<size_t>(15);
+    const size_t stage_w = static_cast<size_t>(win16) * 16;
+    int ww = 8;
+    while (ww > 1 && par + ww * 3 * stage_w > 200 * 1024) ww >>= 1;
+    const size_t smem_w = par + ww * 3 * stage_w;
+    void (*kw)(const uint16_t*, int, int, int, const int32_t*, int, int, int, long long, const float*, const float*,
+               int, uint16_t*, int, int) =
+        regs ? (affine ? gather_rows_wide_kernel<true, 24> : gather_rows_wide_kernel<false, 24>)
+             : (affine ? gather_rows_wide_kernel<true, 0> : gather_rows_wide_kernel<false, 0>);
+    if (const cudaError_t ae = ensure_max_smem(kw)) return cuda_status(ae, "gather_rows_wide attr");
+    const long long npix_w = static_cast<long long>(N) * H * W;
+    int per_sm = static_cast<int>((227 * 1024) / (smem_w + 1024));
+    if (per_sm > 2048 / (32 * ww)) per_sm = 2048 / (32 * ww);
+    if (per_sm < 1) per_sm = 1;
+    const long long want = (npix_w + ww - 1) / ww;
+    const long long cap = static_cast<long long>(num_sms()) * per_sm;
+    const int grid = static_cast<int>(want < cap ? want : cap);
+    const cudaError_t e = launch_pdl(kw, dim3(grid), dim3(32 * ww), smem_w, stream, static_cast<const uint16_t*>(x),
+                                     x_cstride, ws, win16, idx, n_idx, x_coff - ws, n8, npix_w, scale, shift, relu,
+                                     static_cast<uint16_t*>(y), y_cstride, y_coff);
+    count_launch();
+    return cuda_status(e, "gather_rows_wide_kernel");
+  }
   if (!pool2 && stride == 1 && n8 <= 1024) {  // fast form: fixed per-lane ownership of output groups
     const int groups = n8 / 8;
     const int gj = groups <= 32 ? 1 : (groups + 31) / 32;

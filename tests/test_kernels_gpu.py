@@ -780,3 +780,27 @@ def test_se_gate(N, H, C, C1, C2, acts):
     h = fns[acts[0]](pooled @ _bf(W1).t() + b1)
     ref = fns[acts[1]](h @ _bf(W2).t() + b2)
     assert _rel(gate.to_nchw().cpu().reshape(N, C2), ref) < 1e-2
+
+
+@pytest.mark.parametrize("width,n,affine", [(1016, 496, True), (600, 300, False), (2040, 1500, True)])
+def test_gather_rows_wide(width, n, affine):
+    """ub_gather_rows_ex with more than 256 gathered channels (the lane-interleaved form)."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(width + n)
+    N, H, cs = 2, 5, (width + 7) // 8 * 8
+    x = torch.randn(N, cs, H, H, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    idx = sorted(torch.randperm(width, generator=g)[:n].tolist())
+    idx[5] = -1
+    sc, sh = 0.5 + torch.rand(n, generator=g), torch.randn(n, generator=g)
+    y = K.empty_act(N, H, H, n, dev)
+    K.gather_rows_ex(xa, torch.tensor(idx, dtype=torch.int32, device=dev), K.gather_window(idx), 1, y,
+                     scale=sc.to(dev) if affine else None, shift=sh.to(dev) if affine else None, relu=affine)
+    torch.cuda.synchronize()
+    ref = torch.zeros(N, n, H, H)
+    for i, j in enumerate(idx):
+        if j >= 0:
+            v = _bf(x[:, j])
+            ref[:, i] = (sc[i] * v + sh[i]).clamp_min(0) if affine else v
+    got = y.to_nchw().cpu()
+    assert (got - ref).abs().max() <= 1e-2 * ref.abs().max()
