@@ -28,6 +28,7 @@ from .configs import CONFIGS, Config, build_spatial_model
 from .lowering import SpatialModel
 
 plan_model = E.plan_model
+apply_plan = E.apply_plan
 
 
 @dataclass

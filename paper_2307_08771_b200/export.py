@@ -164,6 +164,33 @@ def export_weights(graph: ModelGraph, weights: Mapping[str, torch.Tensor],
     return ew
 
 
+def apply_plan(plan: SegmentPlan, graph: ModelGraph, weights: ExportedWeights) -> tuple[ModelGraph, ExportedWeights]:
+    """planner.py:648-796 with the reference's signature, on 4-D device weights.
+
+    The graph half is the reference's own `apply_plan`; the weight half permutes, on the
+    GPU, exactly the tensors this plan touches (its producers' rows, its consumers'
+    columns, its per-channel vectors).  Pure, like the reference (planner.py:655): the
+    input `weights` is not modified; untouched tensors are shared with the result."""
+    from . import kernels as K
+
+    g_out = export_graph(graph, [plan])
+    maps = compose_maps(graph, [plan])
+    new = ExportedWeights(mix=dict(weights.mix), vec={k: dict(v) for k, v in weights.vec.items()})
+    for lid in sorted(set(maps.rows) | set(maps.cols)):
+        W = weights.mix[lid]
+        O, I = W.shape[0], W.shape[1]
+        new.mix[lid] = K.permute_weights(W.contiguous(), maps.rows.get(lid, range(O)), maps.cols.get(lid, range(I)),
+                                         out_dtype=W.dtype)
+    for uid, perm in maps.vec.items():
+        if uid in weights.vec:
+            new.vec[uid] = {n: K.permute_vector(t.contiguous(), perm) for n, t in weights.vec[uid].items()}
+    from . import _lib
+    bad = _lib.index_faults()
+    if bad:
+        raise ValidationError([f"plan {plan.segment}: {bad} indices outside their source tensors"])
+    return g_out, new
+
+
 def export_model(graph: ModelGraph, weights: Mapping[str, torch.Tensor],
                  vectors: Mapping[str, Mapping[str, torch.Tensor]] | None, masks: ChannelMask,
                  mode: str = MODE_INPUT, strategy: str = STRATEGY_REORDER, on_unsupported: str = "error",

@@ -213,3 +213,23 @@ def test_depthwise_se_models_match_oracle(cfg_name, strategy):
     assert torch.isfinite(got).all()
     assert deviation(got, ref) <= TOL, deviation(got, ref)
     assert top1_agreement(got, ref) == 1.0
+
+
+def test_apply_plan_twin_sequential_equals_export_model():
+    """export.apply_plan (the reference's signature, 4-D device weights) applied plan by plan
+    gives the same graph and bit-identical weights as the composed one-pass export."""
+    sm, plans, eg, maps = _setup("resnet50_s50", "reorder")
+    w64 = {k: t.double().cuda() for k, t in sm.weights.items()}
+    vec64 = {k: {n: t.double().cuda() for n, t in vv.items()} for k, vv in sm.vectors.items()}
+    res = E.export_model(sm.graph, w64, vec64, ir.load_masks(CONFIGS["resnet50_s50"].asset_dir / "masks.json"),
+                         plans=plans, out_dtype=torch.float64)
+    g, ew = sm.graph, E.ExportedWeights(mix=dict(w64), vec={k: dict(v) for k, v in vec64.items()})
+    for p in plans:
+        g, ew = E.apply_plan(p, g, ew)
+    assert ir.graph_to_dict(g) == ir.graph_to_dict(res.graph)
+    for lid, t in res.weights.mix.items():
+        assert torch.equal(ew.mix[lid], t), lid
+    for uid, named in res.weights.vec.items():
+        for n, t in named.items():
+            assert torch.equal(ew.vec[uid][n], t), (uid, n)
+    assert torch.equal(w64["conv1"], sm.weights["conv1"].double().cuda())  # inputs untouched

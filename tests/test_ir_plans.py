@@ -133,3 +133,16 @@ def test_reference_is_imported_unmodified():
         for f in ("graph.py", "planner.py", "pipeline.py", "interp.py"):
             here = Path(reslice.__file__).parent / f
             assert hashlib.sha256(here.read_bytes()).digest() == hashlib.sha256((src / f).read_bytes()).digest()
+
+
+def test_live_plan_model_reproduces_the_committed_plans():
+    """export.plan_model runs the reference planner itself (pipeline.py:99-132): on the
+    ResNet-18 config it reproduces the committed plan file byte for byte."""
+    from paper_2307_08771_b200.configs import CONFIGS
+
+    cfg = CONFIGS["resnet18_s50"]
+    g = ir.load_graph(cfg.asset_dir / "graph.json")
+    masks = ir.load_masks(cfg.asset_dir / "masks.json")
+    plans, fallbacks = E.plan_model(g, masks, "input", "reorder", "baseline")
+    want = P.load_plans(cfg.asset_dir / "plans_reorder.json")
+    assert [P.plan_to_dict(p) for p in sorted(plans, key=lambda p: p.segment)] == [P.plan_to_dict(p) for p in want]
