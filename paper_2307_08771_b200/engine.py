@@ -1121,9 +1121,10 @@ class Engine:
             op.launch = lambda: K.stem_s2d(self.input_buf, idx_dev, sbuf, wg, cout, kk, pd, y, bias=bias, relu=relu)
             op.info["stem_kind"] = "s2d"
             wbytes = 2.0 * wg.numel()
-        elif cin <= 8 and kk <= 7 and cout <= 256 and y.coff % 8 == 0 and y.cstride % 8 == 0:
-            # few input channels (MobileNetV3 / EfficientNetV2 3x3/s2 stems): direct conv on CUDA
-            # cores, the input read once (the im2col operand would be k*k times the input)
+        elif cin <= 8 and kk <= 3 and cout <= 256 and y.coff % 8 == 0 and y.cstride % 8 == 0:
+            # few input channels and a small filter (MobileNetV3 / EfficientNetV2 3x3/s2 stems):
+            # direct conv on CUDA cores, the input read once (the im2col operand would be k*k times
+            # the input); a 7x7 stem on 3 planes (ResNet at low sparsity) stays on the tensor cores
             Wf = W.detach().float().cpu()
             rr = torch.tensor([r_ for r_ in rows], dtype=torch.long)
             cc = torch.tensor([c_ for c_ in cols], dtype=torch.long)
