@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(256) gather_rows_fast_kernel(const uint16_t* _
 template <bool AFFINE, int MPL>  // MPL > 0: the lane's <= MPL (column, scale, shift) triples live in registers
 __global__ void __launch_bounds__(256) gather_rows_wide_kernel(const uint16_t* __restrict__ x, int x_cstride, int ws,
                                                                int win16, const int32_t* __restrict__ idx, int n_idx,
-                                                               int rel, int n8, long long npix,
-                                                               const float* __restrict__ scale,
+                                                               int rel, int n8, long long npix, int stride, int H,
+                                                               int W, int Ho, int Wo, const float* __restrict__ scale,
                                                                const float* __restrict__ shift, int relu,
                                                                uint16_t* __restrict__ y, int y_cstride, int y_coff) {
   constexpr int STAGES = 3;
@@ -503,7 +503,15 @@ __global__ void __launch_bounds__(256) gather_rows_wide_kernel(const uint16_t* _
   griddep_launch_dependents();
   const long long step = static_cast<long long>(gridDim.x) * warps;
   auto issue = [&](long long p, uint8_t* dst) {
-    const uint16_t* src = x + static_cast<size_t>(p) * x_cstride + ws;
+    long long sp = p;  // source pixel (a strided 1x1 conv reads every stride-th pixel)
+    if (stride != 1) {
+      const long long hw = static_cast<long long>(Ho) * Wo;
+      const long long n = p / hw;
+      const int r = static_cast<int>(p - n * hw);
+      const int yo = r / Wo, xo = r - (r / Wo) * Wo;
+      sp = (n * H + static_cast<long long>(yo) * stride) * W + static_cast<long long>(xo) * stride;
+    }
+    const uint16_t* src = x + static_cast<size_t>(sp) * x_cstride + ws;
     for (int j = lane; j < win16; j += 32) cp_async16(dst + j * 16, src + j * 8, 16);
   };
   long long p = static_cast<long long>(blockIdx.x) * warps + warp;
@@ -957,19 +965,20 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   const int ws = (x_coff + lo) & ~7;
   const int we = (x_coff + hi + 8) & ~7;
   const int win16 = (we - ws) / 8;
-  if (!pool2 && stride == 1 && n8 > 256 && win16 <= 256) {  // wide outputs: lane-interleaved ownership
+  if (!pool2 && n8 > 256 && win16 <= 256) {  // wide outputs: lane-interleaved ownership
     const bool regs = n8 <= 32 * 24;  // the lane's tables in registers
     const size_t par = regs ? 0 : ((affine ? 3 : 1) * static_cast<size_t>(n8) * 4 + 15) & ~static_cast<size_t>(15);
     const size_t stage_w = static_cast<size_t>(win16) * 16;
     int ww = 8;
     while (ww > 1 && par + ww * 3 * stage_w > 200 * 1024) ww >>= 1;
     const size_t smem_w = par + ww * 3 * stage_w;
-    void (*kw)(const uint16_t*, int, int, int, const int32_t*, int, int, int, long long, const float*, const float*,
-               int, uint16_t*, int, int) =
+    void (*kw)(const uint16_t*, int, int, int, const int32_t*, int, int, int, long long, int, int, int, int, int,
+               const float*, const float*, int, uint16_t*, int, int) =
         regs ? (affine ? gather_rows_wide_kernel<true, 24> : gather_rows_wide_kernel<false, 24>)
              : (affine ? gather_rows_wide_kernel<true, 0> : gather_rows_wide_kernel<false, 0>);
     if (const cudaError_t ae = ensure_max_smem(kw)) return cuda_status(ae, "gather_rows_wide attr");
-    const long long npix_w = static_cast<long long>(N) * H * W;
+    const int Ho_w = (H + stride - 1) / stride, Wo_w = (W + stride - 1) / stride;
+    const long long npix_w = static_cast<long long>(N) * Ho_w * Wo_w;
     int per_sm = static_cast<int>((227 * 1024) / (smem_w + 1024));
     if (per_sm > 2048 / (32 * ww)) per_sm = 2048 / (32 * ww);
     if (per_sm < 1) per_sm = 1;
@@ -977,8 +986,8 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
     const long long cap = static_cast<long long>(num_sms()) * per_sm;
     const int grid = static_cast<int>(want < cap ? want : cap);
     const cudaError_t e = launch_pdl(kw, dim3(grid), dim3(32 * ww), smem_w, stream, static_cast<const uint16_t*>(x),
-                                     x_cstride, ws, win16, idx, n_idx, x_coff - ws, n8, npix_w, scale, shift, relu,
-                                     static_cast<uint16_t*>(y), y_cstride, y_coff);
+                                     x_cstride, ws, win16, idx, n_idx, x_coff - ws, n8, npix_w, stride, H, W, Ho_w,
+                                     Wo_w, scale, shift, relu, static_cast<uint16_t*>(y), y_cstride, y_coff);
     count_launch();
     return cuda_status(e, "gather_rows_wide_kernel");
   }

@@ -782,8 +782,9 @@ def test_se_gate(N, H, C, C1, C2, acts):
     assert _rel(gate.to_nchw().cpu().reshape(N, C2), ref) < 1e-2
 
 
-@pytest.mark.parametrize("width,n,affine", [(1016, 496, True), (600, 300, False), (2040, 1500, True)])
-def test_gather_rows_wide(width, n, affine):
+@pytest.mark.parametrize("width,n,affine,stride", [(1016, 496, True, 1), (600, 300, False, 1), (2040, 1500, True, 1),
+                                                   (1016, 508, False, 2), (2040, 1020, False, 2)])
+def test_gather_rows_wide(width, n, affine, stride):
     """ub_gather_rows_ex with more than 256 gathered channels (the lane-interleaved form)."""
     dev = "cuda"
     g = torch.Generator().manual_seed(width + n)
@@ -793,14 +794,15 @@ def test_gather_rows_wide(width, n, affine):
     idx = sorted(torch.randperm(width, generator=g)[:n].tolist())
     idx[5] = -1
     sc, sh = 0.5 + torch.rand(n, generator=g), torch.randn(n, generator=g)
-    y = K.empty_act(N, H, H, n, dev)
-    K.gather_rows_ex(xa, torch.tensor(idx, dtype=torch.int32, device=dev), K.gather_window(idx), 1, y,
+    Ho = (H - 1) // stride + 1
+    y = K.empty_act(N, Ho, Ho, n, dev)
+    K.gather_rows_ex(xa, torch.tensor(idx, dtype=torch.int32, device=dev), K.gather_window(idx), stride, y,
                      scale=sc.to(dev) if affine else None, shift=sh.to(dev) if affine else None, relu=affine)
     torch.cuda.synchronize()
-    ref = torch.zeros(N, n, H, H)
+    ref = torch.zeros(N, n, Ho, Ho)
     for i, j in enumerate(idx):
         if j >= 0:
-            v = _bf(x[:, j])
+            v = _bf(x[:, j, ::stride, ::stride])
             ref[:, i] = (sc[i] * v + sh[i]).clamp_min(0) if affine else v
     got = y.to_nchw().cpu()
     assert (got - ref).abs().max() <= 1e-2 * ref.abs().max()
