@@ -314,8 +314,14 @@ def time_sharded(eng, driver, steps: int, warmup: int, world: int, dev, cuda: bo
         dist.barrier()
     clk = _Clock(cuda)
     clk.start()
+    if cuda:  # NVTX range: `ncu --nvtx --nvtx-include "timed/"` profiles exactly these launches
+        import torch
+
+        torch.cuda.nvtx.range_push("timed")
     for _ in range(steps):
         step()
+    if cuda:
+        torch.cuda.nvtx.range_pop()
     driver.drain()
     ms = clk.stop() / steps
     if world > 1:
