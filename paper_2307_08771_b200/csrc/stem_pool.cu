@@ -475,7 +475,7 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
     if (sl < 0) sl = getenv("UB_SP_SLEEP") ? atoi(getenv("UB_SP_SLEEP")) : 0;
     p.sleep_ns = sl;
   }
-  if (!getenv("UB_SP_TMA_STORE")) {  // direct stores (default); the TMA-store path stays for A/B
+  if (getenv("UB_SP_DIRECT_STORE")) {  // direct 2-byte stores; the TMA store is the default (88.8 -> 85.6 us, r2ak)
     p.y = static_cast<uint16_t*>(y) + y_coff;
     p.y_cstride = y_cstride;
   }

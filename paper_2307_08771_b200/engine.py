@@ -1227,7 +1227,7 @@ class Engine:
         autotune the conv variants first.  n_inputs > 1 allocates that many input
         buffers and captures one graph per buffer (double-buffered input for the
         pipelined Runner.run_many)."""
-        if autotune and self.batch >= 16:
+        if autotune and self.batch >= 16:  # at small batches eager timings are launch-bound noise
             self.launch_all()
             self.autotune()
         s = torch.cuda.Stream(device=self.device)
