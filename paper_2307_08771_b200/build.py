@@ -42,10 +42,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     build_dir.mkdir(exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               f"-I{ROOT / 'include'}", f"-I{CSRC}", "-Xptxas", "-v" if verbose else "-O3"]
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = build_dir / (Path(src).stem + ".o")
         cmd = common + ["-c", str(CSRC / src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units are independent: compile them concurrently (nvcc is single-threaded)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")

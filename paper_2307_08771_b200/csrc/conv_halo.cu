@@ -93,7 +93,9 @@ struct HaloGeom {
 // image (negative coordinates; stride 2 through element strides 2 on W and H) -- and the tap
 // shifts are whole rows of that swizzled block.  Otherwise 128 producer threads cp.async the
 // 16-byte channel planes.
-template <int WP, int PLANES, int MT, bool SB, int S, bool AT>
+// XA: the epilogue applies a UB_ACT_* activation other than ReLU (EfficientNetV2's SiLU);
+// a separate instantiation keeps the ReLU epilogue's code unchanged (as conv_tc's XACT).
+template <int WP, int PLANES, int MT, bool SB, int S, bool AT, bool XA>
 __global__ void __maxnreg__(96)
     conv_halo3_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmW,
                       const __grid_constant__ CUtensorMap tmX, const HaloParams p) {
@@ -502,7 +504,11 @@ __global__ void __maxnreg__(96)
             const float2 s3 = add_f32x2(make_float2(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])),
                                         make_float2(b1.z, b1.w));
             uint4 o;
-            if (p.relu) {
+            if (XA) {
+              const int a = p.relu;
+              o = make_uint4(cvt_bf16x2(act_f(s0.x, a), act_f(s0.y, a)), cvt_bf16x2(act_f(s1.x, a), act_f(s1.y, a)),
+                             cvt_bf16x2(act_f(s2.x, a), act_f(s2.y, a)), cvt_bf16x2(act_f(s3.x, a), act_f(s3.y, a)));
+            } else if (p.relu) {
               o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y), cvt_relu_bf16x2(s2.x, s2.y),
                              cvt_relu_bf16x2(s3.x, s3.y));
             } else {
@@ -543,8 +549,8 @@ long long* g_halo_trace = nullptr;
 int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream, bool* handled) {
   *handled = false;
   if (d->kh != 3 || d->kw != 3 || (d->stride != 1 && d->stride != 2) || d->pad != 1 || d->x_nchw_f32 ||
-      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8) || d->y2 || d->relu > 1)
-    return UB_OK;  // (activations other than ReLU: the generic kernel's XACT epilogue)
+      d->gather_idx || d->residual || d->y_dtype != UB_BF16 || (d->variant & 8) || d->y2)
+    return UB_OK;
   const int S = d->stride;
   if (cpad != 16 && cpad != 32 && cpad % 64 != 0) return UB_OK;
   if (S == 2 && (cpad % 64 != 0 || lead != 0)) return UB_OK;  // a folded plane = 8 channels of one pixel
@@ -641,10 +647,14 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
 
   const int grid = p.tiles < num_sms() ? p.tiles : num_sms();
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const HaloParams) = nullptr;
+  const bool xa = d->relu > 1;
   const bool sb = p.groups > 1;
 #define UB_HALO_CASE(WPV, PL, SBV, SV, ATV)                                                     \
   if (Wp == WPV && p.planes == PL && sb == SBV && S == SV && at == ATV)                         \
-    kern = mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV> : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV>;
+    kern = xa ? (mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV, true>                       \
+                         : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV, true>)                       \
+              : (mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV, false>                      \
+                         : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV, false>);
 #define UB_HALO_WP(WPV)                                                                                    \
   UB_HALO_CASE(WPV, 2, false, 1, false) UB_HALO_CASE(WPV, 4, false, 1, false)                              \
   UB_HALO_CASE(WPV, 4, false, 1, true) UB_HALO_CASE(WPV, 8, false, 1, false)                               \
