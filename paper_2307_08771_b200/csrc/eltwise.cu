@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(256) eltwise_kernel(ub_eltwise_desc d) {
   const uint16_t* g = static_cast<const uint16_t*>(d.gate);
   uint16_t* y = static_cast<uint16_t*>(d.y);
   // 32-bit index math (a 64-bit division costs ~100 instructions; totals stay < 2^31 here)
+#pragma unroll 2
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<unsigned>(total);
        e += gridDim.x * blockDim.x) {
     const unsigned pu = e / static_cast<unsigned>(groups);

@@ -948,18 +948,24 @@ class Engine:
         else:
             k_order = sorted(range(cin), key=lambda k: (gather[k], k))
             add_plan("gather", x, self._i32([gather[k] for k in k_order]), [cols[k] for k in k_order], cin)
-            if kk == 1 and pd == 0 and self.gather_mode == "fused":
-                ho, wo = (x.H - 1) // st + 1, (x.W - 1) // st + 1
+            if self.gather_mode == "fused":
+                # copy plan: compact the gathered channels (1x1 / pad 0: only the pixels a strided
+                # conv reads), then a dense conv -- for k x k convs the dense operand also makes
+                # the halo kernel eligible (it takes no fused gather)
+                st_g = st if (kk == 1 and pd == 0) else 1
+                ho, wo = (x.H - 1) // st_g + 1, (x.W - 1) // st_g + 1
+                k_order = sorted(range(cin), key=lambda k: (gather[k] < 0, gather[k], k))
+                g_sorted = [gather[k] for k in k_order]
                 scratch = K.empty_act(self.batch, ho, wo, cin, self.device)
                 self._keep.append(scratch.buf)
-                gdev = self._i32(list(gather))
+                gdev = self._i32(g_sorted)
+                win = K.gather_window(g_sorted)
 
-                win = K.gather_window(gather)
+                def pre(x=x, gdev=gdev, scratch=scratch, win=win, st_g=st_g):
+                    K.gather_rows(x, gdev, win, st_g, scratch)
 
-                def pre(x=x, gdev=gdev, scratch=scratch, win=win):
-                    K.gather_rows(x, gdev, win, st, scratch)
-
-                add_plan("copy", scratch, None, cols, cin, pre=pre, st_eff=1)
+                add_plan("copy", scratch, None, [cols[k] for k in k_order], cin, pre=pre,
+                         st_eff=1 if st_g != 1 else st)
             lo, hi = min(gather), max(gather)
             width = hi - lo + 1
             if (self.gather_mode == "fused" and lo >= 0 and len(set(gather)) == cin
