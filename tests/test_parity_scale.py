@@ -7,7 +7,9 @@ graph and through the fp32 CPU oracle (oracle/spatial_ref.py over the same
 exported graph, weights permuted by the numpy apply_plan restatement).
 
 Gates (SURVEY.md 8d / north_star):
-  * the reference's relative metric (interp.py:119-120) <= 2e-2 over all 1024 x 1000 logits;
+  * the reference's relative metric (interp.py:119-120) <= 2e-2 over all 1024 x 1000 logits,
+    and the max error relative to the logits' own scale <= 2e-2 (the reference metric's
+    max(1, |x|) floor makes it vacuous for tiny random-init logits);
   * top-1 agreement >= 99.9 % (at most one disagreement in 1024) -- where the model's
     logits are decisive.  Random-init ResNet-50/18 with default BN (the bench config) is
     NOT: its logits span |x| <= 0.12 with a median top-1/top-2 margin of 8e-4 (R50), so
@@ -68,7 +70,9 @@ def _record(rec):
     ("densenet121_s50", "reorder", "fused", True),
     ("mobilenet_v3_small_s50", "reorder", "fused", False),  # config 2 model
     ("mobilenet_v3_small_s50", "baseline", "copy", False),
+    ("mobilenet_v3_small_s50", "reorder", "fused", True),
     ("efficientnet_v2_s_s50", "reorder", "fused", False),  # config 5 model
+    ("efficientnet_v2_s_s50", "reorder", "fused", True),
 ])
 def test_logits_at_scale(cfg_name, strategy, gather_mode, rbn):
     torch.set_num_threads(os.cpu_count() or 1)
@@ -96,15 +100,20 @@ def test_logits_at_scale(cfg_name, strategy, gather_mode, rbn):
     assert torch.isfinite(got).all()
     dev, agree = deviation(got, ref), top1_agreement(got, ref)
     top2 = ref.topk(2, dim=1).values
+    scale_rel = float((got - ref).abs().max() / ref.abs().max())
     rec = {"parity": cfg_name, "strategy": strategy, "gather": gather_mode, "randomized_bn": rbn,
-           "images": got.shape[0], "deviation": dev, "top1": agree, "logit_absmax": float(ref.abs().max()),
-           "median_top1_margin": float((top2[:, 0] - top2[:, 1]).median())}
+           "images": got.shape[0], "deviation": dev, "scale_relative_error": scale_rel, "top1": agree,
+           "logit_absmax": float(ref.abs().max()), "median_top1_margin": float((top2[:, 0] - top2[:, 1]).median())}
     if ctrls:
         ctrl = torch.cat(ctrls)
         rec["control_top1"] = top1_agreement(ctrl, ref)
         rec["control_deviation"] = deviation(ctrl, ref)
     _record(rec)
     assert dev <= TOL, f"deviation {dev}"
+    # the reference metric divides by max(1, |a|, |b|): vacuous when the logits are tiny (random-init
+    # MobileNetV3 / EfficientNetV2 reach |x| ~ 1e-11 / 1e-9), so the error is also held to the
+    # same tolerance relative to the logits' own scale
+    assert scale_rel <= TOL, f"error relative to the logit scale {scale_rel}"
     if agree < TOP1:  # only where bf16 rounding alone flips top-1 classes (see above)
         c = rec["control_top1"]
         assert ctrls and agree >= c - 2 * (c * (1 - c) / got.shape[0]) ** 0.5, rec
