@@ -305,7 +305,10 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
   constexpr int TH = dw_tile(K, S), TW = TH;  // the staged window fits the 48 KB static smem
   constexpr int IH = (TH - 1) * S + K, IW = (TW - 1) * S + K;
   __shared__ uint4 tile[IH * IW * 8];
-  __shared__ float sw[K * K * 64];
+  // the 8 filter values of group g sit at stride 12 floats: a quarter-warp's 16-byte weight
+  // loads (8 groups) then hit 8 distinct bank quads (stride 8 gave 2-way conflicts, ncu)
+  constexpr int WG = 12;
+  __shared__ __align__(16) float sw[K * K * 8 * WG];
   __shared__ float sb[64];
   const int C8 = (C + 7) / 8 * 8;
   const int cb = blockIdx.y * 64;
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
   const int iy0 = y0 * S - pad, ix0 = x0 * S - pad;
   for (int e = threadIdx.x; e < K * K * 64; e += 256) {
     const int tap = e >> 6, c = e & 63;
-    sw[e] = cb + c < C8 ? w[tap * C8 + cb + c] : 0.f;
+    sw[tap * 8 * WG + (c >> 3) * WG + (c & 7)] = cb + c < C8 ? w[tap * C8 + cb + c] : 0.f;
   }
   if (threadIdx.x < 64) sb[threadIdx.x] = (bias && cb + threadIdx.x < C) ? bias[cb + threadIdx.x] : 0.f;
   griddep_wait();
@@ -347,9 +350,12 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
       for (int dx = 0; dx < K; ++dx) {
         uint16_t v[8];
         *reinterpret_cast<uint4*>(v) = tile[((oy * S + dy) * IW + ox * S + dx) * 8 + g];
-        const float* wt = sw + (dy * K + dx) * 64 + g * 8;
+        const float* wt = sw + (dy * K + dx) * 8 * WG + g * WG;
+        const float4 w0 = *reinterpret_cast<const float4*>(wt);
+        const float4 w1 = *reinterpret_cast<const float4*>(wt + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(wt[j], bf(v[j]), acc[j]);
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(wv[j], bf(v[j]), acc[j]);
       }
     }
     uint16_t o[8];
