@@ -17,6 +17,27 @@ namespace ub {
 namespace {
 
 UB_DEVI float bf(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+// 8 floats -> 8 bf16 in one uint4, in registers (a uint16_t[8] written element-wise and
+// re-read as uint4 lives on the local-memory stack: ncu flagged it in the depthwise conv)
+UB_DEVI uint4 pack8(const float (&f)[8]) {
+  return make_uint4(cvt_bf16x2(f[0], f[1]), cvt_bf16x2(f[2], f[3]), cvt_bf16x2(f[4], f[5]), cvt_bf16x2(f[6], f[7]));
+}
+// bf16 element j (0..7) of a uint4 of 8 packed values, as fp32
+UB_DEVI float bfj(const uint4& q, int j) {
+  const uint32_t w = j < 2 ? q.x : (j < 4 ? q.y : (j < 6 ? q.z : q.w));
+  return __uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16));
+}
+// store 8 packed bf16 to p (16-byte aligned) or the first n of them
+UB_DEVI void store8(uint16_t* p, const uint4& q, int n) {
+  if (n >= 8) {
+    *reinterpret_cast<uint4*>(p) = q;
+  } else {
+    for (int j = 0; j < n; ++j) {
+      const uint32_t w = j < 2 ? q.x : (j < 4 ? q.y : (j < 6 ? q.z : q.w));
+      p[j] = static_cast<uint16_t>((j & 1) ? (w >> 16) : (w & 0xffffu));
+    }
+  }
+}
 UB_DEVI uint16_t tobf(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
 
 template <bool VEC>
@@ -38,27 +59,23 @@ __global__ void __launch_bounds__(256) eltwise_kernel(ub_eltwise_desc d) {
     const int c0 = static_cast<int>(e - pu * groups) * (VEC ? 8 : 1);
     const int n = static_cast<int>(pu / static_cast<unsigned>(d.HW));
     if (VEC) {
-      uint16_t va[8], vb[8], vg[8], vy[8];
-      *reinterpret_cast<uint4*>(va) = *reinterpret_cast<const uint4*>(a + p * d.a_cstride + d.a_coff + c0);
-      if (b) *reinterpret_cast<uint4*>(vb) = *reinterpret_cast<const uint4*>(b + p * d.b_cstride + d.b_coff + c0);
-      if (g) *reinterpret_cast<uint4*>(vg) = *reinterpret_cast<const uint4*>(g + static_cast<long long>(n) *
-                                                                                   d.gate_cstride + d.gate_coff + c0);
+      const uint4 qa = *reinterpret_cast<const uint4*>(a + p * d.a_cstride + d.a_coff + c0);
+      const uint4 qb = b ? *reinterpret_cast<const uint4*>(b + p * d.b_cstride + d.b_coff + c0) : make_uint4(0, 0, 0, 0);
+      const uint4 qg = g ? *reinterpret_cast<const uint4*>(g + static_cast<long long>(n) * d.gate_cstride + d.gate_coff + c0)
+                         : make_uint4(0, 0, 0, 0);
+      float f[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = c0 + j < d.C ? c0 + j : d.C - 1;
-        float v = bf(va[j]);
+        float v = bfj(qa, j);
         if (d.scale) v *= d.scale[c];
         if (d.shift) v += d.shift[c];
-        if (b) v += bf(vb[j]);
+        if (b) v += bfj(qb, j);
         v = act_f(v, d.act);
-        if (g) v *= bf(vg[j]);
-        vy[j] = tobf(v);
+        if (g) v *= bfj(qg, j);
+        f[j] = v;
       }
-      if (c0 + 8 <= d.C) {
-        *reinterpret_cast<uint4*>(y + p * d.y_cstride + d.y_coff + c0) = *reinterpret_cast<const uint4*>(vy);
-      } else {
-        for (int j = 0; c0 + j < d.C; ++j) y[p * d.y_cstride + d.y_coff + c0 + j] = vy[j];
-      }
+      store8(y + p * d.y_cstride + d.y_coff + c0, pack8(f), d.C - c0);
     } else {
       const int c = c0;
       float v = bf(a[p * d.a_cstride + d.a_coff + c]);
@@ -96,22 +113,15 @@ __global__ void __launch_bounds__(256) avgpool2d_kernel(const uint16_t* __restri
       for (int dx = 0; dx < k; ++dx) {
         const int xi = xo * s - pad + dx;
         if (xi < 0 || xi >= W) continue;
-        uint16_t v[8];
-        *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(
+        const uint4 qv = *reinterpret_cast<const uint4*>(
             x + ((static_cast<long long>(n) * H + yi) * W + xi) * x_cstride + x_coff + c0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+        for (int j = 0; j < 8; ++j) acc[j] += bfj(qv, j);
       }
     }
-    uint16_t o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = tobf(acc[j] * inv);
-    uint16_t* yp = y + p * y_cstride + y_coff + c0;
-    if (c0 + 8 <= C) {
-      *reinterpret_cast<uint4*>(yp) = *reinterpret_cast<const uint4*>(o);
-    } else {
-      for (int j = 0; c0 + j < C; ++j) yp[j] = o[j];
-    }
+    for (int j = 0; j < 8; ++j) acc[j] *= inv;
+    store8(y + p * y_cstride + y_coff + c0, pack8(acc), C - c0);
   }
 }
 
@@ -154,31 +164,24 @@ __global__ void __launch_bounds__(256) dwconv_kernel(const uint16_t* __restrict_
       for (int dx = 0; dx < k; ++dx) {
         const int xi = xo * s - pad + dx;
         if (xi < 0 || xi >= W) continue;
-        uint16_t v[8];
-        *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(
+        const uint4 qv = __ldg(reinterpret_cast<const uint4*>(
             x + ((static_cast<long long>(n) * H + yi) * W + xi) * x_cstride + x_coff + c0));
         const float* wt = w + static_cast<long long>(dy * k + dx) * ((C + 7) / 8 * 8) + c0;
         const float4 w0 = __ldg(reinterpret_cast<const float4*>(wt));
         const float4 w1 = __ldg(reinterpret_cast<const float4*>(wt + 4));
-        acc[0] = fmaf(w0.x, bf(v[0]), acc[0]);
-        acc[1] = fmaf(w0.y, bf(v[1]), acc[1]);
-        acc[2] = fmaf(w0.z, bf(v[2]), acc[2]);
-        acc[3] = fmaf(w0.w, bf(v[3]), acc[3]);
-        acc[4] = fmaf(w1.x, bf(v[4]), acc[4]);
-        acc[5] = fmaf(w1.y, bf(v[5]), acc[5]);
-        acc[6] = fmaf(w1.z, bf(v[6]), acc[6]);
-        acc[7] = fmaf(w1.w, bf(v[7]), acc[7]);
+        acc[0] = fmaf(w0.x, bfj(qv, 0), acc[0]);
+        acc[1] = fmaf(w0.y, bfj(qv, 1), acc[1]);
+        acc[2] = fmaf(w0.z, bfj(qv, 2), acc[2]);
+        acc[3] = fmaf(w0.w, bfj(qv, 3), acc[3]);
+        acc[4] = fmaf(w1.x, bfj(qv, 4), acc[4]);
+        acc[5] = fmaf(w1.y, bfj(qv, 5), acc[5]);
+        acc[6] = fmaf(w1.z, bfj(qv, 6), acc[6]);
+        acc[7] = fmaf(w1.w, bfj(qv, 7), acc[7]);
       }
     }
-    uint16_t o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[j], act));
-    uint16_t* yp = y + p * y_cstride + y_coff + c0;
-    if (c0 + 8 <= C) {
-      *reinterpret_cast<uint4*>(yp) = *reinterpret_cast<const uint4*>(o);
-    } else {
-      for (int j = 0; c0 + j < C; ++j) yp[j] = o[j];
-    }
+    for (int j = 0; j < 8; ++j) acc[j] = act_f(acc[j], act);
+    store8(y + p * y_cstride + y_coff + c0, pack8(acc), C - c0);
   }
 }
 
@@ -204,10 +207,9 @@ __global__ void __launch_bounds__(256) avgpool_split_kernel(const uint16_t* __re
   if (ph < phases) {
     const uint16_t* base = x + static_cast<long long>(n) * HW * x_cstride + x_coff + (g0 + g) * 8;
     for (int p = ph; p < HW; p += phases) {
-      uint16_t v[8];
-      *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(p) * x_cstride));
+      const uint4 qv = __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(p) * x_cstride));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+      for (int j = 0; j < 8; ++j) acc[j] += bfj(qv, j);
     }
   }
 #pragma unroll
@@ -250,11 +252,10 @@ __global__ void __launch_bounds__(256) linear_small_kernel(const uint16_t* __res
     for (int m = 0; m < 16; ++m) acc[m] = 0.f;
     const uint16_t* wr = w + static_cast<long long>(o) * w_stride;
     for (int k = lane * 8; k < K8; k += 256) {
-      uint16_t wv[8];
-      *reinterpret_cast<uint4*>(wv) = __ldg(reinterpret_cast<const uint4*>(wr + k));
+      const uint4 wq = __ldg(reinterpret_cast<const uint4*>(wr + k));
       float wf[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) wf[j] = bf(wv[j]);
+      for (int j = 0; j < 8; ++j) wf[j] = bfj(wq, j);
 #pragma unroll
       for (int m = 0; m < 16; ++m) {
         if (m < M) {
@@ -348,26 +349,20 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
     for (int dy = 0; dy < K; ++dy) {
 #pragma unroll
       for (int dx = 0; dx < K; ++dx) {
-        uint16_t v[8];
-        *reinterpret_cast<uint4*>(v) = tile[((oy * S + dy) * IW + ox * S + dx) * 8 + g];
+        const uint4 q = tile[((oy * S + dy) * IW + ox * S + dx) * 8 + g];
         const float* wt = sw + (dy * K + dx) * 8 * WG + g * WG;
         const float4 w0 = *reinterpret_cast<const float4*>(wt);
         const float4 w1 = *reinterpret_cast<const float4*>(wt + 4);
         const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(wv[j], bf(v[j]), acc[j]);
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(wv[j], bfj(q, j), acc[j]);
       }
     }
-    uint16_t o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[j], act));
+    for (int j = 0; j < 8; ++j) acc[j] = act_f(acc[j], act);
     const int c0 = cb + g * 8;
-    uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy) * Wo + x0 + ox) * y_cstride + y_coff + c0;
-    if (c0 + 8 <= C) {
-      *reinterpret_cast<uint4*>(yp) = *reinterpret_cast<const uint4*>(o);
-    } else {
-      for (int j = 0; c0 + j < C; ++j) yp[j] = o[j];
-    }
+    store8(y + ((static_cast<long long>(n) * Ho + y0 + oy) * Wo + x0 + ox) * y_cstride + y_coff + c0, pack8(acc),
+           C - c0);
   }
 }
 
@@ -434,10 +429,10 @@ __global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restric
       if (cb + 32 <= cout) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint16_t o[8];
+          float f[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] = tobf(act_f(acc[q * 8 + j], act));
-          *reinterpret_cast<uint4*>(yp + q * 8) = *reinterpret_cast<const uint4*>(o);
+          for (int j = 0; j < 8; ++j) f[j] = act_f(acc[q * 8 + j], act);
+          *reinterpret_cast<uint4*>(yp + q * 8) = pack8(f);
         }
       } else {
 #pragma unroll
@@ -466,22 +461,18 @@ __device__ __forceinline__ void warp_rows_dot(const uint16_t* __restrict__ w, in
 #pragma unroll
   for (int r = 0; r < RPW; ++r) acc[r] = 0.f;
   for (int k = lane * 8; k < ld; k += 256) {
-    uint16_t wv[RPW][8];
+    uint4 wv[RPW];
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      if (row0 + r < nrows)
-        *reinterpret_cast<uint4*>(wv[r]) =
-            __ldg(reinterpret_cast<const uint4*>(w + static_cast<long long>(row0 + r) * ld + k));
-      else
-        *reinterpret_cast<uint4*>(wv[r]) = make_uint4(0, 0, 0, 0);
-    }
+    for (int r = 0; r < RPW; ++r)
+      wv[r] = row0 + r < nrows ? __ldg(reinterpret_cast<const uint4*>(w + static_cast<long long>(row0 + r) * ld + k))
+                               : make_uint4(0, 0, 0, 0);
     float xv[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) xv[e] = v[k + e];
 #pragma unroll
     for (int r = 0; r < RPW; ++r)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[r] = fmaf(bf(wv[r][e]), xv[e], acc[r]);
+      for (int e = 0; e < 8; ++e) acc[r] = fmaf(bfj(wv[r], e), xv[e], acc[r]);
   }
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
@@ -526,16 +517,14 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
           q[u] = __ldg(reinterpret_cast<const uint4*>(col + static_cast<long long>(p + u * phases) * x_cstride));
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint16_t* v = reinterpret_cast<const uint16_t*>(&q[u]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+          for (int j = 0; j < 8; ++j) acc[j] += bfj(q[u], j);
         }
       }
       for (; p < HW; p += phases) {
-        uint16_t v[8];
-        *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(col + static_cast<long long>(p) * x_cstride));
+        const uint4 qv = __ldg(reinterpret_cast<const uint4*>(col + static_cast<long long>(p) * x_cstride));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += bf(v[j]);
+        for (int j = 0; j < 8; ++j) acc[j] += bfj(qv, j);
       }
     }
 #pragma unroll
