@@ -49,7 +49,7 @@ extern "C" {
 const char* ub_last_error(void);
 
 /* ABI version (bumped on any signature change). */
-int ub_abi_version(void); /* 5 */
+int ub_abi_version(void); /* 7 */
 
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (used by bench.py's gpu_launches claim). */
@@ -198,6 +198,19 @@ int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_co
               int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);
 
 /*
+ * ub_dwconv with the global average pool of its output fused (the squeeze-excitation pool,
+ * SURVEY.md A.5, that reads the depthwise output in MobileNetV3 / EfficientNetV2): part
+ * (fp32, nullable) receives per-tile channel sums of the stored bf16 outputs,
+ *   part[(n * P + t) * pad8(C) + c],  P = ub_dwconv_pool_parts(k, s, Ho, Wo) tiles per image,
+ * which ub_se_gate_parts adds in tile order (deterministic).  P == 0: the shape has no fused
+ * pool (part must then be null).
+ */
+int ub_dwconv_pool_parts(int k, int s, int Ho, int Wo);
+int ub_dwconv_pool(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w,
+                   const float* bias, int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride,
+                   int y_coff, float* part, cudaStream_t stream);
+
+/*
  * Global average pool for small grids (N x ceil(C/8) too small to fill the GPU, many
  * pixels): pixels split over a CTA's threads, partial sums added in a fixed order.
  * y[n][y_coff + c] = bf16(mean_p x[n][p][x_coff + c]).  16-byte aligned source rows.
@@ -239,6 +252,11 @@ int ub_conv_direct(const float* x, int N, int C, int H, int W, const int32_t* id
 int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1, int C1,
                const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2, int act2, void* gate,
                int g_cstride, int g_coff, cudaStream_t stream);
+/* ub_se_gate pooling from ub_dwconv_pool's partials (part, nparts per image) instead of
+ * re-reading x (x may then be null; HW still scales the mean). */
+int ub_se_gate_parts(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1, int C1,
+                     const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2, int act2, void* gate,
+                     int g_cstride, int g_coff, const float* part, int nparts, cudaStream_t stream);
 
 int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, int k, int s, int pad, int Ho,
                  int Wo, void* y, int y_cstride, int y_coff, cudaStream_t stream);

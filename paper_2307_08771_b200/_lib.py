@@ -90,6 +90,9 @@ SIGNATURES = {
                              c_int, c_int, c_vp]),
     "ub_dwconv": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_int,
                           c_int, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_dwconv_pool_parts": (c_int, [c_int, c_int, c_int, c_int]),
+    "ub_dwconv_pool": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_int,
+                               c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp]),
     "ub_avgpool_split": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_linear_small": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int,
                                 c_int, c_vp]),
@@ -97,6 +100,8 @@ SIGNATURES = {
                                c_int, c_vp, c_int, c_int, c_vp]),
     "ub_se_gate": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int,
                            c_int, c_vp, c_int, c_vp, c_int, c_int, c_vp]),
+    "ub_se_gate_parts": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int,
+                                 c_int, c_vp, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp]),
     "ub_conv_weight_layout": (c_int, [c_int, c_int, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "ub_conv_weight_layout2": (c_int, [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int),
                                        ctypes.POINTER(c_int)]),

@@ -104,7 +104,7 @@ PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
 extern "C" {
 
 const char* ub_last_error(void) { return g_err.c_str(); }
-int ub_abi_version(void) { return 6; }
+int ub_abi_version(void) { return 7; }
 long long ub_launch_count(void) { return g_launches; }
 void ub_reset_launch_count(void) { g_launches = 0; }
 

@@ -367,6 +367,131 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const uint16_t* __rest
 }
 
 
+// 3x3 depthwise conv, register strips: same staged 8 x 8 x 64-channel tile as above, but a
+// thread owns 4 channels x one output column x a strip of DWS_R output rows.  Its 9 x 4
+// filter values live in registers (loaded once), and each staged input pixel it needs is
+// read from shared memory once per strip and applied to every output row of the strip it
+// touches: (DWS_R - 1) * S + 3 rows x 3 columns of 8-byte loads for DWS_R x 4 outputs,
+// against 9 input + 18 weight 16-byte loads per 8 outputs in the per-pixel form (which
+// ncu showed shared-memory-bound).  A half-warp reads 16 x 8 contiguous bytes of a pixel.
+constexpr int DWS_R = 4;
+template <int S>
+__global__ void __launch_bounds__(256) dwconv3_strip_kernel(const uint16_t* __restrict__ x, int N, int H, int W, int C,
+                                                            int x_cstride, int x_coff, const float* __restrict__ w,
+                                                            const float* __restrict__ bias, int pad, int act, int Ho,
+                                                            int Wo, int tiles_h, int tiles_w,
+                                                            uint16_t* __restrict__ y, int y_cstride, int y_coff,
+                                                            float* __restrict__ part) {
+  constexpr int K = 3, TH = 8, TW = 8;
+  constexpr int IH = (TH - 1) * S + K, IW = (TW - 1) * S + K;
+  static_assert(TH % DWS_R == 0 && (TH / DWS_R) * TW * 16 == 256, "one strip per thread");
+  __shared__ uint4 tile[IH * IW * 8];
+  __shared__ __align__(16) float sw[K * K * 64];
+  __shared__ float sb[64];
+  const int C8 = (C + 7) / 8 * 8;
+  const int cb = blockIdx.y * 64;
+  const int G = min(8, (C - cb + 7) / 8);
+  const int t = blockIdx.x;
+  const int n = t / (tiles_h * tiles_w);
+  const int r = t - n * tiles_h * tiles_w;
+  const int y0 = (r / tiles_w) * TH, x0 = (r % tiles_w) * TW;
+  const int iy0 = y0 * S - pad, ix0 = x0 * S - pad;
+  for (int e = threadIdx.x; e < K * K * 64; e += 256) {
+    const int c = e & 63;
+    sw[e] = cb + c < C8 ? w[(e >> 6) * C8 + cb + c] : 0.f;
+  }
+  if (threadIdx.x < 64) sb[threadIdx.x] = (bias && cb + threadIdx.x < C) ? bias[cb + threadIdx.x] : 0.f;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int e = threadIdx.x; e < IH * IW * 8; e += 256) {
+    const int pix = e >> 3, g = e & 7;
+    if (g >= G) continue;
+    const int iy = iy0 + pix / IW, ix = ix0 + pix % IW;
+    uint4* dst = &tile[e];
+    if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+      cp_async16(dst, x + ((static_cast<long long>(n) * H + iy) * W + ix) * x_cstride + x_coff + cb + g * 8, 16);
+    else
+      *dst = make_uint4(0, 0, 0, 0);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int hg = threadIdx.x & 15;          // 4-channel quarter of the 64-channel block
+  const int ox = (threadIdx.x >> 4) & 7;    // output column in the tile
+  const int oy0 = (threadIdx.x >> 7) * DWS_R;
+  const int c0 = cb + hg * 4;
+  const bool live = c0 < C && x0 + ox < Wo && y0 + oy0 < Ho;
+  float psum[4] = {0.f, 0.f, 0.f, 0.f};  // this strip's stored (bf16-rounded) outputs, summed
+  if (live) {
+    float wr[K * K][4];
+#pragma unroll
+    for (int tap = 0; tap < K * K; ++tap) {
+      const float4 v = *reinterpret_cast<const float4*>(&sw[tap * 64 + hg * 4]);
+      wr[tap][0] = v.x; wr[tap][1] = v.y; wr[tap][2] = v.z; wr[tap][3] = v.w;
+    }
+    float acc[DWS_R][4];
+#pragma unroll
+    for (int q = 0; q < DWS_R; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[q][j] = sb[hg * 4 + j];
+    const uint2* tile2 = reinterpret_cast<const uint2*>(tile);
+#pragma unroll
+    for (int i = 0; i < (DWS_R - 1) * S + K; ++i) {
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx) {
+        const uint2 v = tile2[((oy0 * S + i) * IW + ox * S + dx) * 16 + hg];
+        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
+#pragma unroll
+        for (int q = 0; q < DWS_R; ++q) {
+          const int dy = i - q * S;
+          if (dy >= 0 && dy < K) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][j] = fmaf(wr[dy * K + dx][j], f[j], acc[q][j]);
+          }
+        }
+      }
+    }
+    const int nc = min(4, C - c0);
+#pragma unroll
+    for (int q = 0; q < DWS_R; ++q) {
+      if (y0 + oy0 + q >= Ho) break;
+      const uint2 o = make_uint2(cvt_bf16x2(act_f(acc[q][0], act), act_f(acc[q][1], act)),
+                                 cvt_bf16x2(act_f(acc[q][2], act), act_f(acc[q][3], act)));
+      psum[0] += __uint_as_float(o.x << 16);
+      psum[1] += __uint_as_float(o.x & 0xffff0000u);
+      psum[2] += __uint_as_float(o.y << 16);
+      psum[3] += __uint_as_float(o.y & 0xffff0000u);
+      uint16_t* p = y + ((static_cast<long long>(n) * Ho + y0 + oy0 + q) * Wo + x0 + ox) * y_cstride + y_coff + c0;
+      if (nc == 4) {
+        *reinterpret_cast<uint2*>(p) = o;
+      } else {
+        for (int j = 0; j < nc; ++j) {
+          const uint32_t h = j < 2 ? o.x : o.y;
+          p[j] = static_cast<uint16_t>((j & 1) ? (h >> 16) : (h & 0xffffu));
+        }
+      }
+    }
+  }
+  if (part) {
+    // the SE global pool of the output, fused: per-channel sums of this tile, reduced over the
+    // 16 strips of each 4-channel group in (now free) shared memory, one partial per tile
+    // (deterministic: the consumer adds the image's tile partials in a fixed order)
+    __syncthreads();
+    float4* red = reinterpret_cast<float4*>(tile);
+    red[threadIdx.x] = make_float4(psum[0], psum[1], psum[2], psum[3]);
+    __syncthreads();
+    if (threadIdx.x < 64 && cb + threadIdx.x < C8) {
+      const float* rf = reinterpret_cast<const float*>(red);
+      float s = 0.f;
+#pragma unroll
+      for (int it = 0; it < 16; ++it) s += rf[(it * 16 + (threadIdx.x >> 2)) * 4 + (threadIdx.x & 3)];
+      part[static_cast<long long>(t) * C8 + cb + threadIdx.x] = s;
+    }
+  }
+}
+
+
 // Direct stem conv on CUDA cores for few input channels (MobileNetV3 / EfficientNetV2:
 // 3x3/s2 on the 3 image planes).  Reads the fp32 NCHW model input through the INPUT
 // node's GATHER (idx), BN folded into w/bias, activation fused, NHWC bf16 out.  A CTA
@@ -487,7 +612,9 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
                                                       const float* __restrict__ b1, int act1,
                                                       const uint16_t* __restrict__ w2, int ldw2, int C2,
                                                       const float* __restrict__ b2, int act2,
-                                                      uint16_t* __restrict__ gate, int g_cstride, int g_coff) {
+                                                      uint16_t* __restrict__ gate, int g_cstride, int g_coff,
+                                                      const float* __restrict__ part, int nparts,
+                                                      int thread_rows) {
   constexpr int RPW = 8;  // weight rows per warp step (loads in flight)
   extern __shared__ float se_smem[];
   const int C8 = (C + 7) / 8 * 8, C18 = (C1 + 7) / 8 * 8;
@@ -499,8 +626,18 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
   const int t = threadIdx.x;
   griddep_wait();
   griddep_launch_dependents();
+  if (part) {
+    // ---- pool from the producer's per-tile partial sums (ub_dwconv_pool), in tile order
+    const float* pp = part + static_cast<long long>(n) * nparts * C8;
+    for (int c = t; c < C8; c += blockDim.x) {
+      float sum = 0.f;
+      for (int q = 0; q < nparts; ++q) sum += pp[static_cast<long long>(q) * C8 + c];
+      pooled[c] = c < C ? sum / static_cast<float>(HW) : 0.f;
+    }
+    __syncthreads();
+  }
   // ---- pool: groups of 8 channels x pixel phases (4 independent loads in flight per thread)
-  const int G = C8 / 8;
+  const int G = part ? 0 : C8 / 8;
   const uint16_t* base = x + static_cast<long long>(n) * HW * x_cstride + x_coff;
   for (int g0 = 0; g0 < G; g0 += 64) {
     const int gb = min(64, G - g0);
@@ -559,6 +696,30 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
   // ---- fc2 (+ bias, act2): this CTA's share of the gate channels, RPW per warp step
   const int per = (C2 + nsplit - 1) / nsplit;
   const int c_lo = split * per, c_hi = min(C2, c_lo + per);
+  if (thread_rows) {
+    // short rows (ldw2 <= 128, the usual SE squeeze width): a thread per gate channel, its
+    // row's 16-byte chunks loaded four at a time, fc1 read from shared memory as broadcasts
+    // (a warp per row would leave most lanes idle and pay a shuffle reduction per row)
+    const int n8 = ldw2 >> 3;
+    for (int c = c_lo + t; c < c_hi; c += blockDim.x) {
+      const uint4* wr = reinterpret_cast<const uint4*>(w2 + static_cast<long long>(c) * ldw2);
+      float acc = 0.f;
+      for (int k8 = 0; k8 < n8; k8 += 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = k8 + u < n8 ? __ldg(wr + k8 + u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k8 + u < n8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = fmaf(bfj(q[u], e), hidden[(k8 + u) * 8 + e], acc);
+          }
+        }
+      }
+      gate[static_cast<long long>(n) * g_cstride + g_coff + c] = tobf(act_f(acc + (b2 ? b2[c] : 0.f), act2));
+    }
+    return;
+  }
   for (int c0 = c_lo + warp * RPW; c0 < c_hi; c0 += warps * RPW) {
     float o[RPW];
     warp_rows_dot<RPW>(w2, ldw2, c0, c_hi, hidden, lane, o);
@@ -614,28 +775,48 @@ extern "C" int ub_avgpool2d(const void* x, int N, int H, int W, int C, int x_cst
   return cuda_status(e, "avgpool2d_kernel");
 }
 
-extern "C" int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w,
-                         const float* bias, int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride,
-                         int y_coff, cudaStream_t stream) {
+// tiles per image of the register-strip 3x3 form, i.e. the SE pool partials ub_dwconv_pool
+// writes per image; 0 when the shape takes another form (no fused pool)
+static bool dw_strips_enabled() {
+  static const bool on = !std::getenv("UB_DW_NOSTRIP");
+  return on;
+}
+
+extern "C" int ub_dwconv_pool_parts(int k, int s, int Ho, int Wo) {
+  if (k != 3 || (s != 1 && s != 2) || Ho < 1 || Wo < 1 || !dw_strips_enabled()) return 0;
+  return ((Ho + 7) / 8) * ((Wo + 7) / 8);
+}
+
+extern "C" int ub_dwconv_pool(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w,
+                              const float* bias, int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride,
+                              int y_coff, float* part, cudaStream_t stream) {
   if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || s < 1 || pad < 0 || Ho < 1 || Wo < 1 ||
       act < UB_ACT_NONE || act > UB_ACT_SIGMOID)
     return fail(UB_EINVAL, "ub_dwconv: bad arguments");
   if (!a16(x, x_cstride, x_coff) || !a16(y, y_cstride, y_coff) || x_coff + C > x_cstride || y_coff + C > y_cstride ||
       (reinterpret_cast<uintptr_t>(w) & 15))
     return fail(UB_EINVAL, "ub_dwconv: rows must be 16-byte aligned");
-  if ((k == 3 || k == 5) && (s == 1 || s == 2)) {  // smem-tiled form
+  if (part && (ub_dwconv_pool_parts(k, s, Ho, Wo) == 0 || (reinterpret_cast<uintptr_t>(part) & 3)))
+    return fail(UB_EUNSUPPORTED, "ub_dwconv_pool: fused pool needs the 3x3 strip form (k %d s %d)", k, s);
+  if ((k == 3 || k == 5) && (s == 1 || s == 2)) {  // smem-tiled forms
     const int tsz = dw_tile(k, s);
     const int th = (Ho + tsz - 1) / tsz, tw = (Wo + tsz - 1) / tsz;
     const long long tiles = static_cast<long long>(N) * th * tw;
     if (tiles < (1ll << 31)) {
       const dim3 grid(static_cast<unsigned>(tiles), (C + 63) / 64);
-      void (*kern)(const uint16_t*, int, int, int, int, int, int, const float*, const float*, int, int, int, int, int,
-                   int, uint16_t*, int, int) =
-          k == 3 ? (s == 1 ? dwconv_tile_kernel<3, 1> : dwconv_tile_kernel<3, 2>)
-                 : (s == 1 ? dwconv_tile_kernel<5, 1> : dwconv_tile_kernel<5, 2>);
-      const cudaError_t e = launch_pdl(kern, grid, dim3(256), 0, stream, static_cast<const uint16_t*>(x), N, H, W, C,
-                                       x_cstride, x_coff, w, bias, pad, act, Ho, Wo, th, tw,
-                                       static_cast<uint16_t*>(y), y_cstride, y_coff);
+      cudaError_t e;
+      if (k == 3 && dw_strips_enabled()) {
+        e = launch_pdl(s == 1 ? dwconv3_strip_kernel<1> : dwconv3_strip_kernel<2>, grid, dim3(256), 0, stream,
+                       static_cast<const uint16_t*>(x), N, H, W, C, x_cstride, x_coff, w, bias, pad, act, Ho, Wo, th,
+                       tw, static_cast<uint16_t*>(y), y_cstride, y_coff, part);
+      } else {
+        void (*kern)(const uint16_t*, int, int, int, int, int, int, const float*, const float*, int, int, int, int,
+                     int, int, uint16_t*, int, int) =
+            k == 3 ? (s == 1 ? dwconv_tile_kernel<3, 1> : dwconv_tile_kernel<3, 2>)
+                   : (s == 1 ? dwconv_tile_kernel<5, 1> : dwconv_tile_kernel<5, 2>);
+        e = launch_pdl(kern, grid, dim3(256), 0, stream, static_cast<const uint16_t*>(x), N, H, W, C, x_cstride,
+                       x_coff, w, bias, pad, act, Ho, Wo, th, tw, static_cast<uint16_t*>(y), y_cstride, y_coff);
+      }
       count_launch();
       return cuda_status(e, "dwconv_tile_kernel");
     }
@@ -646,6 +827,13 @@ extern "C" int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstrid
                                    act, Ho, Wo, static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "dwconv_kernel");
+}
+
+extern "C" int ub_dwconv(const void* x, int N, int H, int W, int C, int x_cstride, int x_coff, const float* w,
+                         const float* bias, int k, int s, int pad, int act, int Ho, int Wo, void* y, int y_cstride,
+                         int y_coff, cudaStream_t stream) {
+  return ub_dwconv_pool(x, N, H, W, C, x_cstride, x_coff, w, bias, k, s, pad, act, Ho, Wo, y, y_cstride, y_coff,
+                        nullptr, stream);
 }
 
 extern "C" int ub_avgpool_split(const void* x, int N, int HW, int C, int x_cstride, int x_coff, void* y, int y_cstride,
@@ -706,14 +894,15 @@ extern "C" int ub_conv_direct(const float* x, int N, int C, int H, int W, const 
   return cuda_status(e, "conv_direct_kernel");
 }
 
-extern "C" int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1,
-                          int C1, const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2,
-                          int act2, void* gate, int g_cstride, int g_coff, cudaStream_t stream) {
-  if (!x || !w1 || !w2 || !gate || N < 1 || HW < 1 || C < 1 || C1 < 1 || C2 < 1 || act1 < UB_ACT_NONE ||
-      act1 > UB_ACT_SIGMOID || act2 < UB_ACT_NONE || act2 > UB_ACT_SIGMOID)
+extern "C" int ub_se_gate_parts(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1,
+                                int ldw1, int C1, const float* b1, int act1, const void* w2, int ldw2, int C2,
+                                const float* b2, int act2, void* gate, int g_cstride, int g_coff, const float* part,
+                                int nparts, cudaStream_t stream) {
+  if ((!x && !part) || (part && nparts < 1) || !w1 || !w2 || !gate || N < 1 || HW < 1 || C < 1 || C1 < 1 || C2 < 1 ||
+      act1 < UB_ACT_NONE || act1 > UB_ACT_SIGMOID || act2 < UB_ACT_NONE || act2 > UB_ACT_SIGMOID)
     return fail(UB_EINVAL, "ub_se_gate: bad arguments");
-  if (!a16(x, x_cstride, x_coff) || x_coff + (C + 7) / 8 * 8 > x_cstride || (ldw1 & 7) || ldw1 < (C + 7) / 8 * 8 ||
-      (ldw2 & 7) || ldw2 < (C1 + 7) / 8 * 8 || (reinterpret_cast<uintptr_t>(w1) & 15) ||
+  if ((!part && (!a16(x, x_cstride, x_coff) || x_coff + (C + 7) / 8 * 8 > x_cstride)) || (ldw1 & 7) ||
+      ldw1 < (C + 7) / 8 * 8 || (ldw2 & 7) || ldw2 < (C1 + 7) / 8 * 8 || (reinterpret_cast<uintptr_t>(w1) & 15) ||
       (reinterpret_cast<uintptr_t>(w2) & 15) || g_coff + C2 > g_cstride)
     return fail(UB_EINVAL, "ub_se_gate: rows must be 16-byte aligned / weight rows too short");
   const int C8 = (C + 7) / 8 * 8, C18 = (C1 + 7) / 8 * 8;
@@ -725,10 +914,20 @@ extern "C" int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, in
   int nsplit = num_sms() / N;
   nsplit = nsplit < 1 ? 1 : (nsplit > 16 ? 16 : nsplit);
   if (nsplit > (C2 + 63) / 64) nsplit = (C2 + 63) / 64;
+  static const bool rows_env = !std::getenv("UB_SE_WARPROWS");
+  const bool thread_rows = rows_env && ldw2 <= 128;
   const cudaError_t e = launch_pdl(se_gate_kernel, dim3(N, nsplit), dim3(512), smem, stream, static_cast<const uint16_t*>(x),
                                    HW, C, x_cstride, x_coff, static_cast<const uint16_t*>(w1), ldw1, C1, b1, act1,
                                    static_cast<const uint16_t*>(w2), ldw2, C2, b2, act2, static_cast<uint16_t*>(gate),
-                                   g_cstride, g_coff);
+                                   g_cstride, g_coff, part, nparts, thread_rows ? 1 : 0);
   count_launch();
   return cuda_status(e, "se_gate_kernel");
+}
+
+extern "C" int ub_se_gate(const void* x, int N, int HW, int C, int x_cstride, int x_coff, const void* w1, int ldw1,
+                          int C1, const float* b1, int act1, const void* w2, int ldw2, int C2, const float* b2,
+                          int act2, void* gate, int g_cstride, int g_coff, cudaStream_t stream) {
+  if (!x) return fail(UB_EINVAL, "ub_se_gate: bad arguments");
+  return ub_se_gate_parts(x, N, HW, C, x_cstride, x_coff, w1, ldw1, C1, b1, act1, w2, ldw2, C2, b2, act2, gate,
+                          g_cstride, g_coff, nullptr, 0, stream);
 }

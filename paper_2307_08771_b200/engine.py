@@ -20,6 +20,7 @@ This is the spatial, batched twin of the reference interpreter `run`
 
 from __future__ import annotations
 
+import os
 import ctypes
 from dataclasses import dataclass, field
 from typing import Callable, Mapping, Sequence
@@ -476,6 +477,13 @@ class Engine:
             if not ok:
                 continue
             se = _Op("se", pop.anchor, list(pop.inputs), b.output, info={"pool": pop, "fc1": a, "fc2": b})
+            # the pool reads a depthwise conv's output: that launch also writes per-tile channel
+            # sums (ub_dwconv_pool) and the gate pools from them instead of re-reading the tensor
+            src = base(pop.inputs[0])
+            dw = next((o for o in ops if o.kind == "dwconv" and base(o.output) == src), None)
+            if dw is not None and not os.environ.get("UB_SE_NOFUSEPOOL"):
+                dw.info["se_part"] = True
+                se.info["dw"] = dw
             idx = ops.index(pop)
             for o in (pop, a, b):
                 ops.remove(o)
@@ -531,7 +539,9 @@ class Engine:
         w1, w2 = pack(W1), pack(W2)
         gate = self._alloc(b.info["out"], C2)
         xd = self._dense(x)
-        op.launch = lambda: K.se_gate(xd, w1, C1, b1, act1, w2, C2, b2, act2, gate)
+        dw = op.info.get("dw")
+        part, nparts = dw.info.get("part", (None, 0)) if dw is not None else (None, 0)
+        op.launch = lambda: K.se_gate(xd, w1, C1, b1, act1, w2, C2, b2, act2, gate, part, nparts)
         self.conv_stats.append(ConvStats(f"{op.anchor}(se)", 0.0, 2.0 * C * x.H * x.W, 0.0))
 
     def _plan_concats(self, ops, alias, base, pos, output_feed) -> None:
@@ -774,7 +784,13 @@ class Engine:
         self._keep += [wt, b]
         act = self.specs[op.info["act"]].op if op.info["act"] else "none"
         y = self._alloc(op.output, C)
-        op.launch = lambda: K.dwconv(x, wt, b, k, sp.stride, sp.pad, act, y)
+        part = None
+        if op.info.get("se_part"):
+            nparts = K.dwconv_pool_parts(k, sp.stride, y.H, y.W)
+            if nparts > 0:
+                part = torch.empty(y.N * nparts, K.pad8(C), dtype=torch.float32, device=self.device)
+                op.info["part"] = (part, nparts)
+        op.launch = lambda: K.dwconv(x, wt, b, k, sp.stride, sp.pad, act, y, part)
         # roofline bookkeeping: 2*k*k flops per output, input + output bytes
         self.conv_stats.append(ConvStats(lid, 2.0 * k * k * C * y.H * y.W, 2.0 * C * (x.H * x.W + y.H * y.W), 0.0))
 

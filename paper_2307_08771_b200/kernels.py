@@ -315,10 +315,22 @@ def eltwise(a: Act, y: Act, scale=None, shift=None, b: Act | None = None, act: s
 
 
 def dwconv(x: Act, w: torch.Tensor, bias: torch.Tensor | None, k: int, stride: int, pad: int, act: str,
-           y: Act) -> None:
-    """ub_dwconv: depthwise k x k conv, w fp32 [k*k, pad8(C)] (BN folded), fused activation."""
-    _lib.call("ub_dwconv", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, _p(w), _p(bias), k, stride, pad,
-              _lib.UB_ACT[act], y.H, y.W, _p(y.buf), y.cstride, y.coff, _stream())
+           y: Act, part: torch.Tensor | None = None) -> None:
+    """ub_dwconv: depthwise k x k conv, w fp32 [k*k, pad8(C)] (BN folded), fused activation.
+    part (fp32 [N * dwconv_pool_parts(..), pad8(C)]): also write the per-tile channel sums of
+    the output (ub_dwconv_pool, the fused SE pool)."""
+    if part is None:
+        _lib.call("ub_dwconv", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, _p(w), _p(bias), k, stride, pad,
+                  _lib.UB_ACT[act], y.H, y.W, _p(y.buf), y.cstride, y.coff, _stream())
+    else:
+        assert part.dtype == torch.float32 and part.shape == (x.N * dwconv_pool_parts(k, stride, y.H, y.W), pad8(y.C))
+        _lib.call("ub_dwconv_pool", _p(x.buf), x.N, x.H, x.W, x.C, x.cstride, x.coff, _p(w), _p(bias), k, stride, pad,
+                  _lib.UB_ACT[act], y.H, y.W, _p(y.buf), y.cstride, y.coff, _p(part), _stream())
+
+
+def dwconv_pool_parts(k: int, stride: int, Ho: int, Wo: int) -> int:
+    """Pool partials per image ub_dwconv_pool writes for this shape (0: no fused pool)."""
+    return _lib.load().ub_dwconv_pool_parts(k, stride, Ho, Wo)
 
 
 def avgpool_split(x: Act, y: Act) -> None:
@@ -344,10 +356,16 @@ def conv_direct(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, bi
 
 
 def se_gate(x: Act, w1: torch.Tensor, C1: int, b1, act1: int, w2: torch.Tensor, C2: int, b2, act2: int,
-            gate: Act) -> None:
-    """ub_se_gate: pool + fc1 + fc2 of a squeeze-excitation block; w1 [C1, ldw1], w2 [C2, ldw2] bf16."""
-    _lib.call("ub_se_gate", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(w1), w1.shape[1], C1, _p(b1), act1,
-              _p(w2), w2.shape[1], C2, _p(b2), act2, _p(gate.buf), gate.cstride, gate.coff, _stream())
+            gate: Act, part: torch.Tensor | None = None, nparts: int = 0) -> None:
+    """ub_se_gate: pool + fc1 + fc2 of a squeeze-excitation block; w1 [C1, ldw1], w2 [C2, ldw2] bf16.
+    part/nparts: pool from ub_dwconv_pool's per-tile partial sums instead of re-reading x."""
+    if part is None:
+        _lib.call("ub_se_gate", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(w1), w1.shape[1], C1, _p(b1),
+                  act1, _p(w2), w2.shape[1], C2, _p(b2), act2, _p(gate.buf), gate.cstride, gate.coff, _stream())
+    else:
+        _lib.call("ub_se_gate_parts", _p(x.buf), x.N, x.H * x.W, x.C, x.cstride, x.coff, _p(w1), w1.shape[1], C1,
+                  _p(b1), act1, _p(w2), w2.shape[1], C2, _p(b2), act2, _p(gate.buf), gate.cstride, gate.coff,
+                  _p(part), nparts, _stream())
 
 
 def avgpool2d(x: Act, k: int, stride: int, pad: int, y: Act) -> None:

@@ -129,3 +129,8 @@ def test_mobilenet_se_blocks_fuse_into_one_launch(stub_kernels):
     assert kinds.count("avgpool") == 1  # the classifier's pool only
     assert all(op.info.get("bn") is not None for op in eng.ops if op.kind == "dwconv")
     assert len(eng.ops) == 55
+    # every SE pool reads a depthwise output; the 3x3 ones write its pool partials themselves
+    ses = [op for op in eng.ops if op.kind == "se"]
+    assert all(op.info["dw"].kind == "dwconv" for op in ses)
+    fused = [op for op in ses if "part" in op.info["dw"].info]
+    assert len(fused) == sum(1 for op in ses if eng.specs[op.info["dw"].anchor].kernel == 3) >= 1

@@ -782,6 +782,49 @@ def test_se_gate(N, H, C, C1, C2, acts):
     assert _rel(gate.to_nchw().cpu().reshape(N, C2), ref) < 1e-2
 
 
+@pytest.mark.parametrize("H,stride,C", [(14, 1, 730), (28, 2, 192), (7, 1, 13), (17, 1, 96)])
+def test_dwconv_fused_se_pool(H, stride, C):
+    """ub_dwconv_pool's per-tile channel sums == the sums of its own stored output, and
+    ub_se_gate_parts over them == ub_se_gate re-reading the tensor (fp32 order only)."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(H * 100 + C)
+    N, k = 3, 3
+    x = torch.randn(N, C, H, H, generator=g)
+    w = torch.randn(C, 1, k, k, generator=g) / k
+    b = torch.randn(C, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    Ho = (H + 2 - k) // stride + 1
+    nparts = K.dwconv_pool_parts(k, stride, Ho, Ho)
+    assert nparts == ((Ho + 7) // 8) ** 2
+    y = K.empty_act(N, Ho, Ho, C, dev)
+    y0 = K.empty_act(N, Ho, Ho, C, dev)
+    wt = torch.zeros(k * k, K.pad8(C))
+    wt[:, :C] = w.reshape(C, k * k).t()
+    part = torch.full((N * nparts, K.pad8(C)), float("nan"), device=dev)
+    K.dwconv(xa, wt.to(dev), b.to(dev), k, stride, 1, "silu", y, part)
+    K.dwconv(xa, wt.to(dev), b.to(dev), k, stride, 1, "silu", y0)
+    torch.cuda.synchronize()
+    out = y.to_nchw().float()
+    assert torch.equal(out, y0.to_nchw().float())  # the fused pool leaves the output unchanged
+    sums = part.view(N, nparts, -1).sum(1)[:, :C]
+    assert torch.allclose(sums, out.sum(dim=(2, 3)), rtol=1e-5, atol=1e-3)
+    C1, C2 = 24, C
+    W1 = torch.randn(C1, C, generator=g) / C ** 0.5
+    W2 = torch.randn(C2, C1, generator=g) / C1 ** 0.5
+
+    def pack(W):
+        t = torch.zeros(W.shape[0], (W.shape[1] + 7) // 8 * 8, dtype=torch.bfloat16)
+        t[:, :W.shape[1]] = W.to(torch.bfloat16)
+        return t.to(dev)
+
+    g1, g2 = K.empty_act(N, 1, 1, C2, dev), K.empty_act(N, 1, 1, C2, dev)
+    args = (pack(W1), C1, None, _lib.UB_ACT["silu"], pack(W2), C2, None, _lib.UB_ACT["sigmoid"])
+    K.se_gate(y, *args, g1)
+    K.se_gate(y, *args, g2, part, nparts)
+    torch.cuda.synchronize()
+    assert (g1.to_nchw().float() - g2.to_nchw().float()).abs().max().item() <= 2 ** -8
+
+
 @pytest.mark.parametrize("width,n,affine,stride", [(1016, 496, True, 1), (600, 300, False, 1), (2040, 1500, True, 1),
                                                    (1016, 508, False, 2), (2040, 1020, False, 2)])
 def test_gather_rows_wide(width, n, affine, stride):

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_host_only_helpers(lib):
-    assert lib.ub_abi_version() == 6
+    assert lib.ub_abi_version() == 7
     assert _lib.conv_weight_layout(100, 13, False) == (5, 128)   # misaligned slice: lead 5, 105 -> 128
     assert _lib.conv_weight_layout(12, 0, False) == (0, 16)      # BK 16
     assert _lib.conv_weight_layout(32, 0, False) == (0, 32)      # BK 32
