@@ -234,9 +234,11 @@ int ub_linear_small(const void* x, int M, int x_cstride, const int32_t* xcol, in
  * Direct CUDA-core conv for the model's first layer when it reads few image channels
  * (cin <= 8, k <= 7, cout <= 256: the 3x3/s2 stems of MobileNetV3 / EfficientNetV2).
  * x: the fp32 NCHW model input [N][C][H][W]; idx (device): the INPUT GATHER's cin kept
- * channels (interp.py:75-77).  w: fp32 [k*k][cin][pad32(cout)] (BN folded), bias fp32.
+ * channels (interp.py:75-77).  w: fp32 [k*k][cin][ub_conv_direct_wcols(cout)] (BN folded,
+ * zero columns past cout, 16-byte aligned), bias fp32.
  *   y[n][yo][xo][y_coff + o] = bf16(act(bias[o] + sum w * x))   (NHWC, 16-byte aligned rows)
  */
+int ub_conv_direct_wcols(int cout);  /* pad8(cout) below 32 channels, else pad32(cout) */
 int ub_conv_direct(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, const float* w,
                    const float* bias, int cout, int k, int s, int pad, int act, void* y, int y_cstride, int y_coff,
                    cudaStream_t stream);

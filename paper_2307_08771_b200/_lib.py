@@ -96,6 +96,7 @@ SIGNATURES = {
     "ub_avgpool_split": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp]),
     "ub_linear_small": (c_int, [c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int, c_int,
                                 c_int, c_vp]),
+    "ub_conv_direct_wcols": (c_int, [c_int]),
     "ub_conv_direct": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_int, c_int, c_int,
                                c_int, c_vp, c_int, c_int, c_vp]),
     "ub_se_gate": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_int,

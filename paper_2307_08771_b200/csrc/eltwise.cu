@@ -89,6 +89,52 @@ __global__ void __launch_bounds__(256) eltwise_kernel(ub_eltwise_desc d) {
   }
 }
 
+// y = act(a) * gate[n] (the squeeze-excitation `mul`, a positional ADD of the lowering with
+// the gate broadcast over the pixels): one image per grid row, its gate row staged in shared
+// memory as fp32 once, four independent 16-byte loads in flight per thread, no per-element
+// operand branches (the generic kernel above carries every PER_CHANNEL / ADD option).
+constexpr int GM_UNROLL = 4;
+__global__ void __launch_bounds__(256) gate_mul_kernel(const uint16_t* __restrict__ a, int a_cstride, int a_coff,
+                                                       const uint16_t* __restrict__ g, int g_cstride, int g_coff,
+                                                       uint16_t* __restrict__ y, int y_cstride, int y_coff, int HW,
+                                                       int C, int act) {
+  extern __shared__ float gm_gate[];
+  const int n = blockIdx.y;
+  const int C8 = (C + 7) / 8 * 8, groups = C8 / 8;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int c = threadIdx.x; c < C8; c += blockDim.x)
+    gm_gate[c] = c < C ? bf(g[static_cast<long long>(n) * g_cstride + g_coff + c]) : 0.f;
+  __syncthreads();
+  const unsigned total = static_cast<unsigned>(HW) * groups;
+  const long long img = static_cast<long long>(n) * HW;
+  const unsigned step = gridDim.x * blockDim.x;
+  for (unsigned e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += step * GM_UNROLL) {
+    uint4 q[GM_UNROLL];
+    unsigned pix[GM_UNROLL], grp[GM_UNROLL];
+#pragma unroll
+    for (int u = 0; u < GM_UNROLL; ++u) {
+      const unsigned e = e0 + u * step;
+      pix[u] = e / groups;
+      grp[u] = e - pix[u] * groups;
+      q[u] = e < total ? *reinterpret_cast<const uint4*>(a + (img + pix[u]) * a_cstride + a_coff + grp[u] * 8)
+                       : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < GM_UNROLL; ++u) {
+      if (e0 + u * step >= total) break;
+      const int c0 = static_cast<int>(grp[u]) * 8;
+      const float4 g0 = *reinterpret_cast<const float4*>(gm_gate + c0);
+      const float4 g1 = *reinterpret_cast<const float4*>(gm_gate + c0 + 4);
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float f[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = act_f(bfj(q[u], j), act) * gv[j];
+      store8(y + (img + pix[u]) * y_cstride + y_coff + c0, pack8(f), C - c0);
+    }
+  }
+}
+
 // k x k / s average pool with zero padding counted (torch's count_include_pad=True).
 __global__ void __launch_bounds__(256) avgpool2d_kernel(const uint16_t* __restrict__ x, int N, int H, int W, int C,
                                                         int x_cstride, int x_coff, int k, int s, int pad, int Ho,
@@ -492,77 +538,231 @@ __global__ void __launch_bounds__(256) dwconv3_strip_kernel(const uint16_t* __re
 }
 
 
+// The same register-strip 3x3 depthwise conv with the input window staged by ONE 4-D TMA box
+// ([64 channels][IW][IH][1 image], zero-filled outside the image and past channel C) and the
+// thread's filters / bias loaded straight from global (L2) into registers: the per-element
+// staging address math, the cp.async issue and the shared-memory filter copy -- a third of
+// the per-strip instruction stream in the cp.async form (ncu) -- disappear.
+template <int S>
+__global__ void __launch_bounds__(256) dwconv3_tma_kernel(const __grid_constant__ CUtensorMap tmx, int N, int C,
+                                                          const float* __restrict__ w, const float* __restrict__ bias,
+                                                          int pad, int act, int Ho, int Wo, int tiles_h, int tiles_w,
+                                                          uint16_t* __restrict__ y, int y_cstride, int y_coff,
+                                                          float* __restrict__ part) {
+  constexpr int K = 3, TH = 8, TW = 8;
+  constexpr int IH = (TH - 1) * S + K, IW = (TW - 1) * S + K;
+  static_assert(TH % DWS_R == 0 && (TH / DWS_R) * TW * 16 == 256, "one strip per thread");
+  __shared__ __align__(128) uint4 tile[IH * IW * 8];
+  __shared__ uint64_t bar;
+  const int C8 = (C + 7) / 8 * 8;
+  const int cb = blockIdx.y * 64;
+  const int t = blockIdx.x;
+  const int n = t / (tiles_h * tiles_w);
+  const int r = t - n * tiles_h * tiles_w;
+  const int y0 = (r / tiles_w) * TH, x0 = (r % tiles_w) * TW;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    griddep_wait();
+    mbar_arrive_expect_tx(&bar, IH * IW * 128);
+    tma_load_4d(&tmx, &bar, tile, cb, x0 * S - pad, y0 * S - pad, n);
+  }
+  griddep_launch_dependents();
+  const int hg = threadIdx.x & 15;
+  const int ox = (threadIdx.x >> 4) & 7;
+  const int oy0 = (threadIdx.x >> 7) * DWS_R;
+  const int c0 = cb + hg * 4;
+  const bool live = c0 < C && x0 + ox < Wo && y0 + oy0 < Ho;
+  float wr[K * K][4], bv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (live) {
+#pragma unroll
+    for (int tap = 0; tap < K * K; ++tap) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(w + tap * C8 + c0));
+      wr[tap][0] = v.x; wr[tap][1] = v.y; wr[tap][2] = v.z; wr[tap][3] = v.w;
+    }
+    if (bias) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = c0 + j < C ? __ldg(bias + c0 + j) : 0.f;
+    }
+  }
+  mbar_wait(&bar, 0);
+  float psum[4] = {0.f, 0.f, 0.f, 0.f};
+  if (live) {
+    float acc[DWS_R][4];
+#pragma unroll
+    for (int q = 0; q < DWS_R; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[q][j] = bv[j];
+    const uint2* tile2 = reinterpret_cast<const uint2*>(tile);
+#pragma unroll
+    for (int i = 0; i < (DWS_R - 1) * S + K; ++i) {
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx) {
+        const uint2 v = tile2[((oy0 * S + i) * IW + ox * S + dx) * 16 + hg];
+        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
+#pragma unroll
+        for (int q = 0; q < DWS_R; ++q) {
+          const int dy = i - q * S;
+          if (dy >= 0 && dy < K) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[q][j] = fmaf(wr[dy * K + dx][j], f[j], acc[q][j]);
+          }
+        }
+      }
+    }
+    const int nc = min(4, C - c0);
+#pragma unroll
+    for (int q = 0; q < DWS_R; ++q) {
+      if (y0 + oy0 + q >= Ho) break;
+      const uint2 o = make_uint2(cvt_bf16x2(act_f(acc[q][0], act), act_f(acc[q][1], act)),
+                                 cvt_bf16x2(act_f(acc[q][2], act), act_f(acc[q][3], act)));
+      if (part) {
+        psum[0] += __uint_as_float(o.x << 16);
+        psum[1] += __uint_as_float(o.x & 0xffff0000u);
+        psum[2] += __uint_as_float(o.y << 16);
+        psum[3] += __uint_as_float(o.y & 0xffff0000u);
+      }
+      uint16_t* p = y + ((static_cast<long long>(n) * Ho + y0 + oy0 + q) * Wo + x0 + ox) * y_cstride + y_coff + c0;
+      if (nc == 4) {
+        *reinterpret_cast<uint2*>(p) = o;
+      } else {
+        for (int j = 0; j < nc; ++j) {
+          const uint32_t h = j < 2 ? o.x : o.y;
+          p[j] = static_cast<uint16_t>((j & 1) ? (h >> 16) : (h & 0xffffu));
+        }
+      }
+    }
+  }
+  if (part) {
+    __syncthreads();
+    float4* red = reinterpret_cast<float4*>(tile);
+    red[threadIdx.x] = make_float4(psum[0], psum[1], psum[2], psum[3]);
+    __syncthreads();
+    if (threadIdx.x < 64 && cb + threadIdx.x < C8) {
+      const float* rf = reinterpret_cast<const float*>(red);
+      float sum = 0.f;
+#pragma unroll
+      for (int it = 0; it < 16; ++it) sum += rf[(it * 16 + (threadIdx.x >> 2)) * 4 + (threadIdx.x & 3)];
+      part[static_cast<long long>(t) * C8 + cb + threadIdx.x] = sum;
+    }
+  }
+}
+
+
 // Direct stem conv on CUDA cores for few input channels (MobileNetV3 / EfficientNetV2:
 // 3x3/s2 on the 3 image planes).  Reads the fp32 NCHW model input through the INPUT
-// node's GATHER (idx), BN folded into w/bias, activation fused, NHWC bf16 out.  A CTA
-// computes an 8 x 16 output tile: the cin input windows and all weights are staged in
-// shared memory once; a thread owns one pixel x 32 output channels (the warp's 32 pixels
-// share the channel block, so every weight read is a broadcast).  At cin <= 4 the
-// tensor-core im2col stem spends its time building a 9x-expanded operand; here the input
-// is read once and the output written once.
-constexpr int DS_TH = 8, DS_TW = 16;
-__global__ void __launch_bounds__(256) conv_direct_kernel(const float* __restrict__ x, int N, int C, int H, int W,
-                                                          const int32_t* __restrict__ idx, int cin, const float* __restrict__ w,
-                                                          const float* __restrict__ bias, int cout, int k, int s,
-                                                          int pad, int act, int Ho, int Wo, int tiles_h, int tiles_w,
-                                                          uint16_t* __restrict__ y, int y_cstride, int y_coff) {
+// node's GATHER (idx), BN folded into w/bias, activation fused, NHWC bf16 out.  A CTA of
+// 128 threads computes a 16 x 16 output tile: the cin input windows and all weights are
+// staged in shared memory (the window's loads issued DS_BATCH at a time per thread, not as a
+// chain of dependent round trips); a thread owns two pixels (rows oy, oy + 8) x a block of
+// CB output channels, so each 16-byte weight broadcast feeds 8 FMAs and the channel block
+// is pad8(cout) for narrow stems (no FMAs on padding channels beyond the next multiple of 8).
+// At cin <= 4 the tensor-core im2col stem spends its time building a 9x-expanded operand;
+// here the input is read once and the output written once.
+constexpr int DS_TH = 16, DS_TW = 16, DS_THREADS = 128, DS_BATCH = 8;
+template <int CB, int KT, int ST>  // KT / ST: compile-time filter size / stride (0: runtime k, s)
+__global__ void __launch_bounds__(DS_THREADS) conv_direct_kernel(const float* __restrict__ x, int N, int C, int H,
+                                                                 int W, const int32_t* __restrict__ idx, int cin,
+                                                                 const float* __restrict__ w,
+                                                                 const float* __restrict__ bias, int cout, int k_,
+                                                                 int s_, int pad, int act, int Ho, int Wo,
+                                                                 int tiles_h, int tiles_w, uint16_t* __restrict__ y,
+                                                                 int y_cstride, int y_coff) {
   extern __shared__ float ds_smem[];
+  const int k = KT ? KT : k_, s = ST ? ST : s_;
   const int IH = (DS_TH - 1) * s + k, IW = (DS_TW - 1) * s + k;
-  const int cout32 = (cout + 31) / 32 * 32;
-  float* sx = ds_smem;                      // [cin][IH][IW]
-  float* sw = sx + cin * IH * IW;           // [k*k*cin][cout32]
-  float* sb = sw + k * k * cin * cout32;    // [cout32]
+  const int coutp = (cout + CB - 1) / CB * CB;      // weight row length (multiple of CB)
+  float* sx = ds_smem;                              // [cin][IH][IW]
+  float* sw = sx + (cin * IH * IW + 3) / 4 * 4;     // [k*k*cin][coutp], 16-byte aligned rows
+  float* sb = sw + k * k * cin * coutp;             // [coutp]
   const int t = blockIdx.x;
   const int n = t / (tiles_h * tiles_w);
   const int r = t - n * tiles_h * tiles_w;
   const int y0 = (r / tiles_w) * DS_TH, x0 = (r % tiles_w) * DS_TW;
   const int iy0 = y0 * s - pad, ix0 = x0 * s - pad;
-  for (int e = threadIdx.x; e < k * k * cin * cout32; e += blockDim.x) sw[e] = w[e];
-  for (int e = threadIdx.x; e < cout32; e += blockDim.x) sb[e] = (bias && e < cout) ? bias[e] : 0.f;
+  for (int e = threadIdx.x; e < k * k * cin * coutp; e += DS_THREADS) sw[e] = w[e];
+  for (int e = threadIdx.x; e < coutp; e += DS_THREADS) sb[e] = (bias && e < cout) ? bias[e] : 0.f;
   griddep_wait();
   griddep_launch_dependents();
-  for (int e = threadIdx.x; e < cin * IH * IW; e += blockDim.x) {
-    const int c = e / (IH * IW);
-    const int rr = e - c * IH * IW;
-    const int iy = iy0 + rr / IW, ix = ix0 + rr % IW;
-    float v = 0.f;
-    if (iy >= 0 && iy < H && ix >= 0 && ix < W)
-      v = __ldg(x + ((static_cast<long long>(n) * C + __ldg(idx + c)) * H + iy) * W + ix);
-    sx[e] = v;
+  const int total = cin * IH * IW;
+  for (int e0 = threadIdx.x; e0 < total; e0 += DS_THREADS * DS_BATCH) {
+    float v[DS_BATCH];
+#pragma unroll
+    for (int u = 0; u < DS_BATCH; ++u) {
+      const int e = e0 + u * DS_THREADS;
+      v[u] = 0.f;
+      if (e < total) {
+        const int row = e / IW, col = e - row * IW;
+        const int c = row / IH;
+        const int iy = iy0 + row - c * IH, ix = ix0 + col;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+          v[u] = __ldg(x + ((static_cast<long long>(n) * C + __ldg(idx + c)) * H + iy) * W + ix);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DS_BATCH; ++u)
+      if (e0 + u * DS_THREADS < total) sx[e0 + u * DS_THREADS] = v[u];
   }
   __syncthreads();
-  const int pix = threadIdx.x & 127;
-  const int oy = pix / DS_TW, ox = pix % DS_TW;
-  const bool live = y0 + oy < Ho && x0 + ox < Wo;
-  for (int cb = (threadIdx.x >> 7) * 32; cb < cout32; cb += 64) {
-    float acc[32];
+  const int oy = threadIdx.x / DS_TW, ox = threadIdx.x % DS_TW;  // pixels (oy, ox) and (oy + 8, ox)
+  const bool live0 = y0 + oy < Ho && x0 + ox < Wo, live1 = y0 + oy + 8 < Ho && x0 + ox < Wo;
+  const int down = 8 * s * IW;
+  for (int cb = 0; cb < coutp; cb += CB) {
+    float acc0[CB], acc1[CB];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) acc[j] = sb[cb + j];
+    for (int j = 0; j < CB; ++j) acc0[j] = acc1[j] = sb[cb + j];
     for (int c = 0; c < cin; ++c) {
-      for (int dy = 0; dy < k; ++dy) {
-        const float* row = sx + (c * IH + oy * s + dy) * IW + ox * s;
-        for (int dx = 0; dx < k; ++dx) {
-          const float v = row[dx];
-          const float* wt = sw + ((dy * k + dx) * cin + c) * cout32 + cb;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = fmaf(wt[j], v, acc[j]);
+      for (int dy = 0; dy < (KT ? KT : k); ++dy) {
+        const float* row = sx + (c * IH + oy * s + dy) * IW + ox * s;
+#pragma unroll
+        for (int dx = 0; dx < (KT ? KT : k); ++dx) {
+          const float v0 = row[dx], v1 = row[dx + down];
+          const float4* wt = reinterpret_cast<const float4*>(sw + ((dy * k + dx) * cin + c) * coutp + cb);
+#pragma unroll
+          for (int j4 = 0; j4 < CB / 4; ++j4) {
+            const float4 q = wt[j4];
+            acc0[4 * j4] = fmaf(q.x, v0, acc0[4 * j4]);
+            acc0[4 * j4 + 1] = fmaf(q.y, v0, acc0[4 * j4 + 1]);
+            acc0[4 * j4 + 2] = fmaf(q.z, v0, acc0[4 * j4 + 2]);
+            acc0[4 * j4 + 3] = fmaf(q.w, v0, acc0[4 * j4 + 3]);
+            acc1[4 * j4] = fmaf(q.x, v1, acc1[4 * j4]);
+            acc1[4 * j4 + 1] = fmaf(q.y, v1, acc1[4 * j4 + 1]);
+            acc1[4 * j4 + 2] = fmaf(q.z, v1, acc1[4 * j4 + 2]);
+            acc1[4 * j4 + 3] = fmaf(q.w, v1, acc1[4 * j4 + 3]);
+          }
         }
       }
     }
-    if (live) {
-      uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy) * Wo + x0 + ox) * y_cstride + y_coff + cb;
-      if (cb + 32 <= cout) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+    for (int h = 0; h < 2; ++h) {
+      if (!(h ? live1 : live0)) continue;
+      const float* acc = h ? acc1 : acc0;
+      uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy + 8 * h) * Wo + x0 + ox) * y_cstride + y_coff + cb;
+      // whole 8-channel groups as 16-byte stores, then bf16 pairs, then a single channel
+      // (2-byte stores at a 48-byte pixel pitch cost 14x the written bytes in L2 transactions)
+      const int nc = cout - cb;
+#pragma unroll
+      for (int q = 0; q < CB / 8; ++q) {
+        if (8 * q + 8 <= nc) {
           float f[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) f[j] = act_f(acc[q * 8 + j], act);
           *reinterpret_cast<uint4*>(yp + q * 8) = pack8(f);
-        }
-      } else {
+        } else if (8 * q < nc) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cb + j < cout) yp[j] = tobf(act_f(acc[j], act));
+          for (int j = 0; j < 8; j += 2) {
+            if (8 * q + j + 2 <= nc)
+              *reinterpret_cast<uint32_t*>(yp + q * 8 + j) =
+                  cvt_bf16x2(act_f(acc[q * 8 + j], act), act_f(acc[q * 8 + j + 1], act));
+            else if (8 * q + j < nc)
+              yp[q * 8 + j] = tobf(act_f(acc[q * 8 + j], act));
+          }
+        }
       }
     }
   }
@@ -753,6 +953,19 @@ extern "C" int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream) {
                    a16(d->b, d->b_cstride, d->b_coff) && a16(d->gate, d->gate_cstride, d->gate_coff);
   const long long work = static_cast<long long>(d->N) * d->HW * (vec ? (d->C + 7) / 8 : d->C);
   if (work >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_eltwise: tensor too large");
+  static const bool gate_fast = !std::getenv("UB_ELT_GENERIC");
+  if (gate_fast && vec && d->gate && !d->b && !d->scale && !d->shift && d->N <= 65535 && d->C <= 8192) {
+    const long long per_img = static_cast<long long>(d->HW) * ((d->C + 7) / 8);
+    long long gx = (per_img + 256LL * GM_UNROLL - 1) / (256LL * GM_UNROLL);
+    if (gx < 1) gx = 1;
+    const size_t smem = static_cast<size_t>((d->C + 7) / 8 * 8) * sizeof(float);
+    const cudaError_t e = launch_pdl(gate_mul_kernel, dim3(static_cast<unsigned>(gx), d->N), dim3(256), smem, stream,
+                                     static_cast<const uint16_t*>(d->a), d->a_cstride, d->a_coff,
+                                     static_cast<const uint16_t*>(d->gate), d->gate_cstride, d->gate_coff,
+                                     static_cast<uint16_t*>(d->y), d->y_cstride, d->y_coff, d->HW, d->C, d->act);
+    count_launch();
+    return cuda_status(e, "eltwise_kernel");
+  }
   const int grid = grid_for(work, 256, 2);
   const cudaError_t e = vec ? launch_pdl(eltwise_kernel<true>, dim3(grid), dim3(256), 0, stream, *d)
                             : launch_pdl(eltwise_kernel<false>, dim3(grid), dim3(256), 0, stream, *d);
@@ -805,7 +1018,27 @@ extern "C" int ub_dwconv_pool(const void* x, int N, int H, int W, int C, int x_c
     if (tiles < (1ll << 31)) {
       const dim3 grid(static_cast<unsigned>(tiles), (C + 63) / 64);
       cudaError_t e;
-      if (k == 3 && dw_strips_enabled()) {
+      static const bool use_tma = !std::getenv("UB_DW_NOTMA");
+      CUtensorMap tmx{};
+      bool tma_ok = false;
+      if (k == 3 && dw_strips_enabled() && use_tma) {
+        const int ih = 7 * s + 3;
+        const cuuint64_t xs = static_cast<cuuint64_t>(x_cstride) * 2;
+        cuuint64_t xd[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                            static_cast<cuuint64_t>(N)};
+        cuuint64_t xst[3] = {xs, xs * W, xs * W * H};
+        cuuint32_t xb[4] = {64, static_cast<cuuint32_t>(ih), static_cast<cuuint32_t>(ih), 1};
+        cuuint32_t xe[4] = {1, 1, 1, 1};
+        tma_ok = encode_tiled_fn()(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                                   const_cast<uint16_t*>(static_cast<const uint16_t*>(x)) + x_coff, xd, xst, xb, xe,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        if (tma_ok) apply_small_tensor_quirk(&tmx, static_cast<size_t>(N) * H * W * x_cstride * 2);
+      }
+      if (tma_ok) {
+        e = launch_pdl(s == 1 ? dwconv3_tma_kernel<1> : dwconv3_tma_kernel<2>, grid, dim3(256), 0, stream, tmx, N, C,
+                       w, bias, pad, act, Ho, Wo, th, tw, static_cast<uint16_t*>(y), y_cstride, y_coff, part);
+      } else if (k == 3 && dw_strips_enabled()) {
         e = launch_pdl(s == 1 ? dwconv3_strip_kernel<1> : dwconv3_strip_kernel<2>, grid, dim3(256), 0, stream,
                        static_cast<const uint16_t*>(x), N, H, W, C, x_cstride, x_coff, w, bias, pad, act, Ho, Wo, th,
                        tw, static_cast<uint16_t*>(y), y_cstride, y_coff, part);
@@ -869,6 +1102,14 @@ extern "C" int ub_linear_small(const void* x, int M, int x_cstride, const int32_
   return cuda_status(e, "linear_small_kernel");
 }
 
+// the channel block of ub_conv_direct for a given cout: pad8(cout) up to 32, else 32
+int direct_cb(int cout) { return cout >= 32 ? 32 : (cout + 7) / 8 * 8; }
+
+extern "C" int ub_conv_direct_wcols(int cout) {
+  const int cb = direct_cb(cout);
+  return (cout + cb - 1) / cb * cb;
+}
+
 extern "C" int ub_conv_direct(const float* x, int N, int C, int H, int W, const int32_t* idx, int cin, const float* w,
                               const float* bias, int cout, int k, int s, int pad, int act, void* y, int y_cstride,
                               int y_coff, cudaStream_t stream) {
@@ -876,19 +1117,28 @@ extern "C" int ub_conv_direct(const float* x, int N, int C, int H, int W, const 
       pad < 0 || act < UB_ACT_NONE || act > UB_ACT_SIGMOID)
     return fail(UB_EINVAL, "ub_conv_direct: bad arguments");
   if (cin > 8 || k > 7 || cout > 256) return fail(UB_EUNSUPPORTED, "ub_conv_direct: cin %d k %d cout %d", cin, k, cout);
-  if (!a16(y, y_cstride, y_coff) || y_coff + cout > y_cstride)
-    return fail(UB_EINVAL, "ub_conv_direct: output rows must be 16-byte aligned");
+  if (!a16(y, y_cstride, y_coff) || y_coff + cout > y_cstride || (reinterpret_cast<uintptr_t>(w) & 15))
+    return fail(UB_EINVAL, "ub_conv_direct: output rows / weights must be 16-byte aligned");
   const int Ho = (H + 2 * pad - k) / s + 1, Wo = (W + 2 * pad - k) / s + 1;
   const int IH = (DS_TH - 1) * s + k, IW = (DS_TW - 1) * s + k;
-  const int cout32 = (cout + 31) / 32 * 32;
-  const size_t smem = (static_cast<size_t>(cin) * IH * IW + static_cast<size_t>(k) * k * cin * cout32 + cout32) * 4;
+  const int cb = direct_cb(cout), coutp = ub_conv_direct_wcols(cout);
+  const size_t smem =
+      ((static_cast<size_t>(cin) * IH * IW + 3) / 4 * 4 + static_cast<size_t>(k) * k * cin * coutp + coutp) * 4;
   if (smem > 200 * 1024) return fail(UB_EUNSUPPORTED, "ub_conv_direct: shared memory");
-  if (const cudaError_t ae = ensure_max_smem(conv_direct_kernel)) return cuda_status(ae, "conv_direct attr");
+  void (*kern)(const float*, int, int, int, int, const int32_t*, int, const float*, const float*, int, int, int, int,
+               int, int, int, int, int, uint16_t*, int, int);
+  if (k == 3 && s == 2)  // the MobileNetV3 / EfficientNetV2 stems: unrolled taps, constant window geometry
+    kern = cb == 8 ? conv_direct_kernel<8, 3, 2> : cb == 16 ? conv_direct_kernel<16, 3, 2>
+         : cb == 24 ? conv_direct_kernel<24, 3, 2> : conv_direct_kernel<32, 3, 2>;
+  else
+    kern = cb == 8 ? conv_direct_kernel<8, 0, 0> : cb == 16 ? conv_direct_kernel<16, 0, 0>
+         : cb == 24 ? conv_direct_kernel<24, 0, 0> : conv_direct_kernel<32, 0, 0>;
+  if (const cudaError_t ae = ensure_max_smem(kern)) return cuda_status(ae, "conv_direct attr");
   const int th = (Ho + DS_TH - 1) / DS_TH, tw = (Wo + DS_TW - 1) / DS_TW;
   const long long tiles = static_cast<long long>(N) * th * tw;
   if (tiles >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_conv_direct: too many tiles");
-  const cudaError_t e = launch_pdl(conv_direct_kernel, dim3(static_cast<unsigned>(tiles)), dim3(256), smem, stream, x,
-                                   N, C, H, W, idx, cin, w, bias, cout, k, s, pad, act, Ho, Wo, th, tw,
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(tiles)), dim3(DS_THREADS), smem, stream, x, N, C,
+                                   H, W, idx, cin, w, bias, cout, k, s, pad, act, Ho, Wo, th, tw,
                                    static_cast<uint16_t*>(y), y_cstride, y_coff);
   count_launch();
   return cuda_status(e, "conv_direct_kernel");

@@ -1153,8 +1153,7 @@ class Engine:
             Wsel = Wf[rr.clamp_min(0)][:, cc.clamp_min(0)] * (rr >= 0).view(-1, 1, 1, 1) * (cc >= 0).view(1, -1, 1, 1)
             if scale is not None:
                 Wsel = Wsel * scale.detach().float().cpu().view(-1, 1, 1, 1)
-            c32 = (cout + 31) // 32 * 32
-            wd = torch.zeros(kk * kk, cin, c32)
+            wd = torch.zeros(kk * kk, cin, _lib.load().ub_conv_direct_wcols(cout))
             wd[:, :, :cout] = Wsel.permute(2, 3, 1, 0).reshape(kk * kk, cin, cout)
             wd = wd.to(self.device).contiguous()
             self._keep.append(wd)

@@ -349,7 +349,7 @@ def linear_small(x: Act, xcol_dev: torch.Tensor, w: torch.Tensor, O: int, y: Act
 
 def conv_direct(x_nchw: torch.Tensor, idx_dev: torch.Tensor, w: torch.Tensor, bias, cout: int, k: int, stride: int,
                 pad: int, act: int, y: Act) -> None:
-    """ub_conv_direct: few-channel stem on CUDA cores; w fp32 [k*k, cin, pad32(cout)]."""
+    """ub_conv_direct: few-channel stem on CUDA cores; w fp32 [k*k, cin, ub_conv_direct_wcols(cout)]."""
     N, C, H, W = x_nchw.shape
     _lib.call("ub_conv_direct", _p(x_nchw), N, C, H, W, _p(idx_dev), idx_dev.numel(), _p(w), _p(bias), cout, k, stride,
               pad, act, _p(y.buf), y.cstride, y.coff, _stream())

@@ -627,6 +627,31 @@ def test_eltwise(act, aligned):
     assert _rel(y.to_nchw().cpu(), ref) < 1e-2
 
 
+@pytest.mark.parametrize("N,HW,C,act", [(3, 49, 1159, "none"), (2, 196, 710, "silu"), (1, 9, 13, "none"),
+                                        (5, 3, 64, "hardswish")])
+def test_eltwise_gate_only(N, HW, C, act):
+    """The squeeze-excitation `mul` (gate only: ub_eltwise's dedicated gate kernel), output at
+    a channel offset of a wider row; bit-exact against the same bf16 arithmetic in torch."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(N * HW + C)
+    cs = (C + 7) // 8 * 8 + 16
+    a = K.act_from_nchw(torch.randn(N, cs, HW, 1, generator=g).to(dev)).view(8, C)
+    gate = K.act_from_nchw(torch.rand(N, C, 1, 1, generator=g).to(dev))
+    yb = K.empty_act(N, HW, 1, cs, dev)
+    yb.buf.fill_(7.0)
+    y = yb.view(16, C)
+    K.eltwise(a, y, None, None, None, act, gate)
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "silu": torch.nn.functional.silu, "hardswish": torch.nn.functional.hardswish}
+    ref = fns[act](a.to_nchw().cpu()) * gate.to_nchw().cpu()
+    got = y.to_nchw().cpu()
+    assert _rel(got, ref) < 1e-2
+    if act == "none":
+        assert torch.equal(got, ref.to(torch.bfloat16).float())
+    full = yb.buf.float().cpu()
+    assert (full[:, :16] == 7.0).all() and (full[:, 16 + C:] == 7.0).all()  # neighbours untouched
+
+
 def test_avgpool2d():
     dev = "cuda"
     x = torch.randn(2, 45, 13, 14, generator=torch.Generator().manual_seed(3))
@@ -727,7 +752,8 @@ def test_avgpool_split(N, H, C):
 
 
 @pytest.mark.parametrize("cin,k,s,cout,act", [(3, 3, 2, 24, "silu"), (2, 3, 2, 16, "hardswish"), (3, 7, 2, 70, "relu"),
-                                               (1, 5, 1, 40, "none")])
+                                               (1, 5, 1, 40, "none"), (3, 3, 2, 22, "silu"), (2, 3, 2, 13, "relu"),
+                                               (3, 3, 1, 7, "none")])
 def test_conv_direct(cin, k, s, cout, act):
     """ub_conv_direct (few-channel stem on CUDA cores, INPUT GATHER applied) vs torch fp32."""
     dev = "cuda"
@@ -739,8 +765,7 @@ def test_conv_direct(cin, k, s, cout, act):
     b = torch.randn(cout, generator=g)
     pad = k // 2
     Ho, Wo = (H + 2 * pad - k) // s + 1, (W + 2 * pad - k) // s + 1
-    c32 = (cout + 31) // 32 * 32
-    wd = torch.zeros(k * k, cin, c32)
+    wd = torch.zeros(k * k, cin, _lib.load().ub_conv_direct_wcols(cout))
     wd[:, :, :cout] = Wt.permute(2, 3, 1, 0).reshape(k * k, cin, cout)
     y = K.empty_act(N, Ho, Wo, cout, dev)
     K.conv_direct(x.to(dev), torch.tensor(idx, dtype=torch.int32, device=dev), wd.to(dev), b.to(dev), cout, k, s, pad,
