@@ -90,47 +90,55 @@ __global__ void __launch_bounds__(256) eltwise_kernel(ub_eltwise_desc d) {
 }
 
 // y = act(a) * gate[n] (the squeeze-excitation `mul`, a positional ADD of the lowering with
-// the gate broadcast over the pixels): one image per grid row, its gate row staged in shared
-// memory as fp32 once, four independent 16-byte loads in flight per thread, no per-element
-// operand branches (the generic kernel above carries every PER_CHANNEL / ADD option).
+// the gate broadcast over the pixels): one image per grid row; per thread GM_UNROLL
+// independent 16-byte loads of `a` and of the (L1-resident) gate row in flight together,
+// no per-element operand branches (the generic kernel above carries every PER_CHANNEL /
+// ADD option).  ncu: staging the gate row in shared memory first put a dependent global
+// round trip and a barrier in front of every CTA's only batch of loads.
 constexpr int GM_UNROLL = 4;
+template <bool ACT>  // ACT: apply a UB_ACT_* activation to `a` first (else the plain product)
 __global__ void __launch_bounds__(256) gate_mul_kernel(const uint16_t* __restrict__ a, int a_cstride, int a_coff,
                                                        const uint16_t* __restrict__ g, int g_cstride, int g_coff,
                                                        uint16_t* __restrict__ y, int y_cstride, int y_coff, int HW,
                                                        int C, int act) {
-  extern __shared__ float gm_gate[];
   const int n = blockIdx.y;
-  const int C8 = (C + 7) / 8 * 8, groups = C8 / 8;
+  const int groups = (C + 7) / 8;
+  const float inv_groups = 1.f / static_cast<float>(groups);
   griddep_wait();
   griddep_launch_dependents();
-  for (int c = threadIdx.x; c < C8; c += blockDim.x)
-    gm_gate[c] = c < C ? bf(g[static_cast<long long>(n) * g_cstride + g_coff + c]) : 0.f;
-  __syncthreads();
-  const unsigned total = static_cast<unsigned>(HW) * groups;
-  const long long img = static_cast<long long>(n) * HW;
-  const unsigned step = gridDim.x * blockDim.x;
-  for (unsigned e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += step * GM_UNROLL) {
-    uint4 q[GM_UNROLL];
-    unsigned pix[GM_UNROLL], grp[GM_UNROLL];
+  const int total = HW * groups;
+  // per-image base pointers once; 32-bit offsets inside the image
+  const uint16_t* ai = a + static_cast<long long>(n) * HW * a_cstride + a_coff;
+  uint16_t* yi = y + static_cast<long long>(n) * HW * y_cstride + y_coff;
+  const uint16_t* gi = g + static_cast<long long>(n) * g_cstride + g_coff;
+  const int step = gridDim.x * blockDim.x;
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += step * GM_UNROLL) {
+    uint4 q[GM_UNROLL], qg[GM_UNROLL];
+    int pix[GM_UNROLL], grp[GM_UNROLL];
 #pragma unroll
     for (int u = 0; u < GM_UNROLL; ++u) {
-      const unsigned e = e0 + u * step;
-      pix[u] = e / groups;
-      grp[u] = e - pix[u] * groups;
-      q[u] = e < total ? *reinterpret_cast<const uint4*>(a + (img + pix[u]) * a_cstride + a_coff + grp[u] * 8)
-                       : make_uint4(0, 0, 0, 0);
+      const int e = e0 + u * step;
+      // e / groups by a float reciprocal and one correction step (exact for e < 2^24)
+      int pq = static_cast<int>(static_cast<float>(e) * inv_groups);
+      int rm = e - pq * groups;
+      if (rm < 0) { --pq; rm += groups; }
+      if (rm >= groups) { ++pq; rm -= groups; }
+      pix[u] = pq;
+      grp[u] = rm;
+      const bool ok = e < total;
+      q[u] = ok ? *reinterpret_cast<const uint4*>(ai + pq * a_cstride + rm * 8) : make_uint4(0, 0, 0, 0);
+      qg[u] = ok ? __ldg(reinterpret_cast<const uint4*>(gi + rm * 8)) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < GM_UNROLL; ++u) {
       if (e0 + u * step >= total) break;
-      const int c0 = static_cast<int>(grp[u]) * 8;
-      const float4 g0 = *reinterpret_cast<const float4*>(gm_gate + c0);
-      const float4 g1 = *reinterpret_cast<const float4*>(gm_gate + c0 + 4);
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const int c0 = grp[u] * 8;
       float f[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) f[j] = act_f(bfj(q[u], j), act) * gv[j];
-      store8(y + (img + pix[u]) * y_cstride + y_coff + c0, pack8(f), C - c0);
+      for (int j = 0; j < 8; ++j) f[j] = (ACT ? act_f(bfj(q[u], j), act) : bfj(q[u], j)) * bfj(qg[u], j);
+      uint16_t* dst = yi + pix[u] * y_cstride + c0;
+      if (c0 + 8 <= C) *reinterpret_cast<uint4*>(dst) = pack8(f);
+      else store8(dst, pack8(f), C - c0);
     }
   }
 }
@@ -954,12 +962,16 @@ extern "C" int ub_eltwise(const ub_eltwise_desc* d, cudaStream_t stream) {
   const long long work = static_cast<long long>(d->N) * d->HW * (vec ? (d->C + 7) / 8 : d->C);
   if (work >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_eltwise: tensor too large");
   static const bool gate_fast = !std::getenv("UB_ELT_GENERIC");
-  if (gate_fast && vec && d->gate && !d->b && !d->scale && !d->shift && d->N <= 65535 && d->C <= 8192) {
+  if (gate_fast && vec && d->gate && !d->b && !d->scale && !d->shift && d->N <= 65535 &&
+      d->gate_coff + (d->C + 7) / 8 * 8 <= d->gate_cstride) {  // gate rows read as whole 16-byte groups
     const long long per_img = static_cast<long long>(d->HW) * ((d->C + 7) / 8);
     long long gx = (per_img + 256LL * GM_UNROLL - 1) / (256LL * GM_UNROLL);
     if (gx < 1) gx = 1;
-    const size_t smem = static_cast<size_t>((d->C + 7) / 8 * 8) * sizeof(float);
-    const cudaError_t e = launch_pdl(gate_mul_kernel, dim3(static_cast<unsigned>(gx), d->N), dim3(256), smem, stream,
+    if (per_img >= (1ll << 24) || static_cast<long long>(d->HW) * d->a_cstride >= (1ll << 31) ||
+        static_cast<long long>(d->HW) * d->y_cstride >= (1ll << 31))
+      return fail(UB_EUNSUPPORTED, "ub_eltwise: image too large for the gate kernel");
+    const cudaError_t e = launch_pdl(d->act == UB_ACT_NONE ? gate_mul_kernel<false> : gate_mul_kernel<true>,
+                                     dim3(static_cast<unsigned>(gx), d->N), dim3(256), 0, stream,
                                      static_cast<const uint16_t*>(d->a), d->a_cstride, d->a_coff,
                                      static_cast<const uint16_t*>(d->gate), d->gate_cstride, d->gate_coff,
                                      static_cast<uint16_t*>(d->y), d->y_cstride, d->y_coff, d->HW, d->C, d->act);
