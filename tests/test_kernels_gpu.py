@@ -652,6 +652,30 @@ def test_eltwise_gate_only(N, HW, C, act):
     assert (full[:, :16] == 7.0).all() and (full[:, 16 + C:] == 7.0).all()  # neighbours untouched
 
 
+@pytest.mark.parametrize("N,HW,C,act", [(2, 49, 1159, "none"), (3, 196, 24, "relu"), (1, 9, 13, "silu")])
+def test_eltwise_add_only(N, HW, C, act):
+    """A residual ADD no epilogue absorbed (ub_eltwise's add kernel): y = act(a + b) at channel
+    offsets of wider rows; bit-exact against the same fp32 sum rounded to bf16."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(N * HW * 7 + C)
+    cs = (C + 7) // 8 * 8 + 16
+    a = K.act_from_nchw(torch.randn(N, cs, HW, 1, generator=g).to(dev)).view(8, C)
+    b = K.act_from_nchw(torch.randn(N, cs, HW, 1, generator=g).to(dev)).view(16, C)
+    yb = K.empty_act(N, HW, 1, cs, dev)
+    yb.buf.fill_(7.0)
+    y = yb.view(8, C)
+    K.eltwise(a, y, None, None, b, act)
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "relu": torch.relu, "silu": torch.nn.functional.silu}
+    ref = fns[act](a.to_nchw().cpu() + b.to_nchw().cpu())
+    got = y.to_nchw().cpu()
+    assert _rel(got, ref) < 1e-2
+    if act != "silu":
+        assert torch.equal(got, ref.to(torch.bfloat16).float())
+    full = yb.buf.float().cpu()
+    assert (full[:, :8] == 7.0).all() and (full[:, 8 + C:] == 7.0).all()
+
+
 def test_avgpool2d():
     dev = "cuda"
     x = torch.randn(2, 45, 13, 14, generator=torch.Generator().manual_seed(3))
