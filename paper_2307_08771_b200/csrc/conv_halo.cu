@@ -505,9 +505,7 @@ __global__ void __maxnreg__(96)
                                         make_float2(b1.z, b1.w));
             uint4 o;
             if (XA) {
-              const int a = p.relu;
-              o = make_uint4(cvt_bf16x2(act_f(s0.x, a), act_f(s0.y, a)), cvt_bf16x2(act_f(s1.x, a), act_f(s1.y, a)),
-                             cvt_bf16x2(act_f(s2.x, a), act_f(s2.y, a)), cvt_bf16x2(act_f(s3.x, a), act_f(s3.y, a)));
+              o = act_pack8(p.relu, s0.x, s0.y, s1.x, s1.y, s2.x, s2.y, s3.x, s3.y);
             } else if (p.relu) {
               o = make_uint4(cvt_relu_bf16x2(s0.x, s0.y), cvt_relu_bf16x2(s1.x, s1.y), cvt_relu_bf16x2(s2.x, s2.y),
                              cvt_relu_bf16x2(s3.x, s3.y));

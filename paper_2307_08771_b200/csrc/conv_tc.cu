@@ -800,10 +800,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
                 uint4 o;
                 const float* f = reinterpret_cast<const float*>(r) + jj * 8;
                 if (XACT) {  // other UB_ACT_* activations (hardswish, SiLU, ...)
-                  o.x = cvt_bf16x2(act_f(f[0], p.relu), act_f(f[1], p.relu));
-                  o.y = cvt_bf16x2(act_f(f[2], p.relu), act_f(f[3], p.relu));
-                  o.z = cvt_bf16x2(act_f(f[4], p.relu), act_f(f[5], p.relu));
-                  o.w = cvt_bf16x2(act_f(f[6], p.relu), act_f(f[7], p.relu));
+                  o = act_pack8(p.relu, f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]);
                 } else if (p.relu) {
                   o.x = cvt_relu_bf16x2(f[0], f[1]);
                   o.y = cvt_relu_bf16x2(f[2], f[3]);

@@ -342,15 +342,44 @@ UB_DEVI uint32_t cvt_bf16x2(float lo, float hi) {
 }
 // Activation codes of include/upscale_b200.h (UB_ACT_*); conv epilogues take the code in
 // their `relu` field (1 = ReLU keeps its packed cvt.relu fast path).
+// tanh.approx.f32: one MUFU op (max relative error ~2^-11, far below the bf16 rounding that
+// follows every activation here)
+UB_DEVI float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 UB_DEVI float act_f(float v, int act) {
   switch (act) {
     case 1: return fmaxf(v, 0.f);
     case 2: return fminf(fmaxf(v, 0.f), 6.f);
     case 3: return v * fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
     case 4: return fminf(fmaxf(v + 3.f, 0.f), 6.f) * (1.f / 6.f);
-    case 5: return __fdividef(v, 1.f + __expf(-v));  // fast reciprocal: a bf16 store follows
-    case 6: return __fdividef(1.f, 1.f + __expf(-v));
+    // SiLU / sigmoid through sigmoid(v) = (1 + tanh(v / 2)) / 2: one MUFU op per value instead
+    // of exp + reciprocal (the SiLU conv epilogues were bound by the special-function unit)
+    case 5: { const float h = 0.5f * v; return fmaf(h, tanh_fast(h), h); }
+    case 6: return fmaf(0.5f, tanh_fast(0.5f * v), 0.5f);
     default: return v;
+  }
+}
+// 8 fp32 -> activation -> 8 packed bf16, the activation switch resolved ONCE per call: a
+// per-element switch on a runtime code (act_f) compiles to an indirect branch per value and
+// serialises the epilogue's exp / reciprocal chains (ncu: a SiLU conv epilogue ran 4x slower
+// than the ReLU one); here each case is straight-line code with 8 independent chains.
+template <int A>
+UB_DEVI uint4 act_pack8_c(float f0, float f1, float f2, float f3, float f4, float f5, float f6, float f7) {
+  return make_uint4(cvt_bf16x2(act_f(f0, A), act_f(f1, A)), cvt_bf16x2(act_f(f2, A), act_f(f3, A)),
+                    cvt_bf16x2(act_f(f4, A), act_f(f5, A)), cvt_bf16x2(act_f(f6, A), act_f(f7, A)));
+}
+UB_DEVI uint4 act_pack8(int act, float f0, float f1, float f2, float f3, float f4, float f5, float f6, float f7) {
+  switch (act) {
+    case 1: return act_pack8_c<1>(f0, f1, f2, f3, f4, f5, f6, f7);
+    case 2: return act_pack8_c<2>(f0, f1, f2, f3, f4, f5, f6, f7);
+    case 3: return act_pack8_c<3>(f0, f1, f2, f3, f4, f5, f6, f7);
+    case 4: return act_pack8_c<4>(f0, f1, f2, f3, f4, f5, f6, f7);
+    case 5: return act_pack8_c<5>(f0, f1, f2, f3, f4, f5, f6, f7);
+    case 6: return act_pack8_c<6>(f0, f1, f2, f3, f4, f5, f6, f7);
+    default: return act_pack8_c<0>(f0, f1, f2, f3, f4, f5, f6, f7);
   }
 }
 UB_DEVI uint32_t cvt_relu_bf16x2(float lo, float hi) {

@@ -68,7 +68,13 @@ CASES = {
     "small_stem_multi": (4, 224, 224, 8, 0, 2, 64, 7, 2, 3, 0, False, True),
     "stem_s2d_4x4": (256, 115, 115, 8, 0, 8, 64, 4, 1, 0, 0, False, True),
     "l1_conv2_c16": (256, 56, 56, 16, 0, 16, 64, 3, 1, 1, 0, False, True),
+    # EfficientNetV2-S @ 50 % MBConv expands (1x1, few input channels, wide output)
+    "eff_s5_expand": (256, 14, 14, 160, 1, 80, 710, 1, 1, 0, 0, False, True),
+    "eff_s5_expand_dense": (256, 14, 14, 80, 0, 80, 710, 1, 1, 0, 0, False, True),
+    "eff_s6_expand": (256, 7, 7, 256, 2, 128, 1159, 1, 1, 0, 0, False, True),
+    "eff_s4_expand": (256, 14, 14, 128, 0, 64, 387, 1, 1, 0, 0, False, True),
 }
+ACT = os.environ.get("UB_BENCH_ACT")  # e.g. silu: the epilogue activation instead of ReLU (no check)
 
 
 def run(name, check=True, iters=20, once=False):
@@ -95,6 +101,8 @@ def run(name, check=True, iters=20, once=False):
     if res is not None:
         res.buf.normal_(generator=g)
     y = K.empty_act(N, Ho, Wo, cout, dev)
+    if ACT:
+        relu, check = _lib.UB_ACT[ACT], False
     K.conv(xa, wg, lead, cpad, cout, k, k, st, pad, y, gather_idx=idx, bias=bias, residual=res, relu=relu, variant=VARIANT)
     torch.cuda.synchronize()
     if once:
