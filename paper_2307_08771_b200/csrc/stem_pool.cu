@@ -72,6 +72,7 @@ struct PoolParams {
   int raw_half;                            // PACK: floats per row of one of the two boxes
   uint32_t raw_box;                        // PACK: smem bytes of one box (128-byte aligned)
   int raw_xoff;                            // PACK: window column of input column 0 (multiple of 4, >= pad)
+  int quad;  // tiles of FOUR conv rows x 32 channels (cout <= 32): band / tile counts in pooled rows / 2
 };
 
 constexpr int SP_PACK_THREADS = 64;  // warps 0 and 3 when packing
@@ -80,15 +81,17 @@ constexpr int SP_PACK_THREADS = 64;  // warps 0 and 3 when packing
 // pair then the pairs of its pooled rows.
 struct TileIter {
   int u, j, j_end, n, yp0;
+  int step;  // pooled rows per tile: 1 (pair of conv rows) or 2 (quad)
   __device__ void start_band(const PoolParams& p) {
+    step = p.quad ? 2 : 1;
     n = u / p.bands_per_img;
     yp0 = (u - n * p.bands_per_img) * p.band;
     const int yp1 = min(p.Hp, yp0 + p.band);
     j = yp0 > 0 ? -1 : 0;
-    j_end = yp1 - yp0;
+    j_end = (yp1 - yp0 + step - 1) / step;
   }
   __device__ bool valid(const PoolParams& p) const { return u < p.n_bands; }
-  __device__ int yp() const { return yp0 + j; }
+  __device__ int yp() const { return yp0 + j * step; }  // first pooled row of the tile
   __device__ bool emit() const { return j >= 0; }
   __device__ void next(const PoolParams& p) {
     if (++j >= j_end) {
@@ -98,19 +101,26 @@ struct TileIter {
   }
 };
 
-template <int KQ, bool PACK>  // PACK: the producer warps fold the fp32 input (p.x)
+// QUAD (cout <= 32): a tile is FOUR conv rows 4t .. 4t+3 as one 128-row MMA (lane = r * 32 + c),
+// i.e. two pooled rows 2t (conv rows 4t-1, 4t, 4t+1) and 2t+1 (4t+1 .. 4t+3): every
+// accumulator lane holds a kept channel (the pair form leaves lanes of channels 32-63 empty at
+// 50 % sparsity), (KQ+3)*PAIRS MMAs per two pooled rows instead of 2*(KQ+1)*PAIRS, and half
+// the epilogue work per pooled row.  Warps q = 1, 3 hand their rows over (ring slot: [r1 | r3]);
+// q = 0 pools row 2t with the previous tile's r3, q = 2 pools row 2t+1.
+template <int KQ, bool PACK, bool QUAD = false>  // PACK: the producer warps fold the fp32 input (p.x)
 __global__ void __launch_bounds__(SP_THREADS, 1)
     stem_pool_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmX,
                      const PoolParams p) {
-  constexpr int PAIRS = (KQ + 1) / 2, NMMA = (KQ + 1) * PAIRS;
+  constexpr int ROWS = QUAD ? 4 : 2, CH = QUAD ? 32 : 64;  // conv rows per tile, channels per row
+  constexpr int PAIRS = (KQ + 1) / 2, NMMA = (KQ + ROWS - 1) * PAIRS;
   constexpr uint32_t A_BYTES = 128 * 32;  // one MMA's weights: 128 rows x K 16
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t out_sz = (static_cast<uint32_t>(p.Wp) * 128 + 1023) & ~1023u;
   const uint32_t ring_sz = 64u * p.rw * 4;
   uint8_t* sW = base;                                // NMMA x [khalf][128 rows][16 B]
-  uint8_t* sOut = sW + NMMA * A_BYTES;               // per group: pooled row [xp][64 ch] SW128
-  uint8_t* sRing = sOut + SP_GROUPS * out_sz;        // SP_RING x [64 ch][rw words]
+  uint8_t* sOut = sW + NMMA * A_BYTES;               // per group: pooled row(s) [xp][64 ch] SW128
+  uint8_t* sRing = sOut + SP_GROUPS * (QUAD ? 2 : 1) * out_sz;  // SP_RING x [64 ch][rw words]
   uint8_t* sS = sRing + SP_RING * ring_sz;           // stages x folded rows
   uint64_t* full = reinterpret_cast<uint64_t*>(sS + p.stages * p.stage_bytes);
   uint64_t* empty = full + SP_STAGES_MAX;
@@ -137,7 +147,9 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     }
     for (int r = 0; r < SP_RING; ++r) {
       mbar_init(&hready[r], 2);  // the two odd-row warps of the writing tile
-      mbar_init(&hfree[r], 4);   // the even-row warps of the writing tile and of the next
+      // readers: pair -- the even-row warps of the writing tile and of the next; quad -- warps
+      // q = 0, 2 of the writing tile and q = 0 of the next
+      mbar_init(&hfree[r], QUAD ? 3 : 4);
     }
     if (PACK)
       for (int s = 0; s < p.stages; ++s) mbar_init(&rfull[s], 1);
@@ -149,7 +161,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     const int m = i & 127;
     const int jh = i >> 7;
     const int j = jh >> 1, h = jh & 1;
-    const int r = m >> 6, c = m & 63;
+    const int r = m / CH, c = m % CH;
     const int dy = j / PAIRS - r;
     const int dx = (j % PAIRS) * 2 + h;
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -294,6 +306,108 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
         aph ^= 1;
       }
     }
+  } else if (QUAD && warp >= 4) {  // ================= epilogue, quad tiles
+    const int grp = (warp - 4) >> 2;
+    const int q = warp & 3;  // TMEM lane quarter = conv row r of the tile; lane = channel
+    const int c = lane;
+    const float bias = sBias[c];
+    uint8_t* out = sOut + (grp * 2 + (q >> 1)) * out_sz;  // q = 0: row 2t, q = 2: row 2t+1
+    const int nw = (p.Wp + 1) >> 1;
+    const int chunk8 = c >> 3;
+    const uint32_t cbyte2 = (c & 7) * 2;
+    int it = 0;
+    for (; ti.valid(p); ti.next(p), ++it) {
+      if ((it % SP_GROUPS) != grp) continue;
+      const int a = it % SP_ACC;
+      const int slot = it % SP_RING;
+      const int prev = (it + SP_RING - 1) % SP_RING;
+      if (p.sleep_ns) mbar_wait_sleep(&tfull[a], (it / SP_ACC) & 1, p.sleep_ns);
+      else mbar_wait(&tfull[a], (it / SP_ACC) & 1);
+      tc_fence_after();
+      uint32_t h[SP_COLS / 4];
+      float carry = -INFINITY;
+      const uint32_t taddr = tmem_base + a * SP_COLS + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+      for (int k = 0; k < SP_COLS / 32; ++k) {
+        if (32 * k >= p.Wo) break;
+        uint32_t v[32];
+        tmem_ld32(taddr + 32 * k, v);
+        tmem_ld_wait();
+        float m[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float left = i == 0 ? carry : __uint_as_float(v[2 * i - 1]);
+          m[i] = fmaxf(left, fmaxf(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])));
+        }
+        carry = __uint_as_float(v[31]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          h[8 * k + i] = p.relu ? cvt_relu_bf16x2(m[2 * i] + bias, m[2 * i + 1] + bias)
+                                : cvt_bf16x2(m[2 * i] + bias, m[2 * i + 1] + bias);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+      uint32_t* slot_base = reinterpret_cast<uint32_t*>(sRing + slot * ring_sz);
+      if (q & 1) {
+        // ---- rows r1 (q = 1) and r3 (q = 3) -> ring slot halves [0] / [1]
+        if (lane == 0) mbar_wait(&hfree[slot], ((it / SP_RING) & 1) ^ 1);
+        __syncwarp();
+        uint32_t* dst = slot_base + ((q >> 1) * 32 + c) * p.rw;
+#pragma unroll
+        for (int i = 0; i < SP_COLS / 4; i += 4)
+          if (i < nw) *reinterpret_cast<uint4*>(dst + i) = make_uint4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hready[slot]);
+        continue;
+      }
+      // ---- q = 0: pooled row 2t = max(prev r3, r0, r1); q = 2: row 2t+1 = max(r1, r2, r3)
+      const int yp = ti.yp() + (q >> 1);
+      if (ti.emit() && yp < p.Hp && !(p.dbg & 64)) {
+        const bool use_prev = q == 0 && yp > 0;
+        mbar_wait(&hready[slot], (it / SP_RING) & 1);
+        if (use_prev) mbar_wait(&hready[prev], ((it - 1) / SP_RING) & 1);
+        const uint32_t* r1 = slot_base + c * p.rw;
+        const uint32_t* other = q == 0 ? (use_prev ? reinterpret_cast<const uint32_t*>(sRing + prev * ring_sz) +
+                                                         (32 + c) * p.rw
+                                                   : r1)
+                                       : slot_base + (32 + c) * p.rw;
+        if (lane == 0) bulk_wait_read<0>();  // this warp's previous pooled row has left `out`
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < SP_COLS / 4; i += 4) {
+          if (i >= nw) break;
+          const uint4 o = *reinterpret_cast<const uint4*>(r1 + i);
+          const uint4 pv = *reinterpret_cast<const uint4*>(other + i);
+          h[i] = bf16x2_max3(h[i], o.x, pv.x);
+          h[i + 1] = bf16x2_max3(h[i + 1], o.y, pv.y);
+          h[i + 2] = bf16x2_max3(h[i + 2], o.z, pv.z);
+          h[i + 3] = bf16x2_max3(h[i + 3], o.w, pv.w);
+        }
+#pragma unroll
+        for (int i = 0; i < SP_COLS / 4; ++i) {
+          if (i >= nw) break;
+          const int x0 = 2 * i, x1 = 2 * i + 1;
+          *reinterpret_cast<uint16_t*>(out + x0 * 128 + ((chunk8 ^ (x0 & 7)) << 4) + cbyte2) =
+              static_cast<uint16_t>(h[i] & 0xffffu);
+          if (x1 < p.Wp)
+            *reinterpret_cast<uint16_t*>(out + x1 * 128 + ((chunk8 ^ (x1 & 7)) << 4) + cbyte2) =
+                static_cast<uint16_t>(h[i] >> 16);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmY, out, 0, 0, yp, ti.n);
+          bulk_commit();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&hfree[slot]);                         // done with this tile's r1 / r3
+        if (q == 0 && it > 0) mbar_arrive(&hfree[prev]);   // and with the previous tile's r3
+      }
+    }
+    if (lane == 0) bulk_wait_all();
   } else if (warp >= 4) {  // ================= epilogue
     const int grp = (warp - 4) >> 2;
     const int q = warp & 3;              // TMEM lane quarter: (conv row r, channels 32 (q & 1) ..)
@@ -417,11 +531,11 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
   }
 }
 
-template <int KQ, bool PACK>
+template <int KQ, bool PACK, bool QUAD = false>
 void launch_pool(const CUtensorMap& tm, const CUtensorMap& tmx, const PoolParams& p, int grid, size_t smem,
                  cudaStream_t stream) {
-  (void)ensure_max_smem(stem_pool_kernel<KQ, PACK>);
-  (void)launch_pdl(stem_pool_kernel<KQ, PACK>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, tmx, p);
+  (void)ensure_max_smem(stem_pool_kernel<KQ, PACK, QUAD>);
+  (void)launch_pdl(stem_pool_kernel<KQ, PACK, QUAD>, dim3(grid), dim3(SP_THREADS), smem, stream, tm, tmx, p);
 }
 
 }  // namespace
@@ -480,6 +594,10 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
     p.y_cstride = y_cstride;
   }
   p.cout = cout;
+  // quad tiles (four conv rows x 32 channels per MMA) whenever the kept channels fit 32 lanes
+  static const bool quad_env = !getenv("UB_SP_NOQUAD");
+  p.quad = (quad_env && !x && cout <= 32 && (p.Hp % 2) == 0) ? 1 : 0;
+  const int rows = p.quad ? 4 : 2;
   p.rw = ((p.Wp + 1) / 2 + 3) / 4 * 4;
   if (((p.rw / 4) & 1) == 0) p.rw += 4;
   p.w = static_cast<const uint16_t*>(w);
@@ -489,8 +607,8 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
   // stays inside the buffer for the last pair since S holds Hs = Ho + kq - 1 rows per image
   // plus its tail
   const int pairs = (kq + 1) / 2;
-  const uint32_t load_rows = static_cast<uint32_t>(kq * Ws + 2 * pairs + p.n - 1);
-  const long long last_end = (static_cast<long long>(N - 1) * Hs + Ho - 2) * Ws + load_rows;
+  const uint32_t load_rows = static_cast<uint32_t>((kq + rows - 2) * Ws + 2 * pairs + p.n - 1);
+  const long long last_end = (static_cast<long long>(N - 1) * Hs + Ho - rows) * Ws + load_rows;
   if (last_end * 16 > sbytes) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: staging buffer too small");
   p.load_bytes = load_rows * 16;
   p.stage_bytes = (p.load_bytes + 127) & ~127u;
@@ -511,11 +629,11 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
   const int sms = num_sms();
   int best_band = p.Hp;
   long long best_cost = -1;
-  for (int b = 4; b <= p.Hp; ++b) {
+  for (int b = 4; b <= p.Hp; b += p.quad ? 2 : 1) {  // quad bands start on even pooled rows
     const long long per_img = (p.Hp + b - 1) / b;
     const long long nb = per_img * N;
     const long long waves = (nb + sms - 1) / sms;
-    const long long cost = waves * (b + 1);
+    const long long cost = waves * ((b + rows / 2 - 1) / (rows / 2) + 1);  // tiles per band + halo
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best_band = b;
@@ -526,9 +644,9 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
   const long long n_bands = static_cast<long long>(p.bands_per_img) * N;
   if (n_bands >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: too many bands");
   p.n_bands = static_cast<int>(n_bands);
-  const size_t w_bytes = static_cast<size_t>(kq + 1) * pairs * 128 * 32;
+  const size_t w_bytes = static_cast<size_t>(kq + rows - 1) * pairs * 128 * 32;
   const size_t out_bytes = (static_cast<size_t>(p.Wp) * 128 + 1023) & ~static_cast<size_t>(1023);
-  const size_t fixed = 1024 + w_bytes + SP_GROUPS * out_bytes + SP_RING * 64 * p.rw * 4 + 512 + 64 * 4;
+  const size_t fixed = 1024 + w_bytes + SP_GROUPS * (rows / 2) * out_bytes + SP_RING * 64 * p.rw * 4 + 512 + 64 * 4;
   int stages = static_cast<int>((227 * 1024 - fixed) / p.stage_bytes);
   if (stages < 2) return fail(UB_EUNSUPPORTED, "ub_conv_s2d_maxpool: shared memory");
   p.stages = stages > SP_STAGES_MAX ? SP_STAGES_MAX : stages;
@@ -561,6 +679,15 @@ int stem_maxpool_launch(const void* s, const float* x, int C, const int32_t* idx
     if (rx != CUDA_SUCCESS) return fail(UB_ECUDA, "ub_stem_maxpool: encode input tensor map failed (%d)", (int)rx);
   }
   const int grid = p.n_bands < sms ? p.n_bands : sms;
+  if (p.quad) {
+    switch (kq) {
+      case 2: launch_pool<2, false, true>(tm, tmx, p, grid, smem, stream); break;
+      case 3: launch_pool<3, false, true>(tm, tmx, p, grid, smem, stream); break;
+      default: launch_pool<4, false, true>(tm, tmx, p, grid, smem, stream); break;
+    }
+    count_launch();
+    return cuda_status(cudaGetLastError(), "stem_pool_kernel");
+  }
   switch (kq) {
     case 2: x ? launch_pool<2, true>(tm, tmx, p, grid, smem, stream) : launch_pool<2, false>(tm, tmx, p, grid, smem, stream); break;
     case 3: x ? launch_pool<3, true>(tm, tmx, p, grid, smem, stream) : launch_pool<3, false>(tm, tmx, p, grid, smem, stream); break;

@@ -218,10 +218,14 @@ def test_stem_s2d_pack_exact(N, H, k, pad, idx):
     assert bad.numel() == 0, (bad[:8].tolist(), got[tuple(bad[0])].item(), full[tuple(bad[0])].item())
 
 
-@pytest.mark.parametrize("N,H,idx,cout", [(3, 224, [2, 0], 64), (5, 64, [1], 60), (2, 100, [0, 2], 32)])
+@pytest.mark.parametrize("N,H,idx,cout", [(3, 224, [2, 0], 64), (5, 64, [1], 60), (2, 100, [0, 2], 32),
+                                         (3, 224, [2, 0], 32), (2, 224, [1], 24), (4, 112, [0, 2], 16),
+                                         (37, 224, [2, 0], 32)])
 def test_stem_s2d_maxpool_matches_torch(N, H, idx, cout):
     """Stem with the 3x3/s2/p1 max pool fused into its epilogue (bands of pooled rows,
-    halo pairs, hrow hand-over ring) == conv -> bias -> ReLU -> max_pool2d."""
+    halo tiles, row hand-over ring) == conv -> bias -> ReLU -> max_pool2d.  cout <= 32 with an
+    even pooled height takes the four-conv-rows-per-MMA (quad) form; the fused-pack launch
+    (always the pair form) must agree with it bit for bit."""
     dev = "cuda"
     k, pad = 7, 3
     cin = len(idx)

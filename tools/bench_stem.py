@@ -3,6 +3,7 @@
 python tools/bench_stem.py [N]
 """
 
+import os
 import sys
 from pathlib import Path
 
@@ -40,7 +41,7 @@ def main():
     dev = "cuda"
     x = torch.randn(N, 3, 224, 224, device=dev)
     idx = torch.tensor([2, 0], dtype=torch.int32, device=dev)
-    cout, k, pad = 64, 7, 3
+    cout, k, pad = int(os.environ.get("UB_STEM_COUT", "64")), 7, 3  # ResNet-50 @ 50 %: 32 kept
     Wt = torch.randn(cout, 2, k, k, device=dev) / 10
     wg = K.permute_weights(Wt, list(range(cout)), [0, 1], layout="s2d", out_dtype=torch.bfloat16)
     bias = torch.randn(cout, device=dev)
