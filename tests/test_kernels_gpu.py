@@ -835,13 +835,15 @@ def test_se_gate(N, H, C, C1, C2, acts):
     assert _rel(gate.to_nchw().cpu().reshape(N, C2), ref) < 1e-2
 
 
-@pytest.mark.parametrize("H,stride,C", [(14, 1, 730), (28, 2, 192), (7, 1, 13), (17, 1, 96)])
-def test_dwconv_fused_se_pool(H, stride, C):
+@pytest.mark.parametrize("N,H,stride,C", [(3, 14, 1, 730), (3, 28, 2, 192), (3, 7, 1, 13), (3, 17, 1, 96),
+                                          (45, 7, 1, 1159), (32, 14, 1, 100)])
+def test_dwconv_fused_se_pool(N, H, stride, C):
     """ub_dwconv_pool's per-tile channel sums == the sums of its own stored output, and
-    ub_se_gate_parts over them == ub_se_gate re-reading the tensor (fp32 order only)."""
+    ub_se_gate_parts over them == ub_se_gate re-reading the tensor (fp32 order only; N >= 32
+    takes the several-images-per-CTA gate kernel, N = 45 a ragged last image group)."""
     dev = "cuda"
     g = torch.Generator().manual_seed(H * 100 + C)
-    N, k = 3, 3
+    k = 3
     x = torch.randn(N, C, H, H, generator=g)
     w = torch.randn(C, 1, k, k, generator=g) / k
     b = torch.randn(C, generator=g)
