@@ -779,14 +779,18 @@ def test_avgpool_split(N, H, C):
     assert _rel(y.to_nchw().cpu(), _bf(x).mean(dim=(2, 3), keepdim=True)) < 1e-2
 
 
-@pytest.mark.parametrize("cin,k,s,cout,act", [(3, 3, 2, 24, "silu"), (2, 3, 2, 16, "hardswish"), (3, 7, 2, 70, "relu"),
-                                               (1, 5, 1, 40, "none"), (3, 3, 2, 22, "silu"), (2, 3, 2, 13, "relu"),
-                                               (3, 3, 1, 7, "none")])
-def test_conv_direct(cin, k, s, cout, act):
+@pytest.mark.parametrize("cin,k,s,cout,act,H,W", [(3, 3, 2, 24, "silu", 37, 45), (2, 3, 2, 16, "hardswish", 37, 45),
+                                                   (3, 7, 2, 70, "relu", 37, 45), (1, 5, 1, 40, "none", 37, 45),
+                                                   (3, 3, 2, 22, "silu", 37, 45), (2, 3, 2, 13, "relu", 37, 45),
+                                                   (3, 3, 1, 7, "none", 37, 45),
+                                                   # 16-byte-multiple widths
+                                                   (3, 3, 2, 24, "silu", 67, 64), (2, 3, 2, 16, "hardswish", 40, 36),
+                                                   (3, 7, 2, 70, "relu", 33, 52), (1, 3, 1, 9, "none", 21, 20)])
+def test_conv_direct(cin, k, s, cout, act, H, W):
     """ub_conv_direct (few-channel stem on CUDA cores, INPUT GATHER applied) vs torch fp32."""
     dev = "cuda"
     g = torch.Generator().manual_seed(cin * 100 + k * 10 + cout)
-    N, C, H, W = 2, 3, 37, 45
+    N, C = 2, 3
     x = torch.randn(N, C, H, W, generator=g)
     idx = [2, 0, 1][:cin]
     Wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
