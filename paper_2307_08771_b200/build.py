@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     build_dir = PKG / "_build"
     build_dir.mkdir(exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              f"-I{ROOT / 'include'}", f"-I{CSRC}", "-Xptxas", "-v" if verbose else "-O3"]
+              f"-I{ROOT / 'include'}", f"-I{CSRC}", "-Xptxas", "-v" if verbose else "-O3",
+              *os.environ.get("UB_NVCC_EXTRA", "").split()]  # experiments, e.g. -DUB_MBAR_HINT_NS=10000
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):

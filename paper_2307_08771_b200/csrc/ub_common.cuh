@@ -61,11 +61,17 @@ UB_DEVI void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
 }
 
 // Bounded wait: a lost arrival traps (kernel error) instead of hanging the GPU.
+// UB_MBAR_HINT_NS > 0: the retry loop passes a suspend-time hint, so a waiting warp sleeps
+// in hardware instead of re-polling (ncu: polling loops took a quarter of the issued
+// instructions of a small-channel halo conv).
+#ifndef UB_MBAR_HINT_NS
+#define UB_MBAR_HINT_NS 0
+#endif
 UB_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
   long long t0 = clock64();
-  while (!mbar_try_wait(a, parity)) {
+  while (!(UB_MBAR_HINT_NS ? mbar_try_wait_hint(a, parity, UB_MBAR_HINT_NS) : mbar_try_wait(a, parity))) {
     if (clock64() - t0 > (1ll << 33)) {  // ~4 s at 2 GHz
       asm volatile("trap;");
     }
