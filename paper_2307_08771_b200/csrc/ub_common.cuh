@@ -372,10 +372,26 @@ UB_DEVI float act_f(float v, int act) {
 // per-element switch on a runtime code (act_f) compiles to an indirect branch per value and
 // serialises the epilogue's exp / reciprocal chains (ncu: a SiLU conv epilogue ran 4x slower
 // than the ReLU one); here each case is straight-line code with 8 independent chains.
+UB_DEVI uint64_t f2_bits(float lo, float hi) {
+  return static_cast<uint64_t>(__float_as_uint(lo)) | (static_cast<uint64_t>(__float_as_uint(hi)) << 32);
+}
+// SiLU of a pair with the packed fp32x2 pipe (sm_100: mul / fma .f32x2 -- same rounding as the
+// scalar ops, half the instructions): h = v/2, silu = h + h * tanh(h)
+UB_DEVI uint32_t silu_bf16x2(float a, float b) {
+  uint64_t h, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(h) : "l"(f2_bits(a, b)), "l"(f2_bits(0.5f, 0.5f)));
+  const float hx = __uint_as_float(static_cast<uint32_t>(h)), hy = __uint_as_float(static_cast<uint32_t>(h >> 32));
+  asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(r) : "l"(h), "l"(f2_bits(tanh_fast(hx), tanh_fast(hy))));
+  return cvt_bf16x2(__uint_as_float(static_cast<uint32_t>(r)), __uint_as_float(static_cast<uint32_t>(r >> 32)));
+}
+template <int A>
+UB_DEVI uint32_t act_pack2_c(float a, float b) {
+  if (A == 5) return silu_bf16x2(a, b);
+  return cvt_bf16x2(act_f(a, A), act_f(b, A));
+}
 template <int A>
 UB_DEVI uint4 act_pack8_c(float f0, float f1, float f2, float f3, float f4, float f5, float f6, float f7) {
-  return make_uint4(cvt_bf16x2(act_f(f0, A), act_f(f1, A)), cvt_bf16x2(act_f(f2, A), act_f(f3, A)),
-                    cvt_bf16x2(act_f(f4, A), act_f(f5, A)), cvt_bf16x2(act_f(f6, A), act_f(f7, A)));
+  return make_uint4(act_pack2_c<A>(f0, f1), act_pack2_c<A>(f2, f3), act_pack2_c<A>(f4, f5), act_pack2_c<A>(f6, f7));
 }
 UB_DEVI uint4 act_pack8(int act, float f0, float f1, float f2, float f3, float f4, float f5, float f6, float f7) {
   switch (act) {
