@@ -584,12 +584,16 @@ __global__ void __launch_bounds__(256) dwconv3_tma_kernel(const __grid_constant_
   const int oy0 = (threadIdx.x >> 7) * DWS_R;
   const int c0 = cb + hg * 4;
   const bool live = c0 < C && x0 + ox < Wo && y0 + oy0 < Ho;
-  float wr[K * K][4], bv[4] = {0.f, 0.f, 0.f, 0.f};
+  // filters as packed fp32 pairs (channels c0, c0+1 | c0+2, c0+3): the taps run on the
+  // fma.f32x2 pipe, one instruction per two channels
+  uint64_t wr[K * K][2];
+  float bv[4] = {0.f, 0.f, 0.f, 0.f};
   if (live) {
 #pragma unroll
     for (int tap = 0; tap < K * K; ++tap) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(w + tap * C8 + c0));
-      wr[tap][0] = v.x; wr[tap][1] = v.y; wr[tap][2] = v.z; wr[tap][3] = v.w;
+      wr[tap][0] = f2_bits(v.x, v.y);
+      wr[tap][1] = f2_bits(v.z, v.w);
     }
     if (bias) {
 #pragma unroll
@@ -599,25 +603,26 @@ __global__ void __launch_bounds__(256) dwconv3_tma_kernel(const __grid_constant_
   mbar_wait(&bar, 0);
   float psum[4] = {0.f, 0.f, 0.f, 0.f};
   if (live) {
-    float acc[DWS_R][4];
+    uint64_t acc[DWS_R][2];
 #pragma unroll
-    for (int q = 0; q < DWS_R; ++q)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[q][j] = bv[j];
+    for (int q = 0; q < DWS_R; ++q) {
+      acc[q][0] = f2_bits(bv[0], bv[1]);
+      acc[q][1] = f2_bits(bv[2], bv[3]);
+    }
     const uint2* tile2 = reinterpret_cast<const uint2*>(tile);
 #pragma unroll
     for (int i = 0; i < (DWS_R - 1) * S + K; ++i) {
 #pragma unroll
       for (int dx = 0; dx < K; ++dx) {
         const uint2 v = tile2[((oy0 * S + i) * IW + ox * S + dx) * 16 + hg];
-        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
-                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
+        const uint64_t x01 = f2_bits(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u));
+        const uint64_t x23 = f2_bits(__uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
 #pragma unroll
         for (int q = 0; q < DWS_R; ++q) {
           const int dy = i - q * S;
           if (dy >= 0 && dy < K) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[q][j] = fmaf(wr[dy * K + dx][j], f[j], acc[q][j]);
+            acc[q][0] = fma2(wr[dy * K + dx][0], x01, acc[q][0]);
+            acc[q][1] = fma2(wr[dy * K + dx][1], x23, acc[q][1]);
           }
         }
       }
@@ -626,8 +631,7 @@ __global__ void __launch_bounds__(256) dwconv3_tma_kernel(const __grid_constant_
 #pragma unroll
     for (int q = 0; q < DWS_R; ++q) {
       if (y0 + oy0 + q >= Ho) break;
-      const uint2 o = make_uint2(cvt_bf16x2(act_f(acc[q][0], act), act_f(acc[q][1], act)),
-                                 cvt_bf16x2(act_f(acc[q][2], act), act_f(acc[q][3], act)));
+      const uint2 o = act_pack4(act, f2_lo(acc[q][0]), f2_hi(acc[q][0]), f2_lo(acc[q][1]), f2_hi(acc[q][1]));
       if (part) {
         psum[0] += __uint_as_float(o.x << 16);
         psum[1] += __uint_as_float(o.x & 0xffff0000u);

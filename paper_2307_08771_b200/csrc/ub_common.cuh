@@ -389,6 +389,25 @@ UB_DEVI uint32_t act_pack2_c(float a, float b) {
   if (A == 5) return silu_bf16x2(a, b);
   return cvt_bf16x2(act_f(a, A), act_f(b, A));
 }
+UB_DEVI uint2 act_pack4(int act, float a, float b, float c, float d) {
+  switch (act) {
+    case 1: return make_uint2(act_pack2_c<1>(a, b), act_pack2_c<1>(c, d));
+    case 2: return make_uint2(act_pack2_c<2>(a, b), act_pack2_c<2>(c, d));
+    case 3: return make_uint2(act_pack2_c<3>(a, b), act_pack2_c<3>(c, d));
+    case 4: return make_uint2(act_pack2_c<4>(a, b), act_pack2_c<4>(c, d));
+    case 5: return make_uint2(act_pack2_c<5>(a, b), act_pack2_c<5>(c, d));
+    case 6: return make_uint2(act_pack2_c<6>(a, b), act_pack2_c<6>(c, d));
+    default: return make_uint2(act_pack2_c<0>(a, b), act_pack2_c<0>(c, d));
+  }
+}
+// d = a * b + c on packed fp32 pairs (fma.rn.f32x2: the scalar fmaf rounding, one instruction)
+UB_DEVI uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+UB_DEVI float f2_lo(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+UB_DEVI float f2_hi(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
 template <int A>
 UB_DEVI uint4 act_pack8_c(float f0, float f1, float f2, float f3, float f4, float f5, float f6, float f7) {
   return make_uint4(act_pack2_c<A>(f0, f1), act_pack2_c<A>(f2, f3), act_pack2_c<A>(f4, f5), act_pack2_c<A>(f6, f7));
