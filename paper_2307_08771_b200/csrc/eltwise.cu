@@ -724,9 +724,10 @@ __global__ void __launch_bounds__(DS_THREADS) conv_direct_kernel(const float* __
   const bool live0 = y0 + oy < Ho && x0 + ox < Wo, live1 = y0 + oy + 8 < Ho && x0 + ox < Wo;
   const int down = 8 * s * IW;
   for (int cb = 0; cb < coutp; cb += CB) {
-    float acc0[CB], acc1[CB];
+    // channel pairs on the fma.f32x2 pipe: one instruction per two output channels
+    uint64_t acc0[CB / 2], acc1[CB / 2];
 #pragma unroll
-    for (int j = 0; j < CB; ++j) acc0[j] = acc1[j] = sb[cb + j];
+    for (int j = 0; j < CB / 2; ++j) acc0[j] = acc1[j] = f2_bits(sb[cb + 2 * j], sb[cb + 2 * j + 1]);
     for (int c = 0; c < cin; ++c) {
 #pragma unroll
       for (int dy = 0; dy < (KT ? KT : k); ++dy) {
@@ -734,18 +735,15 @@ __global__ void __launch_bounds__(DS_THREADS) conv_direct_kernel(const float* __
 #pragma unroll
         for (int dx = 0; dx < (KT ? KT : k); ++dx) {
           const float v0 = row[dx], v1 = row[dx + down];
-          const float4* wt = reinterpret_cast<const float4*>(sw + ((dy * k + dx) * cin + c) * coutp + cb);
+          const uint64_t p0 = f2_bits(v0, v0), p1 = f2_bits(v1, v1);
+          const ulonglong2* wt = reinterpret_cast<const ulonglong2*>(sw + ((dy * k + dx) * cin + c) * coutp + cb);
 #pragma unroll
           for (int j4 = 0; j4 < CB / 4; ++j4) {
-            const float4 q = wt[j4];
-            acc0[4 * j4] = fmaf(q.x, v0, acc0[4 * j4]);
-            acc0[4 * j4 + 1] = fmaf(q.y, v0, acc0[4 * j4 + 1]);
-            acc0[4 * j4 + 2] = fmaf(q.z, v0, acc0[4 * j4 + 2]);
-            acc0[4 * j4 + 3] = fmaf(q.w, v0, acc0[4 * j4 + 3]);
-            acc1[4 * j4] = fmaf(q.x, v1, acc1[4 * j4]);
-            acc1[4 * j4 + 1] = fmaf(q.y, v1, acc1[4 * j4 + 1]);
-            acc1[4 * j4 + 2] = fmaf(q.z, v1, acc1[4 * j4 + 2]);
-            acc1[4 * j4 + 3] = fmaf(q.w, v1, acc1[4 * j4 + 3]);
+            const ulonglong2 q = wt[j4];
+            acc0[2 * j4] = fma2(q.x, p0, acc0[2 * j4]);
+            acc0[2 * j4 + 1] = fma2(q.y, p0, acc0[2 * j4 + 1]);
+            acc1[2 * j4] = fma2(q.x, p1, acc1[2 * j4]);
+            acc1[2 * j4 + 1] = fma2(q.y, p1, acc1[2 * j4 + 1]);
           }
         }
       }
@@ -753,7 +751,12 @@ __global__ void __launch_bounds__(DS_THREADS) conv_direct_kernel(const float* __
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!(h ? live1 : live0)) continue;
-      const float* acc = h ? acc1 : acc0;
+      float acc[CB];
+#pragma unroll
+      for (int j = 0; j < CB / 2; ++j) {
+        acc[2 * j] = f2_lo(h ? acc1[j] : acc0[j]);
+        acc[2 * j + 1] = f2_hi(h ? acc1[j] : acc0[j]);
+      }
       uint16_t* yp = y + ((static_cast<long long>(n) * Ho + y0 + oy + 8 * h) * Wo + x0 + ox) * y_cstride + y_coff + cb;
       // whole 8-channel groups as 16-byte stores, then bf16 pairs, then a single channel
       // (2-byte stores at a 48-byte pixel pitch cost 14x the written bytes in L2 transactions)
@@ -761,10 +764,9 @@ __global__ void __launch_bounds__(DS_THREADS) conv_direct_kernel(const float* __
 #pragma unroll
       for (int q = 0; q < CB / 8; ++q) {
         if (8 * q + 8 <= nc) {
-          float f[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) f[j] = act_f(acc[q * 8 + j], act);
-          *reinterpret_cast<uint4*>(yp + q * 8) = pack8(f);
+          *reinterpret_cast<uint4*>(yp + q * 8) =
+              act_pack8(act, acc[q * 8], acc[q * 8 + 1], acc[q * 8 + 2], acc[q * 8 + 3], acc[q * 8 + 4],
+                        acc[q * 8 + 5], acc[q * 8 + 6], acc[q * 8 + 7]);
         } else if (8 * q < nc) {
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
