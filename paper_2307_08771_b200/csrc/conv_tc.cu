@@ -104,6 +104,8 @@ struct ConvKParams {
   const int32_t* y2_map;  // [cout] compact column of output channel c, -1 = not stored
   int tail_w;        // (a_tma, BK 64) channels of the narrower last A box (16 / 32), 64 = none
   int epi_alt;       // (epi2, one 64-channel chunk per tile) the groups take alternate tiles
+  int epi4;          // (epi2, 512 producers, generic activation) warps 12-23 too: four epilogue
+                     // groups of four, one output slot per warp
                      // (group g drains accumulator g) instead of alternate chunks
   int mt2;           // (a_tma, streamed B, no residual) pairs of M-adjacent tiles share each B box:
                      // 4 TMEM accumulators, the pair's second A box in the next ring stage
@@ -174,9 +176,10 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
   uint8_t* sB = sA + stages * A_BYTES;  // per-stage B, or all k-blocks of B when resident
   uint8_t* sI = sB + (p.b_res ? p.num_kb : stages) * b_stride;  // identity 64x64 (8 KB)
   // epilogue warps: 4, or 8 when the producers are idle (TMA-fed 1x1): group 1 = warps 12-15
-  const int epi_warps = p.epi2 ? 8 : 4;
-  uint8_t* sE = sI + IDENT_BYTES;                                          // epi_warps x 2 output slots
-  float* sBias = reinterpret_cast<float*>(sE + epi_warps * EPI_WARP_BYTES);  // epi_warps x MAX_BLOCK_N
+  const int epi_warps = p.epi4 ? 16 : (p.epi2 ? 8 : 4);
+  const uint32_t warp_bytes = p.epi4 ? EPI_SLOT : EPI_WARP_BYTES;  // output slots per epilogue warp: 1 or 2
+  uint8_t* sE = sI + IDENT_BYTES;                                      // epi_warps x warp_bytes
+  float* sBias = reinterpret_cast<float*>(sE + epi_warps * warp_bytes);  // epi_warps x MAX_BLOCK_N
   uint16_t* sY2 = reinterpret_cast<uint16_t*>(sBias + epi_warps * MAX_BLOCK_N);  // y2 staging (when set)
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sY2) + (p.y2 ? epi_warps * Y2_STAGE : 0));
   uint64_t* empty = full + stages;
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
         UB_TRACE(2);
       }
     }
-  } else if (warp >= 8 && !(p.epi2 && warp >= 12 && warp < 16)) {
+  } else if (warp >= 8 && !(p.epi2 && warp >= 12 && warp < 16) && !(p.epi4 && warp >= 16)) {
     // ================= producers (256 threads): fill stage s with A and B, then arrive on full[s]
     // Addresses are precomputed per tile so the per-k-block work is one add + one cp.async per
     // 16-byte chunk; smem destinations are constant for the whole kernel.
@@ -713,10 +716,10 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
     // re-arms those accumulator columns with the bias of the tile that uses this
     // accumulator next (tile i+2).
     const int q = warp & 3;  // TMEM lane quarter (warp % 4)
-    const int eg = warp >= 12 ? 1 : 0;
+    const int eg = warp < 8 ? 0 : (warp - 8) >> 2;  // warps 4-7: 0; 12-15: 1; 16-19: 2; 20-23: 3
     const int ngrp = epi_warps / 4;
     const int ew = eg * 4 + q;  // epilogue warp index: slots and bias buffer
-    uint8_t* oslots = sE + ew * EPI_WARP_BYTES;
+    uint8_t* oslots = sE + ew * warp_bytes;
     float* sb = sBias + ew * MAX_BLOCK_N;
     const bool tma = p.epi_tma;
     uint32_t ec = 0;  // chunks processed by this warp (= TMA stores committed)
@@ -779,8 +782,11 @@ __global__ void __launch_bounds__(256 + PRODUCERS, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * p.acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = c0; c < nchunks; c += cstep, ++ec) {
-        uint8_t* oslot = oslots + (ec & 1) * EPI_SLOT;
-        if (tma && lane == 0) bulk_wait_read<1>();  // this slot's store from 2 chunks ago has read it
+        uint8_t* oslot = oslots + (p.epi4 ? 0 : (ec & 1) * EPI_SLOT);
+        if (tma && lane == 0) {  // this slot's previous store (2 chunks ago; 1 with one slot) has read it
+          if (p.epi4) bulk_wait_read<0>();
+          else bulk_wait_read<1>();
+        }
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // two 32-column halves
@@ -1156,8 +1162,19 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   p.a_tma = tiled_1x1 && !(d->variant & 32);
   p.epi2 = p.a_tma && !(d->variant & 64);
   p.epi_alt = p.epi2 && p.block_n <= EPI_CHUNK && !(d->variant & 4096);
-  const int epi_warps = p.epi2 ? 8 : 4;
-  uint32_t fixed = 1024 + IDENT_BYTES + epi_warps * EPI_WARP_BYTES + epi_warps * MAX_BLOCK_N * 4 + BAR_BYTES +
+  // producer width: explicit variant from the caller (engine autotune), else a heuristic
+  const int pw = d->variant & 3;
+  int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
+  if (stem) wide = 1;
+  // generic activations (SiLU, hardswish, ...) make the epilogue the bound of a TMA-fed 1x1:
+  // let the otherwise idle producer warps 16-23 drain too (ncu: time tracked the epilogue's
+  // instruction count at a constant IPC)
+  static const bool epi4_env = !std::getenv("UB_CONV_NOEPI4");
+  p.epi4 = epi4_env && p.epi2 && wide && !p.has_res && d->relu > 1 && !p.epi_alt && p.block_n >= 2 * EPI_CHUNK && !d->y2 &&
+           !(d->variant & 128);
+  const int epi_warps = p.epi4 ? 16 : (p.epi2 ? 8 : 4);
+  const uint32_t warp_bytes = p.epi4 ? EPI_SLOT : EPI_WARP_BYTES;
+  uint32_t fixed = 1024 + IDENT_BYTES + epi_warps * warp_bytes + epi_warps * MAX_BLOCK_N * 4 + BAR_BYTES +
                    (d->y2 ? epi_warps * Y2_STAGE : 0) +
                    ((stem || packed) ? MAX_STEM_K * sizeof(int4) : 0);
   // Weight-stationary B: when all k-blocks of one N tile fit next to >= 4 A stages, each CTA
@@ -1240,10 +1257,6 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int num_tiles = p.mt2 ? (p.m_tiles + 1) / 2 * p.n_tiles : p.m_tiles * p.n_tiles;  // work units
   int grid = num_tiles < num_sms() ? num_tiles : num_sms();
   if (p.b_res && grid % p.n_tiles) grid = grid / p.n_tiles * p.n_tiles;
-  // producer width: explicit variant from the caller (engine autotune), else a heuristic
-  const int pw = d->variant & 3;
-  int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
-  if (stem) wide = 1;
   if (stem) return launch_conv<A_STEM, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
   if (packed) return launch_conv<A_PACKED, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
   if (gather) return launch_conv<A_GATHER, 64>(tmY, tmB, tmA, tmR, tmAt, p, grid, smem, stream, wide);
