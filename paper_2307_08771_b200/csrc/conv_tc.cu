@@ -1166,11 +1166,12 @@ extern "C" int ub_conv_fwd(const ub_conv_desc* d, cudaStream_t stream) {
   const int pw = d->variant & 3;
   int wide = pw == 2 ? 1 : (pw == 1 ? 0 : (p.has_res ? 0 : 1));
   if (stem) wide = 1;
-  // generic activations (SiLU, hardswish, ...) make the epilogue the bound of a TMA-fed 1x1:
-  // let the otherwise idle producer warps 16-23 drain too (ncu: time tracked the epilogue's
-  // instruction count at a constant IPC)
+  // the TMA-fed 1x1 without a residual is epilogue-bound at small K (generic activations
+  // most: ncu showed time tracking the epilogue's instruction count at a constant IPC): let
+  // the otherwise idle producer warps 16-23 drain too.  SiLU expand 46 -> 36 us, its ReLU
+  // twin 24.9 -> 22.6 us; ResNet-50 neutral (109.3 k / 109.6 k images/s, r2ce).
   static const bool epi4_env = !std::getenv("UB_CONV_NOEPI4");
-  p.epi4 = epi4_env && p.epi2 && wide && !p.has_res && d->relu > 1 && !p.epi_alt && p.block_n >= 2 * EPI_CHUNK && !d->y2 &&
+  p.epi4 = epi4_env && p.epi2 && wide && !p.has_res && !p.epi_alt && p.block_n >= 2 * EPI_CHUNK && !d->y2 &&
            !(d->variant & 128);
   const int epi_warps = p.epi4 ? 16 : (p.epi2 ? 8 : 4);
   const uint32_t warp_bytes = p.epi4 ? EPI_SLOT : EPI_WARP_BYTES;
