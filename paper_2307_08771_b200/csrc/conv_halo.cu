@@ -66,6 +66,8 @@ struct HaloParams {
   uint32_t a_box_bytes;  // AT: bytes of one input box (one stacked image's box when ipt > 1)
   int ipt;       // images stacked per tile (small images): image i's row y at staged row 1 + i * (H + 1) + y
   long long* trace;  // profiling (UB_HALO_TRACE): CTA 0 event clocks, [tile][8]
+  int epi4;          // (AT, resident weights) the TMEM-alloc warp issues the input boxes and the
+                     // producer warps 14-17 form a fourth epilogue group
   int dbg;           // profiling ablations (UB_HALO_DBG): 1 no halo loads, 2 no output, 4 no TMEM reads,
                      // 8 no TMA store, 16 no slot wait (races; timing only)
 };
@@ -108,7 +110,7 @@ __global__ void __maxnreg__(96)
   uint8_t* sB = base;
   const int groups = SB ? p.groups : 1;
   uint8_t* sE = sB + (SB ? p.b_stages : TAPS) * p.b_block_bytes;  // epilogue slots (1024-aligned)
-  uint8_t* sA = sE + HALO_EPI_WARPS * HALO_SLOT;        // a_stages x a_stage_bytes
+  uint8_t* sA = sE + (p.epi4 ? 16 : HALO_EPI_WARPS) * HALO_SLOT;  // a_stages x a_stage_bytes
   float* sBias = reinterpret_cast<float*>(sA + p.a_stages * p.a_stage_bytes);  // 256 floats
   uint64_t* afull = reinterpret_cast<uint64_t*>(sBias + 256);
   uint64_t* aempty = afull + 8;
@@ -160,6 +162,42 @@ __global__ void __maxnreg__(96)
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
 
+  // the input boxes of every (tile, group) of this CTA, in order, into the A ring (AT): issued by
+  // producer thread 0, or by the TMEM-alloc warp's lane 0 when the producers drain (epi4)
+  auto issue_input_boxes = [&]() {
+    int s = 0;
+    uint32_t ph = 0;
+    const int ncb = p.cpad >> 6;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
+      for (int g = 0; g < groups; ++g) {
+        const int img = p.ipt > 1 ? t * p.ipt : t / p.tiles_per_img;
+        int c0 = g * 64, ox = -1, oy = -1;  // box origin: channel, column, row (input coordinates)
+        int img_rows = p.H + 1;             // staged rows per stacked image
+        if constexpr (S == 2) {
+          const int qd = g / ncb;
+          c0 = (g - qd * ncb) * 64;
+          ox = (qd & 1) - 1;
+          oy = (qd >> 1) - 1;
+          img_rows = p.Ho + 1;
+        }
+        mbar_wait(&aempty[s], ph ^ 1);
+        uint8_t* dst = sA + s * p.a_stage_bytes;
+        if (p.ipt > 1) {
+          const int n_i = p.N - img < p.ipt ? p.N - img : p.ipt;
+          mbar_arrive_expect_tx(&afull[s], n_i * p.a_box_bytes);
+          for (int i = 0; i < n_i; ++i)
+            tma_load_4d(&tmX, &afull[s], dst + i * img_rows * WP * KB, c0, ox, oy, img + i);
+        } else {
+          const int row0 = (t - img * p.tiles_per_img) * G::RT;  // first output row
+          mbar_arrive_expect_tx(&afull[s], p.a_box_bytes);
+          tma_load_4d(&tmX, &afull[s], dst, c0, ox, S * row0 + oy, img);
+        }
+        if (++s == p.a_stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+  };
   if (warp >= HALO_PROD_WARP0) {
     // ================= producers
     const int pt = threadIdx.x - 32 * HALO_PROD_WARP0;
@@ -177,42 +215,9 @@ __global__ void __maxnreg__(96)
                    : "memory");
     }
     cp_async_arrive_noinc(bres);
-    griddep_wait();  // the input activations come from the previous kernel (PDL)
+    if (!p.epi4) griddep_wait();  // the input activations come from the previous kernel (PDL)
     if constexpr (AT) {
-      if (pt == 0) {
-        int s = 0;
-        uint32_t ph = 0;
-        const int ncb = p.cpad >> 6;
-        for (int t = blockIdx.x; t < p.tiles; t += gridDim.x)
-          for (int g = 0; g < groups; ++g) {
-            const int img = p.ipt > 1 ? t * p.ipt : t / p.tiles_per_img;
-            int c0 = g * 64, ox = -1, oy = -1;  // box origin: channel, column, row (input coordinates)
-            int img_rows = p.H + 1;             // staged rows per stacked image
-            if constexpr (S == 2) {
-              const int qd = g / ncb;
-              c0 = (g - qd * ncb) * 64;
-              ox = (qd & 1) - 1;
-              oy = (qd >> 1) - 1;
-              img_rows = p.Ho + 1;
-            }
-            mbar_wait(&aempty[s], ph ^ 1);
-            uint8_t* dst = sA + s * p.a_stage_bytes;
-            if (p.ipt > 1) {
-              const int n_i = p.N - img < p.ipt ? p.N - img : p.ipt;
-              mbar_arrive_expect_tx(&afull[s], n_i * p.a_box_bytes);
-              for (int i = 0; i < n_i; ++i)
-                tma_load_4d(&tmX, &afull[s], dst + i * img_rows * WP * KB, c0, ox, oy, img + i);
-            } else {
-              const int row0 = (t - img * p.tiles_per_img) * G::RT;  // first output row
-              mbar_arrive_expect_tx(&afull[s], p.a_box_bytes);
-              tma_load_4d(&tmX, &afull[s], dst, c0, ox, S * row0 + oy, img);
-            }
-            if (++s == p.a_stages) {
-              s = 0;
-              ph ^= 1;
-            }
-          }
-      }
+      if (pt == 0 && !p.epi4) issue_input_boxes();
     } else {
     // halo planes: this thread always fills plane pp of positions q0 + i * qstep
     const int pp = pt % PLANES;
@@ -419,12 +424,19 @@ __global__ void __maxnreg__(96)
             }
           }
     }
-  } else if (warp < HALO_EPI_WARPS) {
+  } else if (AT && warp == ALLOC_WARP && p.epi4) {
+    if (lane == 0) {
+      griddep_wait();  // the input activations come from the previous kernel (PDL)
+      issue_input_boxes();
+    }
+    __syncwarp();
+  }
+  if (warp < HALO_EPI_WARPS || (p.epi4 && warp >= HALO_PROD_WARP0)) {
     // ================= epilogue: group g = warp / 4 drains the tiles it % 2 == g; warp q = warp % 4
-    // owns TMEM lanes / tile rows 32q .. 32q+31
-    const int grp = warp >> 2;  // groups >= p.ngroups stay idle
+    // owns TMEM lanes / tile rows 32q .. 32q+31 (epi4: producer warps 14-17 are group 3)
+    const int grp = warp >= HALO_PROD_WARP0 ? 3 : warp >> 2;  // groups >= p.ngroups stay idle
     const int q = warp & 3;
-    uint8_t* slot = sE + warp * HALO_SLOT;  // one store slot per warp (a group's tiles are far apart)
+    uint8_t* slot = sE + (grp * 4 + q) * HALO_SLOT;  // one store slot per warp (a group's tiles are far apart)
     const int nchunks = (p.np + 63) >> 6;
     uint32_t ec = 0;
     int it = 0;
@@ -576,15 +588,19 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
   const int mt = (Ho > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
   p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
-  p.ngroups = (d->variant & 128) ? 2 : HALO_EPI_WARPS / 4;
+  // input by TMA boxes (AT) when a position's channels fill a 64- or 128-byte swizzle row
+  const bool at = (cpad == 32 || cpad % 64 == 0) && !(d->variant & 2048);
+  // AT with resident weights: the producer warps only stage the weights, so they drain as a
+  // fourth epilogue group (the TMEM-alloc warp issues the input boxes)
+  static const bool epi4_env = !std::getenv("UB_HALO_NOEPI4");
+  p.epi4 = (epi4_env && at && p.groups == 1 && !(d->variant & 128)) ? 1 : 0;
+  p.ngroups = (d->variant & 128) ? 2 : (p.epi4 ? 4 : HALO_EPI_WARPS / 4);
   // chunks dealt to all groups when every group gets one (shorter drain per tile), else whole tiles
   p.drainers = (mt * ((p.np + 63) / 64) >= p.ngroups && !(d->variant & 1024)) ? p.ngroups : 1;
-  if (p.drainers == 1 && p.ngroups > p.nacc) p.ngroups = p.nacc;
+  if (p.drainers == 1 && p.ngroups > p.nacc) p.ngroups = p.nacc;  // (epi4 then leaves group 3 idle)
   p.n_pos = S == 1 ? ((mt * p.R + 2) * Wp + 2 + 7) / 8 * 8 : ((mt * p.R + 1) * Wp + 1 + 7) / 8 * 8;  // == N_POS
   p.plane_stride = p.n_pos * 16 + 16;               // == HaloGeom<Wp, mt>::PLANE_STRIDE
   p.a_stage_bytes = (p.planes * p.plane_stride + 127) & ~127u;
-  // input by TMA boxes (AT) when a position's channels fill a 64- or 128-byte swizzle row
-  const bool at = (cpad == 32 || cpad % 64 == 0) && !(d->variant & 2048);
   if (S == 2 && !at) return UB_OK;
   const int kb = p.planes * 16;
   if (at) {
@@ -621,7 +637,7 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
     p.dbg = dbg;
   }
   const size_t fixed = 1024 + (p.groups == 1 ? 9 : p.b_stages) * static_cast<size_t>(p.b_block_bytes) +
-                      HALO_EPI_WARPS * HALO_SLOT + 256 * 4 + 512;
+                      (p.epi4 ? 16 : HALO_EPI_WARPS) * HALO_SLOT + 256 * 4 + 512;
   const size_t budget = 227 * 1024;
   if (fixed + 2 * p.a_stage_bytes > budget) return UB_OK;
   int stages = static_cast<int>((budget - fixed) / p.a_stage_bytes);

@@ -1,0 +1,6 @@
+rm -f gpurun_out/parity_scale.jsonl
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2bq_bench.json 2> gpurun_out/r2bq_bench.err; echo bench rc=$?
+timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2bq_ref.json 2>&1; echo ref rc=$?
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+cp gpurun_out/parity_scale.jsonl gpurun_out/r2bq_parity_scale.jsonl 2>/dev/null

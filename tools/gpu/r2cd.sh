@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_kernels_gpu.py tests/test_engine_gpu.py -m gpu -q -x -k "activation or efficientnet or mobilenet or conv_matches" 2>&1 | tail -2
+for a in silu hardswish; do UB_BENCH_ACT=$a python tools/bench_conv.py eff_s5_expand eff_s6_expand eff_s4_expand 2>&1 | tail -3; done
+UB_CONV_NOEPI4=1 UB_BENCH_ACT=silu python tools/bench_conv.py eff_s5_expand 2>&1 | tail -1
+python tools/bench_conv.py eff_s5_expand l1_conv3 2>&1 | tail -2
+timeout 300 python tools/op_times.py efficientnet_v2_s_s50 256 reorder fused 1 2>&1 | head -1 | cut -c1-300
