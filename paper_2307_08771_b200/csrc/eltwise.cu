@@ -650,15 +650,18 @@ __global__ void __launch_bounds__(256) dwconv3_tma_kernel(const __grid_constant_
     }
   }
   if (part) {
-    __syncthreads();
-    float4* red = reinterpret_cast<float4*>(tile);
-    red[threadIdx.x] = make_float4(psum[0], psum[1], psum[2], psum[3]);
+    // lanes l and l + 16 hold the same 4 channels (columns ox, ox + 1): one shuffle, then the
+    // 8 warps' 64-channel rows through a small smem table and one barrier
+    __shared__ float4 wred[8][16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) psum[j] += __shfl_xor_sync(0xffffffffu, psum[j], 16);
+    if ((threadIdx.x & 31) < 16) wred[threadIdx.x >> 5][hg] = make_float4(psum[0], psum[1], psum[2], psum[3]);
     __syncthreads();
     if (threadIdx.x < 64 && cb + threadIdx.x < C8) {
-      const float* rf = reinterpret_cast<const float*>(red);
+      const float* rf = reinterpret_cast<const float*>(wred);
       float sum = 0.f;
 #pragma unroll
-      for (int it = 0; it < 16; ++it) sum += rf[(it * 16 + (threadIdx.x >> 2)) * 4 + (threadIdx.x & 3)];
+      for (int wi = 0; wi < 8; ++wi) sum += rf[wi * 64 + threadIdx.x];
       part[static_cast<long long>(t) * C8 + cb + threadIdx.x] = sum;
     }
   }
