@@ -846,10 +846,24 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
   if (part) {
     // ---- pool from the producer's per-tile partial sums (ub_dwconv_pool), in tile order
     const float* pp = part + static_cast<long long>(n) * nparts * C8;
-    for (int c = t; c < C8; c += blockDim.x) {
-      float sum = 0.f;
-      for (int q = 0; q < nparts; ++q) sum += pp[static_cast<long long>(q) * C8 + c];
-      pooled[c] = c < C ? sum / static_cast<float>(HW) : 0.f;
+    const float inv_hw = 1.f / static_cast<float>(HW);
+    for (int c0 = t; c0 < C8; c0 += 4 * blockDim.x) {  // four channels' loads in flight per thread
+      float sum[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int q = 0; q < nparts; ++q) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * blockDim.x;
+          v[u] = c < C8 ? __ldg(pp + static_cast<long long>(q) * C8 + c) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sum[u] += v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < C8) pooled[c] = c < C ? sum[u] * inv_hw : 0.f;
+      }
     }
     __syncthreads();
   }
@@ -921,12 +935,12 @@ __global__ void __launch_bounds__(512) se_gate_kernel(const uint16_t* __restrict
     for (int c = c_lo + t; c < c_hi; c += blockDim.x) {
       const uint4* wr = reinterpret_cast<const uint4*>(w2 + static_cast<long long>(c) * ldw2);
       float acc = 0.f;
-      for (int k8 = 0; k8 < n8; k8 += 4) {
-        uint4 q[4];
+      for (int k8 = 0; k8 < n8; k8 += 8) {  // eight 16-byte chunks in flight (one round trip for <= 64 inputs)
+        uint4 q[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) q[u] = k8 + u < n8 ? __ldg(wr + k8 + u) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 8; ++u) q[u] = k8 + u < n8 ? __ldg(wr + k8 + u) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           if (k8 + u < n8) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc = fmaf(bfj(q[u], e), hidden[(k8 + u) * 8 + e], acc);
