@@ -293,10 +293,26 @@ __global__ void __launch_bounds__(256) linear_small_kernel(const uint16_t* __res
   const int K8 = (K + 7) / 8 * 8;
   griddep_wait();
   griddep_launch_dependents();
-  for (int e = threadIdx.x; e < M * K8; e += blockDim.x) {
-    const int m = e / K8, k = e - m * K8;
-    const int col = k < K ? __ldg(xcol + k) : -1;  // -1: a zero-filled GATHER entry
-    xs[e] = col >= 0 ? bf(x[static_cast<long long>(m) * x_cstride + col]) : 0.f;
+  // four elements per thread per step: their column-map loads, then their gathered loads
+  // (a chain of two dependent round trips per element made the staging latency-bound at batch 1)
+  for (int e0 = threadIdx.x; e0 < M * K8; e0 += 4 * blockDim.x) {
+    int col[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int m = e / K8, k = e - m * K8;
+      col[u] = (e < M * K8 && k < K) ? __ldg(xcol + k) : -1;  // -1: a zero-filled GATHER entry
+    }
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int m = e / K8;
+      v[u] = col[u] >= 0 ? bf(x[static_cast<long long>(m) * x_cstride + col[u]]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u * blockDim.x < M * K8) xs[e0 + u * blockDim.x] = v[u];
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -305,6 +321,7 @@ __global__ void __launch_bounds__(256) linear_small_kernel(const uint16_t* __res
 #pragma unroll
     for (int m = 0; m < 16; ++m) acc[m] = 0.f;
     const uint16_t* wr = w + static_cast<long long>(o) * w_stride;
+#pragma unroll 4
     for (int k = lane * 8; k < K8; k += 256) {
       const uint4 wq = __ldg(reinterpret_cast<const uint4*>(wr + k));
       float wf[8];
