@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_engine_gpu.py -m gpu -q -x -k "dwconv or depthwise or se_ or efficientnet" 2>&1 | tail -2
+timeout 300 python tools/op_times.py efficientnet_v2_s_s50 256 reorder fused 1 2>&1 | head -1 | cut -c1-400
