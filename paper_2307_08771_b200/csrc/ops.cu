@@ -237,10 +237,28 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
   // chunk t = lane + 32 i of a batch -> (pixel k, row q, chunk ch): the same for every batch,
   // walked with increments (no divisions in the loop)
   const bool direct = ROWS == 1 && stride == 1;  // source pixel == output pixel
+  // pool2 with one output per lane: this lane's channel offsets and BN scale / shift
+  int reg_a[8];
+  float reg_sc[8], reg_sh[8];
+  if (ROWS == 4) {
+    const int gi0 = lane % groups;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = gi0 * 8 + j;
+      reg_a[j] = c < n8 ? sidx[c] : -1;
+      reg_sc[j] = AFFINE && c < n8 ? sscale[c] : 0.f;
+      reg_sh[j] = AFFINE && c < n8 ? sshift[c] : 0.f;
+    }
+  }
+  const int howo = Ho * Wo;
   auto issue = [&](long long b, uint8_t* dst) {
     const long long p0 = b * pb;
     const int total = pb * pix_chunks;
     int k = lane / pix_chunks, rem = lane - (lane / pix_chunks) * pix_chunks;
+    // the output pixel's source position, recomputed only when the chunk walk moves to the next
+    // pixel, in 32-bit arithmetic (a 64-bit division per chunk made this kernel instruction-bound)
+    int kcur = -1;
+    const uint16_t* pix_base = x;
     for (int t = lane; t < total; t += 32) {
       const long long p = p0 + k;
       if (p >= npix) break;
@@ -248,13 +266,18 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
       if (direct) {
         src = x + static_cast<size_t>(p) * x_cstride + ws + rem * 8;
       } else {
+        if (k != kcur) {
+          kcur = k;
+          const int pi = static_cast<int>(p);  // npix < 2^31 (host-checked)
+          const int n = pi / howo;
+          const int r = pi - n * howo;
+          const int yo = r / Wo, xo = r - (r / Wo) * Wo;
+          const int yb = ROWS == 4 ? 2 * yo : yo * stride, xb = ROWS == 4 ? 2 * xo : xo * stride;
+          pix_base = x + ((static_cast<size_t>(n) * H + yb) * W + xb) * x_cstride + ws;
+        }
         const int q = ROWS == 1 ? 0 : rem / win16, ch = rem - q * win16;
-        const int n = static_cast<int>(p / (static_cast<long long>(Ho) * Wo));
-        const int r = static_cast<int>(p - static_cast<long long>(n) * Ho * Wo);
-        const int yo = r / Wo, xo = r - (r / Wo) * Wo;
-        const int yi = ROWS == 4 ? 2 * yo + (q >> 1) : yo * stride;
-        const int xi = ROWS == 4 ? 2 * xo + (q & 1) : xo * stride;
-        src = x + ((static_cast<size_t>(n) * H + yi) * W + xi) * x_cstride + ws + ch * 8;
+        const int dyx = ROWS == 4 ? ((q >> 1) * W + (q & 1)) : 0;
+        src = pix_base + static_cast<size_t>(dyx) * x_cstride + ch * 8;
       }
       cp_async16(dst + t * 16, src, 16);
       rem += 32;
@@ -282,6 +305,35 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint16_t* __rest
     const long long p0 = b * pb;
     const int work = pb * groups;
     int kp = lane / groups, gi = lane - (lane / groups) * groups;
+    if (ROWS == 4 && work <= 32) {
+      // one output (pixel kp, group gi) per lane, the same every batch: the channel offsets and
+      // the BN scale/shift come from registers (reg_*), not 3 shared loads per channel
+      if (lane < work && p0 + kp < npix) {
+        const uint16_t* row = reinterpret_cast<const uint16_t*>(stage + kp * pix_chunks * 16);
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float acc = 0.f;
+          if (reg_a[j] >= 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float v = __uint_as_float(static_cast<uint32_t>(row[q * win16 * 8 + reg_a[j]]) << 16);
+              if (AFFINE) {
+                v = fmaf(reg_sc[j], v, reg_sh[j]);
+                if (relu) v = fmaxf(v, 0.f);
+              }
+              acc += v;
+            }
+            acc *= 0.25f;
+          }
+          f[j] = acc;
+        }
+        *reinterpret_cast<uint4*>(y + static_cast<size_t>(p0 + kp) * y_cstride + y_coff + gi * 8) =
+            make_uint4(cvt_bf16x2(f[0], f[1]), cvt_bf16x2(f[2], f[3]), cvt_bf16x2(f[4], f[5]), cvt_bf16x2(f[6], f[7]));
+      }
+      __syncwarp();
+      continue;
+    }
     for (int t = lane; t < work; t += 32) {
       const long long p = p0 + kp;
       if (p >= npix) break;
@@ -1029,6 +1081,8 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   // pixels per warp step: ~96 16-byte chunks per cp.async wave (3 per lane), at most 16 pixels
   int pb = 96 / (rows * win16);
   pb = pb < 1 ? 1 : (pb > 16 ? 16 : pb);
+  // ... and enough pixels that every lane owns an output group (pool2 windows are wide)
+  while (pb < 16 && pb * (n8 / 8) < 32 && (pb + 1) * rows * win16 <= 192) ++pb;
   const size_t stage = static_cast<size_t>(pb) * rows * win16 * 16;
   int warps = 8;
   while (warps > 1 && idx_bytes + warps * 3 * stage > 200 * 1024) warps >>= 1;
@@ -1041,6 +1095,7 @@ extern "C" int ub_gather_rows_ex(const void* x, int x_cstride, int x_coff, int l
   if (const cudaError_t ae = ensure_max_smem(kern)) return cuda_status(ae, "gather_rows attr");
   const int Ho = pool2 ? H / 2 : (H + stride - 1) / stride, Wo = pool2 ? W / 2 : (W + stride - 1) / stride;
   const long long npix = static_cast<long long>(N) * Ho * Wo;
+  if (npix >= (1ll << 31)) return fail(UB_EUNSUPPORTED, "ub_gather_rows: too many output pixels");
   int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
   if (per_sm > 2048 / (32 * warps)) per_sm = 2048 / (32 * warps);
   if (per_sm < 1) per_sm = 1;

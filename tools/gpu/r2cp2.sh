@@ -1,0 +1,23 @@
+cat > /tmp/g.py <<'PY'
+import sys, torch
+sys.path.insert(0, '/root/repo')
+from paper_2307_08771_b200 import kernels as K
+dev = "cuda"
+N, H, C = 128, 56, 128
+x = K.empty_act(N, H, H, C, dev); x.buf.normal_()
+idx = torch.randperm(C)[:127].sort().values.to(torch.int32).to(dev)
+y = K.empty_act(N, H // 2, H // 2, 128, dev)
+sc = torch.rand(127, device=dev) + 0.5; sh = torch.randn(127, device=dev)
+for _ in range(3):
+    K.gather_rows_ex(x, idx, K.gather_window(idx.tolist()), 1, y, scale=sc, shift=sh, relu=True, pool2=True)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(20):
+    K.gather_rows_ex(x, idx, K.gather_window(idx.tolist()), 1, y, scale=sc, shift=sh, relu=True, pool2=True)
+b.record(); torch.cuda.synchronize()
+print("pool2 gather 128x56x56x128 -> 28x28:", a.elapsed_time(b) / 20 * 1e3, "us")
+PY
+python /tmp/g.py 2>/dev/null || true
+timeout 900 python -m pytest tests/test_kernels_gpu.py tests/test_engine_gpu.py tests/test_output_mode.py -m gpu -q -x -k "gather or densenet or output or join" 2>&1 | tail -2
+timeout 300 python tools/op_times.py densenet121_s50 128 reorder fused 1 2>&1 | head -1 | cut -c1-300
