@@ -739,6 +739,30 @@ def test_conv_epilogue_activations(act):
         assert _rel(y.to_nchw().cpu(), ref) < 1e-2, (k, act)
 
 
+@pytest.mark.parametrize("act,cin,cout", [("silu", 80, 710), ("hardswish", 64, 320), ("relu", 128, 512),
+                                          ("none", 96, 256), ("silu", 40, 130)])
+def test_conv_1x1_four_epilogue_groups(act, cin, cout):
+    """TMA-fed 1x1 without residual and N tiles >= 128 channels: the four-group epilogue
+    (producer warps 16-23 drain too, one output slot per warp) vs torch fp32."""
+    dev = "cuda"
+    g = torch.Generator().manual_seed(cin * 7 + cout)
+    N, H = 6, 14
+    x = torch.randn(N, cin, H, H, generator=g)
+    Wt = torch.randn(cout, cin, 1, 1, generator=g) / cin ** 0.5
+    bias = torch.randn(cout, generator=g)
+    xa = K.act_from_nchw(x.to(dev))
+    lead, cpad = _lib.conv_weight_layout(cin, 0, False, 1, 1)
+    wg = K.permute_weights(Wt.to(dev).contiguous(), list(range(cout)), list(range(cin)), layout="gemm",
+                           lead=lead, cpad=cpad, out_dtype=torch.bfloat16)
+    y = K.empty_act(N, H, H, cout, dev)
+    K.conv(xa, wg, lead, cpad, cout, 1, 1, 1, 0, y, bias=bias.to(dev), relu=_lib.UB_ACT[act])
+    torch.cuda.synchronize()
+    fns = {"none": lambda v: v, "relu": torch.relu, "silu": torch.nn.functional.silu,
+           "hardswish": torch.nn.functional.hardswish}
+    ref = fns[act](torch.nn.functional.conv2d(_bf(x), _bf(Wt), bias))
+    assert _rel(y.to_nchw().cpu(), ref) < 1e-2
+
+
 @pytest.mark.parametrize("M,KK,O,fp32,act", [(1, 72, 425, False, "hardsigmoid"), (4, 2048, 1000, True, "none"),
                                              (16, 37, 9, False, "relu"), (3, 512, 1000, True, "none")])
 def test_linear_small(M, KK, O, fp32, act):
