@@ -586,7 +586,14 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   p.np = (d->cout + 15) / 16 * 16;
   p.acc_cols = p.np <= 32 ? 32 : (p.np <= 64 ? 64 : (p.np <= 128 ? 128 : 256));
   // two MMA tiles per staged tile when the image has the rows and TMEM holds 2 x 2 of them
-  const int mt = (Ho > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
+  int mt = (Ho > p.R && 4 * p.acc_cols <= 512) ? 2 : 1;
+  // four MMA tiles per staged tile for narrow outputs on wide rows (fewer, longer tiles: the
+  // per-tile barrier / store overheads dominate 32-column tiles)
+  // (measured: EfficientNetV2's 112-wide stages 613 -> 594 us; ResNet-50's 56-wide layer 1 -0.2 %,
+  // so by default only at padded width 128; UB_HALO_MT4=1 / 0 forces it on / off)
+  static const int mt4_env = getenv("UB_HALO_MT4") ? atoi(getenv("UB_HALO_MT4")) : -1;
+  const bool mt4 = mt4_env < 0 ? Wp == 128 : mt4_env != 0;
+  if (mt4 && Wp >= 64 && p.acc_cols <= 32 && Ho >= 4 * p.R && S == 1) mt = 4;
   p.nacc = 512 / (mt * p.acc_cols) >= 4 ? 4 : 2;  // tiles in flight (MMA runs ahead of the epilogue)
   // input by TMA boxes (AT) when a position's channels fill a 64- or 128-byte swizzle row
   const bool at = (cpad == 32 || cpad % 64 == 0) && !(d->variant & 2048);
@@ -664,19 +671,25 @@ int conv_halo_fwd(const ub_conv_desc* d, int lead, int cpad, cudaStream_t stream
   const bool xa = d->relu > 1;
   const bool sb = p.groups > 1;
 #define UB_HALO_CASE(WPV, PL, SBV, SV, ATV)                                                     \
-  if (Wp == WPV && p.planes == PL && sb == SBV && S == SV && at == ATV)                         \
+  if (Wp == WPV && p.planes == PL && sb == SBV && S == SV && at == ATV && mt <= 2)              \
     kern = xa ? (mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV, true>                       \
                          : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV, true>)                       \
               : (mt == 2 ? conv_halo3_kernel<WPV, PL, 2, SBV, SV, ATV, false>                      \
                          : conv_halo3_kernel<WPV, PL, 1, SBV, SV, ATV, false>);
+#define UB_HALO_CASE4(WPV, PL, ATV)                                                              \
+  if (Wp == WPV && p.planes == PL && !sb && S == 1 && at == ATV && mt == 4)                    \
+    kern = xa ? conv_halo3_kernel<WPV, PL, 4, false, 1, ATV, true> : conv_halo3_kernel<WPV, PL, 4, false, 1, ATV, false>;
 #define UB_HALO_WP(WPV)                                                                                    \
   UB_HALO_CASE(WPV, 2, false, 1, false) UB_HALO_CASE(WPV, 4, false, 1, false)                              \
   UB_HALO_CASE(WPV, 4, false, 1, true) UB_HALO_CASE(WPV, 8, false, 1, false)                               \
   UB_HALO_CASE(WPV, 8, false, 1, true) UB_HALO_CASE(WPV, 8, true, 1, false) UB_HALO_CASE(WPV, 8, true, 1, true) \
   UB_HALO_CASE(WPV, 8, true, 2, true)
   UB_HALO_WP(8) UB_HALO_WP(16) UB_HALO_WP(32) UB_HALO_WP(64) UB_HALO_WP(128)
+  UB_HALO_CASE4(64, 4, true) UB_HALO_CASE4(64, 8, true) UB_HALO_CASE4(128, 2, false) UB_HALO_CASE4(128, 4, true)
+  UB_HALO_CASE4(128, 8, true)
 #undef UB_HALO_WP
 #undef UB_HALO_CASE
+#undef UB_HALO_CASE4
   if (!kern) return UB_OK;
   if (const cudaError_t ae = ensure_max_smem(kern)) return cuda_status(ae, "cudaFuncSetAttribute(halo)");
   CUtensorMap tmw{};
